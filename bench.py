@@ -1,0 +1,338 @@
+#!/usr/bin/env python3
+"""Bench: split-KV paged decode attention step (BASELINE configs[1]) on B200.
+
+One "step" = one decode-attention layer step for a 64-request batch:
+64 requests, KV lengths uniform_int(mt19937_64(0), 1024, 32768) (sum 1,068,741
+tokens), GQA 32 q / 8 kv heads, head_dim 128, bf16 paged KV (page 16), i.e.
+K1+K9 over ~4.38 GB of resident KV.  Metric: decode tok/s (requests decoded
+per second through one attention layer) with the kernel's HBM GB/s vs the
+measured peak in the roofline object.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): every rank is an independent DP
+instance with its own cfg2 batch ("replicas", weak scaling); value is the
+whole-job tok/s = N * 64 * K / max-over-ranks device time.
+--impl reference: the reference's own CPU implementation
+(dcpsim::sharded_attention_merge compiled from /root/reference sources into
+oracle/_ref) timed on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HQ, HKV, D, PAGE = 32, 8, 128, 16
+METRIC = "decode tok/s (split-KV paged decode attention step, cfg2: 64 req, KV 1K-32K, GQA 32q/8kv, d128, bf16 paged)"
+UNIT = "tok/s"
+WORKLOAD = "cfg2 single-GPU split-KV decode attention: 64 requests, KV len uniform_int(mt19937_64(0),1024,32768) sum=1068741, GQA 32q/8kv, d=128, bf16 paged KV page=16"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons via NVML during the timed region."""
+
+    def __init__(self, device: int):
+        self.device, self.samples, self.reasons = device, [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    _NAMES = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+        0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self._NAMES.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def _max_over_ranks(x, ws, device):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------ CPU reference
+def cpu_reference_sample(steps: int, token_budget: int = 262_144, threads: int = 0):
+    """Time dcpsim::sharded_attention_merge (the reference, oracle/_ref) over a
+    bounded prefix of the cfg2 requests, outer OpenMP over (request, q-head)
+    (BASELINE.md §4.3).  Returns (tok/s extrapolated to the full cfg2 step,
+    info dict)."""
+    from tests import oracle_lib
+    from paper_2605_21100_b200 import workload
+    L = oracle_lib.reference()
+    kind = "reference"
+    if L is None:
+        raise RuntimeError("oracle/_ref/libdcpsim_ref.so missing (build with make -C oracle)")
+    lens = workload.cfg2_lengths()
+    n, tot = 0, 0
+    while n < len(lens) and tot < token_budget:
+        tot += lens[n]
+        n += 1
+    sl = np.array(lens[:n], np.int64)
+    rng = np.random.default_rng(0)
+    q = rng.standard_normal((n, HQ, D), dtype=np.float32)
+    kv_off = np.zeros(n, np.int64)
+    kv_off[1:] = np.cumsum(sl[:-1] * HKV * D)
+    kv_elems = int(sl.sum()) * HKV * D
+    k = rng.standard_normal(kv_elems, dtype=np.float32)
+    v = rng.standard_normal(kv_elems, dtype=np.float32)
+    bounds = sl.copy()                       # one shard per request (CP = 1 on one GPU)
+    bounds_off = np.arange(n, dtype=np.int64)
+    nb = np.ones(n, np.int32)
+    out = np.zeros((n, HQ, D), np.float32)
+    th = threads or os.cpu_count() or 1
+    P = oracle_lib.P
+    times = []
+    for _ in range(max(steps, 1)):
+        t0 = time.perf_counter()
+        rc = L.dcpref_batch_decode_attn_f32(n, HQ, HKV, D, 1.0 / math.sqrt(D), P(q), P(k), P(v),
+                                            P(kv_off), P(sl), P(bounds), P(bounds_off), P(nb), P(out), th)
+        times.append(time.perf_counter() - t0)
+        assert rc == 0
+    full_tokens = sum(lens)
+    per_step_full = min(times) * full_tokens / float(sl.sum())
+    info = {"kind": kind, "cores": th,
+            "sample": f"first {n} of 64 cfg2 requests ({int(sl.sum())} of {full_tokens} KV tokens, "
+                      f"fp32, one shard each), best of {len(times)}; tok/s scaled by token ratio",
+            "sample_s": min(times)}
+    return 64.0 / per_step_full, info
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    steps = max(1, min(args.steps, 5))
+    for _ in range(min(args.warmup, 1)):
+        cpu_reference_sample(1)
+    val, info = cpu_reference_sample(steps)
+    line = {
+        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": 64.0 / val * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": WORKLOAD, "parallelism": "cpu", "l2": "n/a (host)"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                         "sample": info["sample"]},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ ours
+def run_ours(args, ws, rank, local):
+    import torch
+    from paper_2605_21100_b200 import workload
+    from paper_2605_21100_b200.attention import DcpContext, DecodeAttention
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = DcpContext(local)
+    lens = workload.cfg2_lengths()
+    b = workload.paged_batch(lens, HQ, HKV, D, PAGE)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    pool = torch.randn(b.num_frames, 2, HKV, PAGE, D, generator=g, device=dev, dtype=torch.bfloat16)
+    q = torch.randn(64, HQ, D, generator=g, device=dev, dtype=torch.bfloat16)
+    bt = torch.from_numpy(b.block_table).to(dev)
+    cu = torch.from_numpy(b.cu_pages).to(dev)
+    sl = torch.from_numpy(b.shard_len).to(dev)
+    att = DecodeAttention(ctx, HQ, HKV, D, PAGE, max_shards=64)
+    out, lse = att.prepare(q, pool, bt, cu, sl)
+    stream = torch.cuda.current_stream(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        att.launch(stream)
+    torch.cuda.synchronize(dev)
+    _barrier(ws)
+
+    # ---- device-timed region: K steps, inputs resident in HBM (> L2: no flush needed)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(args.steps):
+            att.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    ms_total = e0.elapsed_time(e1)
+    _barrier(ws)
+    ms_total = _max_over_ranks(ms_total, ws, dev)
+    ms_step = ms_total / args.steps
+    value = ws * 64 * args.steps / (ms_total / 1e3)
+
+    # ---- e2e through the C ABI with host buffers: H2D of Q + block table
+    # metadata each step, D2H of O + LSE each step, inside the timed region.
+    h_q = torch.empty_like(q, device="cpu").pin_memory()
+    h_q.copy_(q.cpu())
+    h_bt = torch.from_numpy(b.block_table).pin_memory()
+    h_cu = torch.from_numpy(b.cu_pages).pin_memory()
+    h_sl = torch.from_numpy(b.shard_len).pin_memory()
+    h_out = torch.empty(out.shape, dtype=out.dtype).pin_memory()
+    h_lse = torch.empty(lse.shape, dtype=lse.dtype).pin_memory()
+    h2d = h_q.numel() * 2 + h_bt.numel() * 4 + h_cu.numel() * 4 + h_sl.numel() * 8
+    d2h = h_out.numel() * 4 + h_lse.numel() * 4
+    for _ in range(3):
+        q.copy_(h_q, non_blocking=True)
+        att.launch(stream)
+        h_out.copy_(out, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    _barrier(ws)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        q.copy_(h_q, non_blocking=True)
+        bt.copy_(h_bt, non_blocking=True)
+        cu.copy_(h_cu, non_blocking=True)
+        sl.copy_(h_sl, non_blocking=True)
+        att.launch(stream)
+        h_out.copy_(out, non_blocking=True)
+        h_lse.copy_(lse, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = _max_over_ranks(f0.elapsed_time(f1), ws, dev)
+    e2e_val = ws * 64 * args.steps / (e2e_ms / 1e3)
+
+    peak, peak_kind = _peaks()
+    alg_bytes = b.algorithmic_bytes()
+    achieved = alg_bytes / (ms_step / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            v, info = cpu_reference_sample(1)
+            cpu = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                   "sample": info["sample"]}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": f"replicas x{ws}" if ws > 1 else "single",
+                       "l2": "no flush: 4.38 GB KV per step >> 126 MB L2",
+                       "kv_tokens": b.total_tokens, "kv_pages": int(b.cu_pages[-1])},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "path": "dcp_splitkv_decode_attn via C ABI; pinned host Q/block-table/lengths in, O+LSE out"},
+            "gpu_launches": args.steps * _capi_launches(),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_kind": peak_kind, "kernel": "splitkv_decode_kernel<8,4>",
+                         "algorithmic_bytes_per_launch": alg_bytes},
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def _capi_launches():
+    from paper_2605_21100_b200 import _capi
+    return _capi.lib().dcp_attn_launches_per_call()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

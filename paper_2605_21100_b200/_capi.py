@@ -1,0 +1,119 @@
+"""ctypes binding of include/dcp_capi.h (the product C ABI).
+
+The product is libdcp_b200.so (sm_100a kernels + C ABI + dcpsim C++ drop-in).
+This module only loads it and maps status codes onto the dcpsim exception
+hierarchy (reference types.hpp:19-30).  There is no fallback: if the library
+or a CUDA device is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from ctypes import (POINTER, Structure, c_char_p, c_float, c_int, c_int32, c_int64, c_size_t,
+                    c_void_p)
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_build" / "libdcp_b200.so"
+
+
+# ---- dcpsim exception hierarchy (types.hpp:19-30) -------------------------------
+class SimError(RuntimeError):
+    pass
+
+
+class InsufficientFrames(SimError):
+    pass
+
+
+class UnknownRequest(SimError):
+    pass
+
+
+class UnknownPage(SimError):
+    pass
+
+
+class InconsistentPlacement(SimError):
+    pass
+
+
+class ShapeOverflow(SimError):
+    pass
+
+
+class EmptyShard(SimError):
+    pass
+
+
+class ConfigError(SimError):
+    pass
+
+
+class DcpInvalidArgument(ValueError):
+    pass
+
+
+class DcpUnsupported(NotImplementedError):
+    pass
+
+
+class DcpCudaError(RuntimeError):
+    pass
+
+
+_CODES = {
+    -1: InsufficientFrames, -2: UnknownRequest, -3: UnknownPage, -4: InconsistentPlacement,
+    -5: ShapeOverflow, -6: EmptyShard, -7: ConfigError, -8: DcpInvalidArgument,
+    -9: DcpUnsupported, -10: DcpCudaError,
+}
+
+
+class AttnArgs(Structure):
+    _fields_ = [
+        ("num_shards", c_int32), ("num_q_heads", c_int32), ("num_kv_heads", c_int32),
+        ("head_dim", c_int32), ("page_size", c_int32), ("num_frames", c_int64),
+        ("q", c_void_p), ("kv_pool", c_void_p), ("block_table", c_void_p),
+        ("cu_pages", c_void_p), ("shard_len", c_void_p), ("page_fill", c_void_p),
+        ("scale", c_float), ("out", c_void_p), ("lse", c_void_p),
+        ("workspace", c_void_p), ("workspace_bytes", c_size_t),
+    ]
+
+
+_lib = None
+
+# (name, restype, argtypes) for every entry point of include/dcp_capi.h.
+_SIGNATURES = [
+    ("dcp_last_error", c_char_p, []),
+    ("dcp_version", c_char_p, []),
+    ("dcp_ctx_create", c_int, [c_int, POINTER(c_void_p)]),
+    ("dcp_ctx_destroy", c_int, [c_void_p]),
+    ("dcp_ctx_num_sms", c_int, [c_void_p]),
+    ("dcp_attn_workspace_bytes", c_size_t, [c_void_p, c_int32, c_int32, c_int32]),
+    ("dcp_splitkv_decode_attn", c_int, [c_void_p, POINTER(AttnArgs), c_void_p]),
+    ("dcp_attn_launches_per_call", c_int, []),
+]
+
+
+def exported_symbols():
+    return [s[0] for s in _SIGNATURES]
+
+
+def lib():
+    """Load libdcp_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2605_21100_b200.build` "
+                              "(no CPU fallback exists)")
+        L = ctypes.CDLL(str(LIB_PATH), mode=ctypes.RTLD_GLOBAL)
+        for name, res, args in _SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().dcp_last_error().decode(errors="replace")
+        raise _CODES.get(rc, RuntimeError)(f"dcp error {rc}: {msg}")

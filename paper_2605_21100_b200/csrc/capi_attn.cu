@@ -1,0 +1,190 @@
+// SPDX-License-Identifier: Apache-2.0
+// C ABI: context + K1/K9 split-KV paged decode attention (dcp_capi.h).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "capi_common.cuh"
+#include "splitkv_decode.cuh"
+
+namespace dcp {
+
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 2-D view of the paged pool: rows = frame*2*HKV*16 + (kv*HKV + head)*16 + tok,
+// columns = head_dim (bf16).  Box = 64 columns (128 B, 128B swizzle) x all
+// rows of one frame.
+static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv, int d,
+                         const CUtensorMap** out) {
+    for (auto& e : ctx->kv_maps) {
+        if (e.base == pool && e.frames == frames && e.hkv == hkv && e.d == d) {
+            *out = &e.map;
+            return DCP_OK;
+        }
+    }
+    auto fn = encode_fn();
+    DCP_REQUIRE(fn != nullptr, DCP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    auto& e = ctx->kv_maps[ctx->kv_map_next];
+    ctx->kv_map_next = (ctx->kv_map_next + 1) % 4;
+    const int rows_per_frame = 2 * hkv * 16;
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(d),
+                          static_cast<cuuint64_t>(frames) * rows_per_frame};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows_per_frame)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims,
+                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        e.base = nullptr;
+        set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+        return DCP_E_CUDA;
+    }
+    e.base = pool;
+    e.frames = frames;
+    e.hkv = hkv;
+    e.d = d;
+    *out = &e.map;
+    return DCP_OK;
+}
+
+template <int HKV, int G>
+static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm,
+                         cudaStream_t stream) {
+    using C = DecodeCfg<HKV, G>;
+    static bool attr_done = false;  // per-instantiation, per-process
+    if (!attr_done) {
+        DCP_CUDA_TRY(cudaFuncSetAttribute(splitkv_decode_kernel<HKV, G>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+        attr_done = true;
+    }
+    splitkv_decode_kernel<HKV, G><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+}  // namespace dcp
+
+using namespace dcp;
+
+extern "C" {
+
+const char* dcp_last_error(void) { return g_err.c_str(); }
+const char* dcp_version(void) { return "dcp-b200 0.1 (sm_100a)"; }
+
+int dcp_ctx_create(int device, dcp_ctx** out) {
+    DCP_REQUIRE(out != nullptr, DCP_E_INVALID_ARG, "out is NULL");
+    int n = 0;
+    DCP_CUDA_TRY(cudaGetDeviceCount(&n));
+    DCP_REQUIRE(device >= 0 && device < n, DCP_E_INVALID_ARG, "device %d of %d", device, n);
+    DCP_CUDA_TRY(cudaSetDevice(device));
+    auto* c = new dcp_ctx();
+    c->device = device;
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&c->cc_major, cudaDevAttrComputeCapabilityMajor, device);
+    cudaDeviceGetAttribute(&c->cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+    if (c->cc_major != 10) {
+        set_error("device %d is sm_%d%d; this library is built for sm_100a only", device,
+                  c->cc_major, c->cc_minor);
+        delete c;
+        return DCP_E_UNSUPPORTED;
+    }
+    *out = c;
+    return DCP_OK;
+}
+
+int dcp_ctx_destroy(dcp_ctx* ctx) {
+    delete ctx;
+    return DCP_OK;
+}
+
+int dcp_ctx_num_sms(const dcp_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+
+size_t dcp_attn_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards, int32_t num_q_heads,
+                                int32_t head_dim) {
+    if (!ctx || num_shards < 0 || num_q_heads <= 0 || head_dim <= 0) return 0;
+    const size_t slots = 2 * static_cast<size_t>(ctx->num_sms);
+    size_t b = slots * num_q_heads * head_dim * sizeof(float);  // ws_acc
+    b += slots * num_q_heads * 2 * sizeof(float);               // ws_ml
+    b += static_cast<size_t>(num_shards) * sizeof(int32_t);     // counters
+    return (b + 255) & ~size_t(255);
+}
+
+int dcp_attn_launches_per_call(void) { return 1; }
+
+int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) {
+    DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");
+    DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
+    if (a->num_shards == 0) return DCP_OK;
+    DCP_REQUIRE(a->head_dim == 128, DCP_E_UNSUPPORTED, "head_dim %d (compiled: 128)", a->head_dim);
+    DCP_REQUIRE(a->page_size == 16, DCP_E_UNSUPPORTED, "page_size %d (compiled: 16)", a->page_size);
+    DCP_REQUIRE(a->num_kv_heads > 0 && a->num_q_heads % a->num_kv_heads == 0, DCP_E_INVALID_ARG,
+                "num_q_heads %d not a multiple of num_kv_heads %d", a->num_q_heads, a->num_kv_heads);
+    DCP_REQUIRE(a->q && a->kv_pool && a->block_table && a->cu_pages && a->shard_len && a->out &&
+                    a->lse && a->workspace,
+                DCP_E_INVALID_ARG, "NULL device pointer in dcp_attn_args");
+    DCP_REQUIRE((reinterpret_cast<uintptr_t>(a->kv_pool) & 15) == 0, DCP_E_INVALID_ARG,
+                "kv_pool must be 16-byte aligned");
+    DCP_REQUIRE(a->num_frames > 0, DCP_E_INVALID_ARG, "num_frames <= 0");
+    const size_t need = dcp_attn_workspace_bytes(ctx, a->num_shards, a->num_q_heads, a->head_dim);
+    DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu bytes",
+                a->workspace_bytes, need);
+    const int G = a->num_q_heads / a->num_kv_heads;
+
+    const CUtensorMap* map = nullptr;
+    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map);
+    if (rc) return rc;
+
+    AttnParams prm;
+    prm.q = static_cast<const __nv_bfloat16*>(a->q);
+    prm.block_table = a->block_table;
+    prm.cu_pages = a->cu_pages;
+    prm.shard_len = a->shard_len;
+    prm.page_fill = a->page_fill;
+    prm.out = a->out;
+    prm.lse = a->lse;
+    const size_t slots = 2 * static_cast<size_t>(ctx->num_sms);
+    char* ws = static_cast<char*>(a->workspace);
+    prm.ws_acc = reinterpret_cast<float*>(ws);
+    ws += slots * a->num_q_heads * a->head_dim * sizeof(float);
+    prm.ws_ml = reinterpret_cast<float*>(ws);
+    ws += slots * a->num_q_heads * 2 * sizeof(float);
+    prm.counters = reinterpret_cast<int32_t*>(ws);
+    prm.num_shards = a->num_shards;
+    prm.scale_log2 = a->scale * 1.4426950408889634f;
+
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int hkv = a->num_kv_heads;
+    if (hkv == 8 && G == 4) return launch_decode<8, 4>(ctx, map, prm, s);
+    if (hkv == 4 && G == 8) return launch_decode<4, 8>(ctx, map, prm, s);
+    if (hkv == 8 && G == 1) return launch_decode<8, 1>(ctx, map, prm, s);
+    if (hkv == 2 && G == 16) return launch_decode<2, 16>(ctx, map, prm, s);
+    if (hkv == 1 && G == 16) return launch_decode<1, 16>(ctx, map, prm, s);
+    set_error("unsupported (num_kv_heads=%d, group=%d)", hkv, G);
+    return DCP_E_UNSUPPORTED;
+}
+
+}  // extern "C"

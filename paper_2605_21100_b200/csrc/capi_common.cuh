@@ -1,0 +1,52 @@
+// SPDX-License-Identifier: Apache-2.0
+// Shared C-ABI plumbing: error state, context object, CUDA error mapping.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "dcp_capi.h"
+
+namespace dcp {
+
+void set_error(const char* fmt, ...);
+
+#define DCP_CUDA_TRY(expr)                                                              \
+    do {                                                                                \
+        cudaError_t e_ = (expr);                                                        \
+        if (e_ != cudaSuccess) {                                                        \
+            ::dcp::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+            return DCP_E_CUDA;                                                          \
+        }                                                                               \
+    } while (0)
+
+#define DCP_REQUIRE(cond, code, ...)        \
+    do {                                    \
+        if (!(cond)) {                      \
+            ::dcp::set_error(__VA_ARGS__);  \
+            return (code);                  \
+        }                                   \
+    } while (0)
+
+struct TmapCacheEntry {
+    const void* base = nullptr;
+    int64_t frames = 0;
+    int hkv = 0;
+    int d = 0;
+    CUtensorMap map;
+};
+
+}  // namespace dcp
+
+struct dcp_ctx {
+    int device = 0;
+    int num_sms = 0;
+    int cc_major = 0, cc_minor = 0;
+    dcp::TmapCacheEntry kv_maps[4];
+    int kv_map_next = 0;
+};

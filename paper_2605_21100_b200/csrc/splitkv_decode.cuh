@@ -1,0 +1,420 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K1 + K9: split-KV paged decode attention for sm_100a.
+//
+// Semantics (per shard r, q-head h):   reference attn_merge.hpp:53-82
+//   s_j  = scale * <q, k_j>                      (hpp:66-67)
+//   O    = sum_j softmax(s)_j v_j                (hpp:68-79, normalised, hpp:79)
+//   lse  = max_j s_j + ln(sum_j exp(s_j - max))  (hpp:80, natural log)
+// and the intra-GPU combine of chunk partials follows lse_merge (hpp:86-100):
+//   out = sum_k w_k O_k / sum_k w_k,  w_k = exp(lse_k - max lse).
+//
+// Design (B200):
+//   * HBM-bound (GQA-4: ~4 flop/B).  One persistent CTA per SM; the flattened
+//     page sequence of all shards is cut into gridDim.x equal page ranges
+//     ("stream-K" over pages), so every SM streams the same number of bytes
+//     regardless of the 1K..32K length skew.
+//   * One producer warp streams whole frames (K and V of every kv-head, the
+//     64 KB page of cfg2) into a STAGES-deep shared-memory ring with two 2-D
+//     TMA tensor loads per page (128-B swizzle, L2 evict-first), completion
+//     tracked by mbarrier transaction counts.
+//   * One consumer warp per kv-head: the GQA group's q-heads are the M rows
+//     of mma.sync m16n8k16 bf16 tiles (tokens on N for QK^T, head-dim on N for
+//     PV), fp32 accumulation, online softmax in the log2 domain.
+//   * A shard cut by a range boundary leaves partials (unnormalised O, max,
+//     sum) in a per-CTA slot; the last CTA to finish the shard (device-scope
+//     atomic ticket) merges them in page order — no second launch.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include "ptx.cuh"
+
+namespace dcp {
+
+struct AttnParams {
+    const __nv_bfloat16* q;      // [R][HQ][D]
+    const int32_t* block_table;  // [P]
+    const int32_t* cu_pages;     // [R+1]
+    const int64_t* shard_len;    // [R]
+    const uint8_t* page_fill;    // [P] or nullptr
+    float* out;                  // [R][HQ][D]
+    float* lse;                  // [R][HQ]
+    float* ws_acc;               // [2*grid][HQ][D]
+    float* ws_ml;                // [2*grid][HQ][2]
+    int32_t* counters;           // [R]
+    int32_t num_shards;
+    float scale_log2;            // scale * log2(e)
+};
+
+template <int HKV, int G>
+struct DecodeCfg {
+    static constexpr int D = 128;
+    static constexpr int PAGE = 16;
+    static constexpr int HQ = HKV * G;
+    static constexpr int ROWS = 2 * HKV * PAGE;       // 2-D tensor rows per frame
+    static constexpr int BOX_BYTES = ROWS * 128;      // one 64-column swizzled box
+    static constexpr int STAGE_BYTES = 2 * BOX_BYTES; // == one frame
+    static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int CONSUMERS = HKV;             // warps
+    static constexpr int THREADS = (HKV + 1) * 32;
+    static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+    static constexpr int SMEM = 1024 + BAR_OFF + 2 * STAGES * 8 + STAGES * 4 + 16;
+    static_assert(ROWS <= 256, "TMA box rows");
+    static_assert(G <= 16, "group must fit the 16 mma rows");
+};
+
+__device__ __forceinline__ int cta_of_page(int64_t p, int64_t P, int64_t grid) {
+    // CTA c owns pages [floor(c*P/grid), floor((c+1)*P/grid)).
+    return static_cast<int>(((p + 1) * grid + P - 1) / P - 1);
+}
+
+template <int HKV, int G>
+__global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
+    splitkv_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnParams p) {
+    using C = DecodeCfg<HKV, G>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t smem_base = smem_u32(smem);
+    const uint32_t full_bar = smem_base + C::BAR_OFF;
+    const uint32_t empty_bar = full_bar + C::STAGES * 8;
+    uint8_t* stage_fill = smem + C::BAR_OFF + 2 * C::STAGES * 8;
+    volatile int* last_flag = reinterpret_cast<volatile int*>(stage_fill + C::STAGES * 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int R = p.num_shards;
+    const int64_t P = p.cu_pages[R];
+    const int64_t grid = gridDim.x;
+    const int cta = blockIdx.x;
+    const int p_begin = static_cast<int>(cta * P / grid);
+    const int p_end = static_cast<int>((cta + 1) * P / grid);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(full_bar + 8 * s, 1);
+            mbar_init(empty_bar + 8 * s, C::CONSUMERS);
+        }
+        fence_mbar_init();
+    }
+    if (warp == C::CONSUMERS && lane == 0) tma_prefetch_desc(&kv_map);
+    __syncthreads();
+
+    if (warp == C::CONSUMERS) {
+        // ===================== producer warp =====================
+        const uint64_t policy = l2_policy_evict_first();
+        for (int base = p_begin; base < p_end; base += 32) {
+            const int mine = base + lane;
+            int frame = 0, fill = C::PAGE;
+            if (mine < p_end) {
+                frame = __ldg(p.block_table + mine);
+                if (p.page_fill) fill = __ldg(p.page_fill + mine);
+            }
+            const int n = min(32, p_end - base);
+            for (int i = 0; i < n; ++i) {
+                const int f = __shfl_sync(0xffffffffu, frame, i);
+                const int fl = __shfl_sync(0xffffffffu, fill, i);
+                if (lane == 0) {
+                    const int it = base - p_begin + i;
+                    const int s = it % C::STAGES;
+                    const uint32_t ph = (it / C::STAGES) & 1;
+                    mbar_wait(empty_bar + 8 * s, ph ^ 1);
+                    stage_fill[s] = static_cast<uint8_t>(fl);
+                    mbar_arrive_expect_tx(full_bar + 8 * s, C::STAGE_BYTES);
+                    const uint32_t dst = smem_base + s * C::STAGE_BYTES;
+                    const int row = f * C::ROWS;
+                    tma_load_2d(dst, &kv_map, 0, row, full_bar + 8 * s, policy);
+                    tma_load_2d(dst + C::BOX_BYTES, &kv_map, 64, row, full_bar + 8 * s, policy);
+                }
+                __syncwarp();
+            }
+        }
+        return;
+    }
+
+    // ===================== consumer warps (one per kv-head) =====================
+    const int h = warp;
+    const int g = lane >> 2;
+    const int t = lane & 3;
+    constexpr int NCT = C::CONSUMERS * 32;
+
+    // Zero-token shards: O = 0, LSE = -inf (weight 0 in any merge).
+    for (int r = cta; r < R; r += gridDim.x) {
+        if (p.cu_pages[r + 1] == p.cu_pages[r]) {
+            for (int row = 0; row < G; ++row) {
+                float* o = p.out + (static_cast<size_t>(r) * C::HQ + h * G + row) * C::D;
+                reinterpret_cast<float4*>(o)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (lane == 0) p.lse[static_cast<size_t>(r) * C::HQ + h * G + row] = -INFINITY;
+            }
+        }
+    }
+    if (p_begin >= p_end) return;
+
+    // Per-lane ldmatrix offsets (stage-relative).  Row & 7 == lane & 7 since
+    // every head tile starts on an 8-row boundary (128B swizzle atom).
+    const int mi = lane >> 3, rr = lane & 7;
+    uint32_t k_off[2][4], v_off[8];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int kp = 0; kp < 4; ++kp) {
+            const int ks = 2 * kp + (mi >> 1);
+            const int box = ks >> 2;
+            const int chunk = ((ks & 3) << 1) | (mi & 1);
+            const int row = h * C::PAGE + nt * 8 + rr;
+            k_off[nt][kp] = box * C::BOX_BYTES + row * 128 + ((chunk ^ rr) << 4);
+        }
+#pragma unroll
+    for (int np = 0; np < 8; ++np) {
+        const int tok = (mi & 1) * 8 + rr;
+        const int dchunk = 2 * np + (mi >> 1);
+        const int box = dchunk >> 3, chunk = dchunk & 7;
+        const int row = HKV * C::PAGE + h * C::PAGE + tok;
+        v_off[np] = box * C::BOX_BYTES + row * 128 + ((chunk ^ rr) << 4);
+    }
+
+    // First shard with a page in [p_begin, ...): last r with cu[r] <= p_begin.
+    int r;
+    {
+        int lo = 0, hi = R;  // answer in [0, R-1]
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (p.cu_pages[mid] <= p_begin) lo = mid; else hi = mid - 1;
+        }
+        r = lo;
+    }
+
+    constexpr bool TWO_HALVES = (G > 8);
+    const bool row0_real = g < G;
+    const bool row1_real = TWO_HALVES && (g + 8) < G;
+
+    int it = 0;
+    int pg = p_begin;
+    while (pg < p_end) {
+        while (p.cu_pages[r + 1] <= pg) ++r;  // skip zero-page shards
+        const int r_first = p.cu_pages[r];
+        const int r_last = p.cu_pages[r + 1];
+        const int seg_begin = pg;
+        const int seg_end = min(r_last, p_end);
+        const int64_t len = p.shard_len[r];
+
+        // Q fragments (A operand, rows = q-heads of this kv group).
+        uint32_t qa[8][4];
+        {
+            const __nv_bfloat16* q0 =
+                p.q + (static_cast<size_t>(r) * C::HQ + h * G + g) * C::D + 2 * t;
+            const __nv_bfloat16* q1 = q0 + 8 * C::D;
+#pragma unroll
+            for (int ks = 0; ks < 8; ++ks) {
+                qa[ks][0] = row0_real ? __ldg(reinterpret_cast<const uint32_t*>(q0 + 16 * ks)) : 0u;
+                qa[ks][2] =
+                    row0_real ? __ldg(reinterpret_cast<const uint32_t*>(q0 + 16 * ks + 8)) : 0u;
+                qa[ks][1] = row1_real ? __ldg(reinterpret_cast<const uint32_t*>(q1 + 16 * ks)) : 0u;
+                qa[ks][3] =
+                    row1_real ? __ldg(reinterpret_cast<const uint32_t*>(q1 + 16 * ks + 8)) : 0u;
+            }
+        }
+
+        float acc[16][4];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
+        float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+        for (; pg < seg_end; ++pg, ++it) {
+            const int s = it % C::STAGES;
+            const uint32_t ph = (it / C::STAGES) & 1;
+            int fill;
+            if (p.page_fill) {
+                mbar_wait(full_bar + 8 * s, ph);
+                fill = stage_fill[s];
+            } else {
+                const int64_t rem = len - static_cast<int64_t>(pg - r_first) * C::PAGE;
+                fill = rem < C::PAGE ? static_cast<int>(rem) : C::PAGE;
+                mbar_wait(full_bar + 8 * s, ph);
+            }
+            const uint32_t st = smem_base + s * C::STAGE_BYTES;
+
+            // ---- S = Q K^T (16 rows x 16 tokens) ----
+            float sc[2][4];
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt) {
+                sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+                for (int kp = 0; kp < 4; ++kp) {
+                    uint32_t b0, b1, b2, b3;
+                    ldsm_x4(st + k_off[nt][kp], b0, b1, b2, b3);
+                    mma_bf16_16816(sc[nt], qa[2 * kp][0], qa[2 * kp][1], qa[2 * kp][2],
+                                   qa[2 * kp][3], b0, b1);
+                    mma_bf16_16816(sc[nt], qa[2 * kp + 1][0], qa[2 * kp + 1][1],
+                                   qa[2 * kp + 1][2], qa[2 * kp + 1][3], b2, b3);
+                }
+            }
+
+            // ---- online softmax (log2 domain), rows g and g+8 ----
+            float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int tok = nt * 8 + 2 * t + j;
+                    const bool ok = tok < fill;
+                    sc[nt][j] = ok ? sc[nt][j] * p.scale_log2 : -INFINITY;
+                    sc[nt][2 + j] = ok ? sc[nt][2 + j] * p.scale_log2 : -INFINITY;
+                    mx0 = fmaxf(mx0, sc[nt][j]);
+                    mx1 = fmaxf(mx1, sc[nt][2 + j]);
+                }
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 1));
+            mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, 2));
+            const float mn0 = fmaxf(m0, mx0);
+            const float al0 = fast_exp2(m0 - mn0);
+            m0 = mn0;
+            float ps0 = 0.f;
+#pragma unroll
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    sc[nt][j] = fast_exp2(sc[nt][j] - mn0);
+                    ps0 += sc[nt][j];
+                }
+            l0 = l0 * al0 + ps0;
+            float al1 = 1.f;
+            if constexpr (TWO_HALVES) {
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 1));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, 2));
+                const float mn1 = fmaxf(m1, mx1);
+                al1 = fast_exp2(m1 - mn1);
+                m1 = mn1;
+                float ps1 = 0.f;
+#pragma unroll
+                for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        sc[nt][2 + j] = fast_exp2(sc[nt][2 + j] - mn1);
+                        ps1 += sc[nt][2 + j];
+                    }
+                l1 = l1 * al1 + ps1;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                acc[i][0] *= al0;
+                acc[i][1] *= al0;
+                if constexpr (TWO_HALVES) {
+                    acc[i][2] *= al1;
+                    acc[i][3] *= al1;
+                }
+            }
+
+            // ---- O += P V ----
+            const uint32_t pa0 = pack_bf16x2(sc[0][0], sc[0][1]);
+            const uint32_t pa2 = pack_bf16x2(sc[1][0], sc[1][1]);
+            const uint32_t pa1 = TWO_HALVES ? pack_bf16x2(sc[0][2], sc[0][3]) : 0u;
+            const uint32_t pa3 = TWO_HALVES ? pack_bf16x2(sc[1][2], sc[1][3]) : 0u;
+#pragma unroll
+            for (int np = 0; np < 8; ++np) {
+                uint32_t b0, b1, b2, b3;
+                ldsm_x4_t(st + v_off[np], b0, b1, b2, b3);
+                mma_bf16_16816(acc[2 * np], pa0, pa1, pa2, pa3, b0, b1);
+                mma_bf16_16816(acc[2 * np + 1], pa0, pa1, pa2, pa3, b2, b3);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+        }
+
+        // ---- finalize the segment [seg_begin, seg_end) of shard r ----
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+        l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+        if constexpr (TWO_HALVES) {
+            l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+            l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+        }
+        const bool complete = (seg_begin == r_first) && (seg_end == r_last);
+        if (complete) {
+            const float ln2 = 0.69314718055994530942f;
+#pragma unroll
+            for (int half = 0; half < (TWO_HALVES ? 2 : 1); ++half) {
+                const bool real = half == 0 ? row0_real : row1_real;
+                if (!real) continue;
+                const int qh = h * G + g + 8 * half;
+                const float l = half == 0 ? l0 : l1;
+                const float m = half == 0 ? m0 : m1;
+                const float inv = 1.f / l;
+                float* o = p.out + (static_cast<size_t>(r) * C::HQ + qh) * C::D + 2 * t;
+#pragma unroll
+                for (int nt = 0; nt < 16; ++nt)
+                    *reinterpret_cast<float2*>(o + nt * 8) =
+                        make_float2(acc[nt][2 * half] * inv, acc[nt][2 * half + 1] * inv);
+                if (t == 0) p.lse[static_cast<size_t>(r) * C::HQ + qh] = (m + __log2f(l)) * ln2;
+            }
+        } else {
+            const int slot = 2 * cta + (seg_begin == p_begin ? 0 : 1);
+#pragma unroll
+            for (int half = 0; half < (TWO_HALVES ? 2 : 1); ++half) {
+                const bool real = half == 0 ? row0_real : row1_real;
+                if (!real) continue;
+                const int qh = h * G + g + 8 * half;
+                float* w = p.ws_acc + (static_cast<size_t>(slot) * C::HQ + qh) * C::D + 2 * t;
+#pragma unroll
+                for (int nt = 0; nt < 16; ++nt)
+                    __stcg(reinterpret_cast<float2*>(w + nt * 8),
+                           make_float2(acc[nt][2 * half], acc[nt][2 * half + 1]));
+                if (t == 0)
+                    __stcg(reinterpret_cast<float2*>(p.ws_ml) + (static_cast<size_t>(slot) * C::HQ + qh),
+                           make_float2(half == 0 ? m0 : m1, half == 0 ? l0 : l1));
+            }
+            __threadfence();
+            named_bar_sync(1, NCT);
+            if (threadIdx.x == 0) {
+                const int a = cta_of_page(r_first, P, grid);
+                const int b = cta_of_page(r_last - 1, P, grid);
+                const int prev = atomicAdd(p.counters + r, 1);
+                *last_flag = (prev == b - a) ? 1 : 0;
+            }
+            named_bar_sync(1, NCT);
+            if (*last_flag) {
+                __threadfence();
+                const int a = cta_of_page(r_first, P, grid);
+                const int b = cta_of_page(r_last - 1, P, grid);
+                const float ln2 = 0.69314718055994530942f;
+                for (int row = 0; row < G; ++row) {
+                    const int qh = h * G + row;
+                    float mmax = -INFINITY;
+                    for (int k = a; k <= b; ++k) {
+                        const int sl = (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
+                        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
+                                                 (static_cast<size_t>(sl) * C::HQ + qh));
+                        mmax = fmaxf(mmax, ml.x);
+                    }
+                    float den = 0.f;
+                    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int k = a; k <= b; ++k) {
+                        const int sl = (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
+                        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
+                                                 (static_cast<size_t>(sl) * C::HQ + qh));
+                        const float w = fast_exp2(ml.x - mmax);
+                        den += w * ml.y;
+                        const float4 v = __ldcg(reinterpret_cast<const float4*>(
+                                                    p.ws_acc + (static_cast<size_t>(sl) * C::HQ + qh) * C::D) +
+                                                lane);
+                        num.x += w * v.x;
+                        num.y += w * v.y;
+                        num.z += w * v.z;
+                        num.w += w * v.w;
+                    }
+                    const float inv = 1.f / den;
+                    float* o = p.out + (static_cast<size_t>(r) * C::HQ + qh) * C::D;
+                    reinterpret_cast<float4*>(o)[lane] =
+                        make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
+                    if (lane == 0) p.lse[static_cast<size_t>(r) * C::HQ + qh] = (mmax + __log2f(den)) * ln2;
+                }
+                if (threadIdx.x == 0) p.counters[r] = 0;  // re-arm for the next launch / graph replay
+            }
+        }
+        ++r;
+    }
+}
+
+}  // namespace dcp
