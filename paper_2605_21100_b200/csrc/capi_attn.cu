@@ -75,11 +75,11 @@ template <int HKV, int G>
 static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm,
                          cudaStream_t stream) {
     using C = DecodeCfg<HKV, G>;
-    static bool attr_done = false;  // per-instantiation, per-process
-    if (!attr_done) {
+    static uint64_t attr_done = 0;  // per-instantiation bit per device
+    if (!(attr_done >> (ctx->device & 63) & 1)) {
         DCP_CUDA_TRY(cudaFuncSetAttribute(splitkv_decode_kernel<HKV, G>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-        attr_done = true;
+        attr_done |= uint64_t(1) << (ctx->device & 63);
     }
     splitkv_decode_kernel<HKV, G><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
     DCP_CUDA_TRY(cudaGetLastError());

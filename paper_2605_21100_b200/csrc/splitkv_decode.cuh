@@ -71,6 +71,10 @@ __device__ __forceinline__ int cta_of_page(int64_t p, int64_t P, int64_t grid) {
     // CTA c owns pages [floor(c*P/grid), floor((c+1)*P/grid)).
     return static_cast<int>(((p + 1) * grid + P - 1) / P - 1);
 }
+// With fewer pages than CTAs some ranges are empty; those CTAs hold no partial.
+__device__ __forceinline__ bool cta_nonempty(int64_t k, int64_t P, int64_t grid) {
+    return P >= grid || (k * P / grid) < ((k + 1) * P / grid);
+}
 
 template <int HKV, int G>
 __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
@@ -370,8 +374,13 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
             if (threadIdx.x == 0) {
                 const int a = cta_of_page(r_first, P, grid);
                 const int b = cta_of_page(r_last - 1, P, grid);
+                int nparts = b - a + 1;
+                if (P < grid) {
+                    nparts = 0;
+                    for (int k = a; k <= b; ++k) nparts += cta_nonempty(k, P, grid);
+                }
                 const int prev = atomicAdd(p.counters + r, 1);
-                *last_flag = (prev == b - a) ? 1 : 0;
+                *last_flag = (prev == nparts - 1) ? 1 : 0;
             }
             named_bar_sync(1, NCT);
             if (*last_flag) {
@@ -383,6 +392,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                     const int qh = h * G + row;
                     float mmax = -INFINITY;
                     for (int k = a; k <= b; ++k) {
+                        if (!cta_nonempty(k, P, grid)) continue;
                         const int sl = (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
                         const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
                                                  (static_cast<size_t>(sl) * C::HQ + qh));
@@ -391,6 +401,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                     float den = 0.f;
                     float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
                     for (int k = a; k <= b; ++k) {
+                        if (!cta_nonempty(k, P, grid)) continue;
                         const int sl = (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
                         const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
                                                  (static_cast<size_t>(sl) * C::HQ + qh));
