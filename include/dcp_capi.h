@@ -62,6 +62,8 @@ typedef struct dcp_ctx dcp_ctx;
 DCP_API int dcp_ctx_create(int device, dcp_ctx** out);
 DCP_API int dcp_ctx_destroy(dcp_ctx* ctx);
 DCP_API int dcp_ctx_num_sms(const dcp_ctx* ctx);
+/* Synchronous device->host copy of `bytes` (for hosts that bind only this ABI). */
+DCP_API int dcp_copy_to_host(void* dst, const void* src, size_t bytes);
 
 /* ---- K1 + K9: split-KV paged decode attention --------------------------------
  *
@@ -118,6 +120,93 @@ DCP_API int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* args, voi
 /* Number of kernel launches the last dcp_splitkv_decode_attn issued (for the
  * bench's gpu_launches accounting). */
 DCP_API int dcp_attn_launches_per_call(void);
+
+
+/* ---- K6 + K7: the DCP planner on the device ----------------------------------
+ *
+ * Device-resident cluster state (InstanceState K_s/B_s/R_i + LIFO free-frame
+ * stacks, page_table.hpp:13-25, make_cluster page_table.cpp:133-148), the
+ * global page table (page_table.hpp:36-74) and the FIFO waiting queue.
+ * Semantics are the reference's, bit-exact:
+ *   dcp_planner_step         Scheduler::step             scheduler.cpp:245-306
+ *                            (rebalance_active, place_dcp / place_single /
+ *                            place_uniform, water_fill, can_allocate,
+ *                            never_fits, GlobalPageTable::allocate)
+ *   dcp_planner_finish       pt_free / GlobalPageTable::release  page_table.cpp:51-66
+ *   dcp_planner_append_token GlobalPageTable::append_token       page_table.cpp:86-121
+ *   dcp_planner_build_routing build_binding_config + derive_routing_tables
+ *                            + bucket_shape              routing.cpp:9-63, 101-109
+ *   dcp_planner_dump_*       GlobalPageTable::dump_csv / dump_routing_csv
+ *                                                        page_table.cpp:123-131, routing.cpp:65-79
+ * The active set of a step is every request committed and not yet finished
+ * (the `active` span of Scheduler::step).  Limits: world size <= 32,
+ * instances_per_node <= 16, capacity_pages < 2^31.
+ * Errors: InsufficientFrames(-1) for a zero-length request reaching
+ * allocate, UnknownRequest(-2) for finish/append of an unknown id,
+ * ConfigError(-7) for an invalid policy (SchedulerPolicy::validate,
+ * scheduler.cpp:35-41), InconsistentPlacement(-4) from build_routing. */
+typedef struct dcp_planner dcp_planner;
+
+enum { DCP_POLICY_DCP = 0, DCP_POLICY_LEAST_BATCH = 1, DCP_POLICY_LEAST_CACHE = 2,
+       DCP_POLICY_UNIFORM_CP = 3 };
+
+typedef struct dcp_planner_config {
+    int32_t nodes;
+    int32_t instances_per_node;
+    int64_t page_size;
+    int64_t capacity_pages;     /* per instance */
+    int32_t policy;             /* DCP_POLICY_* (PolicyKind, scheduler.hpp:29) */
+    int32_t n_bucket;           /* 0 = BucketFn::default_table() */
+    const int64_t* bucket_len;  /* host, inclusive upper bounds */
+    const int32_t* bucket_deg;  /* host */
+    int32_t uniform_degree;
+    int32_t hol_strict;
+    int32_t max_requests;       /* concurrent request slots */
+    int64_t reserve_pages;      /* per-request page-list growth reserve */
+} dcp_planner_config;
+
+/* Read-only device view of one instance after dcp_planner_build_routing:
+ * the K1 inputs of that instance (shards = its N list, in request-id order). */
+typedef struct dcp_instance_view {
+    int32_t n_rows;             /* N: shards held here */
+    int32_t m_rows;             /* M: requests MoE-bound here */
+    int32_t bucket_m, bucket_n; /* bucket_shape(M, N); -1 on ShapeOverflow */
+    const int64_t* n_ids;       /* [N] */
+    const int32_t* n_moe;       /* [N] m_r of each shard request */
+    const uint8_t* q_route;     /* [N][W] */
+    const int64_t* m_ids;       /* [M] */
+    const uint8_t* res_route;   /* [M][W] */
+    const int32_t* cu_pages;    /* [N+1] */
+    const int64_t* shard_len;   /* [N] */
+    const int32_t* block_table; /* [cu_pages[N]] */
+    const uint8_t* page_fill;   /* [cu_pages[N]] */
+} dcp_instance_view;
+
+DCP_API int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* cfg, dcp_planner** out);
+DCP_API int dcp_planner_destroy(dcp_planner* pl);
+/* FIFO append (host arrays). */
+DCP_API int dcp_planner_enqueue(dcp_planner* pl, const int64_t* ids, const int64_t* seq_lens,
+                                int32_t n);
+/* One scheduling round (K6), stream-ordered. */
+DCP_API int dcp_planner_step(dcp_planner* pl, void* stream);
+/* Synchronizes and copies the last StepResult out (host arrays sized >= queued count). */
+DCP_API int dcp_planner_step_result(dcp_planner* pl, int64_t* committed, int32_t* n_committed,
+                                    int64_t* deferred, int32_t* n_deferred, int64_t* unschedulable,
+                                    int32_t* n_unschedulable, int64_t* hol_events);
+DCP_API int dcp_planner_finish(dcp_planner* pl, const int64_t* ids, int32_t n, void* stream);
+DCP_API int dcp_planner_append_token(dcp_planner* pl, const int64_t* ids, int32_t n,
+                                     int32_t* out_instance);
+DCP_API int dcp_planner_placement(dcp_planner* pl, int64_t id, int32_t* kv_binding, int64_t* split,
+                                  int32_t* moe_binding, int32_t* cp_degree);
+DCP_API int dcp_planner_instances(dcp_planner* pl, int64_t* kv_load, int32_t* moe_batch,
+                                  int32_t* shard_count, int64_t* free_frames);
+/* CSV writers; return the full length (write at most cap-1 bytes + NUL). */
+DCP_API int64_t dcp_planner_dump_page_table(dcp_planner* pl, char* buf, int64_t cap);
+DCP_API int dcp_planner_build_routing(dcp_planner* pl, void* stream);
+DCP_API int64_t dcp_planner_dump_routing(dcp_planner* pl, char* buf, int64_t cap);
+DCP_API int dcp_planner_instance_view(dcp_planner* pl, int32_t instance, dcp_instance_view* out);
+/* Kernel launches issued by the last step / build_routing call. */
+DCP_API int dcp_planner_last_launches(const dcp_planner* pl);
 
 #ifdef __cplusplus
 }

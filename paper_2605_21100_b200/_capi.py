@@ -78,6 +78,24 @@ class AttnArgs(Structure):
     ]
 
 
+class PlannerConfig(Structure):
+    _fields_ = [
+        ("nodes", c_int32), ("instances_per_node", c_int32), ("page_size", c_int64),
+        ("capacity_pages", c_int64), ("policy", c_int32), ("n_bucket", c_int32),
+        ("bucket_len", c_void_p), ("bucket_deg", c_void_p), ("uniform_degree", c_int32),
+        ("hol_strict", c_int32), ("max_requests", c_int32), ("reserve_pages", c_int64),
+    ]
+
+
+class InstanceView(Structure):
+    _fields_ = [
+        ("n_rows", c_int32), ("m_rows", c_int32), ("bucket_m", c_int32), ("bucket_n", c_int32),
+        ("n_ids", c_void_p), ("n_moe", c_void_p), ("q_route", c_void_p), ("m_ids", c_void_p),
+        ("res_route", c_void_p), ("cu_pages", c_void_p), ("shard_len", c_void_p),
+        ("block_table", c_void_p), ("page_fill", c_void_p),
+    ]
+
+
 _lib = None
 
 # (name, restype, argtypes) for every entry point of include/dcp_capi.h.
@@ -87,9 +105,24 @@ _SIGNATURES = [
     ("dcp_ctx_create", c_int, [c_int, POINTER(c_void_p)]),
     ("dcp_ctx_destroy", c_int, [c_void_p]),
     ("dcp_ctx_num_sms", c_int, [c_void_p]),
+    ("dcp_copy_to_host", c_int, [c_void_p, c_void_p, c_size_t]),
     ("dcp_attn_workspace_bytes", c_size_t, [c_void_p, c_int32, c_int32, c_int32]),
     ("dcp_splitkv_decode_attn", c_int, [c_void_p, POINTER(AttnArgs), c_void_p]),
     ("dcp_attn_launches_per_call", c_int, []),
+    ("dcp_planner_create", c_int, [c_void_p, POINTER(PlannerConfig), POINTER(c_void_p)]),
+    ("dcp_planner_destroy", c_int, [c_void_p]),
+    ("dcp_planner_enqueue", c_int, [c_void_p, c_void_p, c_void_p, c_int32]),
+    ("dcp_planner_step", c_int, [c_void_p, c_void_p]),
+    ("dcp_planner_step_result", c_int, [c_void_p] + [c_void_p] * 7),
+    ("dcp_planner_finish", c_int, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("dcp_planner_append_token", c_int, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("dcp_planner_placement", c_int, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("dcp_planner_instances", c_int, [c_void_p] + [c_void_p] * 4),
+    ("dcp_planner_dump_page_table", c_int64, [c_void_p, c_char_p, c_int64]),
+    ("dcp_planner_build_routing", c_int, [c_void_p, c_void_p]),
+    ("dcp_planner_dump_routing", c_int64, [c_void_p, c_char_p, c_int64]),
+    ("dcp_planner_instance_view", c_int, [c_void_p, c_int32, POINTER(InstanceView)]),
+    ("dcp_planner_last_launches", c_int, [c_void_p]),
 ]
 
 
@@ -117,3 +150,12 @@ def check(rc: int) -> None:
     if rc != 0:
         msg = lib().dcp_last_error().decode(errors="replace")
         raise _CODES.get(rc, RuntimeError)(f"dcp error {rc}: {msg}")
+
+
+def device_to_numpy(ptr, n, dtype):
+    """Copy n elements of `dtype` from a device pointer (dcp_copy_to_host)."""
+    import numpy as np
+    out = np.zeros(max(int(n), 0), dtype)
+    if n:
+        check(lib().dcp_copy_to_host(out.ctypes.data, ptr, out.nbytes))
+    return out

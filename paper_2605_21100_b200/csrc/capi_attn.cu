@@ -123,6 +123,12 @@ int dcp_ctx_destroy(dcp_ctx* ctx) {
 
 int dcp_ctx_num_sms(const dcp_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
 
+int dcp_copy_to_host(void* dst, const void* src, size_t bytes) {
+    DCP_REQUIRE(dst && (src || bytes == 0), DCP_E_INVALID_ARG, "NULL pointer");
+    if (bytes) DCP_CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));
+    return DCP_OK;
+}
+
 size_t dcp_attn_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards, int32_t num_q_heads,
                                 int32_t head_dim) {
     if (!ctx || num_shards < 0 || num_q_heads <= 0 || head_dim <= 0) return 0;

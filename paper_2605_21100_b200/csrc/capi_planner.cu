@@ -1,0 +1,589 @@
+// SPDX-License-Identifier: Apache-2.0
+// C ABI: device planner (K6) + routing lowering (K7).  See dcp_capi.h.
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "capi_common.cuh"
+#include "planner.cuh"
+#include "routing.cuh"
+
+using namespace dcp;
+
+namespace {
+
+__global__ void init_stacks_kernel(int32_t* stack, int W, int64_t cap) {
+    const int64_t total = (int64_t)W * cap;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t f = i % cap;
+        stack[i] = static_cast<int32_t>(cap - 1 - f);  // make_cluster: ascending hand-out
+    }
+}
+
+__global__ void enqueue_kernel(PlannerState st, const int32_t* slots, const int64_t* ids,
+                               const int64_t* lens, int n) {
+    const int base = *st.nwait;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const int sl = slots[i];
+        st.id[sl] = ids[i];
+        st.seq_len[sl] = lens[i];
+        st.generated[sl] = 0;
+        st.state[sl] = ST_WAITING;
+        st.k[sl] = 0;
+        st.moe[sl] = -1;
+        st.page_cnt[sl] = 0;
+        st.page_cap[sl] = 0;
+        st.trailing_fill[sl] = 0;
+        st.waiting[base + i] = sl;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *st.nwait = base + n;
+}
+
+template <class T>
+int dalloc(T** p, size_t n, std::vector<void*>& owned) {
+    void* q = nullptr;
+    DCP_CUDA_TRY(cudaMalloc(&q, std::max<size_t>(n, 1) * sizeof(T)));
+    DCP_CUDA_TRY(cudaMemset(q, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    owned.push_back(q);
+    *p = static_cast<T*>(q);
+    return DCP_OK;
+}
+
+int64_t pages_for_h(int64_t t, int64_t p) { return (t + p - 1) / p; }
+
+}  // namespace
+
+struct dcp_planner {
+    dcp_ctx* ctx = nullptr;
+    dcp_planner_config cfg{};
+    PlannerState st{};
+    RoutingOut ro{};
+    std::vector<void*> owned;
+    int32_t* arena2_inst = nullptr;
+    int32_t* arena2_frame = nullptr;
+    uint8_t* arena2_fill = nullptr;
+    int64_t* d_new_off = nullptr;
+    int32_t* d_io_slots = nullptr;   // staging
+    int64_t* d_io_ids = nullptr;
+    int64_t* d_io_lens = nullptr;
+    int32_t* d_io_out = nullptr;
+    std::unordered_map<int64_t, int32_t> slot_of;
+    std::vector<int32_t> free_slots;
+    std::vector<int64_t> id_of_slot;
+    int64_t arena_top_host = 0;      // upper bound between syncs
+    int64_t waiting_pages_bound = 0; // sum over queued requests of their max arena demand
+    std::vector<int64_t> queued_len; // per slot (for the bound)
+    int32_t queued = 0;
+    cudaStream_t stream = nullptr;
+    int last_launches = 0;
+    bool routing_valid = false;
+};
+
+namespace {
+
+int sync_arena_top(dcp_planner* pl) {
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    DCP_CUDA_TRY(cudaMemcpy(&pl->arena_top_host, pl->st.arena_top, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return DCP_OK;
+}
+
+int compact_arena(dcp_planner* pl) {
+    PlannerState& st = pl->st;
+    planner_compact_offsets<<<1, 1024, 0, pl->stream>>>(st, pl->d_new_off);
+    planner_compact_copy<<<st.max_slots, 128, 0, pl->stream>>>(st, pl->d_new_off, pl->arena2_inst,
+                                                               pl->arena2_frame, pl->arena2_fill);
+    DCP_CUDA_TRY(cudaGetLastError());
+    std::swap(st.pg_inst, pl->arena2_inst);
+    std::swap(st.pg_frame, pl->arena2_frame);
+    std::swap(st.pg_fill, pl->arena2_fill);
+    return sync_arena_top(pl);
+}
+
+void set_stream(dcp_planner* pl, void* s) { pl->stream = static_cast<cudaStream_t>(s); }
+
+}  // namespace
+
+extern "C" {
+
+int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** out) {
+    DCP_REQUIRE(ctx && c && out, DCP_E_INVALID_ARG, "NULL argument");
+    const int W = c->nodes * c->instances_per_node;
+    DCP_REQUIRE(c->nodes >= 1 && c->instances_per_node >= 1, DCP_E_CONFIG, "empty topology");
+    DCP_REQUIRE(W <= PL_MAXW, DCP_E_UNSUPPORTED, "world size %d > %d", W, PL_MAXW);
+    DCP_REQUIRE(c->instances_per_node <= PL_MAXK, DCP_E_UNSUPPORTED, "instances_per_node %d > %d",
+                c->instances_per_node, PL_MAXK);
+    DCP_REQUIRE(c->page_size >= 1, DCP_E_CONFIG, "page_size < 1");
+    DCP_REQUIRE(c->capacity_pages >= 0 && c->capacity_pages < (1LL << 31), DCP_E_UNSUPPORTED,
+                "capacity_pages out of range");
+    DCP_REQUIRE(c->max_requests >= 1, DCP_E_INVALID_ARG, "max_requests < 1");
+    DCP_REQUIRE(c->policy >= 0 && c->policy <= 3, DCP_E_CONFIG, "unknown policy %d", c->policy);
+    DCP_REQUIRE(c->n_bucket >= 0 && c->n_bucket <= 16, DCP_E_UNSUPPORTED, "n_bucket > 16");
+    DCP_CUDA_TRY(cudaSetDevice(ctx->device));
+
+    auto* pl = new dcp_planner();
+    pl->ctx = ctx;
+    pl->cfg = *c;
+    PlannerState& st = pl->st;
+    st.nodes = c->nodes;
+    st.ipn = c->instances_per_node;
+    st.W = W;
+    st.kind = c->policy;
+    st.udeg = c->uniform_degree;
+    st.hol_strict = c->hol_strict;
+    st.page = c->page_size;
+    st.capacity = c->capacity_pages;
+    st.max_slots = c->max_requests;
+    st.reserve_pages = std::max<int64_t>(c->reserve_pages, 1);
+    if (c->n_bucket == 0) {  // BucketFn::default_table (scheduler.cpp:28-33)
+        const int64_t L[4] = {32768, 131072, 393216, INT64_MAX};
+        const int32_t D[4] = {1, 2, 4, 8};
+        st.nbucket = 4;
+        for (int i = 0; i < 4; ++i) { st.bucket_len[i] = L[i]; st.bucket_deg[i] = D[i]; }
+    } else {
+        st.nbucket = c->n_bucket;
+        for (int i = 0; i < c->n_bucket; ++i) {
+            st.bucket_len[i] = c->bucket_len[i];
+            st.bucket_deg[i] = c->bucket_deg[i];
+        }
+    }
+    // SchedulerPolicy::validate (scheduler.cpp:35-41)
+    if (st.kind == DCP_POLICY_DCP) {
+        int64_t pl_ = 0;
+        int pd = 0;
+        bool bad = st.nbucket == 0;
+        for (int i = 0; i < st.nbucket; ++i) {
+            if (st.bucket_len[i] <= pl_ || st.bucket_deg[i] < pd || st.bucket_deg[i] < 1) bad = true;
+            pl_ = st.bucket_len[i];
+            pd = st.bucket_deg[i];
+        }
+        if (bad) {
+            delete pl;
+            set_error("bucket lengths must strictly increase and degrees be >=1, non-decreasing");
+            return DCP_E_CONFIG;
+        }
+    }
+    if (st.kind == DCP_POLICY_UNIFORM_CP) {
+        if (st.udeg < 1 || st.ipn % st.udeg != 0) {
+            delete pl;
+            set_error("UniformCP degree must divide instances_per_node");
+            return DCP_E_CONFIG;
+        }
+        st.n_groups = (st.ipn / st.udeg) * st.nodes;
+    } else {
+        st.n_groups = 1;
+    }
+    const size_t S = c->max_requests;
+    int sort_cap = 1;
+    while (sort_cap < (int)S) sort_cap <<= 1;
+    st.sort_cap = sort_cap;
+    st.arena_cap = 2 * (int64_t)W * c->capacity_pages + (int64_t)S * (PL_MAXK + st.reserve_pages) + 1024;
+
+    auto& o = pl->owned;
+    int rc = 0;
+    rc |= dalloc(&st.kv_load, W, o);
+    rc |= dalloc(&st.moe_batch, W, o);
+    rc |= dalloc(&st.shard_count, W, o);
+    rc |= dalloc(&st.nfree, W, o);
+    rc |= dalloc(&st.stack, (size_t)W * c->capacity_pages, o);
+    rc |= dalloc(&st.ucp_rr, st.n_groups, o);
+    rc |= dalloc(&st.id, S, o);
+    rc |= dalloc(&st.seq_len, S, o);
+    rc |= dalloc(&st.generated, S, o);
+    rc |= dalloc(&st.state, S, o);
+    rc |= dalloc(&st.k, S, o);
+    rc |= dalloc(&st.moe, S, o);
+    rc |= dalloc(&st.kv, S * PL_MAXK, o);
+    rc |= dalloc(&st.split, S * PL_MAXK, o);
+    rc |= dalloc(&st.page_off, S, o);
+    rc |= dalloc(&st.page_cnt, S, o);
+    rc |= dalloc(&st.page_cap, S, o);
+    rc |= dalloc(&st.trailing_fill, S, o);
+    rc |= dalloc(&st.shard_tokens, S * W, o);
+    rc |= dalloc(&st.pg_inst, st.arena_cap, o);
+    rc |= dalloc(&st.pg_frame, st.arena_cap, o);
+    rc |= dalloc(&st.pg_fill, st.arena_cap, o);
+    rc |= dalloc(&pl->arena2_inst, st.arena_cap, o);
+    rc |= dalloc(&pl->arena2_frame, st.arena_cap, o);
+    rc |= dalloc(&pl->arena2_fill, st.arena_cap, o);
+    rc |= dalloc(&pl->d_new_off, S, o);
+    rc |= dalloc(&st.arena_top, 1, o);
+    rc |= dalloc(&st.waiting, S, o);
+    rc |= dalloc(&st.nwait, 1, o);
+    rc |= dalloc(&st.res_slots, 3 * S, o);
+    rc |= dalloc(&st.res_counts, 4, o);
+    rc |= dalloc(&st.res_hol, 1, o);
+    rc |= dalloc(&st.sk1, sort_cap, o);
+    rc |= dalloc(&st.sk2, sort_cap, o);
+    rc |= dalloc(&st.sval, sort_cap, o);
+    rc |= dalloc(&pl->d_io_slots, S, o);
+    rc |= dalloc(&pl->d_io_ids, S, o);
+    rc |= dalloc(&pl->d_io_lens, S, o);
+    rc |= dalloc(&pl->d_io_out, S, o);
+    RoutingOut& ro = pl->ro;
+    rc |= dalloc(&ro.n_count, W, o);
+    rc |= dalloc(&ro.m_count, W, o);
+    rc |= dalloc(&ro.n_id, (size_t)W * S, o);
+    rc |= dalloc(&ro.n_slot, (size_t)W * S, o);
+    rc |= dalloc(&ro.n_moe, (size_t)W * S, o);
+    rc |= dalloc(&ro.q_route, (size_t)W * S * W, o);
+    rc |= dalloc(&ro.m_id, (size_t)W * S, o);
+    rc |= dalloc(&ro.m_slot, (size_t)W * S, o);
+    rc |= dalloc(&ro.res_route, (size_t)W * S * W, o);
+    rc |= dalloc(&ro.bucket, 2 * W, o);
+    rc |= dalloc(&ro.cu_pages, (size_t)W * (S + 1), o);
+    rc |= dalloc(&ro.shard_len, (size_t)W * S, o);
+    rc |= dalloc(&ro.block_table, (size_t)W * std::max<int64_t>(c->capacity_pages, 1), o);
+    rc |= dalloc(&ro.page_fill, (size_t)W * std::max<int64_t>(c->capacity_pages, 1), o);
+    rc |= dalloc(&ro.status, 1, o);
+    if (rc) {
+        dcp_planner_destroy(pl);
+        return DCP_E_CUDA;
+    }
+    // make_cluster: every instance starts with `capacity` free frames, LIFO stack
+    std::vector<int64_t> nf(W, c->capacity_pages);
+    DCP_CUDA_TRY(cudaMemcpy(st.nfree, nf.data(), W * sizeof(int64_t), cudaMemcpyHostToDevice));
+    {
+        std::vector<int32_t> fs(S, ST_FREE);
+        DCP_CUDA_TRY(cudaMemcpy(st.state, fs.data(), S * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (c->capacity_pages > 0) init_stacks_kernel<<<256, 256>>>(st.stack, W, c->capacity_pages);
+    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(cudaDeviceSynchronize());
+    pl->id_of_slot.assign(S, -1);
+    pl->queued_len.assign(S, 0);
+    for (int i = (int)S - 1; i >= 0; --i) pl->free_slots.push_back(i);
+    *out = pl;
+    return DCP_OK;
+}
+
+int dcp_planner_destroy(dcp_planner* pl) {
+    if (!pl) return DCP_OK;
+    for (void* p : pl->owned) cudaFree(p);
+    delete pl;
+    return DCP_OK;
+}
+
+int dcp_planner_last_launches(const dcp_planner* pl) { return pl ? pl->last_launches : 0; }
+
+int dcp_planner_enqueue(dcp_planner* pl, const int64_t* ids, const int64_t* lens, int32_t n) {
+    DCP_REQUIRE(pl && (n == 0 || (ids && lens)), DCP_E_INVALID_ARG, "NULL argument");
+    if (n == 0) return DCP_OK;
+    DCP_REQUIRE((size_t)n <= pl->free_slots.size(), DCP_E_INVALID_ARG,
+                "request slots exhausted (max_requests=%d)", pl->cfg.max_requests);
+    std::vector<int32_t> slots(n);
+    for (int i = 0; i < n; ++i) {
+        DCP_REQUIRE(!pl->slot_of.count(ids[i]), DCP_E_INVALID_ARG, "request id %lld already tracked",
+                    (long long)ids[i]);
+    }
+    for (int i = 0; i < n; ++i) {
+        const int sl = pl->free_slots.back();
+        pl->free_slots.pop_back();
+        slots[i] = sl;
+        pl->slot_of[ids[i]] = sl;
+        pl->id_of_slot[sl] = ids[i];
+        pl->queued_len[sl] = lens[i];
+        pl->waiting_pages_bound +=
+            pages_for_h(std::max<int64_t>(lens[i], 0), pl->cfg.page_size) + PL_MAXK + pl->st.reserve_pages;
+    }
+    pl->queued += n;
+    DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_slots, slots.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, pl->stream));
+    DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_ids, ids, n * sizeof(int64_t), cudaMemcpyHostToDevice, pl->stream));
+    DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_lens, lens, n * sizeof(int64_t), cudaMemcpyHostToDevice, pl->stream));
+    enqueue_kernel<<<1, 256, 0, pl->stream>>>(pl->st, pl->d_io_slots, pl->d_io_ids, pl->d_io_lens, n);
+    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));  // staging buffers are reused
+    return DCP_OK;
+}
+
+int dcp_planner_step(dcp_planner* pl, void* stream) {
+    DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
+    set_stream(pl, stream);
+    pl->last_launches = 0;
+    if (pl->arena_top_host + pl->waiting_pages_bound > pl->st.arena_cap) {
+        int rc = compact_arena(pl);
+        if (rc) return rc;
+        pl->last_launches += 2;
+    }
+    planner_step_kernel<<<1, PL_THREADS, 0, pl->stream>>>(pl->st);
+    DCP_CUDA_TRY(cudaGetLastError());
+    pl->last_launches += 1;
+    pl->routing_valid = false;
+    // conservative bound until the result is read back
+    pl->arena_top_host += pl->waiting_pages_bound;
+    return DCP_OK;
+}
+
+int dcp_planner_step_result(dcp_planner* pl, int64_t* committed, int32_t* nc, int64_t* deferred,
+                            int32_t* nd, int64_t* unsched, int32_t* nu, int64_t* hol) {
+    DCP_REQUIRE(pl && nc && nd && nu && hol, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    int32_t cnt[4];
+    DCP_CUDA_TRY(cudaMemcpy(cnt, pl->st.res_counts, sizeof(cnt), cudaMemcpyDeviceToHost));
+    DCP_CUDA_TRY(cudaMemcpy(hol, pl->st.res_hol, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    const size_t S = pl->cfg.max_requests;
+    std::vector<int32_t> sl(3 * S);
+    DCP_CUDA_TRY(cudaMemcpy(sl.data(), pl->st.res_slots, 3 * S * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    *nc = cnt[0];
+    *nd = cnt[1];
+    *nu = cnt[2];
+    for (int i = 0; i < cnt[0]; ++i) {
+        const int s = sl[i];
+        if (committed) committed[i] = pl->id_of_slot[s];
+        pl->waiting_pages_bound -=
+            pages_for_h(pl->queued_len[s], pl->cfg.page_size) + PL_MAXK + pl->st.reserve_pages;
+        pl->queued -= 1;
+    }
+    for (int i = 0; i < cnt[1]; ++i)
+        if (deferred) deferred[i] = pl->id_of_slot[sl[S + i]];
+    for (int i = 0; i < cnt[2]; ++i) {
+        const int s = sl[2 * S + i];
+        const int64_t id = pl->id_of_slot[s];
+        if (unsched) unsched[i] = id;
+        // erased from the queue and never placed: release the slot
+        pl->waiting_pages_bound -=
+            pages_for_h(pl->queued_len[s], pl->cfg.page_size) + PL_MAXK + pl->st.reserve_pages;
+        pl->queued -= 1;
+        pl->slot_of.erase(id);
+        pl->id_of_slot[s] = -1;
+        pl->free_slots.push_back(s);
+    }
+    DCP_CUDA_TRY(cudaMemcpy(&pl->arena_top_host, pl->st.arena_top, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    if (cnt[3] == PL_E_FRAMES) {
+        set_error("cannot allocate a zero-length request");
+        return DCP_E_INSUFFICIENT_FRAMES;
+    }
+    if (cnt[3] != 0) {
+        set_error("planner step status %d", cnt[3]);
+        return DCP_E_CUDA;
+    }
+    return DCP_OK;
+}
+
+int dcp_planner_finish(dcp_planner* pl, const int64_t* ids, int32_t n, void* stream) {
+    DCP_REQUIRE(pl && (n == 0 || ids), DCP_E_INVALID_ARG, "NULL argument");
+    if (n == 0) return DCP_OK;
+    set_stream(pl, stream);
+    std::vector<int32_t> slots;
+    std::vector<int32_t> st(n);
+    for (int i = 0; i < n; ++i) {
+        auto it = pl->slot_of.find(ids[i]);
+        DCP_REQUIRE(it != pl->slot_of.end(), DCP_E_UNKNOWN_REQUEST,
+                    "no page-table entries for request %lld", (long long)ids[i]);
+        slots.push_back(it->second);
+    }
+    // only ACTIVE requests have page-table entries (UnknownRequest otherwise)
+    for (int i = 0; i < n; ++i) {
+        int32_t s = 0;
+        DCP_CUDA_TRY(cudaMemcpy(&s, pl->st.state + slots[i], sizeof(int32_t), cudaMemcpyDeviceToHost));
+        DCP_REQUIRE(s == ST_ACTIVE, DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
+                    (long long)ids[i]);
+    }
+    DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_slots, slots.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, pl->stream));
+    planner_release_kernel<<<1, PL_THREADS, 0, pl->stream>>>(pl->st, pl->d_io_slots, n);
+    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    for (int i = 0; i < n; ++i) {
+        pl->slot_of.erase(ids[i]);
+        pl->id_of_slot[slots[i]] = -1;
+        pl->free_slots.push_back(slots[i]);
+    }
+    pl->routing_valid = false;
+    pl->last_launches = 1;
+    return DCP_OK;
+}
+
+int dcp_planner_append_token(dcp_planner* pl, const int64_t* ids, int32_t n, int32_t* out_inst) {
+    DCP_REQUIRE(pl && (n == 0 || (ids && out_inst)), DCP_E_INVALID_ARG, "NULL argument");
+    std::vector<int32_t> slots(n);
+    for (int i = 0; i < n; ++i) {
+        auto it = pl->slot_of.find(ids[i]);
+        DCP_REQUIRE(it != pl->slot_of.end(), DCP_E_UNKNOWN_REQUEST, "unknown request %lld",
+                    (long long)ids[i]);
+        int32_t s = 0;
+        DCP_CUDA_TRY(cudaMemcpy(&s, pl->st.state + it->second, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        DCP_REQUIRE(s == ST_ACTIVE, DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
+                    (long long)ids[i]);
+        slots[i] = it->second;
+    }
+    int done = 0;
+    int guard = 0;
+    while (done < n) {
+        const int m = n - done;
+        DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_slots, slots.data() + done, m * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, pl->stream));
+        planner_append_kernel<<<1, 32, 0, pl->stream>>>(pl->st, pl->d_io_slots, m, pl->d_io_out);
+        DCP_CUDA_TRY(cudaGetLastError());
+        DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+        int32_t cnt[4];
+        DCP_CUDA_TRY(cudaMemcpy(cnt, pl->st.res_counts, sizeof(cnt), cudaMemcpyDeviceToHost));
+        DCP_CUDA_TRY(cudaMemcpy(out_inst + done, pl->d_io_out, cnt[0] * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        done += cnt[0];
+        if (cnt[3] == PL_E_ARENA) {
+            DCP_REQUIRE(++guard < 4, DCP_E_CUDA, "page arena exhausted");
+            int rc = compact_arena(pl);
+            if (rc) return rc;
+        }
+    }
+    DCP_CUDA_TRY(cudaMemcpy(&pl->arena_top_host, pl->st.arena_top, sizeof(int64_t), cudaMemcpyDeviceToHost));
+    pl->routing_valid = false;
+    return DCP_OK;
+}
+
+int dcp_planner_placement(dcp_planner* pl, int64_t id, int32_t* kv, int64_t* split, int32_t* moe,
+                          int32_t* k) {
+    DCP_REQUIRE(pl && kv && split && moe && k, DCP_E_INVALID_ARG, "NULL argument");
+    auto it = pl->slot_of.find(id);
+    DCP_REQUIRE(it != pl->slot_of.end(), DCP_E_UNKNOWN_REQUEST, "unknown request %lld", (long long)id);
+    const int sl = it->second;
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    int32_t state = 0;
+    DCP_CUDA_TRY(cudaMemcpy(&state, pl->st.state + sl, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    DCP_REQUIRE(state == ST_ACTIVE, DCP_E_UNKNOWN_REQUEST, "request %lld has no placement", (long long)id);
+    DCP_CUDA_TRY(cudaMemcpy(k, pl->st.k + sl, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    DCP_CUDA_TRY(cudaMemcpy(moe, pl->st.moe + sl, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    DCP_CUDA_TRY(cudaMemcpy(kv, pl->st.kv + (size_t)sl * PL_MAXK, *k * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    DCP_CUDA_TRY(cudaMemcpy(split, pl->st.split + (size_t)sl * PL_MAXK, *k * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return DCP_OK;
+}
+
+int dcp_planner_instances(dcp_planner* pl, int64_t* kv_load, int32_t* moe_batch, int32_t* shard_count,
+                          int64_t* free_frames) {
+    DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    const int W = pl->st.W;
+    if (kv_load) DCP_CUDA_TRY(cudaMemcpy(kv_load, pl->st.kv_load, W * 8, cudaMemcpyDeviceToHost));
+    if (moe_batch) DCP_CUDA_TRY(cudaMemcpy(moe_batch, pl->st.moe_batch, W * 4, cudaMemcpyDeviceToHost));
+    if (shard_count) DCP_CUDA_TRY(cudaMemcpy(shard_count, pl->st.shard_count, W * 4, cudaMemcpyDeviceToHost));
+    if (free_frames) DCP_CUDA_TRY(cudaMemcpy(free_frames, pl->st.nfree, W * 8, cudaMemcpyDeviceToHost));
+    return W;
+}
+
+static int64_t emit(const std::string& s, char* buf, int64_t cap) {
+    if (buf && cap > 0) {
+        const int64_t n = std::min<int64_t>((int64_t)s.size(), cap - 1);
+        std::memcpy(buf, s.data(), n);
+        buf[n] = 0;
+    }
+    return (int64_t)s.size();
+}
+
+int64_t dcp_planner_dump_page_table(dcp_planner* pl, char* buf, int64_t cap) {
+    if (!pl) return DCP_E_INVALID_ARG;
+    if (cudaStreamSynchronize(pl->stream) != cudaSuccess) return DCP_E_CUDA;
+    const size_t S = pl->cfg.max_requests;
+    std::vector<int32_t> state(S), cnt(S);
+    std::vector<int64_t> off(S), id(S);
+    int64_t top = 0;
+    cudaMemcpy(state.data(), pl->st.state, S * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(cnt.data(), pl->st.page_cnt, S * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(off.data(), pl->st.page_off, S * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(id.data(), pl->st.id, S * 8, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&top, pl->st.arena_top, 8, cudaMemcpyDeviceToHost);
+    std::vector<int32_t> inst(top), frame(top);
+    if (top) {
+        cudaMemcpy(inst.data(), pl->st.pg_inst, top * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(frame.data(), pl->st.pg_frame, top * 4, cudaMemcpyDeviceToHost);
+    }
+    if (cudaGetLastError() != cudaSuccess) return DCP_E_CUDA;
+    std::vector<std::pair<int64_t, int>> live;
+    for (size_t s = 0; s < S; ++s)
+        if (state[s] == ST_ACTIVE) live.push_back({id[s], (int)s});
+    std::sort(live.begin(), live.end());
+    std::string out = "request_id,logical_page,instance_id,frame_id\n";
+    char line[96];
+    for (auto& [rid, s] : live)
+        for (int p = 0; p < cnt[s]; ++p) {
+            std::snprintf(line, sizeof(line), "%lld,%d,%d,%d\n", (long long)rid, p, inst[off[s] + p],
+                          frame[off[s] + p]);
+            out += line;
+        }
+    return emit(out, buf, cap);
+}
+
+int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
+    DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
+    set_stream(pl, stream);
+    routing_rows_kernel<<<1, 1024, 0, pl->stream>>>(pl->st, pl->ro);
+    routing_blocks_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);
+    DCP_CUDA_TRY(cudaGetLastError());
+    pl->last_launches = 2;
+    pl->routing_valid = true;
+    return DCP_OK;
+}
+
+int64_t dcp_planner_dump_routing(dcp_planner* pl, char* buf, int64_t cap) {
+    if (!pl) return DCP_E_INVALID_ARG;
+    if (!pl->routing_valid) {
+        int rc = dcp_planner_build_routing(pl, pl->stream);
+        if (rc) return rc;
+    }
+    if (cudaStreamSynchronize(pl->stream) != cudaSuccess) return DCP_E_CUDA;
+    int32_t status = 0;
+    cudaMemcpy(&status, pl->ro.status, 4, cudaMemcpyDeviceToHost);
+    if (status == -4) {
+        set_error("moe_binding outside kv_binding");
+        return DCP_E_INCONSISTENT;
+    }
+    const int W = pl->st.W;
+    const size_t S = pl->cfg.max_requests;
+    std::vector<int32_t> nc(W), mc(W);
+    cudaMemcpy(nc.data(), pl->ro.n_count, W * 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(mc.data(), pl->ro.m_count, W * 4, cudaMemcpyDeviceToHost);
+    std::string out = "instance,table,row,request_id,columns\n";
+    std::vector<int64_t> ids;
+    std::vector<uint8_t> bits;
+    char line[128];
+    for (int s = 0; s < W; ++s) {
+        for (int t = 0; t < 2; ++t) {
+            const int rows = t == 0 ? nc[s] : mc[s];
+            ids.resize(rows);
+            bits.resize((size_t)rows * W);
+            if (rows) {
+                cudaMemcpy(ids.data(), (t == 0 ? pl->ro.n_id : pl->ro.m_id) + (size_t)s * S, rows * 8,
+                           cudaMemcpyDeviceToHost);
+                cudaMemcpy(bits.data(), (t == 0 ? pl->ro.q_route : pl->ro.res_route) + (size_t)s * S * W,
+                           (size_t)rows * W, cudaMemcpyDeviceToHost);
+            }
+            for (int r = 0; r < rows; ++r) {
+                std::snprintf(line, sizeof(line), "%d,%s,%d,%lld,", s, t == 0 ? "q_route" : "res_route", r,
+                              (long long)ids[r]);
+                out += line;
+                for (int c = 0; c < W; ++c) out += bits[(size_t)r * W + c] ? '1' : '0';
+                out += '\n';
+            }
+        }
+    }
+    if (cudaGetLastError() != cudaSuccess) return DCP_E_CUDA;
+    return emit(out, buf, cap);
+}
+
+int dcp_planner_instance_view(dcp_planner* pl, int32_t s, dcp_instance_view* v) {
+    DCP_REQUIRE(pl && v, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(s >= 0 && s < pl->st.W, DCP_E_INVALID_ARG, "instance %d out of range", s);
+    DCP_REQUIRE(pl->routing_valid, DCP_E_INVALID_ARG, "call dcp_planner_build_routing first");
+    DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+    const size_t S = pl->cfg.max_requests;
+    const int W = pl->st.W;
+    int32_t b[2];
+    DCP_CUDA_TRY(cudaMemcpy(&v->n_rows, pl->ro.n_count + s, 4, cudaMemcpyDeviceToHost));
+    DCP_CUDA_TRY(cudaMemcpy(&v->m_rows, pl->ro.m_count + s, 4, cudaMemcpyDeviceToHost));
+    DCP_CUDA_TRY(cudaMemcpy(b, pl->ro.bucket + 2 * s, 8, cudaMemcpyDeviceToHost));
+    v->bucket_m = b[0];
+    v->bucket_n = b[1];
+    v->n_ids = pl->ro.n_id + (size_t)s * S;
+    v->n_moe = pl->ro.n_moe + (size_t)s * S;
+    v->q_route = pl->ro.q_route + (size_t)s * S * W;
+    v->m_ids = pl->ro.m_id + (size_t)s * S;
+    v->res_route = pl->ro.res_route + (size_t)s * S * W;
+    v->cu_pages = pl->ro.cu_pages + (size_t)s * (S + 1);
+    v->shard_len = pl->ro.shard_len + (size_t)s * S;
+    v->block_table = pl->ro.block_table + (size_t)s * pl->st.capacity;
+    v->page_fill = pl->ro.page_fill + (size_t)s * pl->st.capacity;
+    return DCP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,683 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K6: the DCP planner as device kernels (north_star subsystem 4).
+//
+// Restates, bit-exactly, the integer control plane of the reference:
+//   Scheduler::step            scheduler.cpp:245-306  (FIFO admission, HoL counting)
+//   rebalance_active           scheduler.cpp:43-64    (Alg. 1 lines 1-5)
+//   place_dcp / min_batch      scheduler.cpp:118-170  (Alg. 1 lines 7-12)
+//   place_single               scheduler.cpp:172-187  (LeastBatch / LeastCache)
+//   place_uniform              scheduler.cpp:189-223  (UniformCP, round-robin m_r)
+//   never_fits / can_allocate  scheduler.cpp:225-243, 104-113
+//   water_fill                 scheduler.cpp:70-102
+//   cp_degree / BucketFn       scheduler.cpp:10-33, 66-68
+//   GlobalPageTable::allocate / release / append_token   page_table.cpp:9-121
+//   make_cluster LIFO stacks   page_table.cpp:133-148
+//
+// The admission loop is inherently sequential (each commit mutates the K/B/
+// free-frame state the next request reads), so it runs in ONE CTA: instance
+// state lives in shared memory, warp 0 makes each decision with one lane per
+// instance (warp argmin / rank / ballot replace the reference's loops and
+// std::stable_sort), and the whole CTA copies the popped frame ids.  Rebalance
+// exploits the (cp_degree, id) order: all CP=1 requests come first and pin
+// m_r to their single instance (a parallel histogram), only CP>=2 requests
+// need the sequential argmin.
+#pragma once
+
+#include <cstdint>
+
+namespace dcp {
+
+constexpr int PL_MAXW = 32;   // instances (one warp lane each)
+constexpr int PL_MAXK = 16;   // max CP degree (node size)
+constexpr int PL_THREADS = 512;
+
+enum : int32_t { PL_OK = 0, PL_E_FRAMES = -1, PL_E_UNKNOWN = -2, PL_E_ARENA = -11 };
+enum : int32_t { KIND_DCP = 0, KIND_LEAST_BATCH = 1, KIND_LEAST_CACHE = 2, KIND_UNIFORM = 3 };
+enum : int32_t { ST_WAITING = 0, ST_ACTIVE = 1, ST_FINISHED = 2, ST_FREE = 3 };
+
+struct PlannerState {
+    // ---- configuration
+    int32_t nodes, ipn, W, kind, udeg, hol_strict, nbucket, max_slots;
+    int64_t page, capacity, arena_cap, reserve_pages;
+    int64_t bucket_len[16];
+    int32_t bucket_deg[16];
+    int32_t n_groups;
+    // ---- instance state (InstanceState, page_table.hpp:13-25)
+    int64_t* kv_load;      // [W]  K_s
+    int32_t* moe_batch;    // [W]  B_s
+    int32_t* shard_count;  // [W]  R_i
+    int64_t* nfree;        // [W]  |free_frames|
+    int32_t* stack;        // [W][capacity] LIFO, top at nfree-1
+    int32_t* ucp_rr;       // [n_groups] UniformCP round robin (scheduler.hpp:88)
+    // ---- request slots (Request + Placement + GlobalPageTable::Entry)
+    int64_t* id;
+    int64_t* seq_len;
+    int64_t* generated;
+    int32_t* state;
+    int32_t* k;
+    int32_t* moe;
+    int32_t* kv;           // [S][PL_MAXK]
+    int64_t* split;        // [S][PL_MAXK]
+    int64_t* page_off;     // [S] segment start in the page arena
+    int32_t* page_cnt;     // [S]
+    int32_t* page_cap;     // [S]
+    int64_t* trailing_fill;// [S]
+    int64_t* shard_tokens; // [S][W]
+    int32_t* pg_inst;      // arena [arena_cap]
+    int32_t* pg_frame;     // arena
+    uint8_t* pg_fill;      // arena: valid tokens of each page
+    int64_t* arena_top;    // [1]
+    // ---- waiting queue (deque<size_t>) of slots
+    int32_t* waiting;      // [S]
+    int32_t* nwait;        // [1]
+    // ---- step results (StepResult, scheduler.hpp:58-65)
+    int32_t* res_slots;    // [3][S]: committed, deferred, unschedulable (slot ids)
+    int32_t* res_counts;   // [4]: n_committed, n_deferred, n_unsched, status
+    int64_t* res_hol;      // [1]
+    // ---- scratch
+    int64_t* sk1;          // [sort_cap]
+    int64_t* sk2;
+    int32_t* sval;
+    int32_t sort_cap;
+};
+
+// ------------------------------------------------------------------ warp helpers
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const int64_t u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+// argmin of (value) with ties to the lowest index; returns the winning index.
+__device__ __forceinline__ int warp_argmin_i64(int64_t v, int idx) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const int64_t ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+        if (ov < v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+    }
+    return idx;
+}
+
+__device__ __forceinline__ int64_t pages_for_d(int64_t tokens, int64_t page) {
+    return (tokens + page - 1) / page;
+}
+
+__device__ __forceinline__ int bucket_lookup_d(const PlannerState& st, int64_t len) {
+    for (int i = 0; i < st.nbucket; ++i)
+        if (len <= st.bucket_len[i]) return st.bucket_deg[i];
+    return st.bucket_deg[st.nbucket - 1];
+}
+__device__ __forceinline__ int cp_degree_d(const PlannerState& st, int64_t len) {
+    const int d = bucket_lookup_d(st, len);
+    return d < st.ipn ? d : st.ipn;
+}
+
+// Shared-memory image of the instance state during a step.
+struct SmemInst {
+    int64_t K[PL_MAXW];
+    int64_t nfree[PL_MAXW];
+    int32_t B[PL_MAXW];
+    int32_t shards[PL_MAXW];
+};
+
+struct SmemPlace {
+    int32_t k, moe;
+    int32_t kv[PL_MAXK];
+    int64_t split[PL_MAXK];
+    int64_t need_off[PL_MAXK + 1];  // page prefix over members
+    int32_t ok;                     // can_allocate
+    int32_t unsched;
+};
+
+// water_fill (scheduler.cpp:70-102) with one lane per participant (lanes < n).
+__device__ __forceinline__ int64_t warp_water_fill(int lane, int n, int64_t len, int64_t K) {
+    const bool part = lane < n;
+    int64_t lo = 0;
+    int64_t hi = warp_max_i64(part ? K : 0) + len;
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        const int64_t cap = warp_sum_i64(part && mid > K ? mid - K : 0);
+        if (cap >= len) hi = mid; else lo = mid + 1;
+    }
+    const int64_t level = lo;
+    int64_t s = part && level - 1 - K > 0 ? level - 1 - K : 0;
+    const int64_t rem = len - warp_sum_i64(s);
+    const bool elig = part && (K + s < level);
+    const unsigned bal = __ballot_sync(0xffffffffu, elig);
+    const int rank = __popc(bal & ((1u << lane) - 1u));
+    if (elig && rank < rem) s += 1;
+    return s;
+}
+
+// Placement decision for one request (warp 0).  Writes *pl.
+__device__ void place_request(const PlannerState& st, const SmemInst& si, SmemPlace& pl, int lane,
+                              int64_t L) {
+    const int W = st.W, ipn = st.ipn;
+    if (st.kind == KIND_DCP) {
+        // node = argmin_n sum_{s in n} B_s, ties by node id (scheduler.cpp:133-141)
+        int64_t bn = INT64_MAX;
+        if (lane < st.nodes) {
+            bn = 0;
+            for (int s = lane * ipn; s < (lane + 1) * ipn; ++s) bn += si.B[s];
+        }
+        const int node = warp_argmin_i64(bn, lane);
+        const int k = cp_degree_d(st, L);
+        const int nb = node * ipn;
+        // m_r = min_batch_instance over the node, ties to lowest id (cpp:118-126)
+        const int moe = nb + warp_argmin_i64(lane < ipn ? (int64_t)si.B[nb + lane] : INT64_MAX, lane);
+        // SelectSmallestKV: node minus m_r by (K, id) (cpp:148-156) -> rank per lane
+        if (lane < ipn) {
+            const int s = nb + lane;
+            if (s != moe) {
+                int rank = 0;
+                for (int j = nb; j < nb + ipn; ++j) {
+                    if (j == moe || j == s) continue;
+                    if (si.K[j] < si.K[s] || (si.K[j] == si.K[s] && j < s)) ++rank;
+                }
+                if (rank < k - 1) pl.kv[1 + rank] = s;
+            }
+        }
+        if (lane == 0) {
+            pl.kv[0] = moe;
+            pl.moe = moe;
+            pl.k = k;
+        }
+        __syncwarp();
+        const int64_t Kl = lane < k ? si.K[pl.kv[lane]] : 0;
+        const int64_t s = warp_water_fill(lane, k, L, Kl);
+        if (lane < k) pl.split[lane] = s;
+    } else if (st.kind == KIND_LEAST_BATCH || st.kind == KIND_LEAST_CACHE) {
+        // argmin over all instances, first minimum (cpp:172-187)
+        int64_t v = INT64_MAX;
+        if (lane < W) v = st.kind == KIND_LEAST_BATCH ? (int64_t)si.B[lane] : si.K[lane];
+        const int best = warp_argmin_i64(v, lane);
+        if (lane == 0) {
+            pl.k = 1;
+            pl.moe = best;
+            pl.kv[0] = best;
+            pl.split[0] = L;
+        }
+    } else {
+        // UniformCP (cpp:189-223): group with fewest MoE-bound requests
+        const int d = st.udeg;
+        int64_t bg = INT64_MAX;
+        if (lane < st.n_groups) {
+            bg = 0;
+            for (int s = lane * d; s < lane * d + d; ++s) bg += si.B[s];
+        }
+        const int g = warp_argmin_i64(bg, lane);
+        const int gb = g * d;
+        if (lane < d) {
+            const int64_t base = L / d;
+            const int64_t rem = L % d;
+            pl.kv[lane] = gb + lane;
+            pl.split[lane] = base + (lane < rem ? 1 : 0);
+        }
+        if (lane == 0) {
+            pl.k = d;
+            const int rr = st.ucp_rr[g];
+            pl.moe = gb + rr;
+            st.ucp_rr[g] = (rr + 1) % d;  // advanced even if the request is deferred
+        }
+    }
+    __syncwarp();
+    // can_allocate (cpp:104-113) + page prefix for the allocation
+    const int k = pl.k;
+    int64_t need = 0;
+    bool ok = true;
+    if (lane < k) {
+        need = pages_for_d(pl.split[lane], st.page);
+        ok = si.nfree[pl.kv[lane]] >= need;
+    }
+    const bool all_ok = __all_sync(0xffffffffu, ok);
+    // inclusive scan of need over lanes
+    int64_t incl = need;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
+    }
+    if (lane < k) pl.need_off[lane + 1] = incl;
+    if (lane == 0) {
+        pl.need_off[0] = 0;
+        pl.ok = all_ok ? 1 : 0;
+    }
+    __syncwarp();
+}
+
+// never_fits (scheduler.cpp:225-243): uses the first instance's capacity.
+__device__ __forceinline__ bool never_fits_d(const PlannerState& st, int64_t L) {
+    const int64_t demand = pages_for_d(L, st.page);
+    const int64_t per = st.capacity;
+    int64_t reach;
+    if (st.kind == KIND_DCP) {
+        const int k = cp_degree_d(st, L);
+        reach = per * k - (k - 1);
+    } else if (st.kind == KIND_UNIFORM) {
+        reach = per * st.udeg - (st.udeg - 1);
+    } else {
+        reach = per;
+    }
+    return demand > reach;
+}
+
+// ------------------------------------------------------------------ single-CTA bitonic sort
+// Sorts n (<= sort_cap, padded to pow2 internally) entries by (k1, k2) ascending.
+__device__ void cta_bitonic_sort(int64_t* k1, int64_t* k2, int32_t* val, int n) {
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + threadIdx.x; i < np2; i += blockDim.x) {
+        k1[i] = INT64_MAX;
+        k2[i] = INT64_MAX;
+        val[i] = -1;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < np2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool up = ((lo & size) == 0);
+                const bool gt = k1[lo] > k1[hi] || (k1[lo] == k1[hi] && k2[lo] > k2[hi]);
+                if (gt == up) {
+                    int64_t t1 = k1[lo]; k1[lo] = k1[hi]; k1[hi] = t1;
+                    int64_t t2 = k2[lo]; k2[lo] = k2[hi]; k2[hi] = t2;
+                    int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K6 step
+__global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(PlannerState st) {
+    __shared__ SmemInst si;
+    __shared__ SmemPlace pl;
+    __shared__ int32_t s_n2;
+    __shared__ int32_t s_cnt[3];
+    __shared__ int64_t s_hol;
+    __shared__ int32_t s_status;
+    __shared__ int64_t s_arena_top;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = st.W;
+    const int S = st.max_slots;
+
+    if (tid < W) {
+        si.K[tid] = st.kv_load[tid];
+        si.nfree[tid] = st.nfree[tid];
+        si.B[tid] = 0;
+        si.shards[tid] = st.shard_count[tid];
+    }
+    if (tid == 0) {
+        s_n2 = 0;
+        s_cnt[0] = s_cnt[1] = s_cnt[2] = 0;
+        s_hol = 0;
+        s_status = PL_OK;
+        s_arena_top = *st.arena_top;
+    }
+    __syncthreads();
+
+    // ---- Alg. 1 line 1: recompute B (scheduler.cpp:250-261) ----
+    if (st.kind == KIND_DCP) {
+        for (int sl = tid; sl < S; sl += blockDim.x) {
+            if (st.state[sl] != ST_ACTIVE) continue;
+            if (st.k[sl] == 1) {
+                const int s = st.kv[sl * PL_MAXK];
+                st.moe[sl] = s;
+                atomicAdd(&si.B[s], 1);
+            } else {
+                const int i = atomicAdd(&s_n2, 1);
+                st.sk1[i] = st.k[sl];
+                st.sk2[i] = st.id[sl];
+                st.sval[i] = sl;
+            }
+        }
+        __syncthreads();
+        const int n2 = s_n2;
+        if (n2 > 1) cta_bitonic_sort(st.sk1, st.sk2, st.sval, n2);
+        __syncthreads();
+        if (warp == 0) {
+            for (int i = 0; i < n2; ++i) {
+                const int sl = st.sval[i];
+                const int kk = st.k[sl];
+                const int s = lane < kk ? st.kv[sl * PL_MAXK + lane] : 0x7fffffff;
+                const int64_t b = lane < kk ? (int64_t)si.B[s] : INT64_MAX;
+                // argmin over P_r of B, ties to the lowest instance id (cpp:54-59)
+                int64_t bv = b;
+                int bs = s;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+                    if (ov < bv || (ov == bv && os < bs)) { bv = ov; bs = os; }
+                }
+                if (lane == 0) {
+                    st.moe[sl] = bs;
+                    si.B[bs] += 1;
+                }
+                __syncwarp();
+            }
+        }
+    } else {
+        for (int sl = tid; sl < S; sl += blockDim.x)
+            if (st.state[sl] == ST_ACTIVE) atomicAdd(&si.B[st.moe[sl]], 1);
+    }
+    __syncthreads();
+
+    // ---- FIFO admission (scheduler.cpp:263-304) ----
+    const int nw = *st.nwait;
+    int wq = 0;              // entries kept so far == the reference's `scan`
+    bool head_recorded = false;
+    int i = 0;
+    for (; i < nw; ++i) {
+        const int sl = st.waiting[i];
+        const int64_t L = st.seq_len[sl];
+        if (never_fits_d(st, L)) {  // -> unschedulable, erased
+            if (tid == 0) st.res_slots[2 * S + s_cnt[2]++] = sl;
+            __syncthreads();
+            continue;
+        }
+        if (warp == 0) place_request(st, si, pl, lane, L);
+        __syncthreads();
+        if (pl.ok) {
+            // GlobalPageTable::allocate (page_table.cpp:9-49)
+            const int k = pl.k;
+            const int64_t np = pl.need_off[k];
+            const int64_t cap = np + st.reserve_pages;
+            const int64_t off = s_arena_top;
+            if (L < 1 || off + cap > st.arena_cap) {
+                if (tid == 0) s_status = L < 1 ? PL_E_FRAMES : PL_E_ARENA;
+                __syncthreads();
+                break;
+            }
+            for (int64_t t = tid; t < np; t += blockDim.x) {
+                int m = 0;
+                while (pl.need_off[m + 1] <= t) ++m;
+                const int s = pl.kv[m];
+                const int64_t j = t - pl.need_off[m];
+                st.pg_inst[off + t] = s;
+                st.pg_frame[off + t] = st.stack[(int64_t)s * st.capacity + si.nfree[s] - 1 - j];
+                const int64_t rem = pl.split[m] - j * st.page;
+                st.pg_fill[off + t] = (uint8_t)(rem < st.page ? rem : st.page);
+            }
+            __syncthreads();
+            if (warp == 0) {
+                if (lane < k) {
+                    const int s = pl.kv[lane];
+                    st.kv[sl * PL_MAXK + lane] = s;
+                    st.split[sl * PL_MAXK + lane] = pl.split[lane];
+                }
+                for (int s = lane; s < W; s += 32) st.shard_tokens[(int64_t)sl * W + s] = 0;
+                __syncwarp();
+                if (lane == 0) {
+                    int64_t trailing = 0;
+                    for (int m = 0; m < k; ++m) {  // members in order: allocate() mutations
+                        const int s = pl.kv[m];
+                        si.nfree[s] -= pl.need_off[m + 1] - pl.need_off[m];
+                        si.K[s] += pl.split[m];
+                        st.shard_tokens[(int64_t)sl * W + s] += pl.split[m];
+                        if (pl.split[m] > 0) {
+                            const int64_t r = pl.split[m] % st.page;
+                            trailing = r == 0 ? st.page : r;
+                        }
+                        si.shards[s] += 1;
+                    }
+                    st.k[sl] = k;
+                    st.moe[sl] = pl.moe;
+                    st.state[sl] = ST_ACTIVE;
+                    st.page_off[sl] = off;
+                    st.page_cnt[sl] = (int32_t)np;
+                    st.page_cap[sl] = (int32_t)cap;
+                    st.trailing_fill[sl] = trailing;
+                    si.B[pl.moe] += 1;
+                    s_arena_top = off + cap;
+                    st.res_slots[s_cnt[0]++] = sl;
+                }
+            }
+            __syncthreads();
+            continue;
+        }
+        // deferred (cpp:296-303)
+        if (warp == 0) {
+            const int64_t tf = warp_sum_i64(lane < W ? si.nfree[lane] : 0);
+            if (lane == 0) {
+                st.res_slots[S + s_cnt[1]++] = sl;
+                if (wq == 0 && !head_recorded) {
+                    if (tf >= pages_for_d(L, st.page)) s_hol += 1;
+                }
+            }
+        }
+        head_recorded = head_recorded || (wq == 0);
+        __syncthreads();
+        if (tid == 0) st.waiting[wq] = sl;
+        __syncthreads();
+        ++wq;
+        if (st.hol_strict) {
+            ++i;
+            break;
+        }
+    }
+    // keep the untouched tail of the queue in order
+    __syncthreads();
+    if (s_status == PL_OK) {
+        for (int j = i; j < nw; ++j) {
+            if (tid == 0) st.waiting[wq] = st.waiting[j];
+            ++wq;
+        }
+    } else {
+        // allocation failure: stop like the reference's exception, keep the rest queued
+        for (int j = i; j < nw; ++j) {
+            if (tid == 0) st.waiting[wq] = st.waiting[j];
+            ++wq;
+        }
+    }
+    __syncthreads();
+    if (tid < W) {
+        st.kv_load[tid] = si.K[tid];
+        st.nfree[tid] = si.nfree[tid];
+        st.moe_batch[tid] = si.B[tid];
+        st.shard_count[tid] = si.shards[tid];
+    }
+    if (tid == 0) {
+        *st.nwait = wq;
+        *st.arena_top = s_arena_top;
+        st.res_counts[0] = s_cnt[0];
+        st.res_counts[1] = s_cnt[1];
+        st.res_counts[2] = s_cnt[2];
+        st.res_counts[3] = s_status;
+        *st.res_hol = s_hol;
+    }
+}
+
+// ------------------------------------------------------------------ release (pt_free)
+// GlobalPageTable::release (page_table.cpp:51-66): frames pushed back in page
+// order, K_s -= shard tokens.  Requests are released sequentially in the given
+// order (the LIFO contents depend on it); each request's pages are pushed in
+// parallel with per-instance stable ranks.
+__global__ void __launch_bounds__(PL_THREADS, 1)
+    planner_release_kernel(PlannerState st, const int32_t* slots, int n) {
+    __shared__ int32_t cnt[PL_THREADS / 32][PL_MAXW];
+    __shared__ int64_t base[PL_MAXW];
+    __shared__ int64_t nfree[PL_MAXW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int W = st.W;
+    constexpr int NWARP = PL_THREADS / 32;
+    if (tid < W) nfree[tid] = st.nfree[tid];
+    __syncthreads();
+    for (int q = 0; q < n; ++q) {
+        const int sl = slots[q];
+        const int64_t off = st.page_off[sl];
+        const int np = st.page_cnt[sl];
+        for (int c0 = 0; c0 < np; c0 += PL_THREADS) {
+            const int t = c0 + tid;
+            const bool live = t < np;
+            const int s = live ? st.pg_inst[off + t] : -1;
+            const unsigned same = __match_any_sync(0xffffffffu, s);
+            const int rank = __popc(same & ((1u << lane) - 1u));
+            for (int j = lane; j < W; j += 32) cnt[warp][j] = 0;
+            __syncwarp();
+            if (live && rank == 0) cnt[warp][s] = __popc(same);
+            __syncthreads();
+            if (tid < W) {  // exclusive scan over warps per instance
+                int64_t run = 0;
+                for (int w = 0; w < NWARP; ++w) {
+                    const int c = cnt[w][tid];
+                    cnt[w][tid] = (int32_t)run;
+                    run += c;
+                }
+                base[tid] = run;  // total in this chunk
+            }
+            __syncthreads();
+            if (live) {
+                const int64_t pos = nfree[s] + cnt[warp][s] + rank;
+                st.stack[(int64_t)s * st.capacity + pos] = st.pg_frame[off + t];
+            }
+            __syncthreads();
+            if (tid < W) nfree[tid] += base[tid];
+            __syncthreads();
+        }
+        if (tid < W) st.kv_load[tid] -= st.shard_tokens[(int64_t)sl * W + tid];
+        if (tid == 0) st.state[sl] = ST_FINISHED;
+        __syncthreads();
+    }
+    if (tid < W) st.nfree[tid] = nfree[tid];
+}
+
+// ------------------------------------------------------------------ append_token
+// GlobalPageTable::append_token (page_table.cpp:86-121), sequential over the
+// batch (frames popped depend on order).  out_inst[q] = receiving instance or
+// -1 (growth stall).  Stops with PL_E_ARENA at the first request whose page
+// segment must grow past the arena; res_counts[0] = processed count.
+__global__ void planner_append_kernel(PlannerState st, const int32_t* slots, int n,
+                                      int32_t* out_inst) {
+    const int lane = threadIdx.x & 31;
+    const int W = st.W;
+    int q = 0;
+    int status = PL_OK;
+    for (; q < n; ++q) {
+        const int sl = slots[q];
+        int64_t off = st.page_off[sl];
+        const int cnt = st.page_cnt[sl];
+        int target;
+        if (cnt > 0 && st.trailing_fill[sl] < st.page) {
+            target = st.pg_inst[off + cnt - 1];
+            if (lane == 0) {
+                st.trailing_fill[sl] += 1;
+                st.pg_fill[off + cnt - 1] += 1;
+                st.kv_load[target] += 1;
+                st.shard_tokens[(int64_t)sl * W + target] += 1;
+                st.generated[sl] += 1;
+                out_inst[q] = target;
+            }
+            __syncwarp();
+            continue;
+        }
+        target = cnt == 0 ? st.kv[sl * PL_MAXK] : st.pg_inst[off + cnt - 1];
+        if (st.nfree[target] == 0) {
+            target = -1;
+            for (int m = 0; m < st.k[sl]; ++m) {
+                const int s = st.kv[sl * PL_MAXK + m];
+                if (st.nfree[s] > 0) { target = s; break; }
+            }
+        }
+        if (target < 0) {
+            if (lane == 0) out_inst[q] = -1;
+            __syncwarp();
+            continue;
+        }
+        if (cnt == st.page_cap[sl]) {  // grow the page segment (vector-style)
+            const int newcap = cnt * 2 > cnt + 16 ? cnt * 2 : cnt + 16;
+            const int64_t noff = *st.arena_top;
+            if (noff + newcap > st.arena_cap) {
+                status = PL_E_ARENA;
+                break;
+            }
+            for (int t = lane; t < cnt; t += 32) {
+                st.pg_inst[noff + t] = st.pg_inst[off + t];
+                st.pg_frame[noff + t] = st.pg_frame[off + t];
+                st.pg_fill[noff + t] = st.pg_fill[off + t];
+            }
+            __syncwarp();
+            if (lane == 0) {
+                *st.arena_top = noff + newcap;
+                st.page_off[sl] = noff;
+                st.page_cap[sl] = newcap;
+            }
+            __syncwarp();
+            off = noff;
+        }
+        if (lane == 0) {
+            const int64_t nf = st.nfree[target];
+            st.pg_inst[off + cnt] = target;
+            st.pg_frame[off + cnt] = st.stack[(int64_t)target * st.capacity + nf - 1];
+            st.pg_fill[off + cnt] = 1;
+            st.nfree[target] = nf - 1;
+            st.page_cnt[sl] = cnt + 1;
+            st.trailing_fill[sl] = 1;
+            st.kv_load[target] += 1;
+            st.shard_tokens[(int64_t)sl * W + target] += 1;
+            st.generated[sl] += 1;
+            out_inst[q] = target;
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        st.res_counts[0] = q;
+        st.res_counts[3] = status;
+    }
+}
+
+// ------------------------------------------------------------------ arena compaction
+// Moves every live page segment (ACTIVE slots) to a fresh arena, packed in slot order.
+__global__ void planner_compact_offsets(PlannerState st, int64_t* new_off) {
+    __shared__ int64_t part[1024];
+    const int tid = threadIdx.x;
+    const int S = st.max_slots;
+    const int per = (S + blockDim.x - 1) / blockDim.x;
+    int64_t sum = 0;
+    for (int j = tid * per; j < min(S, (tid + 1) * per); ++j)
+        if (st.state[j] == ST_ACTIVE) sum += st.page_cap[j];
+    part[tid] = sum;
+    __syncthreads();
+    if (tid == 0) {
+        int64_t run = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            const int64_t v = part[t];
+            part[t] = run;
+            run += v;
+        }
+        *st.arena_top = run;
+    }
+    __syncthreads();
+    int64_t run = part[tid];
+    for (int j = tid * per; j < min(S, (tid + 1) * per); ++j) {
+        new_off[j] = run;
+        if (st.state[j] == ST_ACTIVE) run += st.page_cap[j];
+    }
+}
+
+__global__ void planner_compact_copy(PlannerState st, const int64_t* new_off, int32_t* inst2,
+                                     int32_t* frame2, uint8_t* fill2) {
+    const int sl = blockIdx.x;
+    if (st.state[sl] != ST_ACTIVE) return;
+    const int64_t off = st.page_off[sl], noff = new_off[sl];
+    for (int t = threadIdx.x; t < st.page_cnt[sl]; t += blockDim.x) {
+        inst2[noff + t] = st.pg_inst[off + t];
+        frame2[noff + t] = st.pg_frame[off + t];
+        fill2[noff + t] = st.pg_fill[off + t];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) st.page_off[sl] = noff;
+}
+
+}  // namespace dcp

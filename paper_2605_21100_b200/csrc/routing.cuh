@@ -1,0 +1,201 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K7: lowering of committed placements to per-instance metadata (north_star
+// subsystem 4), restating bit-exactly
+//   build_binding_config   routing.cpp:9-32   (M / N lists ordered by request id,
+//                                             zero-split members included)
+//   derive_routing_tables  routing.cpp:34-63  (q_route N x W one-hot at m_r,
+//                                             res_route M x W ones at P_r)
+//   bucket_shape           routing.cpp:89-109 (default 48-bucket space)
+// and additionally emitting each instance's K1 inputs (the shard list = the N
+// list, its block table, per-page fill and shard lengths) so the planner's
+// output feeds the attention kernel without leaving the device.
+//
+// r1 (1 CTA x 32 warps): sort ACTIVE slots by id, then warp s builds instance
+// s's M/N rows with ballots (stable, id order).  r2 (1 CTA per instance):
+// count each row's pages on the instance, block-scan, scatter frames in
+// logical page order.
+#pragma once
+
+#include <cstdint>
+
+#include "planner.cuh"
+
+namespace dcp {
+
+struct RoutingOut {
+    int32_t* n_count;     // [W]
+    int32_t* m_count;     // [W]
+    int64_t* n_id;        // [W][S]
+    int32_t* n_slot;      // [W][S]
+    int32_t* n_moe;       // [W][S]  shard_request_moe
+    uint8_t* q_route;     // [W][S][W]
+    int64_t* m_id;        // [W][S]
+    int32_t* m_slot;      // [W][S]
+    uint8_t* res_route;   // [W][S][W]
+    int32_t* bucket;      // [W][2]  (M^, N^) or (-1,-1) on ShapeOverflow
+    int32_t* cu_pages;    // [W][S+1]
+    int64_t* shard_len;   // [W][S]
+    int32_t* block_table; // [W][capacity]
+    uint8_t* page_fill;   // [W][capacity]
+    int32_t* status;      // [1]
+};
+
+__device__ __forceinline__ void bucket_shape_default_d(int m, int n, int32_t* out) {
+    const int ms[6] = {8, 16, 32, 64, 128, 256};
+    const int ns[8] = {8, 16, 32, 64, 128, 256, 384, 512};
+    if (m > 256 || n > 512) {
+        out[0] = out[1] = -1;  // ShapeOverflow (routing.cpp:102-105)
+        return;
+    }
+    for (int i = 0; i < 6; ++i)
+        for (int j = 0; j < 8; ++j)
+            if (ms[i] >= m && ns[j] >= n) {
+                out[0] = ms[i];
+                out[1] = ns[j];
+                return;
+            }
+    out[0] = 256;
+    out[1] = 512;
+}
+
+__global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int32_t s_n;
+    __shared__ int32_t s_bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int S = st.max_slots, W = st.W;
+    if (tid == 0) {
+        s_n = 0;
+        s_bad = 0;
+    }
+    __syncthreads();
+    for (int sl = tid; sl < S; sl += blockDim.x) {
+        if (st.state[sl] != ST_ACTIVE) continue;
+        const int i = atomicAdd(&s_n, 1);
+        st.sk1[i] = st.id[sl];
+        st.sk2[i] = 0;
+        st.sval[i] = sl;
+        bool holds = false;  // InconsistentPlacement check (routing.cpp:19-21)
+        for (int m = 0; m < st.k[sl]; ++m) holds |= st.kv[sl * PL_MAXK + m] == st.moe[sl];
+        if (!holds) s_bad = 1;
+    }
+    __syncthreads();
+    const int n = s_n;
+    if (n > 1) cta_bitonic_sort(st.sk1, st.sk2, st.sval, n);
+    __syncthreads();
+    if (s_bad) {
+        if (tid == 0) *ro.status = -4;
+        return;
+    }
+    if (warp < W) {
+        const int s = warp;
+        int nrow = 0, mrow = 0;
+        for (int c = 0; c < n; c += 32) {
+            const int a = c + lane;
+            bool inN = false, inM = false;
+            int sl = -1;
+            if (a < n) {
+                sl = st.sval[a];
+                for (int m = 0; m < st.k[sl]; ++m) inN |= st.kv[sl * PL_MAXK + m] == s;
+                inM = st.moe[sl] == s;
+            }
+            const unsigned bn = __ballot_sync(0xffffffffu, inN);
+            const unsigned bm = __ballot_sync(0xffffffffu, inM);
+            const unsigned lt = (1u << lane) - 1u;
+            if (inN) {
+                const int row = nrow + __popc(bn & lt);
+                const size_t r = (size_t)s * S + row;
+                ro.n_id[r] = st.id[sl];
+                ro.n_slot[r] = sl;
+                ro.n_moe[r] = st.moe[sl];
+                uint8_t* q = ro.q_route + r * W;
+                for (int c2 = 0; c2 < W; ++c2) q[c2] = (c2 == st.moe[sl]) ? 1 : 0;
+                ro.shard_len[r] = st.shard_tokens[(size_t)sl * W + s];
+            }
+            if (inM) {
+                const int row = mrow + __popc(bm & lt);
+                const size_t r = (size_t)s * S + row;
+                ro.m_id[r] = st.id[sl];
+                ro.m_slot[r] = sl;
+                uint8_t* q = ro.res_route + r * W;
+                for (int c2 = 0; c2 < W; ++c2) q[c2] = 0;
+                for (int m = 0; m < st.k[sl]; ++m) q[st.kv[sl * PL_MAXK + m]] = 1;
+            }
+            nrow += __popc(bn);
+            mrow += __popc(bm);
+        }
+        if (lane == 0) {
+            ro.n_count[s] = nrow;
+            ro.m_count[s] = mrow;
+            bucket_shape_default_d(mrow, nrow, ro.bucket + 2 * s);
+        }
+    }
+    if (tid == 0) *ro.status = 0;
+}
+
+// One CTA per instance: block table + fill + cu_pages for its N rows.
+__global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int64_t part[1024];
+    const int s = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = blockDim.x >> 5;
+    const int S = st.max_slots;
+    const int rows = ro.n_count[s];
+    int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
+    // (a) pages of each row on this instance
+    for (int row = warp; row < rows; row += nw) {
+        const int sl = ro.n_slot[(size_t)s * S + row];
+        const int64_t off = st.page_off[sl];
+        const int np = st.page_cnt[sl];
+        int c = 0;
+        for (int t = lane; t - lane < np; t += 32) {
+            const bool on = t < np && st.pg_inst[off + t] == s;
+            c += __popc(__ballot_sync(0xffffffffu, on));
+        }
+        if (lane == 0) cu[row + 1] = c;
+    }
+    __syncthreads();
+    // (b) exclusive scan of counts -> cu_pages
+    const int per = (rows + blockDim.x - 1) / blockDim.x;
+    int64_t sum = 0;
+    for (int j = tid * per; j < min(rows, (tid + 1) * per); ++j) sum += cu[j + 1];
+    part[tid] = sum;
+    __syncthreads();
+    if (tid == 0) {
+        int64_t run = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            const int64_t v = part[t];
+            part[t] = run;
+            run += v;
+        }
+        cu[0] = 0;
+    }
+    __syncthreads();
+    int64_t run = part[tid];
+    for (int j = tid * per; j < min(rows, (tid + 1) * per); ++j) {
+        run += cu[j + 1];
+        cu[j + 1] = (int32_t)run;
+    }
+    __syncthreads();
+    // (c) scatter frames in logical page order
+    int32_t* bt = ro.block_table + (size_t)s * st.capacity;
+    uint8_t* pf = ro.page_fill + (size_t)s * st.capacity;
+    for (int row = warp; row < rows; row += nw) {
+        const int sl = ro.n_slot[(size_t)s * S + row];
+        const int64_t off = st.page_off[sl];
+        const int np = st.page_cnt[sl];
+        int pos = cu[row];
+        for (int t = lane; t - lane < np; t += 32) {
+            const bool on = t < np && st.pg_inst[off + t] == s;
+            const unsigned b = __ballot_sync(0xffffffffu, on);
+            if (on) {
+                const int p = pos + __popc(b & ((1u << lane) - 1u));
+                bt[p] = st.pg_frame[off + t];
+                pf[p] = st.pg_fill[off + t];
+            }
+            pos += __popc(b);
+        }
+    }
+}
+
+}  // namespace dcp

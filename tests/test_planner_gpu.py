@@ -1,0 +1,124 @@
+"""K6/K7 device planner vs the reference (bit-exact).
+
+Every scenario is replayed through the device planner (dcp_planner_*) and
+compared with (a) the golden fixtures generated from the reference itself and
+(b) the oracle port / compiled reference on seeded random scripts: StepResult
+(committed / deferred / unschedulable / hol_events), every Placement, the
+instance counters, GlobalPageTable::dump_csv (frame ids => LIFO order) and
+dump_routing_csv.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from tests import oracle_lib
+from tests.oracle_lib import World
+from tests.test_oracle import _random_world_script
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2605_21100_b200.attention import DcpContext
+    assert torch.cuda.is_available(), "GPU test selected but no CUDA device"
+    return DcpContext(0)
+
+
+def _dev(ctx, sc, max_requests=1024):
+    from paper_2605_21100_b200.planner import DevicePlanner
+    return DevicePlanner(ctx, sc["nodes"], sc["ipn"], sc["page"], sc["capacity"], sc["kind"], sc.get("bucket"),
+                         sc.get("uniform_degree", 1), sc.get("hol_strict", True), max_requests=max_requests)
+
+
+def _replay(w, sc):
+    log = []
+    for ev in sc["events"]:
+        if ev[0] == "enqueue":
+            w.enqueue(ev[1], ev[2])
+        elif ev[0] == "step":
+            log.append(w.step())
+        elif ev[0] in ("finish", "finish?"):
+            log.append(("finish", w.finish(ev[1])))
+        elif ev[0] == "append":
+            rc, inst = w.append_token(ev[1])
+            log.append({"append": ev[1], "instance": inst, "rc": rc})
+    return log
+
+
+def test_golden_scenarios(ctx):
+    for item in json.load(open(os.path.join(GOLD, "planner_scenarios.json"))):
+        sc, res = item["scenario"], item["result"]
+        w = _dev(ctx, sc)
+        log = [x for x in _replay(w, sc) if not (isinstance(x, tuple) and x[0] == "finish")]
+        assert log == res["steps"], sc["name"]
+        assert w.instances() == res["instances"], sc["name"]
+        ids = sorted({e[1] for e in sc["events"] if e[0] == "enqueue"})
+        assert {str(i): w.placement(i) for i in ids} == res["placements"], sc["name"]
+        pt, rt = w.page_table_csv(), w.routing_csv()
+        assert hashlib.sha256(pt.encode()).hexdigest() == res["page_table_csv_sha256"], sc["name"]
+        assert hashlib.sha256(rt.encode()).hexdigest() == res["routing_csv_sha256"], sc["name"]
+
+
+def test_fuzz_vs_oracle(ctx):
+    port = oracle_lib.port()
+    ref = oracle_lib.reference()
+    rng = np.random.default_rng(11)
+    for trial in range(120):
+        sc = _random_world_script(rng)
+        wd = _dev(ctx, sc)
+        wo = World(port, "dcpora_", sc["nodes"], sc["ipn"], sc["page"], sc["capacity"], sc["kind"],
+                   sc.get("bucket"), sc.get("uniform_degree", 1), sc.get("hol_strict", True))
+        ld, lo = _replay(wd, sc), _replay(wo, sc)
+        assert ld == lo, trial
+        assert wd.instances() == wo.instances(), trial
+        assert wd.page_table_csv() == wo.page_table_csv(), trial
+        assert wd.routing_csv() == wo.routing_csv(), trial
+        if ref is not None and trial % 10 == 0:
+            wr = World(ref, "dcpref_", sc["nodes"], sc["ipn"], sc["page"], sc["capacity"], sc["kind"],
+                       sc.get("bucket"), sc.get("uniform_degree", 1), sc.get("hol_strict", True))
+            _replay(wr, sc)
+            assert wd.routing_csv() == wr.routing_csv() and wd.page_table_csv() == wr.page_table_csv()
+
+
+def test_block_tables_match_page_table(ctx):
+    """K7's per-instance K1 inputs agree with the page table: for every
+    instance, rows = N list, frames = that request's pages on the instance in
+    logical order, fills sum to the shard's tokens."""
+    from paper_2605_21100_b200.planner import DevicePlanner
+    rng = np.random.default_rng(3)
+    w = DevicePlanner(ctx, 1, 4, 16, 4000, "dcp", [[2000, 1], [8000, 2], [2**63 - 1, 4]], max_requests=256)
+    o = World(oracle_lib.port(), "dcpora_", 1, 4, 16, 4000, "dcp", [[2000, 1], [8000, 2], [2**63 - 1, 4]])
+    ids = list(range(60))
+    lens = rng.integers(1, 20000, size=60).tolist()
+    for i, L in zip(ids, lens):
+        w.enqueue(i, L)
+        o.enqueue(i, L)
+    assert w.step() == o.step()
+    for rid in rng.choice(ids, 25).tolist():
+        assert w.append_token(rid) == o.append_token(rid)
+    w.build_routing()
+    pt = [list(map(int, l.split(","))) for l in w.page_table_csv().strip().split("\n")[1:]]
+    for s in range(4):
+        v = w.instance_view(s)
+        n = v.n_rows
+        cu = _d2h(v.cu_pages, n + 1, np.int32)
+        nid = _d2h(v.n_ids, n, np.int64)
+        bt = _d2h(v.block_table, int(cu[-1]), np.int32)
+        fill = _d2h(v.page_fill, int(cu[-1]), np.uint8)
+        slen = _d2h(v.shard_len, n, np.int64)
+        assert list(nid) == sorted(nid)
+        for row, rid in enumerate(nid):
+            frames = [f for (r, p, i, f) in pt if r == rid and i == s]
+            assert list(bt[cu[row]:cu[row + 1]]) == frames
+            assert int(fill[cu[row]:cu[row + 1]].sum()) == int(slen[row])
+
+
+def _d2h(ptr, n, dtype):
+    from paper_2605_21100_b200._capi import device_to_numpy
+    return device_to_numpy(ptr, n, dtype)
