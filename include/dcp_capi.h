@@ -180,6 +180,15 @@ typedef struct dcp_instance_view {
     const int64_t* shard_len;   /* [N] */
     const int32_t* block_table; /* [cu_pages[N]] */
     const uint8_t* page_fill;   /* [cu_pages[N]] */
+    /* exchange maps for the routed step (dcp_route_q / dcp_decode_attn_routed / dcp_merge_partials) */
+    const int32_t* n_mrow;      /* [N] row of each shard's request in m_r's M list */
+    const int32_t* m_nrow;      /* [M][W] row of each M request in s' N list (-1: s' not in P_r) */
+    const int32_t* m_k;         /* [M] |P_r| */
+    const int32_t* m_kv;        /* [M][16] P_r in kv_binding order */
+    const int32_t* m_count_all; /* [W] device copy of every instance's M */
+    const int32_t* n_count_dev; /* device copy of this instance's N */
+    int32_t world;
+    int32_t instance;
 } dcp_instance_view;
 
 DCP_API int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* cfg, dcp_planner** out);
@@ -207,6 +216,52 @@ DCP_API int64_t dcp_planner_dump_routing(dcp_planner* pl, char* buf, int64_t cap
 DCP_API int dcp_planner_instance_view(dcp_planner* pl, int32_t instance, dcp_instance_view* out);
 /* Kernel launches issued by the last step / build_routing call. */
 DCP_API int dcp_planner_last_launches(const dcp_planner* pl);
+
+/* ---- K2 / K1-routed / K3: the routing-based exchange of one DCP step ---------
+ *
+ * The paper's backend: the sender reads the routing mask
+ * and stores the payload directly into the peer's pre-allocated receive slot
+ * (NVLink P2P when the peer is another GPU), the receiver polls an arrival
+ * flag.  Phases (Fig. 7): 1 Q-route (dcp_route_q), 2 partial attention with
+ * the Res-route put fused into its epilogue (dcp_decode_attn_routed), 4 LSE
+ * merge at the MoE binding (dcp_merge_partials; math of lse_merge,
+ * attn_merge.hpp:86-100, in kv_binding order, zero-token shards weight 0).
+ * Pools per instance (one allocation, exported by CUDA IPC for peers):
+ *   q_recv [n_max][HQ][D] bf16 + flags, res [m_max][W][HQ][D] fp32 + LSE + flags.
+ * Local buffers: q_local [m_max][HQ][D] bf16 (queries of the requests
+ * MoE-bound here, in M-row order), out [m_max][HQ][D] fp32 + out_lse.
+ * Flags carry a per-step epoch (dcp_xchg_begin_step), so graph replay needs no
+ * reset.  All instances must call begin_step once per step. */
+typedef struct dcp_xchg dcp_xchg;
+typedef struct dcp_xchg_config {
+    int32_t world;
+    int32_t self;
+    int32_t num_q_heads;
+    int32_t head_dim;
+    int32_t n_max;   /* ShapeSpace n_max (routing.hpp:62-63) */
+    int32_t m_max;   /* ShapeSpace m_max */
+} dcp_xchg_config;
+
+DCP_API int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* cfg, dcp_xchg** out);
+DCP_API int dcp_xchg_destroy(dcp_xchg* x);
+DCP_API int dcp_xchg_ipc_handle(dcp_xchg* x, void* handle64);
+DCP_API int dcp_xchg_open_peer_ipc(dcp_xchg* x, int32_t peer, const void* handle64);
+DCP_API int dcp_xchg_set_peer_local(dcp_xchg* x, int32_t peer, const dcp_xchg* other);
+DCP_API int dcp_xchg_commit(dcp_xchg* x);
+DCP_API int dcp_xchg_begin_step(dcp_xchg* x, void* stream);
+DCP_API int dcp_xchg_buffers(dcp_xchg* x, void** q_local, void** q_recv, float** out,
+                             float** out_lse);
+/* Stage the queries of this instance's M requests (device bf16 [rows][HQ][D],
+ * M-row order) into q_local (the output of the query projection in a model). */
+DCP_API int dcp_xchg_write_queries(dcp_xchg* x, const void* q_rows, int32_t rows, void* stream);
+DCP_API int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream);
+/* K1 over this instance's N list (q from q_recv, waits on Q-route flags),
+ * outputs stored into each row's m_r result slot.  `a` supplies kv_pool,
+ * num_frames, head counts, scale and workspace (sized for n_max shards); its
+ * q/out/lse/shard arrays are ignored. */
+DCP_API int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
+                                   const dcp_attn_args* a, void* stream);
+DCP_API int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream);
 
 #ifdef __cplusplus
 }

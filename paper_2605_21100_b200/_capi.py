@@ -93,7 +93,14 @@ class InstanceView(Structure):
         ("n_ids", c_void_p), ("n_moe", c_void_p), ("q_route", c_void_p), ("m_ids", c_void_p),
         ("res_route", c_void_p), ("cu_pages", c_void_p), ("shard_len", c_void_p),
         ("block_table", c_void_p), ("page_fill", c_void_p),
+        ("n_mrow", c_void_p), ("m_nrow", c_void_p), ("m_k", c_void_p), ("m_kv", c_void_p),
+        ("m_count_all", c_void_p), ("n_count_dev", c_void_p), ("world", c_int32), ("instance", c_int32),
     ]
+
+
+class XchgConfig(Structure):
+    _fields_ = [("world", c_int32), ("self", c_int32), ("num_q_heads", c_int32), ("head_dim", c_int32),
+                ("n_max", c_int32), ("m_max", c_int32)]
 
 
 _lib = None
@@ -123,6 +130,18 @@ _SIGNATURES = [
     ("dcp_planner_dump_routing", c_int64, [c_void_p, c_char_p, c_int64]),
     ("dcp_planner_instance_view", c_int, [c_void_p, c_int32, POINTER(InstanceView)]),
     ("dcp_planner_last_launches", c_int, [c_void_p]),
+    ("dcp_xchg_create", c_int, [c_void_p, POINTER(XchgConfig), POINTER(c_void_p)]),
+    ("dcp_xchg_destroy", c_int, [c_void_p]),
+    ("dcp_xchg_ipc_handle", c_int, [c_void_p, c_void_p]),
+    ("dcp_xchg_open_peer_ipc", c_int, [c_void_p, c_int32, c_void_p]),
+    ("dcp_xchg_set_peer_local", c_int, [c_void_p, c_int32, c_void_p]),
+    ("dcp_xchg_commit", c_int, [c_void_p]),
+    ("dcp_xchg_begin_step", c_int, [c_void_p, c_void_p]),
+    ("dcp_xchg_buffers", c_int, [c_void_p] + [POINTER(c_void_p)] * 4),
+    ("dcp_xchg_write_queries", c_int, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("dcp_route_q", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
+    ("dcp_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
+    ("dcp_merge_partials", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
 ]
 
 

@@ -6,6 +6,7 @@
 
 #include "capi_common.cuh"
 #include "splitkv_decode.cuh"
+#include "xchg_internal.cuh"
 
 namespace dcp {
 
@@ -86,6 +87,17 @@ static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams&
     return DCP_OK;
 }
 
+static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm, int hkv, int G,
+                           cudaStream_t s) {
+    if (hkv == 8 && G == 4) return launch_decode<8, 4>(ctx, map, prm, s);
+    if (hkv == 4 && G == 8) return launch_decode<4, 8>(ctx, map, prm, s);
+    if (hkv == 8 && G == 1) return launch_decode<8, 1>(ctx, map, prm, s);
+    if (hkv == 2 && G == 16) return launch_decode<2, 16>(ctx, map, prm, s);
+    if (hkv == 1 && G == 16) return launch_decode<1, 16>(ctx, map, prm, s);
+    set_error("unsupported (num_kv_heads=%d, group=%d)", hkv, G);
+    return DCP_E_UNSUPPORTED;
+}
+
 }  // namespace dcp
 
 using namespace dcp;
@@ -164,7 +176,7 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map);
     if (rc) return rc;
 
-    AttnParams prm;
+    AttnParams prm{};
     prm.q = static_cast<const __nv_bfloat16*>(a->q);
     prm.block_table = a->block_table;
     prm.cu_pages = a->cu_pages;
@@ -182,15 +194,47 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     prm.num_shards = a->num_shards;
     prm.scale_log2 = a->scale * 1.4426950408889634f;
 
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int hkv = a->num_kv_heads;
-    if (hkv == 8 && G == 4) return launch_decode<8, 4>(ctx, map, prm, s);
-    if (hkv == 4 && G == 8) return launch_decode<4, 8>(ctx, map, prm, s);
-    if (hkv == 8 && G == 1) return launch_decode<8, 1>(ctx, map, prm, s);
-    if (hkv == 2 && G == 16) return launch_decode<2, 16>(ctx, map, prm, s);
-    if (hkv == 1 && G == 16) return launch_decode<1, 16>(ctx, map, prm, s);
-    set_error("unsupported (num_kv_heads=%d, group=%d)", hkv, G);
-    return DCP_E_UNSUPPORTED;
+    return dispatch_decode(ctx, map, prm, a->num_kv_heads, G, static_cast<cudaStream_t>(stream));
+}
+
+int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
+                           const dcp_attn_args* a, void* stream) {
+    DCP_REQUIRE(ctx && x && v && a, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    DCP_REQUIRE(a->head_dim == 128 && a->page_size == 16, DCP_E_UNSUPPORTED, "head_dim/page_size");
+    DCP_REQUIRE(a->num_q_heads == x->cfg.num_q_heads && a->head_dim == x->cfg.head_dim, DCP_E_INVALID_ARG,
+                "exchange pool shape differs from the attention shape");
+    DCP_REQUIRE(a->kv_pool && a->workspace && a->num_frames > 0, DCP_E_INVALID_ARG, "kv_pool/workspace");
+    DCP_REQUIRE(a->num_kv_heads > 0 && a->num_q_heads % a->num_kv_heads == 0, DCP_E_INVALID_ARG, "heads");
+    const size_t need = dcp_attn_workspace_bytes(ctx, x->cfg.n_max, a->num_q_heads, a->head_dim);
+    DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu", a->workspace_bytes, need);
+    const CUtensorMap* map = nullptr;
+    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map);
+    if (rc) return rc;
+    AttnParams prm{};
+    prm.q = reinterpret_cast<const __nv_bfloat16*>(x->pool + x->off_qrecv);
+    prm.block_table = v->block_table;
+    prm.cu_pages = v->cu_pages;
+    prm.shard_len = v->shard_len;
+    prm.page_fill = v->page_fill;
+    prm.out = nullptr;
+    prm.lse = nullptr;
+    char* ws = static_cast<char*>(a->workspace);
+    const size_t slots = 2 * static_cast<size_t>(ctx->num_sms);
+    prm.ws_acc = reinterpret_cast<float*>(ws);
+    ws += slots * a->num_q_heads * a->head_dim * sizeof(float);
+    prm.ws_ml = reinterpret_cast<float*>(ws);
+    ws += slots * a->num_q_heads * 2 * sizeof(float);
+    prm.counters = reinterpret_cast<int32_t*>(ws);
+    prm.num_shards = 0;
+    prm.scale_log2 = a->scale * 1.4426950408889634f;
+    prm.xp = x->dev;
+    prm.n_mrow = v->n_mrow;
+    prm.n_moe = v->n_moe;
+    prm.q_flag = reinterpret_cast<const uint32_t*>(x->pool + x->off_qflag);
+    prm.num_shards_ptr = v->n_count_dev;
+    return dispatch_decode(ctx, map, prm, a->num_kv_heads, a->num_q_heads / a->num_kv_heads,
+                           static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

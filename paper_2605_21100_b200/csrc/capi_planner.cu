@@ -78,6 +78,14 @@ struct dcp_planner {
     int64_t waiting_pages_bound = 0; // sum over queued requests of their max arena demand
     std::vector<int64_t> queued_len; // per slot (for the bound)
     int32_t queued = 0;
+    struct Retired {
+        int32_t k, moe;
+        int32_t kv[PL_MAXK];
+        int64_t split[PL_MAXK];
+    };
+    // Finished requests keep their Placement (Request::placement is not cleared
+    // by pt_free, page_table.cpp:51-66), so placement queries still answer.
+    std::unordered_map<int64_t, Retired> retired;
     cudaStream_t stream = nullptr;
     int last_launches = 0;
     bool routing_valid = false;
@@ -239,6 +247,12 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     rc |= dalloc(&ro.block_table, (size_t)W * std::max<int64_t>(c->capacity_pages, 1), o);
     rc |= dalloc(&ro.page_fill, (size_t)W * std::max<int64_t>(c->capacity_pages, 1), o);
     rc |= dalloc(&ro.status, 1, o);
+    rc |= dalloc(&ro.slot_nrow, S * W, o);
+    rc |= dalloc(&ro.slot_mrow, S, o);
+    rc |= dalloc(&ro.n_mrow, (size_t)W * S, o);
+    rc |= dalloc(&ro.m_nrow, (size_t)W * S * W, o);
+    rc |= dalloc(&ro.m_k, (size_t)W * S, o);
+    rc |= dalloc(&ro.m_kv, (size_t)W * S * PL_MAXK, o);
     if (rc) {
         dcp_planner_destroy(pl);
         return DCP_E_CUDA;
@@ -279,6 +293,7 @@ int dcp_planner_enqueue(dcp_planner* pl, const int64_t* ids, const int64_t* lens
         DCP_REQUIRE(!pl->slot_of.count(ids[i]), DCP_E_INVALID_ARG, "request id %lld already tracked",
                     (long long)ids[i]);
     }
+    for (int i = 0; i < n; ++i) pl->retired.erase(ids[i]);
     for (int i = 0; i < n; ++i) {
         const int sl = pl->free_slots.back();
         pl->free_slots.pop_back();
@@ -382,6 +397,14 @@ int dcp_planner_finish(dcp_planner* pl, const int64_t* ids, int32_t n, void* str
         DCP_REQUIRE(s == ST_ACTIVE, DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
                     (long long)ids[i]);
     }
+    for (int i = 0; i < n; ++i) {
+        dcp_planner::Retired r{};
+        DCP_CUDA_TRY(cudaMemcpy(&r.k, pl->st.k + slots[i], 4, cudaMemcpyDeviceToHost));
+        DCP_CUDA_TRY(cudaMemcpy(&r.moe, pl->st.moe + slots[i], 4, cudaMemcpyDeviceToHost));
+        DCP_CUDA_TRY(cudaMemcpy(r.kv, pl->st.kv + (size_t)slots[i] * PL_MAXK, r.k * 4, cudaMemcpyDeviceToHost));
+        DCP_CUDA_TRY(cudaMemcpy(r.split, pl->st.split + (size_t)slots[i] * PL_MAXK, r.k * 8, cudaMemcpyDeviceToHost));
+        pl->retired[ids[i]] = r;
+    }
     DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_slots, slots.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, pl->stream));
     planner_release_kernel<<<1, PL_THREADS, 0, pl->stream>>>(pl->st, pl->d_io_slots, n);
     DCP_CUDA_TRY(cudaGetLastError());
@@ -437,7 +460,17 @@ int dcp_planner_placement(dcp_planner* pl, int64_t id, int32_t* kv, int64_t* spl
                           int32_t* k) {
     DCP_REQUIRE(pl && kv && split && moe && k, DCP_E_INVALID_ARG, "NULL argument");
     auto it = pl->slot_of.find(id);
-    DCP_REQUIRE(it != pl->slot_of.end(), DCP_E_UNKNOWN_REQUEST, "unknown request %lld", (long long)id);
+    if (it == pl->slot_of.end()) {
+        auto rt = pl->retired.find(id);
+        DCP_REQUIRE(rt != pl->retired.end(), DCP_E_UNKNOWN_REQUEST, "unknown request %lld", (long long)id);
+        *k = rt->second.k;
+        *moe = rt->second.moe;
+        for (int m = 0; m < *k; ++m) {
+            kv[m] = rt->second.kv[m];
+            split[m] = rt->second.split[m];
+        }
+        return DCP_OK;
+    }
     const int sl = it->second;
     DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
     int32_t state = 0;
@@ -583,6 +616,14 @@ int dcp_planner_instance_view(dcp_planner* pl, int32_t s, dcp_instance_view* v) 
     v->shard_len = pl->ro.shard_len + (size_t)s * S;
     v->block_table = pl->ro.block_table + (size_t)s * pl->st.capacity;
     v->page_fill = pl->ro.page_fill + (size_t)s * pl->st.capacity;
+    v->n_mrow = pl->ro.n_mrow + (size_t)s * S;
+    v->m_nrow = pl->ro.m_nrow + (size_t)s * S * W;
+    v->m_k = pl->ro.m_k + (size_t)s * S;
+    v->m_kv = pl->ro.m_kv + (size_t)s * S * PL_MAXK;
+    v->m_count_all = pl->ro.m_count;
+    v->n_count_dev = pl->ro.n_count + s;
+    v->world = W;
+    v->instance = s;
     return DCP_OK;
 }
 

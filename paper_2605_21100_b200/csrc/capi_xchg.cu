@@ -1,0 +1,174 @@
+// SPDX-License-Identifier: Apache-2.0
+// C ABI: the routing-based exchange (K2 Q-route, K3 LSE merge) — dcp_capi.h.
+#include <cstring>
+
+#include "exchange_kernels.cuh"
+#include "xchg_internal.cuh"
+
+using namespace dcp;
+
+namespace {
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+void fill_peer(dcp_xchg* x, int peer, char* base) {
+    x->host.qrecv[peer] = reinterpret_cast<__nv_bfloat16*>(base + x->off_qrecv);
+    x->host.qflag[peer] = reinterpret_cast<uint32_t*>(base + x->off_qflag);
+    x->host.res_o[peer] = reinterpret_cast<float*>(base + x->off_res_o);
+    x->host.res_lse[peer] = reinterpret_cast<float*>(base + x->off_res_lse);
+    x->host.res_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_res_flag);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c, dcp_xchg** out) {
+    DCP_REQUIRE(ctx && c && out, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(c->world >= 1 && c->world <= PL_MAXW, DCP_E_UNSUPPORTED, "world %d", c->world);
+    DCP_REQUIRE(c->self >= 0 && c->self < c->world, DCP_E_INVALID_ARG, "self %d", c->self);
+    DCP_REQUIRE(c->head_dim % 32 == 0 && c->num_q_heads > 0, DCP_E_UNSUPPORTED, "head_dim %d", c->head_dim);
+    DCP_REQUIRE(c->n_max > 0 && c->m_max > 0, DCP_E_INVALID_ARG, "n_max/m_max");
+    DCP_CUDA_TRY(cudaSetDevice(ctx->device));
+    auto* x = new dcp_xchg();
+    x->ctx = ctx;
+    x->cfg = *c;
+    const size_t W = c->world, hq = c->num_q_heads, d = c->head_dim, n = c->n_max, m = c->m_max;
+    size_t o = 0;
+    x->off_qrecv = o;    o = align256(o + n * hq * d * 2);
+    x->off_qflag = o;    o = align256(o + n * 4);
+    x->off_res_o = o;    o = align256(o + m * W * hq * d * 4);
+    x->off_res_lse = o;  o = align256(o + m * W * hq * 4);
+    x->off_res_flag = o; o = align256(o + m * W * 4);
+    x->pool_bytes = o;
+    DCP_CUDA_TRY(cudaMalloc(&x->pool, x->pool_bytes));
+    DCP_CUDA_TRY(cudaMemset(x->pool, 0, x->pool_bytes));
+    size_t lb = 0;
+    const size_t off_q = lb;   lb = align256(lb + m * hq * d * 2);
+    const size_t off_out = lb; lb = align256(lb + m * hq * d * 4);
+    const size_t off_lse = lb; lb = align256(lb + m * hq * 4);
+    const size_t off_ep = lb;  lb = align256(lb + 4);
+    const size_t off_dev = lb; lb = align256(lb + sizeof(XchgPeers));
+    DCP_CUDA_TRY(cudaMalloc(&x->local, lb));
+    DCP_CUDA_TRY(cudaMemset(x->local, 0, lb));
+    x->q_local = x->local + off_q;
+    x->out = reinterpret_cast<float*>(x->local + off_out);
+    x->out_lse = reinterpret_cast<float*>(x->local + off_lse);
+    x->epoch = reinterpret_cast<uint32_t*>(x->local + off_ep);
+    x->dev = reinterpret_cast<XchgPeers*>(x->local + off_dev);
+    x->host.W = c->world;
+    x->host.self = c->self;
+    x->host.hq = c->num_q_heads;
+    x->host.d = c->head_dim;
+    x->host.n_max = c->n_max;
+    x->host.m_max = c->m_max;
+    x->host.epoch = x->epoch;
+    fill_peer(x, c->self, x->pool);
+    *out = x;
+    return DCP_OK;
+}
+
+int dcp_xchg_destroy(dcp_xchg* x) {
+    if (!x) return DCP_OK;
+    for (int i = 0; i < PL_MAXW; ++i)
+        if (x->opened[i]) cudaIpcCloseMemHandle(x->opened[i]);
+    cudaFree(x->pool);
+    cudaFree(x->local);
+    delete x;
+    return DCP_OK;
+}
+
+int dcp_xchg_ipc_handle(dcp_xchg* x, void* handle64) {
+    DCP_REQUIRE(x && handle64, DCP_E_INVALID_ARG, "NULL argument");
+    cudaIpcMemHandle_t h;
+    DCP_CUDA_TRY(cudaIpcGetMemHandle(&h, x->pool));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    std::memcpy(handle64, &h, 64);
+    return DCP_OK;
+}
+
+int dcp_xchg_open_peer_ipc(dcp_xchg* x, int32_t peer, const void* handle64) {
+    DCP_REQUIRE(x && handle64, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(peer >= 0 && peer < x->cfg.world && peer != x->cfg.self, DCP_E_INVALID_ARG, "peer %d", peer);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, 64);
+    void* base = nullptr;
+    DCP_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    x->opened[peer] = base;
+    fill_peer(x, peer, static_cast<char*>(base));
+    return DCP_OK;
+}
+
+int dcp_xchg_set_peer_local(dcp_xchg* x, int32_t peer, const dcp_xchg* other) {
+    DCP_REQUIRE(x && other, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(peer >= 0 && peer < x->cfg.world, DCP_E_INVALID_ARG, "peer %d", peer);
+    DCP_REQUIRE(std::memcmp(&x->cfg.num_q_heads, &other->cfg.num_q_heads, 4 * sizeof(int32_t)) == 0 &&
+                    x->cfg.world == other->cfg.world,
+                DCP_E_INVALID_ARG, "peer pool shapes differ");
+    if (other->ctx->device != x->ctx->device) {
+        cudaError_t e = cudaDeviceEnablePeerAccess(other->ctx->device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+            set_error("cudaDeviceEnablePeerAccess: %s", cudaGetErrorString(e));
+            return DCP_E_CUDA;
+        }
+        cudaGetLastError();
+    }
+    fill_peer(x, peer, other->pool);
+    return DCP_OK;
+}
+
+int dcp_xchg_commit(dcp_xchg* x) {
+    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
+    for (int s = 0; s < x->cfg.world; ++s)
+        DCP_REQUIRE(x->host.qrecv[s] != nullptr, DCP_E_INVALID_ARG, "peer %d not set", s);
+    DCP_CUDA_TRY(cudaMemcpy(x->dev, &x->host, sizeof(XchgPeers), cudaMemcpyHostToDevice));
+    return DCP_OK;
+}
+
+int dcp_xchg_begin_step(dcp_xchg* x, void* stream) {
+    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
+    epoch_bump_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(x->epoch);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+int dcp_xchg_buffers(dcp_xchg* x, void** q_local, void** q_recv, float** out, float** out_lse) {
+    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
+    if (q_local) *q_local = x->q_local;
+    if (q_recv) *q_recv = x->pool + x->off_qrecv;
+    if (out) *out = x->out;
+    if (out_lse) *out_lse = x->out_lse;
+    return DCP_OK;
+}
+
+int dcp_xchg_write_queries(dcp_xchg* x, const void* q_rows, int32_t rows, void* stream) {
+    DCP_REQUIRE(x && (rows == 0 || q_rows), DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(rows >= 0 && rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "rows %d > m_max %d", rows,
+                x->cfg.m_max);
+    const size_t bytes = (size_t)rows * x->cfg.num_q_heads * x->cfg.head_dim * 2;
+    if (bytes)
+        DCP_CUDA_TRY(cudaMemcpyAsync(x->q_local, q_rows, bytes, cudaMemcpyDeviceToDevice,
+                                     static_cast<cudaStream_t>(stream)));
+    return DCP_OK;
+}
+
+int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
+    DCP_REQUIRE(x && v, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(v->instance == x->cfg.self && v->world == x->cfg.world, DCP_E_INVALID_ARG,
+                "view of instance %d used on instance %d", v->instance, x->cfg.self);
+    q_route_put_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        x->dev, static_cast<const __nv_bfloat16*>(x->q_local), v->m_count_all, v->m_nrow);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
+    DCP_REQUIRE(x && v, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    lse_merge_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+}  // extern "C"

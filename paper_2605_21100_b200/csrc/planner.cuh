@@ -26,10 +26,10 @@
 
 #include <cstdint>
 
+#include "limits.cuh"
+
 namespace dcp {
 
-constexpr int PL_MAXW = 32;   // instances (one warp lane each)
-constexpr int PL_MAXK = 16;   // max CP degree (node size)
 constexpr int PL_THREADS = 512;
 
 enum : int32_t { PL_OK = 0, PL_E_FRAMES = -1, PL_E_UNKNOWN = -2, PL_E_ARENA = -11 };

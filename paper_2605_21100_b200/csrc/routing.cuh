@@ -39,6 +39,13 @@ struct RoutingOut {
     int32_t* block_table; // [W][capacity]
     uint8_t* page_fill;   // [W][capacity]
     int32_t* status;      // [1]
+    // exchange maps (K2/K3 destinations)
+    int32_t* slot_nrow;   // [S][W] row of a slot in instance s's N list
+    int32_t* slot_mrow;   // [S]    row of a slot in m_r's M list
+    int32_t* n_mrow;      // [W][S] for N row: row in m_r's M list
+    int32_t* m_nrow;      // [W][S][W] for M row: row in s' N list, -1 if s' not in P_r
+    int32_t* m_k;         // [W][S] |P_r|
+    int32_t* m_kv;        // [W][S][PL_MAXK] P_r in kv_binding order
 };
 
 __device__ __forceinline__ void bucket_shape_default_d(int m, int n, int32_t* out) {
@@ -111,6 +118,7 @@ __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, 
                 uint8_t* q = ro.q_route + r * W;
                 for (int c2 = 0; c2 < W; ++c2) q[c2] = (c2 == st.moe[sl]) ? 1 : 0;
                 ro.shard_len[r] = st.shard_tokens[(size_t)sl * W + s];
+                ro.slot_nrow[(size_t)sl * W + s] = row;
             }
             if (inM) {
                 const int row = mrow + __popc(bm & lt);
@@ -120,6 +128,7 @@ __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, 
                 uint8_t* q = ro.res_route + r * W;
                 for (int c2 = 0; c2 < W; ++c2) q[c2] = 0;
                 for (int m = 0; m < st.k[sl]; ++m) q[st.kv[sl * PL_MAXK + m]] = 1;
+                ro.slot_mrow[sl] = row;
             }
             nrow += __popc(bn);
             mrow += __popc(bm);
@@ -177,6 +186,23 @@ __global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerState st
         cu[j + 1] = (int32_t)run;
     }
     __syncthreads();
+    // (c0) exchange maps for this instance's N and M rows
+    for (int row = tid; row < rows; row += blockDim.x)
+        ro.n_mrow[(size_t)s * S + row] = ro.slot_mrow[ro.n_slot[(size_t)s * S + row]];
+    const int mrows = ro.m_count[s];
+    const int W = st.W;
+    for (int row = tid; row < mrows; row += blockDim.x) {
+        const int sl = ro.m_slot[(size_t)s * S + row];
+        const int k = st.k[sl];
+        ro.m_k[(size_t)s * S + row] = k;
+        int32_t* dst = ro.m_nrow + ((size_t)s * S + row) * W;
+        for (int c = 0; c < W; ++c) dst[c] = -1;
+        for (int m = 0; m < k; ++m) {
+            const int sp = st.kv[sl * PL_MAXK + m];
+            ro.m_kv[((size_t)s * S + row) * PL_MAXK + m] = sp;
+            dst[sp] = ro.slot_nrow[(size_t)sl * W + sp];
+        }
+    }
     // (c) scatter frames in logical page order
     int32_t* bt = ro.block_table + (size_t)s * st.capacity;
     uint8_t* pf = ro.page_fill + (size_t)s * st.capacity;

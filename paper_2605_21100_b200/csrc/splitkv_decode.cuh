@@ -30,6 +30,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "exchange.cuh"
 #include "ptx.cuh"
 
 namespace dcp {
@@ -47,7 +48,32 @@ struct AttnParams {
     int32_t* counters;           // [R]
     int32_t num_shards;
     float scale_log2;            // scale * log2(e)
+    // ---- routed mode (DCP exchange, exchange.cuh); all NULL for a local step
+    const XchgPeers* xp;         // peer pools; outputs go to m_r's result slot
+    const int32_t* n_mrow;       // [R] row of the shard's request in m_r's M list
+    const int32_t* n_moe;        // [R] m_r
+    const uint32_t* q_flag;      // [R] Q-route arrival flags (wait == *xp->epoch)
+    const int32_t* num_shards_ptr;  // device-resident R (graph replay); overrides num_shards
 };
+
+// Destination of shard r's normalised partial O / LSE: local [R][HQ][D] for a
+// local step, else m_r's result pool slot [mrow][self] (Res-route put, fused).
+__device__ __forceinline__ float* row_out(const AttnParams& p, int r, int HQ, int D) {
+    if (!p.xp) return p.out + (size_t)r * HQ * D;
+    const XchgPeers& x = *p.xp;
+    return x.res_o[p.n_moe[r]] + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ * D;
+}
+__device__ __forceinline__ float* row_lse(const AttnParams& p, int r, int HQ) {
+    if (!p.xp) return p.lse + (size_t)r * HQ;
+    const XchgPeers& x = *p.xp;
+    return x.res_lse[p.n_moe[r]] + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ;
+}
+// Called by thread 0 after a consumer barrier: every warp's stores of row r
+// happen-before this system-scope release.
+__device__ __forceinline__ void publish_row(const AttnParams& p, int r) {
+    const XchgPeers& x = *p.xp;
+    st_release_sys(x.res_flag[p.n_moe[r]] + (size_t)p.n_mrow[r] * x.W + x.self, *x.epoch);
+}
 
 template <int HKV, int G>
 struct DecodeCfg {
@@ -91,7 +117,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int R = p.num_shards;
+    const int R = p.num_shards_ptr ? *p.num_shards_ptr : p.num_shards;
     const int64_t P = p.cu_pages[R];
     const int64_t grid = gridDim.x;
     const int cta = blockIdx.x;
@@ -149,10 +175,16 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
     // Zero-token shards: O = 0, LSE = -inf (weight 0 in any merge).
     for (int r = cta; r < R; r += gridDim.x) {
         if (p.cu_pages[r + 1] == p.cu_pages[r]) {
+            float* ob = row_out(p, r, C::HQ, C::D);
+            float* lb = row_lse(p, r, C::HQ);
             for (int row = 0; row < G; ++row) {
-                float* o = p.out + (static_cast<size_t>(r) * C::HQ + h * G + row) * C::D;
+                float* o = ob + (h * G + row) * C::D;
                 reinterpret_cast<float4*>(o)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (lane == 0) p.lse[static_cast<size_t>(r) * C::HQ + h * G + row] = -INFINITY;
+                if (lane == 0) lb[h * G + row] = -INFINITY;
+            }
+            if (p.xp) {
+                named_bar_sync(1, NCT);
+                if (threadIdx.x == 0) publish_row(p, r);
             }
         }
     }
@@ -207,6 +239,10 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
         const int64_t len = p.shard_len[r];
 
         // Q fragments (A operand, rows = q-heads of this kv group).
+        if (p.q_flag) {  // routed: wait for the Q-route put of this row
+            if (lane == 0) wait_flag(p.q_flag + r, *p.xp->epoch);
+            __syncwarp();
+        }
         uint32_t qa[8][4];
         {
             const __nv_bfloat16* q0 =
@@ -214,12 +250,12 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
             const __nv_bfloat16* q1 = q0 + 8 * C::D;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
-                qa[ks][0] = row0_real ? __ldg(reinterpret_cast<const uint32_t*>(q0 + 16 * ks)) : 0u;
+                qa[ks][0] = row0_real ? __ldcg(reinterpret_cast<const uint32_t*>(q0 + 16 * ks)) : 0u;
                 qa[ks][2] =
-                    row0_real ? __ldg(reinterpret_cast<const uint32_t*>(q0 + 16 * ks + 8)) : 0u;
-                qa[ks][1] = row1_real ? __ldg(reinterpret_cast<const uint32_t*>(q1 + 16 * ks)) : 0u;
+                    row0_real ? __ldcg(reinterpret_cast<const uint32_t*>(q0 + 16 * ks + 8)) : 0u;
+                qa[ks][1] = row1_real ? __ldcg(reinterpret_cast<const uint32_t*>(q1 + 16 * ks)) : 0u;
                 qa[ks][3] =
-                    row1_real ? __ldg(reinterpret_cast<const uint32_t*>(q1 + 16 * ks + 8)) : 0u;
+                    row1_real ? __ldcg(reinterpret_cast<const uint32_t*>(q1 + 16 * ks + 8)) : 0u;
             }
         }
 
@@ -346,12 +382,16 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                 const float l = half == 0 ? l0 : l1;
                 const float m = half == 0 ? m0 : m1;
                 const float inv = 1.f / l;
-                float* o = p.out + (static_cast<size_t>(r) * C::HQ + qh) * C::D + 2 * t;
+                float* o = row_out(p, r, C::HQ, C::D) + qh * C::D + 2 * t;
 #pragma unroll
                 for (int nt = 0; nt < 16; ++nt)
                     *reinterpret_cast<float2*>(o + nt * 8) =
                         make_float2(acc[nt][2 * half] * inv, acc[nt][2 * half + 1] * inv);
-                if (t == 0) p.lse[static_cast<size_t>(r) * C::HQ + qh] = (m + __log2f(l)) * ln2;
+                if (t == 0) row_lse(p, r, C::HQ)[qh] = (m + __log2f(l)) * ln2;
+            }
+            if (p.xp) {
+                named_bar_sync(1, NCT);
+                if (threadIdx.x == 0) publish_row(p, r);
             }
         } else {
             const int slot = 2 * cta + (seg_begin == p_begin ? 0 : 1);
@@ -416,12 +456,16 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                         num.w += w * v.w;
                     }
                     const float inv = 1.f / den;
-                    float* o = p.out + (static_cast<size_t>(r) * C::HQ + qh) * C::D;
+                    float* o = row_out(p, r, C::HQ, C::D) + qh * C::D;
                     reinterpret_cast<float4*>(o)[lane] =
                         make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
-                    if (lane == 0) p.lse[static_cast<size_t>(r) * C::HQ + qh] = (mmax + __log2f(den)) * ln2;
+                    if (lane == 0) row_lse(p, r, C::HQ)[qh] = (mmax + __log2f(den)) * ln2;
                 }
                 if (threadIdx.x == 0) p.counters[r] = 0;  // re-arm for the next launch / graph replay
+                if (p.xp) {
+                    named_bar_sync(2, NCT);
+                    if (threadIdx.x == 0) publish_row(p, r);
+                }
             }
         }
         ++r;

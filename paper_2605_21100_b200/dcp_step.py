@@ -1,0 +1,138 @@
+"""One DCP decode-attention step across W instances (Fig. 7).
+
+    planner (K6) -> routing / block tables (K7) -> per instance:
+        Q-route puts (K2) -> split-KV attention with fused Res-route puts (K1)
+        -> LSE merge at the MoE binding (K3)
+
+An instance is one KV/MoE binding target (one GPU in production).  This
+driver can host all W instances in one process — on distinct GPUs, or all on
+one GPU for testing, where the "peer" stores are local stores through the
+identical code path.  Multi-process deployments (one rank per GPU) use
+DcpInstance with CUDA-IPC peer handles instead (see bench_dcp.py).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _capi
+from .attention import DcpContext
+
+
+class DcpInstance:
+    """Exchange pools + KV pool + attention workspace of one instance."""
+
+    def __init__(self, ctx: DcpContext, world: int, self_id: int, hq: int, hkv: int, capacity_pages: int,
+                 head_dim: int = 128, page_size: int = 16, n_max: int = 512, m_max: int = 256,
+                 kv_pool: torch.Tensor | None = None):
+        L = _capi.lib()
+        self.ctx, self.world, self.id = ctx, world, self_id
+        self.hq, self.hkv, self.d, self.page = hq, hkv, head_dim, page_size
+        self.n_max, self.m_max = n_max, m_max
+        cfg = _capi.XchgConfig(world, self_id, hq, head_dim, n_max, m_max)
+        h = ctypes.c_void_p()
+        _capi.check(L.dcp_xchg_create(ctx.handle, ctypes.byref(cfg), ctypes.byref(h)))
+        self.x = h
+        dev = torch.device("cuda", ctx.device)
+        self.kv_pool = kv_pool if kv_pool is not None else torch.zeros(
+            max(capacity_pages, 1), 2, hkv, page_size, head_dim, dtype=torch.bfloat16, device=dev)
+        nbytes = L.dcp_attn_workspace_bytes(ctx.handle, n_max, hq, head_dim)
+        self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        ql, qr, out, lse = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _capi.check(L.dcp_xchg_buffers(h, ctypes.byref(ql), ctypes.byref(qr), ctypes.byref(out),
+                                       ctypes.byref(lse)))
+        self.q_local_ptr, self.out_ptr, self.lse_ptr = ql.value, out.value, lse.value
+        self.args = _capi.AttnArgs()
+        a = self.args
+        a.num_q_heads, a.num_kv_heads, a.head_dim, a.page_size = hq, hkv, head_dim, page_size
+        a.num_frames = self.kv_pool.shape[0]
+        a.kv_pool = self.kv_pool.data_ptr()
+        a.scale = 1.0 / math.sqrt(head_dim)
+        a.workspace, a.workspace_bytes = self.workspace.data_ptr(), self.workspace.numel()
+
+    def ipc_handle(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _capi.check(_capi.lib().dcp_xchg_ipc_handle(self.x, buf))
+        return buf.raw
+
+    def open_peer(self, peer: int, handle: bytes):
+        _capi.check(_capi.lib().dcp_xchg_open_peer_ipc(self.x, peer, ctypes.create_string_buffer(handle, 64)))
+
+    def set_peer_local(self, peer: int, other: "DcpInstance"):
+        _capi.check(_capi.lib().dcp_xchg_set_peer_local(self.x, peer, other.x))
+
+    def commit(self):
+        _capi.check(_capi.lib().dcp_xchg_commit(self.x))
+
+    # ---- per step ------------------------------------------------------------
+    def write_queries(self, q_rows: torch.Tensor, stream=None):
+        """q_rows: bf16 [M, hq, d] in this instance's M-row order."""
+        s = (stream or torch.cuda.current_stream(self.ctx.device)).cuda_stream
+        q_rows = q_rows.contiguous()
+        self._q_keep = q_rows
+        _capi.check(_capi.lib().dcp_xchg_write_queries(self.x, ctypes.c_void_p(q_rows.data_ptr()),
+                                                       q_rows.shape[0], ctypes.c_void_p(s)))
+
+    def run(self, view: _capi.InstanceView, stream=None, phase: str = "all"):
+        L = _capi.lib()
+        s = ctypes.c_void_p((stream or torch.cuda.current_stream(self.ctx.device)).cuda_stream)
+        if phase in ("all", "q"):
+            _capi.check(L.dcp_xchg_begin_step(self.x, s))
+            _capi.check(L.dcp_route_q(self.x, ctypes.byref(view), s))
+        if phase in ("all", "attn"):
+            _capi.check(L.dcp_decode_attn_routed(self.ctx.handle, self.x, ctypes.byref(view),
+                                                 ctypes.byref(self.args), s))
+        if phase in ("all", "merge"):
+            _capi.check(L.dcp_merge_partials(self.x, ctypes.byref(view), s))
+
+    def results(self, m_rows: int):
+        out = _capi.device_to_numpy(self.out_ptr, m_rows * self.hq * self.d, np.float32)
+        lse = _capi.device_to_numpy(self.lse_ptr, m_rows * self.hq, np.float32)
+        return out.reshape(m_rows, self.hq, self.d), lse.reshape(m_rows, self.hq)
+
+    def close(self):
+        if getattr(self, "x", None):
+            _capi.lib().dcp_xchg_destroy(self.x)
+            self.x = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def run_local_step(planner, instances, q_of_request: dict, stream=None):
+    """Run one routed step with all instances in this process.
+
+    q_of_request: request id -> bf16 [hq, d] CUDA tensor (on instance m_r's device).
+    Returns {request id: (O [hq, d] float32, LSE [hq])} read at each MoE binding.
+    """
+    planner.build_routing()
+    W = len(instances)
+    views = [planner.instance_view(s) for s in range(W)]
+    m_ids = []
+    for s, inst in enumerate(instances):
+        v = views[s]
+        ids = _capi.device_to_numpy(v.m_ids, v.m_rows, np.int64).tolist()
+        m_ids.append(ids)
+        if ids:
+            q = torch.stack([q_of_request[i] for i in ids]).contiguous()
+            inst.write_queries(q, stream)
+    # phase order keeps a single GPU free of cross-kernel spin dependencies
+    for s, inst in enumerate(instances):
+        inst.run(views[s], stream, "q")
+    for s, inst in enumerate(instances):
+        inst.run(views[s], stream, "attn")
+    for s, inst in enumerate(instances):
+        inst.run(views[s], stream, "merge")
+    torch.cuda.synchronize()
+    res = {}
+    for s, inst in enumerate(instances):
+        o, l = inst.results(len(m_ids[s]))
+        for j, rid in enumerate(m_ids[s]):
+            res[rid] = (o[j], l[j])
+    return res, views
