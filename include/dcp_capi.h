@@ -263,6 +263,60 @@ DCP_API int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance
                                    const dcp_attn_args* a, void* stream);
 DCP_API int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream);
 
+/* ---- entry points backing the dcpsim C++ drop-in (include/dcpsim/) ---------- */
+/* Replace the active policy (SchedulerPolicy, scheduler.hpp:31-39).  The
+ * UniformCP round-robin counters reset when the group count changes, as
+ * ucp_round_robin_.assign does (scheduler.cpp:195-196). */
+DCP_API int dcp_planner_set_policy(dcp_planner* pl, int32_t policy, int32_t n_bucket,
+                                   const int64_t* bucket_len, const int32_t* bucket_deg,
+                                   int32_t uniform_degree, int32_t hol_strict);
+/* Make the device waiting queue exactly `ids` (FIFO order).  Unknown ids are
+ * admitted as new waiting requests with seq_lens[i]; known ids must be waiting.
+ * Waiting requests not listed are dropped. */
+DCP_API int dcp_planner_set_queue(dcp_planner* pl, const int64_t* ids, const int64_t* seq_lens,
+                                  int32_t n);
+/* GlobalPageTable::allocate with a caller-supplied placement
+ * (page_table.cpp:9-49): InsufficientFrames(-1) leaves no partial state. */
+DCP_API int dcp_planner_allocate(dcp_planner* pl, int64_t id, int64_t seq_len, int32_t cp_degree,
+                                 const int32_t* kv_binding, const int64_t* split, int32_t moe_binding);
+/* Page list of one tracked request (logical order); returns the page count. */
+DCP_API int64_t dcp_planner_pages(dcp_planner* pl, int64_t id, int32_t* instance, int32_t* frame,
+                                  int64_t cap);
+/* moe_binding of every active request (ids and bindings, any order); returns count. */
+DCP_API int32_t dcp_planner_active_moe(dcp_planner* pl, int64_t* ids, int32_t* moe, int32_t cap);
+/* rebalance_active over an explicit active list (scheduler.cpp:43-64). */
+DCP_API int dcp_planner_rebalance(dcp_planner* pl, const int64_t* ids, int32_t n);
+/* Upload host instance state (kv_load, moe_batch, shard_count, LIFO stacks:
+ * stacks[s*capacity .. + nfree[s]), bottom first) into an idle planner. */
+DCP_API int dcp_planner_load_instances(dcp_planner* pl, const int64_t* kv_load,
+                                       const int32_t* moe_batch, const int32_t* shard_count,
+                                       const int64_t* nfree, const int32_t* stacks);
+/* water_fill (scheduler.cpp:70-102) on the device; n <= 32 participants. */
+DCP_API int dcp_water_fill(dcp_ctx* ctx, int32_t n, const int64_t* kv_loads, int64_t seq_len,
+                           int64_t* split);
+/* build_binding_config (routing.cpp:9-32) on the device for explicit placements
+ * (host arrays; kv_binding flattened [n][16]).  Per instance s, n_rows[s*n ..]
+ * and m_rows[s*n ..] receive the input indices of its N and M lists (id order). */
+DCP_API int dcp_binding_config(dcp_ctx* ctx, int32_t n, const int64_t* ids, const int32_t* cp_degree,
+                               const int32_t* moe_binding, const int32_t* kv_binding, int32_t world,
+                               int32_t* n_count, int32_t* m_count, int32_t* n_rows, int32_t* m_rows);
+/* derive_routing_tables (routing.cpp:34-63) expansion on the device: q bits
+ * one-hot at shard_moe[r]; res bits at the set bits of res_mask[r]. */
+DCP_API int dcp_route_tables(dcp_ctx* ctx, int32_t world, int32_t n_rows, const int32_t* shard_moe,
+                             int32_t m_rows, const uint32_t* res_mask, uint8_t* q_bits,
+                             uint8_t* res_bits);
+/* shard_attention<T> (attn_merge.hpp:53-82) for a batch of items on the
+ * device; dtype_bytes 4 (float) or 8 (double); device pointers. */
+DCP_API int dcp_shard_attention_batch(dcp_ctx* ctx, int32_t dtype_bytes, int32_t n_items,
+                                      int32_t head_dim, double scale, const void* q,
+                                      const void* keys, const void* values, const int64_t* q_off,
+                                      const int64_t* kv_off, const int64_t* len, void* out,
+                                      void* lse, void* stream);
+/* lse_merge<T> (attn_merge.hpp:86-100) per group of partials; device pointers. */
+DCP_API int dcp_lse_merge_batch(dcp_ctx* ctx, int32_t dtype_bytes, int32_t n_groups,
+                                int32_t head_dim, const int64_t* group_off, const void* outs,
+                                const void* lses, void* merged, void* merged_lse, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

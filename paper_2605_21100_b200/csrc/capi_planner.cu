@@ -9,6 +9,7 @@
 #include "capi_common.cuh"
 #include "planner.cuh"
 #include "routing.cuh"
+#include "planner_internal.cuh"
 
 using namespace dcp;
 
@@ -57,39 +58,6 @@ int64_t pages_for_h(int64_t t, int64_t p) { return (t + p - 1) / p; }
 
 }  // namespace
 
-struct dcp_planner {
-    dcp_ctx* ctx = nullptr;
-    dcp_planner_config cfg{};
-    PlannerState st{};
-    RoutingOut ro{};
-    std::vector<void*> owned;
-    int32_t* arena2_inst = nullptr;
-    int32_t* arena2_frame = nullptr;
-    uint8_t* arena2_fill = nullptr;
-    int64_t* d_new_off = nullptr;
-    int32_t* d_io_slots = nullptr;   // staging
-    int64_t* d_io_ids = nullptr;
-    int64_t* d_io_lens = nullptr;
-    int32_t* d_io_out = nullptr;
-    std::unordered_map<int64_t, int32_t> slot_of;
-    std::vector<int32_t> free_slots;
-    std::vector<int64_t> id_of_slot;
-    int64_t arena_top_host = 0;      // upper bound between syncs
-    int64_t waiting_pages_bound = 0; // sum over queued requests of their max arena demand
-    std::vector<int64_t> queued_len; // per slot (for the bound)
-    int32_t queued = 0;
-    struct Retired {
-        int32_t k, moe;
-        int32_t kv[PL_MAXK];
-        int64_t split[PL_MAXK];
-    };
-    // Finished requests keep their Placement (Request::placement is not cleared
-    // by pt_free, page_table.cpp:51-66), so placement queries still answer.
-    std::unordered_map<int64_t, Retired> retired;
-    cudaStream_t stream = nullptr;
-    int last_launches = 0;
-    bool routing_valid = false;
-};
 
 namespace {
 
@@ -114,6 +82,11 @@ int compact_arena(dcp_planner* pl) {
 void set_stream(dcp_planner* pl, void* s) { pl->stream = static_cast<cudaStream_t>(s); }
 
 }  // namespace
+
+namespace dcp {
+int planner_sync_arena_top(dcp_planner* pl) { return sync_arena_top(pl); }
+int planner_compact(dcp_planner* pl) { return compact_arena(pl); }
+}  // namespace dcp
 
 extern "C" {
 

@@ -5,11 +5,11 @@
 
 namespace dcp {
 
-__global__ void epoch_bump_kernel(uint32_t* epoch) { *epoch += 1; }
+static __global__ void epoch_bump_kernel(uint32_t* epoch) { *epoch += 1; }
 
 // K2: grid = m_max (graph-stable), block = 128.  q_local: [m_max][hq][d] bf16
 // in M-row order; m_nrow: [M][W] destination rows (-1 = not in P_r).
-__global__ void __launch_bounds__(128) q_route_put_kernel(const XchgPeers* __restrict__ xp,
+static __global__ void __launch_bounds__(128) q_route_put_kernel(const XchgPeers* __restrict__ xp,
                                                           const __nv_bfloat16* __restrict__ q_local,
                                                           const int32_t* __restrict__ m_count,
                                                           const int32_t* __restrict__ m_nrow) {
@@ -32,7 +32,7 @@ __global__ void __launch_bounds__(128) q_route_put_kernel(const XchgPeers* __res
 
 // K3 merge: grid = m_max, block = 128.  m_k / m_kv: P_r of each M row in
 // kv_binding order.  out: [m_max][hq][d] fp32, out_lse: [m_max][hq].
-__global__ void __launch_bounds__(128) lse_merge_kernel(const XchgPeers* __restrict__ xp,
+static __global__ void __launch_bounds__(128) lse_merge_kernel(const XchgPeers* __restrict__ xp,
                                                         const int32_t* __restrict__ m_count,
                                                         const int32_t* __restrict__ m_k,
                                                         const int32_t* __restrict__ m_kv,

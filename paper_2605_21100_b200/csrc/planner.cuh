@@ -159,7 +159,7 @@ __device__ __forceinline__ int64_t warp_water_fill(int lane, int n, int64_t len,
 }
 
 // Placement decision for one request (warp 0).  Writes *pl.
-__device__ void place_request(const PlannerState& st, const SmemInst& si, SmemPlace& pl, int lane,
+static __device__ void place_request(const PlannerState& st, const SmemInst& si, SmemPlace& pl, int lane,
                               int64_t L) {
     const int W = st.W, ipn = st.ipn;
     if (st.kind == KIND_DCP) {
@@ -272,7 +272,7 @@ __device__ __forceinline__ bool never_fits_d(const PlannerState& st, int64_t L) 
 
 // ------------------------------------------------------------------ single-CTA bitonic sort
 // Sorts n (<= sort_cap, padded to pow2 internally) entries by (k1, k2) ascending.
-__device__ void cta_bitonic_sort(int64_t* k1, int64_t* k2, int32_t* val, int n) {
+static __device__ void cta_bitonic_sort(int64_t* k1, int64_t* k2, int32_t* val, int n) {
     int np2 = 1;
     while (np2 < n) np2 <<= 1;
     for (int i = n + threadIdx.x; i < np2; i += blockDim.x) {
@@ -299,8 +299,59 @@ __device__ void cta_bitonic_sort(int64_t* k1, int64_t* k2, int32_t* val, int n) 
     }
 }
 
+// rebalance_active (scheduler.cpp:43-64) on the shared-memory B (already
+// zeroed): the given slots, or every ACTIVE slot when slots == nullptr.
+// (cp_degree, id) order: CP=1 first (m_r pinned, parallel histogram), then the
+// CP>=2 requests sequentially with a warp argmin over P_r.
+static __device__ void rebalance_core(const PlannerState& st, SmemInst& si, int32_t& s_n2, const int32_t* slots,
+                               int n) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int S = st.max_slots;
+    const int lim = slots ? n : S;
+    for (int j = tid; j < lim; j += blockDim.x) {
+        const int sl = slots ? slots[j] : j;
+        if (!slots && st.state[sl] != ST_ACTIVE) continue;
+        if (st.k[sl] == 1) {
+            const int s = st.kv[sl * PL_MAXK];
+            st.moe[sl] = s;
+            atomicAdd(&si.B[s], 1);
+        } else {
+            const int i = atomicAdd(&s_n2, 1);
+            st.sk1[i] = st.k[sl];
+            st.sk2[i] = st.id[sl];
+            st.sval[i] = sl;
+        }
+    }
+    __syncthreads();
+    const int n2 = s_n2;
+    if (n2 > 1) cta_bitonic_sort(st.sk1, st.sk2, st.sval, n2);
+    __syncthreads();
+    if (warp == 0) {
+        for (int i = 0; i < n2; ++i) {
+            const int sl = st.sval[i];
+            const int kk = st.k[sl];
+            const int s = lane < kk ? st.kv[sl * PL_MAXK + lane] : 0x7fffffff;
+            int64_t bv = lane < kk ? (int64_t)si.B[s] : INT64_MAX;
+            int bs = s;
+            // argmin over P_r of B, ties to the lowest instance id (cpp:54-59)
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+                if (ov < bv || (ov == bv && os < bs)) { bv = ov; bs = os; }
+            }
+            if (lane == 0) {
+                st.moe[sl] = bs;
+                si.B[bs] += 1;
+            }
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+}
+
 // ------------------------------------------------------------------ K6 step
-__global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(PlannerState st) {
+static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(PlannerState st) {
     __shared__ SmemInst si;
     __shared__ SmemPlace pl;
     __shared__ int32_t s_n2;
@@ -329,45 +380,7 @@ __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(PlannerStat
 
     // ---- Alg. 1 line 1: recompute B (scheduler.cpp:250-261) ----
     if (st.kind == KIND_DCP) {
-        for (int sl = tid; sl < S; sl += blockDim.x) {
-            if (st.state[sl] != ST_ACTIVE) continue;
-            if (st.k[sl] == 1) {
-                const int s = st.kv[sl * PL_MAXK];
-                st.moe[sl] = s;
-                atomicAdd(&si.B[s], 1);
-            } else {
-                const int i = atomicAdd(&s_n2, 1);
-                st.sk1[i] = st.k[sl];
-                st.sk2[i] = st.id[sl];
-                st.sval[i] = sl;
-            }
-        }
-        __syncthreads();
-        const int n2 = s_n2;
-        if (n2 > 1) cta_bitonic_sort(st.sk1, st.sk2, st.sval, n2);
-        __syncthreads();
-        if (warp == 0) {
-            for (int i = 0; i < n2; ++i) {
-                const int sl = st.sval[i];
-                const int kk = st.k[sl];
-                const int s = lane < kk ? st.kv[sl * PL_MAXK + lane] : 0x7fffffff;
-                const int64_t b = lane < kk ? (int64_t)si.B[s] : INT64_MAX;
-                // argmin over P_r of B, ties to the lowest instance id (cpp:54-59)
-                int64_t bv = b;
-                int bs = s;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                    const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-                    if (ov < bv || (ov == bv && os < bs)) { bv = ov; bs = os; }
-                }
-                if (lane == 0) {
-                    st.moe[sl] = bs;
-                    si.B[bs] += 1;
-                }
-                __syncwarp();
-            }
-        }
+        rebalance_core(st, si, s_n2, nullptr, 0);
     } else {
         for (int sl = tid; sl < S; sl += blockDim.x)
             if (st.state[sl] == ST_ACTIVE) atomicAdd(&si.B[st.moe[sl]], 1);
@@ -504,7 +517,7 @@ __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(PlannerStat
 // order, K_s -= shard tokens.  Requests are released sequentially in the given
 // order (the LIFO contents depend on it); each request's pages are pushed in
 // parallel with per-instance stable ranks.
-__global__ void __launch_bounds__(PL_THREADS, 1)
+static __global__ void __launch_bounds__(PL_THREADS, 1)
     planner_release_kernel(PlannerState st, const int32_t* slots, int n) {
     __shared__ int32_t cnt[PL_THREADS / 32][PL_MAXW];
     __shared__ int64_t base[PL_MAXW];
@@ -558,7 +571,7 @@ __global__ void __launch_bounds__(PL_THREADS, 1)
 // batch (frames popped depend on order).  out_inst[q] = receiving instance or
 // -1 (growth stall).  Stops with PL_E_ARENA at the first request whose page
 // segment must grow past the arena; res_counts[0] = processed count.
-__global__ void planner_append_kernel(PlannerState st, const int32_t* slots, int n,
+static __global__ void planner_append_kernel(PlannerState st, const int32_t* slots, int n,
                                       int32_t* out_inst) {
     const int lane = threadIdx.x & 31;
     const int W = st.W;
@@ -639,7 +652,7 @@ __global__ void planner_append_kernel(PlannerState st, const int32_t* slots, int
 
 // ------------------------------------------------------------------ arena compaction
 // Moves every live page segment (ACTIVE slots) to a fresh arena, packed in slot order.
-__global__ void planner_compact_offsets(PlannerState st, int64_t* new_off) {
+static __global__ void planner_compact_offsets(PlannerState st, int64_t* new_off) {
     __shared__ int64_t part[1024];
     const int tid = threadIdx.x;
     const int S = st.max_slots;
@@ -666,7 +679,7 @@ __global__ void planner_compact_offsets(PlannerState st, int64_t* new_off) {
     }
 }
 
-__global__ void planner_compact_copy(PlannerState st, const int64_t* new_off, int32_t* inst2,
+static __global__ void planner_compact_copy(PlannerState st, const int64_t* new_off, int32_t* inst2,
                                      int32_t* frame2, uint8_t* fill2) {
     const int sl = blockIdx.x;
     if (st.state[sl] != ST_ACTIVE) return;
@@ -678,6 +691,93 @@ __global__ void planner_compact_copy(PlannerState st, const int64_t* new_off, in
     }
     __syncthreads();
     if (threadIdx.x == 0) st.page_off[sl] = noff;
+}
+
+
+// ------------------------------------------------------------------ standalone entry kernels
+// rebalance_active over an explicit active list (scheduler.cpp:43-64): B is
+// reset for every instance, then recomputed from the list only.
+static __global__ void __launch_bounds__(PL_THREADS, 1)
+    planner_rebalance_kernel(PlannerState st, const int32_t* slots, int n) {
+    __shared__ SmemInst si;
+    __shared__ int32_t s_n2;
+    if (threadIdx.x < st.W) si.B[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_n2 = 0;
+    __syncthreads();
+    rebalance_core(st, si, s_n2, slots, n);
+    if (threadIdx.x < st.W) st.moe_batch[threadIdx.x] = si.B[threadIdx.x];
+}
+
+// GlobalPageTable::allocate with a caller-supplied placement (page_table.cpp:9-49):
+// feasibility first (no partial state on failure), then LIFO pops in
+// kv_binding order.  Does not touch B_s / R_i (those belong to Scheduler::step).
+static __global__ void __launch_bounds__(PL_THREADS, 1)
+    planner_allocate_kernel(PlannerState st, int sl, int k, const int32_t* kv, const int64_t* split, int moe) {
+    __shared__ int64_t need_off[PL_MAXK + 1];
+    __shared__ int32_t ok;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        need_off[0] = 0;
+        ok = st.seq_len[sl] >= 1;
+        for (int m = 0; m < k; ++m) {
+            const int64_t need = pages_for_d(split[m], st.page);
+            if (st.nfree[kv[m]] < need) ok = 0;
+            need_off[m + 1] = need_off[m] + need;
+        }
+        if (*st.arena_top + need_off[k] + st.reserve_pages > st.arena_cap) ok = -1;
+    }
+    __syncthreads();
+    if (ok != 1) {
+        if (tid == 0) st.res_counts[3] = ok == 0 ? PL_E_FRAMES : PL_E_ARENA;
+        return;
+    }
+    const int64_t np = need_off[k];
+    const int64_t off = *st.arena_top;
+    for (int64_t t = tid; t < np; t += blockDim.x) {
+        int m = 0;
+        while (need_off[m + 1] <= t) ++m;
+        const int s = kv[m];
+        const int64_t j = t - need_off[m];
+        st.pg_inst[off + t] = s;
+        st.pg_frame[off + t] = st.stack[(int64_t)s * st.capacity + st.nfree[s] - 1 - j];
+        const int64_t rem = split[m] - j * st.page;
+        st.pg_fill[off + t] = (uint8_t)(rem < st.page ? rem : st.page);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const int W = st.W;
+        for (int s = 0; s < W; ++s) st.shard_tokens[(int64_t)sl * W + s] = 0;
+        int64_t trailing = 0;
+        for (int m = 0; m < k; ++m) {
+            const int s = kv[m];
+            st.nfree[s] -= need_off[m + 1] - need_off[m];
+            st.kv_load[s] += split[m];
+            st.shard_tokens[(int64_t)sl * W + s] += split[m];
+            st.kv[sl * PL_MAXK + m] = s;
+            st.split[sl * PL_MAXK + m] = split[m];
+            if (split[m] > 0) {
+                const int64_t r = split[m] % st.page;
+                trailing = r == 0 ? st.page : r;
+            }
+        }
+        st.k[sl] = k;
+        st.moe[sl] = moe;
+        st.state[sl] = ST_ACTIVE;
+        st.page_off[sl] = off;
+        st.page_cnt[sl] = (int32_t)np;
+        st.page_cap[sl] = (int32_t)(np + st.reserve_pages);
+        st.trailing_fill[sl] = trailing;
+        *st.arena_top = off + np + st.reserve_pages;
+        st.res_counts[3] = PL_OK;
+    }
+}
+
+// water_fill (scheduler.cpp:70-102) for one participant list, one warp.
+static __global__ void water_fill_kernel(int n, const int64_t* loads, int64_t len, int64_t* split) {
+    const int lane = threadIdx.x & 31;
+    const int64_t K = lane < n ? loads[lane] : 0;
+    const int64_t s = warp_water_fill(lane, n, len, K);
+    if (lane < n) split[lane] = s;
 }
 
 }  // namespace dcp

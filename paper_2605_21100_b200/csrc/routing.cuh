@@ -66,7 +66,7 @@ __device__ __forceinline__ void bucket_shape_default_d(int m, int n, int32_t* ou
     out[1] = 512;
 }
 
-__global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, RoutingOut ro) {
+static __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, RoutingOut ro) {
     __shared__ int32_t s_n;
     __shared__ int32_t s_bad;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, 
 }
 
 // One CTA per instance: block table + fill + cu_pages for its N rows.
-__global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerState st, RoutingOut ro) {
+static __global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerState st, RoutingOut ro) {
     __shared__ int64_t part[1024];
     const int s = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

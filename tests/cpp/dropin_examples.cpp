@@ -1,0 +1,216 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// SPEC known-answer examples through the dcpsim drop-in C++ API (device
+// backed).  Prints "OK <name>" per check, "FAIL <name> ..." otherwise.
+#include <cmath>
+#include <iostream>
+#include <limits>
+#include <random>
+#include <vector>
+
+#include "dcpsim/attn_merge.hpp"
+#include "dcpsim/page_table.hpp"
+#include "dcpsim/routing.hpp"
+#include "dcpsim/scheduler.hpp"
+
+using namespace dcpsim;
+
+static int fails = 0;
+#define CHECK(name, cond)                                   \
+    do {                                                    \
+        if (cond) std::cout << "OK " << name << "\n";       \
+        else { std::cout << "FAIL " << name << "\n"; ++fails; } \
+    } while (0)
+
+int main() {
+    // water_fill (scheduler.cpp:94-100)
+    {
+        std::vector<InstanceId> p2{0, 1}, p3{0, 1, 2};
+        std::vector<Tokens> k1{10, 30}, k2{0, 0, 50}, k3{5, 5, 5}, k4{50, 0};
+        CHECK("water_fill_10_30", (water_fill(p2, 40, k1) == std::vector<Tokens>{30, 10}));
+        CHECK("water_fill_0_0_50", (water_fill(p3, 60, k2) == std::vector<Tokens>{30, 30, 0}));
+        CHECK("water_fill_5_5_5", (water_fill(p3, 10, k3) == std::vector<Tokens>{4, 3, 3}));
+        CHECK("water_fill_50_0", (water_fill(p2, 10, k4) == std::vector<Tokens>{0, 10}));
+    }
+    // cp_degree
+    {
+        auto b = BucketFn::default_table();
+        CHECK("cp_degree", cp_degree(2048, b, 8) == 1 && cp_degree(524288, b, 8) == 8 && cp_degree(524288, b, 4) == 4 &&
+                               cp_degree(131072, b, 8) == 2 && cp_degree(131073, b, 8) == 4);
+    }
+    // page table l=40 split {A:30,B:10}
+    {
+        ClusterTopology t;
+        t.nodes = 1;
+        t.instances_per_node = 2;
+        auto c = make_cluster(t, 8);
+        Request r;
+        r.id = 7;
+        r.seq_len = 40;
+        Placement p;
+        p.kv_binding = {0, 1};
+        p.split = {30, 10};
+        p.moe_binding = 0;
+        const auto& pages = pt_allocate(r, p, c);
+        CHECK("pt_allocate_layout", pages.size() == 3 && pages[0].instance == 0 && pages[1].instance == 0 &&
+                                        pages[2].instance == 1 && pages[0].frame == 0 && pages[1].frame == 1 &&
+                                        pages[2].frame == 0);
+        CHECK("pt_lookup", pt_lookup(c, 7, 2).instance == 1);
+        bool threw = false;
+        try {
+            pt_lookup(c, 7, 3);
+        } catch (const UnknownPage&) {
+            threw = true;
+        }
+        CHECK("pt_lookup_out_of_range", threw);
+        CHECK("kv_load", c.instances[0].kv_load == 30 && c.instances[1].kv_load == 10);
+        auto rel = pt_free(7, c);
+        CHECK("pt_free_counts", rel.size() == 2 && rel[0].second == 2 && rel[1].second == 1);
+        threw = false;
+        try {
+            pt_free(7, c);
+        } catch (const UnknownRequest&) {
+            threw = true;
+        }
+        CHECK("double_free", threw);
+        // frames return in page order: the next allocation reuses them LIFO
+        Request r2;
+        r2.id = 8;
+        r2.seq_len = 16;
+        Placement p2;
+        p2.kv_binding = {0};
+        p2.split = {16};
+        p2.moe_binding = 0;
+        CHECK("lifo_reuse", pt_allocate(r2, p2, c)[0].frame == 1);
+        Request big;
+        big.id = 9;
+        big.seq_len = 1000;
+        Placement pb;
+        pb.kv_binding = {1};
+        pb.split = {1000};
+        pb.moe_binding = 1;
+        threw = false;
+        try {
+            pt_allocate(big, pb, c);
+        } catch (const InsufficientFrames&) {
+            threw = true;
+        }
+        CHECK("insufficient_frames", threw && c.instances[1].free_frames.size() == 8);
+    }
+    // rebalance_active: X(P={2}), Y(P={1,2}), Z(P={1,2,3}) -> X->2, Y->1, Z->3
+    {
+        ClusterTopology t;
+        t.nodes = 1;
+        t.instances_per_node = 4;
+        auto c = make_cluster(t, 64);
+        std::vector<Request> rs(3);
+        const std::vector<std::vector<InstanceId>> bind = {{2}, {1, 2}, {1, 2, 3}};
+        for (int i = 0; i < 3; ++i) {
+            rs[i].id = 100 + i;
+            rs[i].seq_len = 30 * (i + 1);
+            Placement p;
+            p.kv_binding = bind[i];
+            p.split.assign(bind[i].size(), 30);
+            p.moe_binding = bind[i][0];
+            rs[i].placement = p;
+            rs[i].state = RequestState::Active;
+            pt_allocate(rs[i], p, c);
+        }
+        std::vector<Request*> act{&rs[2], &rs[0], &rs[1]};
+        rebalance_active(act, c);
+        CHECK("rebalance_moe", rs[0].placement->moe_binding == 2 && rs[1].placement->moe_binding == 1 &&
+                                   rs[2].placement->moe_binding == 3);
+        CHECK("rebalance_B", c.instances[0].moe_batch == 0 && c.instances[1].moe_batch == 1 &&
+                                 c.instances[2].moe_batch == 1 && c.instances[3].moe_batch == 1);
+        CHECK("rebalance_order", act[0] == &rs[0] && act[1] == &rs[1] && act[2] == &rs[2]);
+        // Fig. 6-style routing check: invariants and row sums
+        std::vector<const Request*> ca{&rs[0], &rs[1], &rs[2]};
+        auto cfg = build_binding_config(ca, 4);
+        auto rt = derive_routing_tables(cfg);
+        bool ok = cfg[2].n() == 3 && cfg[2].m() == 1 && cfg[1].m() == 1;
+        int q1 = 0, r1 = 0;
+        for (int s = 0; s < 4; ++s) {
+            for (int r = 0; r < rt[s].q_route.rows; ++r) {
+                ok = ok && rt[s].q_route.row_sum(r) == 1;
+                q1 += 1;
+            }
+            for (int r = 0; r < rt[s].res_route.rows; ++r) r1 += rt[s].res_route.row_sum(r);
+        }
+        CHECK("routing_invariants", ok && q1 == 6 && r1 == 6);
+    }
+    // bucket_shape / footprint
+    {
+        auto sp = ShapeSpace::default_space();
+        CHECK("bucket_shape", bucket_shape(5, 9, sp) == std::make_pair(8, 16) &&
+                                  bucket_shape(17, 4, sp) == std::make_pair(32, 8) &&
+                                  bucket_shape(200, 500, sp) == std::make_pair(256, 512));
+        bool threw = false;
+        try {
+            bucket_shape(257, 1, sp);
+        } catch (const ShapeOverflow&) {
+            threw = true;
+        }
+        CHECK("shape_overflow", threw);
+        auto f = graph_memory_footprint(sp);
+        sp.world_size = 8;
+        auto f8 = graph_memory_footprint(sp);
+        CHECK("footprint", f.graph_count == 48 && f.buffer_bytes == 17368064 && f8.buffer_bytes == 105907200);
+    }
+    // attention math on the device vs an fp64 host evaluation of the definition
+    {
+        std::mt19937_64 rng(3);
+        std::normal_distribution<double> nd(0.0, 1.0);
+        double worst = 0.0, worst_lse = 0.0;
+        for (int trial = 0; trial < 50; ++trial) {
+            const int d = trial % 3 == 0 ? 8 : (trial % 3 == 1 ? 16 : 64);
+            const int L = 1 + static_cast<int>(rng() % 512);
+            std::vector<double> q(d), k(static_cast<size_t>(L) * d), v(static_cast<size_t>(L) * d);
+            for (auto& x : q) x = nd(rng);
+            for (auto& x : k) x = nd(rng);
+            for (auto& x : v) x = nd(rng);
+            // exact fp64 softmax attention (definition), for the oracle value
+            std::vector<double> s(L);
+            double mx = -INFINITY;
+            for (int j = 0; j < L; ++j) {
+                double a = 0;
+                for (int i = 0; i < d; ++i) a += k[static_cast<size_t>(j) * d + i] * q[i];
+                s[j] = a / std::sqrt(double(d));
+                mx = std::max(mx, s[j]);
+            }
+            double den = 0;
+            std::vector<double> o(d, 0.0);
+            for (int j = 0; j < L; ++j) {
+                const double w = std::exp(s[j] - mx);
+                den += w;
+                for (int i = 0; i < d; ++i) o[i] += w * v[static_cast<size_t>(j) * d + i];
+            }
+            for (auto& x : o) x /= den;
+            const double lse = mx + std::log(den);
+            std::vector<float> qf(q.begin(), q.end()), kf(k.begin(), k.end()), vf(v.begin(), v.end());
+            const int ns = 1 << (trial % 4);
+            std::vector<std::int64_t> bounds;
+            for (int i = 1; i <= ns; ++i) bounds.push_back(static_cast<std::int64_t>(L) * i / ns);
+            auto m32 = sharded_attention_merge(qf, kf, vf, d, 1.0f / std::sqrt(float(d)), bounds, true);
+            double num = 0, dd = 0;
+            for (int i = 0; i < d; ++i) {
+                num += (m32[i] - o[i]) * (m32[i] - o[i]);
+                dd += o[i] * o[i];
+            }
+            worst = std::max(worst, std::sqrt(num / dd));
+            auto sr = shard_attention<double>(q, k, v, L, d, 1.0 / std::sqrt(double(d)));
+            worst_lse = std::max(worst_lse, std::abs(sr.lse - lse) / std::max(1.0, std::abs(lse)));
+        }
+        CHECK("sharded_merge_f32_rel_l2_1e-5", worst <= 1e-5);
+        CHECK("shard_attention_f64_lse", worst_lse <= 1e-12);
+        bool threw = false;
+        try {
+            std::vector<double> q(8, 1.0), kv;
+            shard_attention<double>(q, kv, kv, 0, 8, 1.0);
+        } catch (const EmptyShard&) {
+            threw = true;
+        }
+        CHECK("empty_shard", threw);
+    }
+    std::cout << (fails ? "FAILED" : "ALL OK") << "\n";
+    return fails ? 1 : 0;
+}
