@@ -142,6 +142,18 @@ _SIGNATURES = [
     ("dcp_route_q", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
     ("dcp_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
     ("dcp_merge_partials", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
+    ("dcp_planner_set_policy", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32, c_int32]),
+    ("dcp_planner_set_queue", c_int, [c_void_p, c_void_p, c_void_p, c_int32]),
+    ("dcp_planner_allocate", c_int, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_int32]),
+    ("dcp_planner_pages", c_int64, [c_void_p, c_int64, c_void_p, c_void_p, c_int64]),
+    ("dcp_planner_active_moe", c_int32, [c_void_p, c_void_p, c_void_p, c_int32]),
+    ("dcp_planner_rebalance", c_int, [c_void_p, c_void_p, c_int32]),
+    ("dcp_planner_load_instances", c_int, [c_void_p] + [c_void_p] * 5),
+    ("dcp_water_fill", c_int, [c_void_p, c_int32, c_void_p, c_int64, c_void_p]),
+    ("dcp_binding_config", c_int, [c_void_p, c_int32] + [c_void_p] * 4 + [c_int32] + [c_void_p] * 4),
+    ("dcp_route_tables", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
+    ("dcp_shard_attention_batch", c_int, [c_void_p, c_int32, c_int32, c_int32, ctypes.c_double] + [c_void_p] * 9),
+    ("dcp_lse_merge_batch", c_int, [c_void_p, c_int32, c_int32, c_int32] + [c_void_p] * 6),
 ]
 
 
