@@ -317,6 +317,48 @@ DCP_API int dcp_lse_merge_batch(dcp_ctx* ctx, int32_t dtype_bytes, int32_t n_gro
                                 int32_t head_dim, const int64_t* group_off, const void* outs,
                                 const void* lses, void* merged, void* merged_lse, void* stream);
 
+/* ---- K4 / K5: MoE dispatch / combine over peer pools ------------------------
+ *
+ * No reference symbol exists (the reference's MoE surface is the M list,
+ * BindingConfig::moe_bound routing.hpp:18-19): parity is against our own CPU
+ * restatement (oracle dcpora_moe_layer_f64), out_t = sum over its top-k
+ * experts in ascending id of w * FFN_e(x_t).  Token t of an instance is the
+ * t-th request of its M list.  Experts are partitioned contiguously:
+ * rank = expert / (num_experts / world).  The expert FFN between receive and
+ * combine_put is the caller's (a library GEMM; out of scope of this path). */
+typedef struct dcp_moe dcp_moe;
+typedef struct dcp_moe_config {
+    int32_t world;
+    int32_t self;
+    int32_t hidden;       /* multiple of 8 */
+    int32_t topk;         /* <= 16 */
+    int32_t num_experts;  /* multiple of world */
+    int32_t m_max;        /* max tokens per instance (<= 1024) */
+} dcp_moe_config;
+
+DCP_API int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* cfg, dcp_moe** out);
+DCP_API int dcp_moe_destroy(dcp_moe* x);
+DCP_API int dcp_moe_ipc_handle(dcp_moe* x, void* handle64);
+DCP_API int dcp_moe_open_peer_ipc(dcp_moe* x, int32_t peer, const void* handle64);
+DCP_API int dcp_moe_set_peer_local(dcp_moe* x, int32_t peer, const dcp_moe* other);
+DCP_API int dcp_moe_commit(dcp_moe* x);
+DCP_API int dcp_moe_begin_step(dcp_moe* x, void* stream);
+/* int32 per received row of meta_rows: src token, n_local, (expert, weight bits) * topk */
+DCP_API int32_t dcp_moe_meta_width(const dcp_moe* x);
+/* K4: x_local bf16 [M][hidden], topk_idx int32 [M][topk], topk_w fp32 [M][topk]
+ * (device); *m_count_dev = M (e.g. dcp_instance_view.m_count_all + self). */
+DCP_API int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* topk_idx,
+                             const float* topk_w, const int32_t* m_count_dev, void* stream);
+/* K5a: wait for all sources; compact received rows into x_rows (bf16
+ * [world*m_max][hidden]) and meta_rows (int32 [world*m_max][meta_width]);
+ * copies the per-source counts to host `counts` and returns the row count. */
+DCP_API int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* counts,
+                                void* stream);
+/* K5b: y_rows bf16 [R][hidden] (same row order as receive) back to each token's home. */
+DCP_API int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream);
+/* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */
+DCP_API int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

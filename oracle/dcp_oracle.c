@@ -945,3 +945,50 @@ void dcpora_uniform_int(uint64_t seed, int64_t lo, int64_t hi, int n, int64_t* o
         out[i] = v > hi ? hi : v;
     }
 }
+
+/* MoE expert layer oracle (see dcp_oracle.h).  Experts are visited in
+ * ascending id order; every product is fp64 over widened bf16 values. */
+int dcpora_moe_layer_f64(int T, int H, int I, int E, int k, const uint16_t* x, const int32_t* idx,
+                         const float* w, const uint16_t* w_gate, const uint16_t* w_up,
+                         const uint16_t* w_down, double* out, int threads) {
+    (void)E;
+#pragma omp parallel for schedule(dynamic) num_threads(threads > 0 ? threads : 1)
+    for (int t = 0; t < T; ++t) {
+        double* o = out + (size_t)t * H;
+        for (int h = 0; h < H; ++h) o[h] = 0.0;
+        int order[64];
+        for (int j = 0; j < k; ++j) order[j] = j;
+        for (int a = 1; a < k; ++a) { /* ascending expert id */
+            const int v = order[a];
+            int b = a - 1;
+            while (b >= 0 && idx[(size_t)t * k + order[b]] > idx[(size_t)t * k + v]) { order[b + 1] = order[b]; --b; }
+            order[b + 1] = v;
+        }
+        double* act = malloc(sizeof(double) * (size_t)I);
+        double* xd = malloc(sizeof(double) * (size_t)H);
+        for (int h = 0; h < H; ++h) xd[h] = bf16_to_f64(x[(size_t)t * H + h]);
+        for (int j = 0; j < k; ++j) {
+            const int e = idx[(size_t)t * k + order[j]];
+            const double we = (double)w[(size_t)t * k + order[j]];
+            const uint16_t* g = w_gate + (size_t)e * I * H;
+            const uint16_t* u = w_up + (size_t)e * I * H;
+            const uint16_t* dn = w_down + (size_t)e * H * I;
+            for (int i = 0; i < I; ++i) {
+                double a = 0.0, b = 0.0;
+                for (int h = 0; h < H; ++h) {
+                    a += bf16_to_f64(g[(size_t)i * H + h]) * xd[h];
+                    b += bf16_to_f64(u[(size_t)i * H + h]) * xd[h];
+                }
+                act[i] = a / (1.0 + exp(-a)) * b;
+            }
+            for (int h = 0; h < H; ++h) {
+                double acc = 0.0;
+                for (int i = 0; i < I; ++i) acc += bf16_to_f64(dn[(size_t)h * I + i]) * act[i];
+                o[h] += we * acc;
+            }
+        }
+        free(act);
+        free(xd);
+    }
+    return 0;
+}

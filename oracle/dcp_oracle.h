@@ -73,6 +73,17 @@ int dcpora_world_dump_routing(void* h, char* buf, int64_t cap);
 int dcpora_world_instance_shards(void* h, int inst, int64_t* ids, int32_t* cu, int32_t* frames,
                                  int64_t* tokens, int cap_shards, int cap_frames);
 
+/* MoE layer oracle (no reference implementation exists: parity unpinned vs the
+ * reference; this restatement is the definition the device K4/K5 path is
+ * checked against).  Per token t:
+ *   out_t = sum over its top-k experts e in ascending id order of
+ *           w_{t,e} * W_down_e( silu(W_gate_e x_t) * (W_up_e x_t) )
+ * in fp64 over exactly-widened bf16 inputs.  w_gate/w_up: [E][I][H],
+ * w_down: [E][H][I] (bf16 bits), x: [T][H], idx/w: [T][k]. */
+int dcpora_moe_layer_f64(int T, int H, int I, int E, int k, const uint16_t* x, const int32_t* idx,
+                         const float* w, const uint16_t* w_gate, const uint16_t* w_up,
+                         const uint16_t* w_down, double* out, int threads);
+
 void dcpora_uniform_int(uint64_t seed, int64_t lo, int64_t hi, int n, int64_t* out);
 
 #ifdef __cplusplus

@@ -98,6 +98,11 @@ class InstanceView(Structure):
     ]
 
 
+class MoeConfig(Structure):
+    _fields_ = [("world", c_int32), ("self", c_int32), ("hidden", c_int32), ("topk", c_int32),
+                ("num_experts", c_int32), ("m_max", c_int32)]
+
+
 class XchgConfig(Structure):
     _fields_ = [("world", c_int32), ("self", c_int32), ("num_q_heads", c_int32), ("head_dim", c_int32),
                 ("n_max", c_int32), ("m_max", c_int32)]
@@ -154,6 +159,18 @@ _SIGNATURES = [
     ("dcp_route_tables", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("dcp_shard_attention_batch", c_int, [c_void_p, c_int32, c_int32, c_int32, ctypes.c_double] + [c_void_p] * 9),
     ("dcp_lse_merge_batch", c_int, [c_void_p, c_int32, c_int32, c_int32] + [c_void_p] * 6),
+    ("dcp_moe_create", c_int, [c_void_p, POINTER(MoeConfig), POINTER(c_void_p)]),
+    ("dcp_moe_destroy", c_int, [c_void_p]),
+    ("dcp_moe_ipc_handle", c_int, [c_void_p, c_void_p]),
+    ("dcp_moe_open_peer_ipc", c_int, [c_void_p, c_int32, c_void_p]),
+    ("dcp_moe_set_peer_local", c_int, [c_void_p, c_int32, c_void_p]),
+    ("dcp_moe_commit", c_int, [c_void_p]),
+    ("dcp_moe_begin_step", c_int, [c_void_p, c_void_p]),
+    ("dcp_moe_meta_width", c_int32, [c_void_p]),
+    ("dcp_moe_dispatch", c_int, [c_void_p] + [c_void_p] * 5),
+    ("dcp_moe_receive", c_int32, [c_void_p] + [c_void_p] * 4),
+    ("dcp_moe_combine_put", c_int, [c_void_p, c_void_p, c_void_p]),
+    ("dcp_moe_combine_reduce", c_int, [c_void_p, c_void_p, c_void_p]),
 ]
 
 

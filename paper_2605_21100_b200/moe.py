@@ -1,0 +1,117 @@
+"""Host mirror of the MoE dispatch/combine path (K4/K5, dcp_moe_* in dcp_capi.h).
+
+One MoeInstance per DP-EP instance: the tokens are the instance's M list
+(requests MoE-bound here, BindingConfig::moe_bound routing.hpp:18-19), each
+routed to its top-k experts' ranks and combined back.  `expert_stage` is the
+(out of scope) expert FFN between receive and combine, done with library
+GEMMs (torch -> cuBLAS): y = sum over the row's local experts, ascending id,
+of w * W_down(silu(W_gate x) * W_up x).
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _capi
+
+
+def _s(stream, dev):
+    return ctypes.c_void_p((stream or torch.cuda.current_stream(dev)).cuda_stream)
+
+
+class MoeInstance:
+    def __init__(self, ctx, world, self_id, hidden, topk, num_experts, m_max):
+        L = _capi.lib()
+        cfg = _capi.MoeConfig(world, self_id, hidden, topk, num_experts, m_max)
+        h = ctypes.c_void_p()
+        _capi.check(L.dcp_moe_create(ctx.handle, ctypes.byref(cfg), ctypes.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.world, self.id, self.H, self.k, self.E, self.m_max = world, self_id, hidden, topk, num_experts, m_max
+        self.meta_w = L.dcp_moe_meta_width(h)
+        dev = torch.device("cuda", ctx.device)
+        self.x_rows = torch.empty(world * m_max, hidden, dtype=torch.bfloat16, device=dev)
+        self.meta_rows = torch.zeros(world * m_max, self.meta_w, dtype=torch.int32, device=dev)
+        self.y_rows = torch.zeros(world * m_max, hidden, dtype=torch.bfloat16, device=dev)
+        self.out = torch.zeros(m_max, hidden, dtype=torch.float32, device=dev)
+        self.m_count = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def ipc_handle(self):
+        b = ctypes.create_string_buffer(64)
+        _capi.check(_capi.lib().dcp_moe_ipc_handle(self.h, b))
+        return b.raw
+
+    def open_peer(self, peer, handle):
+        _capi.check(_capi.lib().dcp_moe_open_peer_ipc(self.h, peer, ctypes.create_string_buffer(handle, 64)))
+
+    def set_peer_local(self, peer, other):
+        _capi.check(_capi.lib().dcp_moe_set_peer_local(self.h, peer, other.h))
+
+    def commit(self):
+        _capi.check(_capi.lib().dcp_moe_commit(self.h))
+
+    def dispatch(self, x, topk_idx, topk_w, m_count_ptr=None, stream=None):
+        """x bf16 [M, H], topk_idx int32 [M, k], topk_w fp32 [M, k] (device)."""
+        L = _capi.lib()
+        s = _s(stream, self.ctx.device)
+        if m_count_ptr is None:
+            self.m_count.fill_(x.shape[0])
+            m_count_ptr = self.m_count.data_ptr()
+        self._keep = (x, topk_idx, topk_w)
+        _capi.check(L.dcp_moe_begin_step(self.h, s))
+        _capi.check(L.dcp_moe_dispatch(self.h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(topk_idx.data_ptr()),
+                                       ctypes.c_void_p(topk_w.data_ptr()), ctypes.c_void_p(m_count_ptr), s))
+
+    def receive(self, stream=None):
+        counts = np.zeros(self.world, np.int32)
+        R = _capi.lib().dcp_moe_receive(self.h, ctypes.c_void_p(self.x_rows.data_ptr()),
+                                        ctypes.c_void_p(self.meta_rows.data_ptr()),
+                                        counts.ctypes.data_as(ctypes.c_void_p), _s(stream, self.ctx.device))
+        if R < 0:
+            _capi.check(R)
+        return int(R), counts
+
+    def expert_stage(self, R, w_gate, w_up, w_down):
+        """Library-GEMM expert FFN over the R received rows (local experts
+        w_*[e - first_local_expert])."""
+        e0 = self.id * (self.E // self.world)
+        meta = self.meta_rows[:R].cpu().numpy()
+        x = self.x_rows[:R].float()
+        y = torch.zeros(R, self.H, dtype=torch.float32, device=x.device)
+        per = {}
+        for r in range(R):
+            n = int(meta[r, 1])
+            for j in range(n):
+                e = int(meta[r, 2 + 2 * j])
+                wv = float(np.int32(meta[r, 3 + 2 * j]).view(np.float32))
+                per.setdefault(e, []).append((r, wv))
+        for e in sorted(per):
+            rows = torch.tensor([r for r, _ in per[e]], device=x.device)
+            wts = torch.tensor([wv for _, wv in per[e]], device=x.device, dtype=torch.float32)
+            xe = x[rows].to(torch.bfloat16)
+            g = xe @ w_gate[e - e0].T
+            u = xe @ w_up[e - e0].T
+            a = (torch.nn.functional.silu(g.float()) * u.float()).to(torch.bfloat16)
+            o = (a @ w_down[e - e0].T).float()
+            y.index_add_(0, rows, o * wts[:, None])
+        self.y_rows[:R] = y.to(torch.bfloat16)
+
+    def combine_put(self, stream=None):
+        _capi.check(_capi.lib().dcp_moe_combine_put(self.h, ctypes.c_void_p(self.y_rows.data_ptr()),
+                                                    _s(stream, self.ctx.device)))
+
+    def combine_reduce(self, stream=None):
+        _capi.check(_capi.lib().dcp_moe_combine_reduce(self.h, ctypes.c_void_p(self.out.data_ptr()),
+                                                       _s(stream, self.ctx.device)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _capi.lib().dcp_moe_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

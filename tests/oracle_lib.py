@@ -54,6 +54,7 @@ def _load(path, prefix):
         sigs["sharded_attention_merge_f64"] = (c_int, [vp, vp, vp, c_int64, c_int, c_double, vp, c_int, vp])
         sigs["sharded_attention_merge_f32"] = (c_int, [vp, vp, vp, c_int64, c_int, c_float, vp, c_int, vp])
         sigs["world_instance_shards"] = (c_int, [c_void_p, c_int, vp, vp, vp, vp, c_int, c_int])
+        sigs["moe_layer_f64"] = (c_int, [c_int] * 5 + [vp] * 7 + [c_int])
     else:
         sigs["sharded_attention_merge_f64"] = (c_int, [vp, vp, vp, c_int64, c_int, c_double, vp, c_int, c_int, vp])
         sigs["sharded_attention_merge_f32"] = (c_int, [vp, vp, vp, c_int64, c_int, c_float, vp, c_int, c_int, vp])
