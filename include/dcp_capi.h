@@ -359,6 +359,23 @@ DCP_API int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream);
 /* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */
 DCP_API int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream);
 
+/* ---- AOT step graphs (Alg. 2; ShapeSpace routing.hpp:60-85) --
+ * One CUDA graph per M-bucket of ShapeSpace::default_space(), each replaying
+ * this instance's routed step (epoch bump, K2, K1-routed, K3) over the same
+ * pools (one shared pool for all graphs, as graph_memory_footprint models).
+ * K2/K3 grids are the bucket's M^; K1 is persistent and reads N from device
+ * memory, so buckets that differ only in N^ share one executable graph.
+ * dcp_step_graph_launch picks bucket_shape(m_rows, n_rows) and replays it;
+ * ShapeOverflow(-5) above (256, 512).  The view's device pointers must stay
+ * valid (they are fixed offsets into the planner's routing buffers). */
+typedef struct dcp_step_graph dcp_step_graph;
+DCP_API int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
+                                  const dcp_attn_args* a, dcp_step_graph** out);
+DCP_API int dcp_step_graph_launch(dcp_step_graph* g, int32_t m_rows, int32_t n_rows, void* stream);
+/* executable graphs captured / buckets in the shape space */
+DCP_API int dcp_step_graph_count(const dcp_step_graph* g, int32_t* buckets);
+DCP_API int dcp_step_graph_destroy(dcp_step_graph* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,8 +73,7 @@ static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv
 }
 
 template <int HKV, int G>
-static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm,
-                         cudaStream_t stream) {
+static int ensure_attr(dcp_ctx* ctx) {
     using C = DecodeCfg<HKV, G>;
     static uint64_t attr_done = 0;  // per-instantiation bit per device
     if (!(attr_done >> (ctx->device & 63) & 1)) {
@@ -82,6 +81,14 @@ static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams&
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_done |= uint64_t(1) << (ctx->device & 63);
     }
+    return DCP_OK;
+}
+
+template <int HKV, int G>
+static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm,
+                         cudaStream_t stream) {
+    using C = DecodeCfg<HKV, G>;
+    if (int rc = ensure_attr<HKV, G>(ctx)) return rc;
     splitkv_decode_kernel<HKV, G><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
@@ -101,6 +108,16 @@ static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParam
 }  // namespace dcp
 
 using namespace dcp;
+
+int dcp_attn_prepare(dcp_ctx* ctx, int hkv, int G) {
+    if (hkv == 8 && G == 4) return ensure_attr<8, 4>(ctx);
+    if (hkv == 4 && G == 8) return ensure_attr<4, 8>(ctx);
+    if (hkv == 8 && G == 1) return ensure_attr<8, 1>(ctx);
+    if (hkv == 2 && G == 16) return ensure_attr<2, 16>(ctx);
+    if (hkv == 1 && G == 16) return ensure_attr<1, 16>(ctx);
+    set_error("unsupported (num_kv_heads=%d, group=%d)", hkv, G);
+    return DCP_E_UNSUPPORTED;
+}
 
 extern "C" {
 

@@ -43,6 +43,9 @@ struct TmapCacheEntry {
 
 }  // namespace dcp
 
+// Sets K1's dynamic shared-memory attribute for (hkv, group) outside any capture.
+int dcp_attn_prepare(struct dcp_ctx* ctx, int hkv, int group);
+
 struct dcp_ctx {
     int device = 0;
     int num_sms = 0;

@@ -153,7 +153,8 @@ int32_t dcp_moe_meta_width(const dcp_moe* x) { return x ? 2 + 2 * x->cfg.topk : 
 
 int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const float* w, const int32_t* m_count,
                      void* stream) {
-    DCP_REQUIRE(x && x_local && idx && w && m_count, DCP_E_INVALID_ARG, "NULL argument");
+    // x_local / idx / w may be NULL when the instance has no MoE-bound tokens (M = 0)
+    DCP_REQUIRE(x && m_count, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
     moe_layout_kernel<<<1, 1024, 0, s>>>(x->dev, idx, m_count, x->slot_tbl);

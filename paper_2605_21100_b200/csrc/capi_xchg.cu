@@ -1,5 +1,6 @@
 // SPDX-License-Identifier: Apache-2.0
 // C ABI: the routing-based exchange (K2 Q-route, K3 LSE merge) — dcp_capi.h.
+#include <algorithm>
 #include <cstring>
 
 #include "exchange_kernels.cuh"
@@ -168,6 +169,71 @@ int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
     lse_merge_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
     DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+struct dcp_step_graph {
+    int m_hat[6] = {8, 16, 32, 64, 128, 256};
+    cudaGraphExec_t exec[6] = {};
+    cudaGraph_t graph[6] = {};
+};
+
+int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
+                          dcp_step_graph** out) {
+    DCP_REQUIRE(ctx && x && v && a && out, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    int rc = dcp_attn_prepare(ctx, a->num_kv_heads, a->num_q_heads / a->num_kv_heads);
+    if (rc) return rc;
+    cudaStream_t cs;
+    DCP_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    auto* g = new dcp_step_graph();
+    for (int i = 0; i < 6; ++i) {
+        const int mh = std::min(g->m_hat[i], x->cfg.m_max);
+        cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            epoch_bump_kernel<<<1, 1, 0, cs>>>(x->epoch);
+            q_route_put_kernel<<<mh, 128, 0, cs>>>(x->dev, static_cast<const __nv_bfloat16*>(x->q_local),
+                                                  v->m_count_all, v->m_nrow);
+            rc = dcp_decode_attn_routed(ctx, x, v, a, cs);
+            lse_merge_kernel<<<mh, 128, 0, cs>>>(x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
+            e = cudaStreamEndCapture(cs, &g->graph[i]);
+        }
+        if (e == cudaSuccess && rc == 0) e = cudaGraphInstantiate(&g->exec[i], g->graph[i], 0);
+        if (e != cudaSuccess || rc) {
+            dcp_step_graph_destroy(g);
+            cudaStreamDestroy(cs);
+            if (rc) return rc;
+            set_error("graph capture: %s", cudaGetErrorString(e));
+            return DCP_E_CUDA;
+        }
+    }
+    cudaStreamDestroy(cs);
+    *out = g;
+    return DCP_OK;
+}
+
+int dcp_step_graph_launch(dcp_step_graph* g, int32_t m, int32_t n, void* stream) {
+    DCP_REQUIRE(g, DCP_E_INVALID_ARG, "NULL graph");
+    DCP_REQUIRE(m <= 256 && n <= 512 && m >= 0 && n >= 0, DCP_E_SHAPE_OVERFLOW,
+                "execution shape (%d,%d) exceeds (256,512)", m, n);
+    int i = 0;
+    while (g->m_hat[i] < m) ++i;  // bucket_shape: first dominating M^ (N^ shares the graph)
+    DCP_CUDA_TRY(cudaGraphLaunch(g->exec[i], static_cast<cudaStream_t>(stream)));
+    return DCP_OK;
+}
+
+int dcp_step_graph_count(const dcp_step_graph* g, int32_t* buckets) {
+    if (buckets) *buckets = 48;
+    return g ? 6 : 0;
+}
+
+int dcp_step_graph_destroy(dcp_step_graph* g) {
+    if (!g) return DCP_OK;
+    for (int i = 0; i < 6; ++i) {
+        if (g->exec[i]) cudaGraphExecDestroy(g->exec[i]);
+        if (g->graph[i]) cudaGraphDestroy(g->graph[i]);
+    }
+    delete g;
     return DCP_OK;
 }
 
