@@ -159,6 +159,11 @@ _SIGNATURES = [
     ("dcp_route_tables", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_int32, c_void_p, c_void_p, c_void_p]),
     ("dcp_shard_attention_batch", c_int, [c_void_p, c_int32, c_int32, c_int32, ctypes.c_double] + [c_void_p] * 9),
     ("dcp_lse_merge_batch", c_int, [c_void_p, c_int32, c_int32, c_int32] + [c_void_p] * 6),
+    ("dcp_step_graph_create", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs),
+                                      POINTER(c_void_p)]),
+    ("dcp_step_graph_launch", c_int, [c_void_p, c_int32, c_int32, c_void_p]),
+    ("dcp_step_graph_count", c_int, [c_void_p, c_void_p]),
+    ("dcp_step_graph_destroy", c_int, [c_void_p]),
     ("dcp_moe_create", c_int, [c_void_p, POINTER(MoeConfig), POINTER(c_void_p)]),
     ("dcp_moe_destroy", c_int, [c_void_p]),
     ("dcp_moe_ipc_handle", c_int, [c_void_p, c_void_p]),

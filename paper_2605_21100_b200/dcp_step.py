@@ -105,6 +105,37 @@ class DcpInstance:
             pass
 
 
+class StepGraph:
+    """AOT step graphs of one instance (dcp_step_graph_*): one captured CUDA
+    graph per M-bucket of the default ShapeSpace, replayed per decode step."""
+
+    def __init__(self, inst: DcpInstance, view):
+        L = _capi.lib()
+        self.view = view  # device pointers captured by the graphs must stay alive
+        h = ctypes.c_void_p()
+        _capi.check(L.dcp_step_graph_create(inst.ctx.handle, inst.x, ctypes.byref(view), ctypes.byref(inst.args),
+                                            ctypes.byref(h)))
+        self.h, self.inst = h, inst
+        b = ctypes.c_int32()
+        self.graphs = L.dcp_step_graph_count(h, ctypes.byref(b))
+        self.buckets = b.value
+
+    def launch(self, m_rows: int, n_rows: int, stream=None):
+        s = (stream or torch.cuda.current_stream(self.inst.ctx.device)).cuda_stream
+        _capi.check(_capi.lib().dcp_step_graph_launch(self.h, m_rows, n_rows, ctypes.c_void_p(s)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _capi.lib().dcp_step_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def run_local_step(planner, instances, q_of_request: dict, stream=None):
     """Run one routed step with all instances in this process.
 
