@@ -274,6 +274,7 @@ int dcp_planner_allocate(dcp_planner* pl, int64_t id, int64_t seq_len, int32_t k
         pl->id_of_slot[sl] = id;
         pl->retired.erase(id);
     }
+    pl->is_active[sl] = 1;
     pl->routing_valid = false;
     return planner_sync_arena_top(pl);
 }

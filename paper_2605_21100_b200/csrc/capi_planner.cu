@@ -242,6 +242,7 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     DCP_CUDA_TRY(cudaDeviceSynchronize());
     pl->id_of_slot.assign(S, -1);
     pl->queued_len.assign(S, 0);
+    pl->is_active.assign(S, 0);
     for (int i = (int)S - 1; i >= 0; --i) pl->free_slots.push_back(i);
     *out = pl;
     return DCP_OK;
@@ -321,6 +322,7 @@ int dcp_planner_step_result(dcp_planner* pl, int64_t* committed, int32_t* nc, in
     for (int i = 0; i < cnt[0]; ++i) {
         const int s = sl[i];
         if (committed) committed[i] = pl->id_of_slot[s];
+        pl->is_active[s] = 1;
         pl->waiting_pages_bound -=
             pages_for_h(pl->queued_len[s], pl->cfg.page_size) + PL_MAXK + pl->st.reserve_pages;
         pl->queued -= 1;
@@ -364,12 +366,9 @@ int dcp_planner_finish(dcp_planner* pl, const int64_t* ids, int32_t n, void* str
         slots.push_back(it->second);
     }
     // only ACTIVE requests have page-table entries (UnknownRequest otherwise)
-    for (int i = 0; i < n; ++i) {
-        int32_t s = 0;
-        DCP_CUDA_TRY(cudaMemcpy(&s, pl->st.state + slots[i], sizeof(int32_t), cudaMemcpyDeviceToHost));
-        DCP_REQUIRE(s == ST_ACTIVE, DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
+    for (int i = 0; i < n; ++i)
+        DCP_REQUIRE(pl->is_active[slots[i]], DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
                     (long long)ids[i]);
-    }
     for (int i = 0; i < n; ++i) {
         dcp_planner::Retired r{};
         DCP_CUDA_TRY(cudaMemcpy(&r.k, pl->st.k + slots[i], 4, cudaMemcpyDeviceToHost));
@@ -385,6 +384,7 @@ int dcp_planner_finish(dcp_planner* pl, const int64_t* ids, int32_t n, void* str
     for (int i = 0; i < n; ++i) {
         pl->slot_of.erase(ids[i]);
         pl->id_of_slot[slots[i]] = -1;
+        pl->is_active[slots[i]] = 0;
         pl->free_slots.push_back(slots[i]);
     }
     pl->routing_valid = false;
@@ -399,14 +399,34 @@ int dcp_planner_append_token(dcp_planner* pl, const int64_t* ids, int32_t n, int
         auto it = pl->slot_of.find(ids[i]);
         DCP_REQUIRE(it != pl->slot_of.end(), DCP_E_UNKNOWN_REQUEST, "unknown request %lld",
                     (long long)ids[i]);
-        int32_t s = 0;
-        DCP_CUDA_TRY(cudaMemcpy(&s, pl->st.state + it->second, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        DCP_REQUIRE(s == ST_ACTIVE, DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
+        DCP_REQUIRE(pl->is_active[it->second], DCP_E_UNKNOWN_REQUEST, "no page-table entries for request %lld",
                     (long long)ids[i]);
         slots[i] = it->second;
     }
     int done = 0;
     int guard = 0;
+    // Batches without duplicate requests take the parallel kernel; it declines
+    // (res_counts[2] = 1, nothing mutated) when a frame fallback could occur.
+    bool unique = true;
+    {
+        std::vector<int32_t> sorted(slots);
+        std::sort(sorted.begin(), sorted.end());
+        unique = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    }
+    if (unique && n > 0) {
+        DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_slots, slots.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                     pl->stream));
+        planner_append_parallel_kernel<<<1, PL_APPEND_THREADS, 0, pl->stream>>>(pl->st, pl->d_io_slots, n,
+                                                                               pl->d_io_out);
+        DCP_CUDA_TRY(cudaGetLastError());
+        int32_t cnt[4];
+        DCP_CUDA_TRY(cudaMemcpyAsync(cnt, pl->st.res_counts, sizeof(cnt), cudaMemcpyDeviceToHost, pl->stream));
+        DCP_CUDA_TRY(cudaStreamSynchronize(pl->stream));
+        if (cnt[2] == 0) {
+            DCP_CUDA_TRY(cudaMemcpy(out_inst, pl->d_io_out, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+            done = n;
+        }
+    }
     while (done < n) {
         const int m = n - done;
         DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_io_slots, slots.data() + done, m * sizeof(int32_t),

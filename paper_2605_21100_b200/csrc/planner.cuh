@@ -650,6 +650,126 @@ static __global__ void planner_append_kernel(PlannerState st, const int32_t* slo
     }
 }
 
+
+// ------------------------------------------------------------------ append_token, batched
+// The same semantics as planner_append_kernel for a batch WITHOUT duplicate
+// requests, in parallel: a request appends to its trailing page when it has
+// room; otherwise it takes the top free frame of the instance holding its last
+// page.  Requests needing a frame on the same instance pop consecutive stack
+// entries in batch order (per-instance ranks from a block scan), which is what
+// the sequential loop does as long as no instance runs out.  When some
+// instance's demand exceeds its free frames (the fallback path of
+// page_table.cpp:104-113 would trigger) or the page arena cannot absorb the
+// segment growth, nothing is mutated and res_counts[2] = 1 asks the host to
+// run the sequential kernel instead.
+constexpr int PL_APPEND_THREADS = 256;
+static __global__ void __launch_bounds__(PL_APPEND_THREADS, 1)
+    planner_append_parallel_kernel(PlannerState st, const int32_t* slots, int n, int32_t* out_inst) {
+    __shared__ int32_t cnt[PL_APPEND_THREADS][PL_MAXW];
+    __shared__ int64_t grow_part[PL_APPEND_THREADS];
+    __shared__ int32_t demand[PL_MAXW];
+    __shared__ int32_t bail;
+    __shared__ unsigned long long kv_add[PL_MAXW];
+    __shared__ int64_t arena_base;
+    const int tid = threadIdx.x, W = st.W;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int q0 = min(n, tid * per), q1 = min(n, (tid + 1) * per);
+    for (int s = 0; s < W; ++s) cnt[tid][s] = 0;
+    int64_t grow = 0;
+    for (int q = q0; q < q1; ++q) {
+        const int sl = slots[q];
+        const int c = st.page_cnt[sl];
+        if (c > 0 && st.trailing_fill[sl] < st.page) continue;
+        const int tgt = c == 0 ? st.kv[sl * PL_MAXK] : st.pg_inst[st.page_off[sl] + c - 1];
+        cnt[tid][tgt] += 1;
+        if (c == st.page_cap[sl]) grow += c * 2 > c + 16 ? c * 2 : c + 16;
+    }
+    grow_part[tid] = grow;
+    if (tid < W) kv_add[tid] = 0;
+    __syncthreads();
+    if (tid < W) {  // exclusive scan over threads per instance
+        int run = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            const int v = cnt[t][tid];
+            cnt[t][tid] = run;
+            run += v;
+        }
+        demand[tid] = run;
+    }
+    if (tid == 0) {
+        int64_t g = 0;
+        for (int t = 0; t < (int)blockDim.x; ++t) {
+            const int64_t v = grow_part[t];
+            grow_part[t] = g;
+            g += v;
+        }
+        bail = (*st.arena_top + g > st.arena_cap) ? 1 : 0;
+        arena_base = *st.arena_top;
+        if (!bail) *st.arena_top = arena_base + g;
+    }
+    __syncthreads();
+    if (tid < W && demand[tid] > st.nfree[tid]) atomicExch(&bail, 1);
+    __syncthreads();
+    if (bail) {
+        if (tid == 0) {
+            if (arena_base != *st.arena_top) *st.arena_top = arena_base;
+            st.res_counts[0] = 0;
+            st.res_counts[2] = 1;
+            st.res_counts[3] = PL_OK;
+        }
+        return;
+    }
+    int rank[PL_MAXW];
+    for (int s = 0; s < W; ++s) rank[s] = cnt[tid][s];
+    int64_t goff = arena_base + grow_part[tid];
+    for (int q = q0; q < q1; ++q) {
+        const int sl = slots[q];
+        int64_t off = st.page_off[sl];
+        const int c = st.page_cnt[sl];
+        int tgt;
+        if (c > 0 && st.trailing_fill[sl] < st.page) {
+            tgt = st.pg_inst[off + c - 1];
+            st.trailing_fill[sl] += 1;
+            st.pg_fill[off + c - 1] += 1;
+        } else {
+            tgt = c == 0 ? st.kv[sl * PL_MAXK] : st.pg_inst[off + c - 1];
+            if (c == st.page_cap[sl]) {
+                const int newcap = c * 2 > c + 16 ? c * 2 : c + 16;
+                for (int t = 0; t < c; ++t) {
+                    st.pg_inst[goff + t] = st.pg_inst[off + t];
+                    st.pg_frame[goff + t] = st.pg_frame[off + t];
+                    st.pg_fill[goff + t] = st.pg_fill[off + t];
+                }
+                st.page_off[sl] = goff;
+                st.page_cap[sl] = newcap;
+                off = goff;
+                goff += newcap;
+            }
+            const int64_t pos = st.nfree[tgt] - 1 - rank[tgt];
+            rank[tgt] += 1;
+            st.pg_inst[off + c] = tgt;
+            st.pg_frame[off + c] = st.stack[(int64_t)tgt * st.capacity + pos];
+            st.pg_fill[off + c] = 1;
+            st.page_cnt[sl] = c + 1;
+            st.trailing_fill[sl] = 1;
+        }
+        atomicAdd(&kv_add[tgt], 1ull);
+        st.shard_tokens[(int64_t)sl * W + tgt] += 1;
+        st.generated[sl] += 1;
+        out_inst[q] = tgt;
+    }
+    __syncthreads();
+    if (tid < W) {
+        st.nfree[tid] -= demand[tid];
+        st.kv_load[tid] += (int64_t)kv_add[tid];
+    }
+    if (tid == 0) {
+        st.res_counts[0] = n;
+        st.res_counts[2] = 0;
+        st.res_counts[3] = PL_OK;
+    }
+}
+
 // ------------------------------------------------------------------ arena compaction
 // Moves every live page segment (ACTIVE slots) to a fresh arena, packed in slot order.
 static __global__ void planner_compact_offsets(PlannerState st, int64_t* new_off) {

@@ -28,6 +28,7 @@ struct dcp_planner {
     int64_t arena_top_host = 0;      // upper bound between syncs
     int64_t waiting_pages_bound = 0; // sum over queued requests of their max arena demand
     std::vector<int64_t> queued_len; // per slot (for the bound)
+    std::vector<uint8_t> is_active;  // host mirror of state == ACTIVE (set by step results / allocate)
     int32_t queued = 0;
     struct Retired {
         int32_t k, moe;
