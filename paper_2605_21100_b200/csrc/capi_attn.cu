@@ -2,6 +2,7 @@
 // C ABI: context + K1/K9 split-KV paged decode attention (dcp_capi.h).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "capi_common.cuh"
@@ -39,9 +40,9 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // columns = head_dim (bf16).  Box = 64 columns (128 B, 128B swizzle) x all
 // rows of one frame.
 static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv, int d,
-                         const CUtensorMap** out) {
+                         const CUtensorMap** out, bool split) {
     for (auto& e : ctx->kv_maps) {
-        if (e.base == pool && e.frames == frames && e.hkv == hkv && e.d == d) {
+        if (e.base == pool && e.frames == frames && e.hkv == hkv && e.d == d && e.split == split) {
             *out = &e.map;
             return DCP_OK;
         }
@@ -54,7 +55,7 @@ static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(d),
                           static_cast<cuuint64_t>(frames) * rows_per_frame};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows_per_frame)};
+    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(split ? rows_per_frame / 2 : rows_per_frame)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims,
                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -68,39 +69,54 @@ static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv
     e.frames = frames;
     e.hkv = hkv;
     e.d = d;
+    e.split = split;
     *out = &e.map;
     return DCP_OK;
 }
 
-template <int HKV, int G>
+template <int HKV, int G, bool SPLIT>
 static int ensure_attr(dcp_ctx* ctx) {
-    using C = DecodeCfg<HKV, G>;
+    using C = DecodeCfg<HKV, G, SPLIT>;
     static uint64_t attr_done = 0;  // per-instantiation bit per device
     if (!(attr_done >> (ctx->device & 63) & 1)) {
-        DCP_CUDA_TRY(cudaFuncSetAttribute(splitkv_decode_kernel<HKV, G>,
+        DCP_CUDA_TRY(cudaFuncSetAttribute(splitkv_decode_kernel<HKV, G, SPLIT>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_done |= uint64_t(1) << (ctx->device & 63);
     }
     return DCP_OK;
 }
 
-template <int HKV, int G>
+template <int HKV, int G, bool SPLIT>
 static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm,
                          cudaStream_t stream) {
-    using C = DecodeCfg<HKV, G>;
-    if (int rc = ensure_attr<HKV, G>(ctx)) return rc;
-    splitkv_decode_kernel<HKV, G><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
+    using C = DecodeCfg<HKV, G, SPLIT>;
+    if (int rc = ensure_attr<HKV, G, SPLIT>(ctx)) return rc;
+    splitkv_decode_kernel<HKV, G, SPLIT><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
 
+// K1 ring variant: env DCP_K1_SPLIT=1 selects split half-frame stages (default: whole frames).
+static bool k1_split() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = std::getenv("DCP_K1_SPLIT");
+        v = e ? (std::atoi(e) != 0) : 0;
+    }
+    return v != 0;
+}
+
 static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm, int hkv, int G,
                            cudaStream_t s) {
-    if (hkv == 8 && G == 4) return launch_decode<8, 4>(ctx, map, prm, s);
-    if (hkv == 4 && G == 8) return launch_decode<4, 8>(ctx, map, prm, s);
-    if (hkv == 8 && G == 1) return launch_decode<8, 1>(ctx, map, prm, s);
-    if (hkv == 2 && G == 16) return launch_decode<2, 16>(ctx, map, prm, s);
-    if (hkv == 1 && G == 16) return launch_decode<1, 16>(ctx, map, prm, s);
+    const bool sp = k1_split();
+#define DCP_K1(H_, G_) \
+    if (hkv == H_ && G == G_) return sp ? launch_decode<H_, G_, true>(ctx, map, prm, s) : launch_decode<H_, G_, false>(ctx, map, prm, s);
+    DCP_K1(8, 4)
+    DCP_K1(4, 8)
+    DCP_K1(8, 1)
+    DCP_K1(2, 16)
+    DCP_K1(1, 16)
+#undef DCP_K1
     set_error("unsupported (num_kv_heads=%d, group=%d)", hkv, G);
     return DCP_E_UNSUPPORTED;
 }
@@ -110,11 +126,15 @@ static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParam
 using namespace dcp;
 
 int dcp_attn_prepare(dcp_ctx* ctx, int hkv, int G) {
-    if (hkv == 8 && G == 4) return ensure_attr<8, 4>(ctx);
-    if (hkv == 4 && G == 8) return ensure_attr<4, 8>(ctx);
-    if (hkv == 8 && G == 1) return ensure_attr<8, 1>(ctx);
-    if (hkv == 2 && G == 16) return ensure_attr<2, 16>(ctx);
-    if (hkv == 1 && G == 16) return ensure_attr<1, 16>(ctx);
+    const bool sp = k1_split();
+#define DCP_K1A(H_, G_) \
+    if (hkv == H_ && G == G_) return sp ? ensure_attr<H_, G_, true>(ctx) : ensure_attr<H_, G_, false>(ctx);
+    DCP_K1A(8, 4)
+    DCP_K1A(4, 8)
+    DCP_K1A(8, 1)
+    DCP_K1A(2, 16)
+    DCP_K1A(1, 16)
+#undef DCP_K1A
     set_error("unsupported (num_kv_heads=%d, group=%d)", hkv, G);
     return DCP_E_UNSUPPORTED;
 }
@@ -190,7 +210,7 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     const int G = a->num_q_heads / a->num_kv_heads;
 
     const CUtensorMap* map = nullptr;
-    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map);
+    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, k1_split());
     if (rc) return rc;
 
     AttnParams prm{};
@@ -226,7 +246,7 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     const size_t need = dcp_attn_workspace_bytes(ctx, x->cfg.n_max, a->num_q_heads, a->head_dim);
     DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu", a->workspace_bytes, need);
     const CUtensorMap* map = nullptr;
-    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map);
+    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, k1_split());
     if (rc) return rc;
     AttnParams prm{};
     prm.q = reinterpret_cast<const __nv_bfloat16*>(x->pool + x->off_qrecv);

@@ -38,6 +38,7 @@ struct TmapCacheEntry {
     int64_t frames = 0;
     int hkv = 0;
     int d = 0;
+    bool split = false;
     CUtensorMap map;
 };
 

@@ -75,16 +75,23 @@ __device__ __forceinline__ void publish_row(const AttnParams& p, int r) {
     st_release_sys(x.res_flag[p.n_moe[r]] + (size_t)p.n_mrow[r] * x.W + x.self, *x.epoch);
 }
 
-template <int HKV, int G>
+// SPLIT = false: a ring stage is one whole frame (K and V of every kv-head).
+// SPLIT = true:  a ring stage is half a frame (the K part or the V part); the
+// K half is released right after QK^T, and the finer ring fits 3.5 frames in
+// flight instead of 3 (7 x 32 KB vs 3 x 64 KB at 8 kv-heads).
+template <int HKV, int G, bool SPLIT = false>
 struct DecodeCfg {
     static constexpr int D = 128;
     static constexpr int PAGE = 16;
     static constexpr int HQ = HKV * G;
     static constexpr int ROWS = 2 * HKV * PAGE;       // 2-D tensor rows per frame
-    static constexpr int BOX_BYTES = ROWS * 128;      // one 64-column swizzled box
-    static constexpr int STAGE_BYTES = 2 * BOX_BYTES; // == one frame
-    static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int HALF = HKV * PAGE;           // rows of the K (or V) part
+    static constexpr int BOX_ROWS = SPLIT ? HALF : ROWS;
+    static constexpr int BOX_BYTES = BOX_ROWS * 128;  // one 64-column swizzled box
+    static constexpr int STAGE_BYTES = 2 * BOX_BYTES; // a frame, or half a frame when SPLIT
+    static constexpr int V_ROW = SPLIT ? 0 : HALF;    // first V row inside a stage
+    static constexpr int STAGES_RAW = ((SPLIT ? 224 : 192) * 1024) / STAGE_BYTES;
+    static constexpr int STAGES = STAGES_RAW > 16 ? 16 : STAGES_RAW;
     static constexpr int CONSUMERS = HKV;             // warps
     static constexpr int THREADS = (HKV + 1) * 32;
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
@@ -102,10 +109,10 @@ __device__ __forceinline__ bool cta_nonempty(int64_t k, int64_t P, int64_t grid)
     return P >= grid || (k * P / grid) < ((k + 1) * P / grid);
 }
 
-template <int HKV, int G>
-__global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
+template <int HKV, int G, bool SPLIT = false>
+__global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT>::THREADS, 1)
     splitkv_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnParams p) {
-    using C = DecodeCfg<HKV, G>;
+    using C = DecodeCfg<HKV, G, SPLIT>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -150,15 +157,19 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                 const int fl = __shfl_sync(0xffffffffu, fill, i);
                 if (lane == 0) {
                     const int it = base - p_begin + i;
-                    const int s = it % C::STAGES;
-                    const uint32_t ph = (it / C::STAGES) & 1;
-                    mbar_wait(empty_bar + 8 * s, ph ^ 1);
-                    stage_fill[s] = static_cast<uint8_t>(fl);
-                    mbar_arrive_expect_tx(full_bar + 8 * s, C::STAGE_BYTES);
-                    const uint32_t dst = smem_base + s * C::STAGE_BYTES;
-                    const int row = f * C::ROWS;
-                    tma_load_2d(dst, &kv_map, 0, row, full_bar + 8 * s, policy);
-                    tma_load_2d(dst + C::BOX_BYTES, &kv_map, 64, row, full_bar + 8 * s, policy);
+#pragma unroll
+                    for (int part = 0; part < (SPLIT ? 2 : 1); ++part) {
+                        const int j = SPLIT ? 2 * it + part : it;
+                        const int s = j % C::STAGES;
+                        const uint32_t ph = (j / C::STAGES) & 1;
+                        mbar_wait(empty_bar + 8 * s, ph ^ 1);
+                        if (part == 0) stage_fill[s] = static_cast<uint8_t>(fl);
+                        mbar_arrive_expect_tx(full_bar + 8 * s, C::STAGE_BYTES);
+                        const uint32_t dst = smem_base + s * C::STAGE_BYTES;
+                        const int row = f * C::ROWS + part * C::HALF;
+                        tma_load_2d(dst, &kv_map, 0, row, full_bar + 8 * s, policy);
+                        tma_load_2d(dst + C::BOX_BYTES, &kv_map, 64, row, full_bar + 8 * s, policy);
+                    }
                 }
                 __syncwarp();
             }
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
         const int tok = (mi & 1) * 8 + rr;
         const int dchunk = 2 * np + (mi >> 1);
         const int box = dchunk >> 3, chunk = dchunk & 7;
-        const int row = HKV * C::PAGE + h * C::PAGE + tok;
+        const int row = C::V_ROW + h * C::PAGE + tok;
         v_off[np] = box * C::BOX_BYTES + row * 128 + ((chunk ^ rr) << 4);
     }
 
@@ -265,8 +276,11 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
         float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
         for (; pg < seg_end; ++pg, ++it) {
-            const int s = it % C::STAGES;
-            const uint32_t ph = (it / C::STAGES) & 1;
+            const int jk = SPLIT ? 2 * it : it;      // ring item of the K part
+            const int s = jk % C::STAGES;
+            const uint32_t ph = (jk / C::STAGES) & 1;
+            const int sv = SPLIT ? (jk + 1) % C::STAGES : s;
+            const uint32_t phv = SPLIT ? ((jk + 1) / C::STAGES) & 1 : ph;
             int fill;
             if (p.page_fill) {
                 mbar_wait(full_bar + 8 * s, ph);
@@ -277,6 +291,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                 mbar_wait(full_bar + 8 * s, ph);
             }
             const uint32_t st = smem_base + s * C::STAGE_BYTES;
+            const uint32_t stv = smem_base + sv * C::STAGE_BYTES;
 
             // ---- S = Q K^T (16 rows x 16 tokens) ----
             float sc[2][4];
@@ -348,6 +363,12 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
                 }
             }
 
+            if constexpr (SPLIT) {  // K half consumed: hand it back before waiting for V
+                __syncwarp();
+                if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+                mbar_wait(full_bar + 8 * sv, phv);
+            }
+
             // ---- O += P V ----
             const uint32_t pa0 = pack_bf16x2(sc[0][0], sc[0][1]);
             const uint32_t pa2 = pack_bf16x2(sc[1][0], sc[1][1]);
@@ -356,12 +377,12 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G>::THREADS, 1)
 #pragma unroll
             for (int np = 0; np < 8; ++np) {
                 uint32_t b0, b1, b2, b3;
-                ldsm_x4_t(st + v_off[np], b0, b1, b2, b3);
+                ldsm_x4_t(stv + v_off[np], b0, b1, b2, b3);
                 mma_bf16_16816(acc[2 * np], pa0, pa1, pa2, pa3, b0, b1);
                 mma_bf16_16816(acc[2 * np + 1], pa0, pa1, pa2, pa3, b2, b3);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(empty_bar + 8 * s);
+            if (lane == 0) mbar_arrive(empty_bar + 8 * sv);
         }
 
         // ---- finalize the segment [seg_begin, seg_end) of shard r ----
