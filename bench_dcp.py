@@ -132,8 +132,74 @@ def run_policy(policy, args, ctx, pools):
     return res
 
 
+def run_multi(args):
+    """One instance per rank (torchrun): the routed step with real peer stores
+    over NVLink between GPUs.  The planner runs as an identical replica on
+    every rank (checked by digest); ranks step in lock-step (host barrier
+    between steps, outside the timed region); step latency = max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2605_21100_b200 import multi
+    from paper_2605_21100_b200.attention import DcpContext
+    from paper_2605_21100_b200.dcp_step import DcpInstance
+    from paper_2605_21100_b200.planner import DevicePlanner
+    from paper_2605_21100_b200._capi import device_to_numpy
+
+    rank, ws, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    ctx = DcpContext(local)
+    results = []
+    for policy in args.policies.split(","):
+        pl = DevicePlanner(ctx, 1, ws, 16, args.capacity, policy, None, max_requests=2048, reserve_pages=64)
+        n_short = args.short_per * ws
+        pos_long = set(np.linspace(0, n_short, args.long + 2, dtype=int)[1:-1].tolist())
+        lens = [args.long_len if i in pos_long else args.short_len for i in range(n_short + args.long)]
+        ids = list(range(len(lens)))
+        pl.enqueue_many(ids, lens)
+        active = pl.step()["committed"]
+        g = torch.Generator(device=dev).manual_seed(1 + rank)
+        pool = torch.randn(args.capacity, 2, 8, 16, 128, generator=g, device=dev, dtype=torch.bfloat16)
+        inst = DcpInstance(ctx, ws, rank, 32, 8, args.capacity, kv_pool=pool, n_max=512, m_max=512)
+        multi.connect_peers(inst, multi.exchange_handles(inst.ipc_handle()))
+        pl.build_routing()
+        multi.check_replicas(pl.routing_csv())
+        q_all = torch.randn(len(ids), 32, 128, generator=torch.Generator(device=dev).manual_seed(3), device=dev
+                            ).to(torch.bfloat16)
+        steps = []
+        for step in range(args.warmup + args.steps):
+            pl.append_many(active)
+            pl.build_routing()
+            v = pl.instance_view(rank)
+            mids = device_to_numpy(v.m_ids, v.m_rows, np.int64)
+            if len(mids):
+                inst.write_queries(q_all[torch.from_numpy(mids).to(dev)])
+            torch.cuda.synchronize(dev)
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            inst.run(v)
+            b.record()
+            torch.cuda.synchronize(dev)
+            if step >= args.warmup:
+                steps.append(multi.max_over_ranks(a.elapsed_time(b), dev))
+        st = np.array(steps)
+        results.append({"policy": policy, "ranks": ws, "requests": len(active),
+                        "step_ms_p50": float(np.percentile(st, 50)), "step_ms_p99": float(np.percentile(st, 99)),
+                        "step_ms_mean": float(st.mean()), "decode_tok_s": len(active) / (st.mean() / 1e3)})
+        dist.barrier()
+        inst.close()
+        pl.close()
+    if rank == 0:
+        for r in results:
+            print(json.dumps(r), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
+    ap.add_argument("--multi", action="store_true", help="torchrun: one instance per GPU, real NVLink exchange")
     ap.add_argument("--instances", type=int, default=4)
     ap.add_argument("--short-per", type=int, default=64)
     ap.add_argument("--short-len", type=int, default=2048)
@@ -145,6 +211,8 @@ def main():
     ap.add_argument("--n-sched", type=int, default=8)
     ap.add_argument("--policies", default="dcp,least_batch,least_cache")
     args = ap.parse_args()
+    if args.multi:
+        return run_multi(args)
     import torch
     from paper_2605_21100_b200.attention import DcpContext
     ctx = DcpContext(0)
