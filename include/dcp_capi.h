@@ -376,6 +376,17 @@ DCP_API int dcp_step_graph_launch(dcp_step_graph* g, int32_t m_rows, int32_t n_r
 DCP_API int dcp_step_graph_count(const dcp_step_graph* g, int32_t* buckets);
 DCP_API int dcp_step_graph_destroy(dcp_step_graph* g);
 
+/* ---- K8: kv_append — the decode step's new K/V into the paged pools ----------
+ * After dcp_planner_append_token + dcp_planner_build_routing, write each
+ * request's new-token K and V (bf16 [M][2][num_kv_heads][head_dim], in the
+ * M-row order of `instance`, i.e. produced at the MoE binding) into the frame
+ * and slot that append_token chose (page_table.cpp:86-121) — on whichever
+ * instance holds it.  pools[s] (host array of W device pointers) is instance
+ * s's KV pool [frames][2][num_kv_heads][page_size][head_dim] as addressable
+ * from this device (local pointer, or a peer / CUDA-IPC mapping). */
+DCP_API int dcp_kv_append(dcp_planner* pl, int32_t instance, const void* kv_new, void* const* pools,
+                          int32_t num_kv_heads, int32_t head_dim, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -164,6 +164,7 @@ _SIGNATURES = [
     ("dcp_step_graph_launch", c_int, [c_void_p, c_int32, c_int32, c_void_p]),
     ("dcp_step_graph_count", c_int, [c_void_p, c_void_p]),
     ("dcp_step_graph_destroy", c_int, [c_void_p]),
+    ("dcp_kv_append", c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
     ("dcp_moe_create", c_int, [c_void_p, POINTER(MoeConfig), POINTER(c_void_p)]),
     ("dcp_moe_destroy", c_int, [c_void_p]),
     ("dcp_moe_ipc_handle", c_int, [c_void_p, c_void_p]),

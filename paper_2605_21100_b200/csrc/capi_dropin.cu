@@ -29,6 +29,7 @@ __global__ void set_queue_kernel(PlannerState st, const int32_t* slots, const in
             st.page_cnt[sl] = 0;
             st.page_cap[sl] = 0;
             st.trailing_fill[sl] = 0;
+            st.last_append[sl] = -1;
         }
         st.waiting[i] = sl;
     }
@@ -419,6 +420,7 @@ int dcp_binding_config(dcp_ctx* ctx, int32_t n, const int64_t* ids, const int32_
     rc |= dalloc_tmp(&st.moe, n, tf.v);
     rc |= dalloc_tmp(&st.kv, (size_t)n * PL_MAXK, tf.v);
     rc |= dalloc_tmp(&st.shard_tokens, (size_t)n * W, tf.v);
+    rc |= dalloc_tmp(&st.last_append, n, tf.v);
     rc |= dalloc_tmp(&st.sk1, sort_cap, tf.v);
     rc |= dalloc_tmp(&st.sk2, sort_cap, tf.v);
     rc |= dalloc_tmp(&st.sval, sort_cap, tf.v);

@@ -6,6 +6,8 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cuda_bf16.h>
+
 #include "capi_common.cuh"
 #include "planner.cuh"
 #include "routing.cuh"
@@ -24,6 +26,31 @@ __global__ void init_stacks_kernel(int32_t* stack, int W, int64_t cap) {
     }
 }
 
+// K8: one warp per M row; 16-byte stores of the new K and V rows of every
+// kv-head into the (frame, slot) of the request's last page.
+__global__ void kv_append_kernel(PlannerState st, const int32_t* m_slot, const int32_t* m_count,
+                                 const __nv_bfloat16* kv_new, __nv_bfloat16* const* pools, int hkv, int d) {
+    const int M = *m_count;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int r = warp; r < M; r += nwarps) {
+        const int sl = m_slot[r];
+        if (st.last_append[sl] < 0) continue;  // growth stall: the token was not added
+        const int c = st.page_cnt[sl];
+        const int64_t last = st.page_off[sl] + c - 1;
+        const int tgt = st.pg_inst[last];
+        const int64_t frame = st.pg_frame[last];
+        const int64_t slot = st.trailing_fill[sl] - 1;
+        const int vec = d / 8;
+        for (int i = lane; i < 2 * hkv * vec; i += 32) {
+            const int kvh = i / vec, v = i % vec;  // kvh = kv * hkv + head
+            const uint4* src = reinterpret_cast<const uint4*>(kv_new + ((size_t)r * 2 * hkv + kvh) * d) + v;
+            uint4* dst = reinterpret_cast<uint4*>(pools[tgt] + (((frame * 2 * hkv) + kvh) * st.page + slot) * d) + v;
+            *dst = *src;
+        }
+    }
+}
+
 __global__ void enqueue_kernel(PlannerState st, const int32_t* slots, const int64_t* ids,
                                const int64_t* lens, int n) {
     const int base = *st.nwait;
@@ -38,6 +65,7 @@ __global__ void enqueue_kernel(PlannerState st, const int32_t* slots, const int6
         st.page_cnt[sl] = 0;
         st.page_cap[sl] = 0;
         st.trailing_fill[sl] = 0;
+        st.last_append[sl] = -1;
         st.waiting[base + i] = sl;
     }
     __syncthreads();
@@ -184,6 +212,7 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     rc |= dalloc(&st.page_cap, S, o);
     rc |= dalloc(&st.trailing_fill, S, o);
     rc |= dalloc(&st.shard_tokens, S * W, o);
+    rc |= dalloc(&st.last_append, S, o);
     rc |= dalloc(&st.pg_inst, st.arena_cap, o);
     rc |= dalloc(&st.pg_frame, st.arena_cap, o);
     rc |= dalloc(&st.pg_fill, st.arena_cap, o);
@@ -585,6 +614,28 @@ int64_t dcp_planner_dump_routing(dcp_planner* pl, char* buf, int64_t cap) {
     }
     if (cudaGetLastError() != cudaSuccess) return DCP_E_CUDA;
     return emit(out, buf, cap);
+}
+
+int dcp_kv_append(dcp_planner* pl, int32_t s, const void* kv_new, void* const* pools, int32_t hkv, int32_t d,
+                  void* stream) {
+    DCP_REQUIRE(pl && pools, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(s >= 0 && s < pl->st.W, DCP_E_INVALID_ARG, "instance %d out of range", s);
+    DCP_REQUIRE(pl->routing_valid, DCP_E_INVALID_ARG, "call dcp_planner_build_routing after append_token");
+    DCP_REQUIRE(d % 8 == 0 && hkv >= 1, DCP_E_UNSUPPORTED, "head_dim %d", d);
+    if (!pl->d_pools) {
+        void* q = nullptr;
+        DCP_CUDA_TRY(cudaMalloc(&q, PL_MAXW * sizeof(void*)));
+        pl->owned.push_back(q);
+        pl->d_pools = static_cast<__nv_bfloat16**>(q);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    DCP_CUDA_TRY(cudaMemcpyAsync(pl->d_pools, pools, pl->st.W * sizeof(void*), cudaMemcpyHostToDevice, st));
+    const size_t S = pl->cfg.max_requests;
+    kv_append_kernel<<<64, 256, 0, st>>>(pl->st, pl->ro.m_slot + (size_t)s * S, pl->ro.m_count + s,
+                                         static_cast<const __nv_bfloat16*>(kv_new), pl->d_pools, hkv, d);
+    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(cudaStreamSynchronize(st));  // the staged pool table is reused
+    return DCP_OK;
 }
 
 int dcp_planner_instance_view(dcp_planner* pl, int32_t s, dcp_instance_view* v) {

@@ -64,6 +64,7 @@ struct PlannerState {
     int32_t* page_cap;     // [S]
     int64_t* trailing_fill;// [S]
     int64_t* shard_tokens; // [S][W]
+    int32_t* last_append;  // [S] instance that received the latest append_token, -1 = stall
     int32_t* pg_inst;      // arena [arena_cap]
     int32_t* pg_frame;     // arena
     uint8_t* pg_fill;      // arena: valid tokens of each page
@@ -590,6 +591,7 @@ static __global__ void planner_append_kernel(PlannerState st, const int32_t* slo
                 st.kv_load[target] += 1;
                 st.shard_tokens[(int64_t)sl * W + target] += 1;
                 st.generated[sl] += 1;
+                st.last_append[sl] = target;
                 out_inst[q] = target;
             }
             __syncwarp();
@@ -604,7 +606,10 @@ static __global__ void planner_append_kernel(PlannerState st, const int32_t* slo
             }
         }
         if (target < 0) {
-            if (lane == 0) out_inst[q] = -1;
+            if (lane == 0) {
+                out_inst[q] = -1;
+                st.last_append[sl] = -1;
+            }
             __syncwarp();
             continue;
         }
@@ -640,6 +645,7 @@ static __global__ void planner_append_kernel(PlannerState st, const int32_t* slo
             st.kv_load[target] += 1;
             st.shard_tokens[(int64_t)sl * W + target] += 1;
             st.generated[sl] += 1;
+            st.last_append[sl] = target;
             out_inst[q] = target;
         }
         __syncwarp();
@@ -756,6 +762,7 @@ static __global__ void __launch_bounds__(PL_APPEND_THREADS, 1)
         atomicAdd(&kv_add[tgt], 1ull);
         st.shard_tokens[(int64_t)sl * W + tgt] += 1;
         st.generated[sl] += 1;
+        st.last_append[sl] = tgt;
         out_inst[q] = tgt;
     }
     __syncthreads();

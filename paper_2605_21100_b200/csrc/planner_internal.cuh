@@ -1,6 +1,8 @@
 // SPDX-License-Identifier: Apache-2.0
 // Host-side definition of dcp_planner shared by capi_planner.cu and capi_dropin.cu.
 #pragma once
+#include <cuda_bf16.h>
+
 #include <unordered_map>
 #include <vector>
 
@@ -41,6 +43,7 @@ struct dcp_planner {
     cudaStream_t stream = nullptr;
     int last_launches = 0;
     bool routing_valid = false;
+    __nv_bfloat16** d_pools = nullptr;  // K8 pool table
 };
 
 namespace dcp {

@@ -135,3 +135,11 @@ class DevicePlanner:
         v = _capi.InstanceView()
         _capi.check(_capi.lib().dcp_planner_instance_view(self.h, s, ctypes.byref(v)))
         return v
+
+    def kv_append(self, instance, kv_new, pools, stream=None):
+        """K8: new-token K/V (bf16 [M, 2, hkv, d], M-row order of `instance`)
+        into the frame/slot append_token chose, on whichever instance holds it."""
+        arr = (ctypes.c_void_p * self.W)(*[p.data_ptr() for p in pools])
+        s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        hkv, d = kv_new.shape[2], kv_new.shape[3]
+        _capi.check(_capi.lib().dcp_kv_append(self.h, instance, ctypes.c_void_p(kv_new.data_ptr()), arr, hkv, d, s))
