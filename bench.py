@@ -222,15 +222,16 @@ def run_ours(args, ws, rank, local):
     _barrier(ws)
 
     # ---- device-timed region: K steps, inputs resident in HBM (> L2: no flush needed)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
-        e0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             att.launch(stream)
-        e1.record(stream)
+            evs[i + 1].record(stream)
         torch.cuda.synchronize(dev)
-    ms_total = e0.elapsed_time(e1)
+    ms_total = evs[0].elapsed_time(evs[-1])
+    per_step = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)])
     _barrier(ws)
     ms_total = _max_over_ranks(ms_total, ws, dev)
     ms_step = ms_total / args.steps
@@ -301,6 +302,7 @@ def run_ours(args, ws, rank, local):
                     "d2h_bytes_per_step": d2h,
                     "path": "dcp_splitkv_decode_attn via C ABI; pinned host Q/block-table/lengths in, O+LSE out"},
             "gpu_launches": args.steps * _capi_launches(),
+            "step_ms_p50": float(np.percentile(per_step, 50)), "step_ms_p99": float(np.percentile(per_step, 99)),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel": "splitkv_decode_kernel<8,4>",

@@ -1,0 +1,187 @@
+#!/usr/bin/env python3
+"""Trace-driven decode serving on the device path: DCP vs CP=1 baselines.
+
+The simengine-equivalent metrics driver of SURVEY §8(f)#3 over real GPU steps
+(SPEC.md:432-460 metrics: per-step latency P50/P99, TPOT, SLO attainment,
+HoL events, CP histogram).  Requests arrive from the reference's gen_trace
+(ShareGPT-4o short mix + GitHub-Issue long mix, workload.cpp:73-106); every
+n_sched iterations the device planner (K6) admits arrivals; every iteration
+each active request decodes one token: append_token (K6), routing (K7), the
+routed attention step per instance (K2 + K1 + K3), finished requests are
+released.  Single-GPU emulation of a W-instance node: each instance's kernels
+are timed alone; the iteration's attention latency is the max over
+instances, and the simulated clock advances by layers x that latency.
+
+    python bench_trace.py [--instances 8] [--rate 8] [--duration 20] [--long-ratio 0.01]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def run(policy, trace, args, ctx, pools):
+    import torch
+    from paper_2605_21100_b200.dcp_step import DcpInstance
+    from paper_2605_21100_b200.planner import DevicePlanner
+    from paper_2605_21100_b200._capi import device_to_numpy
+
+    W, HQ, HKV = args.instances, 32, 8
+    dev = torch.device("cuda:0")
+    pl = DevicePlanner(ctx, 1, W, 16, args.capacity, policy, None, hol_strict=True,
+                       uniform_degree=args.uniform_degree, max_requests=4096, reserve_pages=64)
+    insts = [DcpInstance(ctx, W, s, HQ, HKV, args.capacity, kv_pool=pools[s], n_max=512, m_max=256)
+             for s in range(W)]
+    for s in range(W):
+        for t in range(W):
+            insts[s].set_peer_local(t, insts[t])
+        insts[s].commit()
+    g = torch.Generator(device=dev).manual_seed(11)
+    qbank = torch.randn(64, HQ, 128, generator=g, device=dev).to(torch.bfloat16)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_ms, it = 0.0, 0
+    nxt = 0
+    queued = set()
+    active, remaining, start, out_len = [], {}, {}, {}
+    step_ms, tpot, cp_of, hol, sched_ms = [], [], {}, 0, []
+    finished = 0
+    while it < args.max_iters:
+        if it % args.n_sched == 0:
+            new = []
+            while nxt < len(trace) and trace[nxt][1] <= t_ms:
+                new.append(trace[nxt])
+                nxt += 1
+            if new:
+                pl.enqueue_many([r[0] for r in new], [r[2] for r in new])
+                for r in new:
+                    queued.add(r[0])
+                    out_len[r[0]] = r[3]
+            if queued:
+                a, b = ev(), ev()
+                a.record()
+                pl.step_async()
+                b.record()
+                res = pl.step_result()
+                sched_ms.append(a.elapsed_time(b))
+                hol += res["hol_events"]
+                for rid in res["committed"]:
+                    queued.discard(rid)
+                    active.append(rid)
+                    remaining[rid] = out_len[rid]
+                    start[rid] = t_ms
+                    cp_of[rid] = len(pl.placement(rid)["kv"])
+                for rid in res["unschedulable"]:
+                    queued.discard(rid)
+        if not active:
+            if nxt >= len(trace) and not queued:
+                break
+            t_ms = max(t_ms, trace[nxt][1]) if nxt < len(trace) else t_ms + 1.0
+            it += 1
+            continue
+        pl.append_many(active)
+        pl.build_routing()
+        views = [pl.instance_view(s) for s in range(W)]
+        for s in range(W):
+            v = views[s]
+            mids = device_to_numpy(v.m_ids, v.m_rows, np.int64)
+            if len(mids):
+                insts[s].write_queries(qbank[torch.from_numpy(mids % 64).to(dev)])
+        per = [0.0] * W
+        marks = []
+        for ph in ("q", "attn", "merge"):
+            for s in range(W):
+                a, b = ev(), ev()
+                a.record()
+                insts[s].run(views[s], None, ph)
+                b.record()
+                marks.append((s, a, b))
+        torch.cuda.synchronize(dev)
+        for s, a, b in marks:
+            per[s] += a.elapsed_time(b)
+        lat = max(per)
+        step_ms.append(lat)
+        t_ms += args.layers * lat
+        done = []
+        for rid in active:
+            remaining[rid] -= 1
+            if remaining[rid] <= 0:
+                done.append(rid)
+        for rid in done:
+            pl.finish(rid)
+            active.remove(rid)
+            tpot.append((t_ms - start[rid]) / out_len[rid])
+            finished += 1
+        it += 1
+    for x in insts:
+        x.close()
+    pl.close()
+    st, tp = np.array(step_ms), np.array(tpot) if tpot else np.array([0.0])
+    ks = list(cp_of.values())
+    return {
+        "policy": policy if policy != "uniform" else f"uniform{args.uniform_degree}",
+        "iterations": len(step_ms), "finished": finished, "admitted": len(cp_of),
+        "step_ms_p50": float(np.percentile(st, 50)), "step_ms_p99": float(np.percentile(st, 99)),
+        "step_ms_max": float(st.max()),
+        "tpot_ms_mean": float(tp.mean()), "tpot_ms_p99": float(np.percentile(tp, 99)),
+        "slo_attainment": float((tp <= args.slo_ms).mean()),
+        "hol_events": hol, "cp_histogram": {str(k): ks.count(k) for k in sorted(set(ks))},
+        "planner_step_ms_mean": float(np.mean(sched_ms)) if sched_ms else None,
+        "sim_time_s": t_ms / 1e3,
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--instances", type=int, default=8)
+    ap.add_argument("--capacity", type=int, default=64000)
+    ap.add_argument("--rate", type=float, default=8.0)
+    ap.add_argument("--duration", type=float, default=20.0)
+    ap.add_argument("--long-ratio", type=float, default=0.01)
+    ap.add_argument("--seed", type=int, default=7)
+    ap.add_argument("--out-min", type=int, default=32)
+    ap.add_argument("--out-max", type=int, default=128)
+    ap.add_argument("--layers", type=int, default=48, help="attention layers per decode iteration")
+    ap.add_argument("--slo-ms", type=float, default=50.0)
+    ap.add_argument("--n-sched", type=int, default=4)
+    ap.add_argument("--max-iters", type=int, default=4000)
+    ap.add_argument("--uniform-degree", type=int, default=8)
+    ap.add_argument("--policies", default="dcp,least_batch,least_cache,uniform")
+    args = ap.parse_args()
+    import torch
+    from paper_2605_21100_b200 import workload
+    from paper_2605_21100_b200.attention import DcpContext
+    trace = workload.gen_trace(args.seed, args.long_ratio, args.rate, args.duration, poisson=True,
+                               output_len=(args.out_min, args.out_max))
+    ctx = DcpContext(0)
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev).manual_seed(1)
+    pools = [torch.randn(args.capacity, 2, 8, 16, 128, generator=g, device=dev, dtype=torch.bfloat16)
+             for _ in range(args.instances)]
+    longs = sum(1 for r in trace if r[2] >= 100000)
+    print(json.dumps({"trace": {"requests": len(trace), "long": longs, "rate_per_s": args.rate,
+                                "duration_s": args.duration, "long_ratio": args.long_ratio,
+                                "max_len": max(r[2] for r in trace)},
+                      "setup": f"{args.instances} instances (single-GPU emulation), GQA 32q/8kv d128 bf16, "
+                               f"{args.layers} layers/iteration, SLO {args.slo_ms} ms TPOT"}), flush=True)
+    results = []
+    for pol in args.policies.split(","):
+        r = run(pol, trace, args, ctx, pools)
+        results.append(r)
+        print(json.dumps(r), flush=True)
+    dcp = next(r for r in results if r["policy"] == "dcp")
+    base = [r for r in results if r["policy"] != "dcp"]
+    if base:
+        best = min(base, key=lambda r: r["step_ms_p99"])
+        print(json.dumps({"p99_step_dcp_vs_best_baseline": best["step_ms_p99"] / dcp["step_ms_p99"],
+                          "best_baseline": best["policy"]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

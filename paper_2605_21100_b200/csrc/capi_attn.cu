@@ -238,6 +238,7 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
                            const dcp_attn_args* a, void* stream) {
     DCP_REQUIRE(ctx && x && v && a, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    DCP_REQUIRE(v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW, "N %d > n_max %d", v->n_rows, x->cfg.n_max);
     DCP_REQUIRE(a->head_dim == 128 && a->page_size == 16, DCP_E_UNSUPPORTED, "head_dim/page_size");
     DCP_REQUIRE(a->num_q_heads == x->cfg.num_q_heads && a->head_dim == x->cfg.head_dim, DCP_E_INVALID_ARG,
                 "exchange pool shape differs from the attention shape");

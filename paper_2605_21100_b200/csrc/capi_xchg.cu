@@ -157,6 +157,10 @@ int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
     DCP_REQUIRE(x && v, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self && v->world == x->cfg.world, DCP_E_INVALID_ARG,
                 "view of instance %d used on instance %d", v->instance, x->cfg.self);
+    // rows beyond the pools would never be put and the receivers would wait forever
+    DCP_REQUIRE(v->m_rows <= x->cfg.m_max && v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW,
+                "execution shape (%d,%d) exceeds the exchange pools (%d,%d)", v->m_rows, v->n_rows, x->cfg.m_max,
+                x->cfg.n_max);
     q_route_put_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         x->dev, static_cast<const __nv_bfloat16*>(x->q_local), v->m_count_all, v->m_nrow);
     DCP_CUDA_TRY(cudaGetLastError());
@@ -166,6 +170,7 @@ int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
 int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
     DCP_REQUIRE(x && v, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    DCP_REQUIRE(v->m_rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", v->m_rows, x->cfg.m_max);
     lse_merge_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
         x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
     DCP_CUDA_TRY(cudaGetLastError());
@@ -174,6 +179,7 @@ int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
 
 struct dcp_step_graph {
     int m_hat[6] = {8, 16, 32, 64, 128, 256};
+    int m_max = 0, n_max = 0;
     cudaGraphExec_t exec[6] = {};
     cudaGraph_t graph[6] = {};
 };
@@ -187,6 +193,8 @@ int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
     cudaStream_t cs;
     DCP_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     auto* g = new dcp_step_graph();
+    g->m_max = x->cfg.m_max;
+    g->n_max = x->cfg.n_max;
     for (int i = 0; i < 6; ++i) {
         const int mh = std::min(g->m_hat[i], x->cfg.m_max);
         cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
@@ -216,6 +224,8 @@ int dcp_step_graph_launch(dcp_step_graph* g, int32_t m, int32_t n, void* stream)
     DCP_REQUIRE(g, DCP_E_INVALID_ARG, "NULL graph");
     DCP_REQUIRE(m <= 256 && n <= 512 && m >= 0 && n >= 0, DCP_E_SHAPE_OVERFLOW,
                 "execution shape (%d,%d) exceeds (256,512)", m, n);
+    DCP_REQUIRE(m <= g->m_max && n <= g->n_max, DCP_E_SHAPE_OVERFLOW, "execution shape (%d,%d) exceeds the pools",
+                m, n);
     int i = 0;
     while (g->m_hat[i] < m) ++i;  // bucket_shape: first dominating M^ (N^ shares the graph)
     DCP_CUDA_TRY(cudaGraphLaunch(g->exec[i], static_cast<cudaStream_t>(stream)));

@@ -114,3 +114,56 @@ def paged_batch(shard_len, num_q_heads, num_kv_heads, head_dim=128, page_size=16
 def cfg2_lengths():
     """BASELINE configs[1]: 64 requests, uniform_int(mt19937_64(0), 1024, 32768)."""
     return lengths(0, 64, 1024, 32768)
+
+
+# ------------------------------------------------------------------ traces
+# Input generation for the trace-driven benches: the reference's Table-1
+# distributions and gen_trace (workload.hpp:28-74, workload.cpp:11-106),
+# restated so a seed gives the same (arrival, seq_len, output_len) sequence.
+SHAREGPT4O = [(1, 1000, 85.7 / 99.9), (1000, 10000, 10.7 / 99.9), (10000, 100000, 3.5 / 99.9)]
+GITHUB_ISSUE = [(100000, 500000, 0.6506), (500000, 1000000, 0.3494)]
+
+
+def sample_length(dist, rng: MT19937_64, log_uniform: bool = False) -> int:  # workload.cpp:56-71
+    import math
+    u = uniform01(rng)
+    cum = 0.0
+    lo, hi, _ = dist[-1]
+    for b in dist:
+        cum += b[2]
+        if u < cum:
+            lo, hi, _ = b
+            break
+    if log_uniform:
+        a, c = math.log(lo), math.log(hi)
+        v = int(math.exp(a + uniform01(rng) * (c - a)))
+        return min(max(v, lo), hi - 1)
+    return uniform_int(rng, lo, hi - 1)
+
+
+def gen_trace(seed: int, long_ratio: float, rate_per_s: float, duration_s: float, poisson: bool = False,
+              output_len=(64, 512), short=SHAREGPT4O, long=GITHUB_ISSUE):
+    """[(id, arrival_ms, seq_len, output_len)], sorted by arrival (workload.cpp:73-106)."""
+    import math
+    rng = MT19937_64(seed)
+    horizon = duration_s * 1000.0
+    arrivals = []
+    if not poisson:
+        gap = 1000.0 / rate_per_s
+        i = 0
+        while i * gap < horizon:
+            arrivals.append(i * gap)
+            i += 1
+    else:
+        t, mean_gap = 0.0, 1000.0 / rate_per_s
+        while True:
+            t += -math.log(1.0 - uniform01(rng)) * mean_gap
+            if t >= horizon:
+                break
+            arrivals.append(t)
+    out = []
+    for i, a in enumerate(arrivals):
+        is_long = long_ratio > 0.0 and uniform01(rng) < long_ratio
+        L = sample_length(long if is_long else short, rng)
+        out.append((i, a, L, uniform_int(rng, output_len[0], output_len[1])))
+    return out

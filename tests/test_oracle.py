@@ -326,3 +326,18 @@ def test_paged_oracle_matches_reference_on_gathered_kv(port, ref):
                                                   P(np.ascontiguousarray(vv)), L, 128, 1 / np.sqrt(128),
                                                   P(o), P(l)) == 0
             assert np.array_equal(o, out[r, h]) and l[0] == lse[r, h]
+
+
+def test_trace_generator_matches_reference(ref):
+    """The bench trace source (paper_2605_21100_b200.workload.gen_trace) is the
+    reference's gen_trace (workload.cpp:73-106), draw for draw."""
+    from paper_2605_21100_b200 import workload
+    n = 4000
+    for seed, lr, rate, dur, pois in [(42, 0.05, 100.0, 1.0, 0), (7, 0.01, 37.5, 20.0, 1), (0, 0.0, 5.0, 3.0, 1)]:
+        ids, sl, arr, ol = (np.zeros(n, np.int64), np.zeros(n, np.int64), np.zeros(n), np.zeros(n, np.int64))
+        cnt = ref.dcpref_gen_trace(seed, lr, rate, dur, pois, P(ids), P(sl), P(arr), P(ol), n)
+        mine = workload.gen_trace(seed, lr, rate, dur, bool(pois))
+        assert len(mine) == cnt
+        assert [m[2] for m in mine] == sl[:cnt].tolist()
+        assert [m[3] for m in mine] == ol[:cnt].tolist()
+        assert np.allclose([m[1] for m in mine], arr[:cnt], rtol=0, atol=1e-9)
