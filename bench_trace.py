@@ -27,6 +27,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 
+def gate(ctx, us=3000):
+    import ctypes
+    import torch
+    from paper_2605_21100_b200 import _capi
+    s = torch.cuda.current_stream(ctx.device).cuda_stream
+    _capi.check(_capi.lib().dcp_device_sleep(ctx.handle, us, ctypes.c_void_p(s)))
+
+
 def run(policy, trace, args, ctx, pools):
     import torch
     from paper_2605_21100_b200.dcp_step import DcpInstance
@@ -95,6 +103,7 @@ def run(policy, trace, args, ctx, pools):
                 insts[s].write_queries(qbank[torch.from_numpy(mids % 64).to(dev)])
         per = [0.0] * W
         marks = []
+        gate(ctx)  # host enqueues the whole step behind a device sleep: events time device work only
         for ph in ("q", "attn", "merge"):
             for s in range(W):
                 a, b = ev(), ev()

@@ -62,6 +62,10 @@ typedef struct dcp_ctx dcp_ctx;
 DCP_API int dcp_ctx_create(int device, dcp_ctx** out);
 DCP_API int dcp_ctx_destroy(dcp_ctx* ctx);
 DCP_API int dcp_ctx_num_sms(const dcp_ctx* ctx);
+/* Measurement helper: a one-thread kernel that sleeps ~`microseconds` on the
+ * stream, so a host can enqueue a whole step behind it and per-kernel events
+ * then time device work only (no host launch gaps). */
+DCP_API int dcp_device_sleep(dcp_ctx* ctx, int32_t microseconds, void* stream);
 /* Synchronous device->host copy of `bytes` (for hosts that bind only this ABI). */
 DCP_API int dcp_copy_to_host(void* dst, const void* src, size_t bytes);
 

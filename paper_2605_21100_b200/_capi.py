@@ -118,6 +118,7 @@ _SIGNATURES = [
     ("dcp_ctx_destroy", c_int, [c_void_p]),
     ("dcp_ctx_num_sms", c_int, [c_void_p]),
     ("dcp_copy_to_host", c_int, [c_void_p, c_void_p, c_size_t]),
+    ("dcp_device_sleep", c_int, [c_void_p, c_int32, c_void_p]),
     ("dcp_attn_workspace_bytes", c_size_t, [c_void_p, c_int32, c_int32, c_int32]),
     ("dcp_splitkv_decode_attn", c_int, [c_void_p, POINTER(AttnArgs), c_void_p]),
     ("dcp_attn_launches_per_call", c_int, []),

@@ -172,6 +172,22 @@ int dcp_ctx_destroy(dcp_ctx* ctx) {
 
 int dcp_ctx_num_sms(const dcp_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
 
+static __global__ void device_sleep_kernel(int64_t ns) {
+    int64_t g0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+    do {
+        __nanosleep(2000);
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    } while (now - g0 < ns);
+}
+
+int dcp_device_sleep(dcp_ctx* ctx, int32_t us, void* stream) {
+    DCP_REQUIRE(ctx && us >= 0 && us <= 1000000, DCP_E_INVALID_ARG, "sleep %d us", us);
+    device_sleep_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>((int64_t)us * 1000);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
 int dcp_copy_to_host(void* dst, const void* src, size_t bytes) {
     DCP_REQUIRE(dst && (src || bytes == 0), DCP_E_INVALID_ARG, "NULL pointer");
     if (bytes) DCP_CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost));

@@ -563,9 +563,12 @@ int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
     DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
     set_stream(pl, stream);
     routing_rows_kernel<<<1, 1024, 0, pl->stream>>>(pl->st, pl->ro);
-    routing_blocks_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);
+    const dim3 wide(pl->st.W, RT_SPLIT);
+    routing_count_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
+    routing_scan_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);
+    routing_scatter_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
     DCP_CUDA_TRY(cudaGetLastError());
-    pl->last_launches = 2;
+    pl->last_launches = 4;
     pl->routing_valid = true;
     return DCP_OK;
 }

@@ -224,4 +224,100 @@ static __global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerS
     }
 }
 
+
+// ------------------------------------------------------------------ K7 (wide): count / scan / scatter
+// The same output as routing_blocks_kernel, spread over gridDim.y CTAs per
+// instance so a long shard's thousands of pages are not walked by one CTA.
+constexpr int RT_SPLIT = 16;
+static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState st, RoutingOut ro) {
+    const int s = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.y * (blockDim.x >> 5);
+    const int S = st.max_slots, W = st.W;
+    const int rows = ro.n_count[s];
+    int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
+    for (int row = gw; row < rows; row += nw) {
+        const int sl = ro.n_slot[(size_t)s * S + row];
+        const int64_t off = st.page_off[sl];
+        const int np = st.page_cnt[sl];
+        int c = 0;
+        for (int t = lane; t - lane < np; t += 32) {
+            const bool on = t < np && st.pg_inst[off + t] == s;
+            c += __popc(__ballot_sync(0xffffffffu, on));
+        }
+        if (lane == 0) {
+            cu[row + 1] = c;
+            ro.n_mrow[(size_t)s * S + row] = ro.slot_mrow[sl];
+        }
+    }
+    const int mrows = ro.m_count[s];
+    const int gt = blockIdx.y * blockDim.x + threadIdx.x;
+    for (int row = gt; row < mrows; row += gridDim.y * blockDim.x) {
+        const int sl = ro.m_slot[(size_t)s * S + row];
+        const int k = st.k[sl];
+        ro.m_k[(size_t)s * S + row] = k;
+        int32_t* dst = ro.m_nrow + ((size_t)s * S + row) * W;
+        for (int c = 0; c < W; ++c) dst[c] = -1;
+        for (int m = 0; m < k; ++m) {
+            const int sp = st.kv[sl * PL_MAXK + m];
+            ro.m_kv[((size_t)s * S + row) * PL_MAXK + m] = sp;
+            dst[sp] = ro.slot_nrow[(size_t)sl * W + sp];
+        }
+    }
+}
+
+static __global__ void __launch_bounds__(1024) routing_scan_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int64_t part[1024];
+    const int s = blockIdx.x, tid = threadIdx.x;
+    const int S = st.max_slots;
+    const int rows = ro.n_count[s];
+    int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
+    const int per = (rows + blockDim.x - 1) / blockDim.x;
+    int64_t sum = 0;
+    for (int j = tid * per; j < min(rows, (tid + 1) * per); ++j) sum += cu[j + 1];
+    part[tid] = sum;
+    __syncthreads();
+    for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // Hillis-Steele inclusive scan
+        const int64_t v = tid >= o ? part[tid - o] : 0;
+        __syncthreads();
+        part[tid] += v;
+        __syncthreads();
+    }
+    int64_t run = part[tid] - sum;
+    if (tid == 0) cu[0] = 0;
+    for (int j = tid * per; j < min(rows, (tid + 1) * per); ++j) {
+        run += cu[j + 1];
+        cu[j + 1] = (int32_t)run;
+    }
+}
+
+static __global__ void __launch_bounds__(256) routing_scatter_kernel(PlannerState st, RoutingOut ro) {
+    const int s = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int gw = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int nw = gridDim.y * (blockDim.x >> 5);
+    const int S = st.max_slots;
+    const int rows = ro.n_count[s];
+    const int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
+    int32_t* bt = ro.block_table + (size_t)s * st.capacity;
+    uint8_t* pf = ro.page_fill + (size_t)s * st.capacity;
+    for (int row = gw; row < rows; row += nw) {
+        const int sl = ro.n_slot[(size_t)s * S + row];
+        const int64_t off = st.page_off[sl];
+        const int np = st.page_cnt[sl];
+        int pos = cu[row];
+        for (int t = lane; t - lane < np; t += 32) {
+            const bool on = t < np && st.pg_inst[off + t] == s;
+            const unsigned b = __ballot_sync(0xffffffffu, on);
+            if (on) {
+                const int p = pos + __popc(b & ((1u << lane) - 1u));
+                bt[p] = st.pg_frame[off + t];
+                pf[p] = st.pg_fill[off + t];
+            }
+            pos += __popc(b);
+        }
+    }
+}
+
 }  // namespace dcp
