@@ -172,6 +172,68 @@ def cpu_reference_sample(steps: int, token_budget: int = 262_144, threads: int =
     return 64.0 / per_step_full, info
 
 
+# ------------------------------------------------------------------ planner path
+PLANNER_SCENARIO = ("SURVEY §3.1: 1 node x 8 instances, gen_trace(seed 3, 1% long) — 2,336 active requests "
+                    "then one DCP round admitting 64 new (Scheduler::step) + build_binding_config / "
+                    "derive_routing_tables over the 2,400 actives")
+
+
+def _planner_trace():
+    from paper_2605_21100_b200 import workload
+    tr = workload.gen_trace(3, 0.01, 240.0, 10.0, poisson=False)[:2400]
+    return [(r[0], r[2]) for r in tr]
+
+
+def planner_device(ctx):
+    """K6 step + K7 routing on the device for PLANNER_SCENARIO (CUDA events)."""
+    import torch
+    from paper_2605_21100_b200.planner import DevicePlanner
+    tr = _planner_trace()
+    cap = 1 << 21
+    times = []
+    for rep in range(3):
+        pl = DevicePlanner(ctx, 1, 8, 16, cap, "dcp", None, max_requests=4096, reserve_pages=8)
+        pl.enqueue_many([r[0] for r in tr[:2336]], [r[1] for r in tr[:2336]])
+        assert len(pl.step()["committed"]) == 2336
+        pl.enqueue_many([r[0] for r in tr[2336:]], [r[1] for r in tr[2336:]])
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e[0].record()
+        pl.step_async()
+        e[1].record()
+        pl.build_routing()
+        e[2].record()
+        r = pl.step_result()
+        torch.cuda.synchronize()
+        assert len(r["committed"]) == 64
+        times.append((e[0].elapsed_time(e[1]) * 1e3, e[1].elapsed_time(e[2]) * 1e3))
+        pl.close()
+    best = min(times)
+    return {"device_step_us": best[0], "device_routing_us": best[1]}
+
+
+def planner_cpu_reference():
+    """The same round through the reference (oracle/_ref, single thread)."""
+    from tests import oracle_lib
+    L = oracle_lib.reference()
+    tr = _planner_trace()
+    best_s, best_r = 1e9, 1e9
+    for rep in range(3):
+        w = oracle_lib.World(L, "dcpref_", 1, 8, 16, 1 << 21, "dcp")
+        for rid, ln in tr[:2336]:
+            w.enqueue(rid, ln)
+        w.step()
+        for rid, ln in tr[2336:]:
+            w.enqueue(rid, ln)
+        t0 = time.perf_counter()
+        r = w.step()
+        t1 = time.perf_counter()
+        w.routing_csv()  # build_binding_config + derive_routing_tables + the CSV writer
+        t2 = time.perf_counter()
+        assert len(r["committed"]) == 64
+        best_s, best_r = min(best_s, t1 - t0), min(best_r, t2 - t1)
+    return {"cpu_reference_step_us": best_s * 1e6, "cpu_reference_routing_and_csv_us": best_r * 1e6, "cores": 1}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -306,12 +368,20 @@ def run_ours(args, ws, rank, local):
         except Exception:
             traffic = None
 
+    planner = None
+    if rank == 0:
+        try:
+            planner = dict(scenario=PLANNER_SCENARIO, **planner_device(ctx))
+        except Exception as e:  # reported, not fatal
+            planner = {"scenario": PLANNER_SCENARIO, "error": str(e)}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             v, info = cpu_reference_sample(1)
             cpu = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                    "sample": info["sample"]}
+            if planner is not None and "error" not in planner:
+                planner.update(planner_cpu_reference())
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -335,6 +405,7 @@ def run_ours(args, ws, rank, local):
                          "algorithmic_bytes_per_launch": alg_bytes},
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "planner": planner,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
