@@ -92,7 +92,7 @@ DCP_API int dcp_copy_to_host(void* dst, const void* src, size_t bytes);
  * q:   bf16 [num_shards][num_q_heads][head_dim]
  * out: fp32 [num_shards][num_q_heads][head_dim]   softmax-normalised over the shard
  * lse: fp32 [num_shards][num_q_heads]             natural log, as hpp:80
- * Compiled shapes: head_dim 128, page_size 16, (num_kv_heads, group) in
+ * Compiled shapes: head_dim 128, page_size 16 / 32 / 64, (num_kv_heads, group) in
  * {(8,4), (4,8), (8,1), (2,16), (1,16)}.  Other shapes return DCP_E_UNSUPPORTED.
  *
  * workspace: device buffer of dcp_attn_workspace_bytes(...) bytes, zeroed once

@@ -40,9 +40,10 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // columns = head_dim (bf16).  Box = 64 columns (128 B, 128B swizzle) x all
 // rows of one frame.
 static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv, int d,
-                         const CUtensorMap** out, bool split) {
+                         const CUtensorMap** out, bool split, int page = 16) {
     for (auto& e : ctx->kv_maps) {
-        if (e.base == pool && e.frames == frames && e.hkv == hkv && e.d == d && e.split == split) {
+        if (e.base == pool && e.frames == frames && e.hkv == hkv && e.d == d && e.split == split &&
+            e.page == page) {
             *out = &e.map;
             return DCP_OK;
         }
@@ -51,15 +52,28 @@ static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv
     DCP_REQUIRE(fn != nullptr, DCP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     auto& e = ctx->kv_maps[ctx->kv_map_next];
     ctx->kv_map_next = (ctx->kv_map_next + 1) % 4;
-    const int rows_per_frame = 2 * hkv * 16;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(d),
-                          static_cast<cuuint64_t>(frames) * rows_per_frame};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
-    cuuint32_t box[2] = {64, static_cast<cuuint32_t>(split ? rows_per_frame / 2 : rows_per_frame)};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims,
-                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (!split) {
+        // whole-frame ring: rows = frame*2*HKV*16 + (kv*HKV + head)*16 + tok, box = one frame
+        const int rows_per_frame = 2 * hkv * 16;
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(frames) * rows_per_frame};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(d) * 2};
+        cuuint32_t box[2] = {64, static_cast<cuuint32_t>(rows_per_frame)};
+        cuuint32_t estr[2] = {1, 1};
+        r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(pool), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        // split ring: (d, token-in-page, frame*2*HKV + kv*HKV + head); box = 16 tokens of every head
+        cuuint64_t dims[3] = {static_cast<cuuint64_t>(d), static_cast<cuuint64_t>(page),
+                              static_cast<cuuint64_t>(frames) * 2 * hkv};
+        cuuint64_t strides[2] = {static_cast<cuuint64_t>(d) * 2, static_cast<cuuint64_t>(page) * d * 2};
+        cuuint32_t box[3] = {64, 16, static_cast<cuuint32_t>(hkv)};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = fn(&e.map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(pool), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS) {
         e.base = nullptr;
         set_error("cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
@@ -70,28 +84,29 @@ static int kv_tensor_map(dcp_ctx* ctx, const void* pool, int64_t frames, int hkv
     e.hkv = hkv;
     e.d = d;
     e.split = split;
+    e.page = page;
     *out = &e.map;
     return DCP_OK;
 }
 
-template <int HKV, int G, bool SPLIT>
+template <int HKV, int G, bool SPLIT, int PAGE = 16>
 static int ensure_attr(dcp_ctx* ctx) {
-    using C = DecodeCfg<HKV, G, SPLIT>;
+    using C = DecodeCfg<HKV, G, SPLIT, PAGE>;
     static uint64_t attr_done = 0;  // per-instantiation bit per device
     if (!(attr_done >> (ctx->device & 63) & 1)) {
-        DCP_CUDA_TRY(cudaFuncSetAttribute(splitkv_decode_kernel<HKV, G, SPLIT>,
+        DCP_CUDA_TRY(cudaFuncSetAttribute(splitkv_decode_kernel<HKV, G, SPLIT, PAGE>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
         attr_done |= uint64_t(1) << (ctx->device & 63);
     }
     return DCP_OK;
 }
 
-template <int HKV, int G, bool SPLIT>
+template <int HKV, int G, bool SPLIT, int PAGE = 16>
 static int launch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm,
                          cudaStream_t stream) {
-    using C = DecodeCfg<HKV, G, SPLIT>;
-    if (int rc = ensure_attr<HKV, G, SPLIT>(ctx)) return rc;
-    splitkv_decode_kernel<HKV, G, SPLIT><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
+    using C = DecodeCfg<HKV, G, SPLIT, PAGE>;
+    if (int rc = ensure_attr<HKV, G, SPLIT, PAGE>(ctx)) return rc;
+    splitkv_decode_kernel<HKV, G, SPLIT, PAGE><<<ctx->num_sms, C::THREADS, C::SMEM, stream>>>(*map, prm);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
@@ -107,10 +122,14 @@ static bool k1_split() {
 }
 
 static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm, int hkv, int G,
-                           cudaStream_t s) {
+                           cudaStream_t s, int page = 16) {
     const bool sp = k1_split();
-#define DCP_K1(H_, G_) \
-    if (hkv == H_ && G == G_) return sp ? launch_decode<H_, G_, true>(ctx, map, prm, s) : launch_decode<H_, G_, false>(ctx, map, prm, s);
+#define DCP_K1(H_, G_)                                                                                  \
+    if (hkv == H_ && G == G_) {                                                                          \
+        if (page == 32) return launch_decode<H_, G_, true, 32>(ctx, map, prm, s);                        \
+        if (page == 64) return launch_decode<H_, G_, true, 64>(ctx, map, prm, s);                        \
+        return sp ? launch_decode<H_, G_, true>(ctx, map, prm, s) : launch_decode<H_, G_, false>(ctx, map, prm, s); \
+    }
     DCP_K1(8, 4)
     DCP_K1(4, 8)
     DCP_K1(8, 1)
@@ -125,10 +144,14 @@ static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParam
 
 using namespace dcp;
 
-int dcp_attn_prepare(dcp_ctx* ctx, int hkv, int G) {
+int dcp_attn_prepare(dcp_ctx* ctx, int hkv, int G, int page) {
     const bool sp = k1_split();
-#define DCP_K1A(H_, G_) \
-    if (hkv == H_ && G == G_) return sp ? ensure_attr<H_, G_, true>(ctx) : ensure_attr<H_, G_, false>(ctx);
+#define DCP_K1A(H_, G_)                                                               \
+    if (hkv == H_ && G == G_) {                                                       \
+        if (page == 32) return ensure_attr<H_, G_, true, 32>(ctx);                    \
+        if (page == 64) return ensure_attr<H_, G_, true, 64>(ctx);                    \
+        return sp ? ensure_attr<H_, G_, true>(ctx) : ensure_attr<H_, G_, false>(ctx); \
+    }
     DCP_K1A(8, 4)
     DCP_K1A(4, 8)
     DCP_K1A(8, 1)
@@ -211,7 +234,8 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
     if (a->num_shards == 0) return DCP_OK;
     DCP_REQUIRE(a->head_dim == 128, DCP_E_UNSUPPORTED, "head_dim %d (compiled: 128)", a->head_dim);
-    DCP_REQUIRE(a->page_size == 16, DCP_E_UNSUPPORTED, "page_size %d (compiled: 16)", a->page_size);
+    DCP_REQUIRE(a->page_size == 16 || a->page_size == 32 || a->page_size == 64, DCP_E_UNSUPPORTED,
+                "page_size %d (compiled: 16, 32, 64)", a->page_size);
     DCP_REQUIRE(a->num_kv_heads > 0 && a->num_q_heads % a->num_kv_heads == 0, DCP_E_INVALID_ARG,
                 "num_q_heads %d not a multiple of num_kv_heads %d", a->num_q_heads, a->num_kv_heads);
     DCP_REQUIRE(a->q && a->kv_pool && a->block_table && a->cu_pages && a->shard_len && a->out &&
@@ -226,7 +250,8 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     const int G = a->num_q_heads / a->num_kv_heads;
 
     const CUtensorMap* map = nullptr;
-    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, k1_split());
+    const bool split = k1_split() || a->page_size != 16;
+    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, split, a->page_size);
     if (rc) return rc;
 
     AttnParams prm{};
@@ -247,7 +272,7 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     prm.num_shards = a->num_shards;
     prm.scale_log2 = a->scale * 1.4426950408889634f;
 
-    return dispatch_decode(ctx, map, prm, a->num_kv_heads, G, static_cast<cudaStream_t>(stream));
+    return dispatch_decode(ctx, map, prm, a->num_kv_heads, G, static_cast<cudaStream_t>(stream), a->page_size);
 }
 
 int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
@@ -255,7 +280,8 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     DCP_REQUIRE(ctx && x && v && a, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
     DCP_REQUIRE(v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW, "N %d > n_max %d", v->n_rows, x->cfg.n_max);
-    DCP_REQUIRE(a->head_dim == 128 && a->page_size == 16, DCP_E_UNSUPPORTED, "head_dim/page_size");
+    DCP_REQUIRE(a->head_dim == 128 && (a->page_size == 16 || a->page_size == 32 || a->page_size == 64),
+                DCP_E_UNSUPPORTED, "head_dim/page_size");
     DCP_REQUIRE(a->num_q_heads == x->cfg.num_q_heads && a->head_dim == x->cfg.head_dim, DCP_E_INVALID_ARG,
                 "exchange pool shape differs from the attention shape");
     DCP_REQUIRE(a->kv_pool && a->workspace && a->num_frames > 0, DCP_E_INVALID_ARG, "kv_pool/workspace");
@@ -263,7 +289,8 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     const size_t need = dcp_attn_workspace_bytes(ctx, x->cfg.n_max, a->num_q_heads, a->head_dim);
     DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu", a->workspace_bytes, need);
     const CUtensorMap* map = nullptr;
-    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, k1_split());
+    const bool split = k1_split() || a->page_size != 16;
+    int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, split, a->page_size);
     if (rc) return rc;
     AttnParams prm{};
     prm.q = reinterpret_cast<const __nv_bfloat16*>(x->pool + x->off_qrecv);
@@ -288,7 +315,7 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     prm.q_flag = reinterpret_cast<const uint32_t*>(x->pool + x->off_qflag);
     prm.num_shards_ptr = v->n_count_dev;
     return dispatch_decode(ctx, map, prm, a->num_kv_heads, a->num_q_heads / a->num_kv_heads,
-                           static_cast<cudaStream_t>(stream));
+                           static_cast<cudaStream_t>(stream), a->page_size);
 }
 
 }  // extern "C"

@@ -39,13 +39,14 @@ struct TmapCacheEntry {
     int hkv = 0;
     int d = 0;
     bool split = false;
+    int page = 16;
     CUtensorMap map;
 };
 
 }  // namespace dcp
 
 // Sets K1's dynamic shared-memory attribute for (hkv, group) outside any capture.
-int dcp_attn_prepare(struct dcp_ctx* ctx, int hkv, int group);
+int dcp_attn_prepare(struct dcp_ctx* ctx, int hkv, int group, int page);
 
 struct dcp_ctx {
     int device = 0;

@@ -188,7 +188,7 @@ int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
                           dcp_step_graph** out) {
     DCP_REQUIRE(ctx && x && v && a && out, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
-    int rc = dcp_attn_prepare(ctx, a->num_kv_heads, a->num_q_heads / a->num_kv_heads);
+    int rc = dcp_attn_prepare(ctx, a->num_kv_heads, a->num_q_heads / a->num_kv_heads, a->page_size);
     if (rc) return rc;
     cudaStream_t cs;
     DCP_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));

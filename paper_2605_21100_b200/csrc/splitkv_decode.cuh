@@ -79,13 +79,19 @@ __device__ __forceinline__ void publish_row(const AttnParams& p, int r) {
 // SPLIT = true:  a ring stage is half a frame (the K part or the V part); the
 // K half is released right after QK^T, and the finer ring fits 3.5 frames in
 // flight instead of 3 (7 x 32 KB vs 3 x 64 KB at 8 kv-heads).
-template <int HKV, int G, bool SPLIT = false>
+//
+// Pages larger than 16 tokens (page_size 32, 64, ... — ClusterTopology::page_size,
+// types.hpp:92) use the split ring with a 3-D tensor map (d, token-in-page,
+// frame*2*HKV + kv*HKV + head): each ring item is a 16-token chunk of one
+// part of one page, so the consumer code is identical for every page size.
+template <int HKV, int G, bool SPLIT = false, int PAGE_ = 16>
 struct DecodeCfg {
     static constexpr int D = 128;
-    static constexpr int PAGE = 16;
+    static constexpr int PAGE = PAGE_;
+    static constexpr int CHUNKS = PAGE / 16;          // 16-token chunks per page
     static constexpr int HQ = HKV * G;
-    static constexpr int ROWS = 2 * HKV * PAGE;       // 2-D tensor rows per frame
-    static constexpr int HALF = HKV * PAGE;           // rows of the K (or V) part
+    static constexpr int ROWS = 2 * HKV * 16;         // 2-D tensor rows per frame (whole-frame ring)
+    static constexpr int HALF = HKV * 16;             // rows of one part of one 16-token chunk
     static constexpr int BOX_ROWS = SPLIT ? HALF : ROWS;
     static constexpr int BOX_BYTES = BOX_ROWS * 128;  // one 64-column swizzled box
     static constexpr int STAGE_BYTES = 2 * BOX_BYTES; // a frame, or half a frame when SPLIT
@@ -97,6 +103,7 @@ struct DecodeCfg {
     static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
     static constexpr int SMEM = 1024 + BAR_OFF + 2 * STAGES * 8 + STAGES * 4 + 16;
     static_assert(ROWS <= 256, "TMA box rows");
+    static_assert(PAGE % 16 == 0 && (SPLIT || PAGE == 16), "pages > 16 tokens need the split ring");
     static_assert(G <= 16, "group must fit the 16 mma rows");
 };
 
@@ -109,18 +116,17 @@ __device__ __forceinline__ bool cta_nonempty(int64_t k, int64_t P, int64_t grid)
     return P >= grid || (k * P / grid) < ((k + 1) * P / grid);
 }
 
-template <int HKV, int G, bool SPLIT = false>
-__global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT>::THREADS, 1)
+template <int HKV, int G, bool SPLIT = false, int PAGE_ = 16>
+__global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     splitkv_decode_kernel(const __grid_constant__ CUtensorMap kv_map, const AttnParams p) {
-    using C = DecodeCfg<HKV, G, SPLIT>;
+    using C = DecodeCfg<HKV, G, SPLIT, PAGE_>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t smem_base = smem_u32(smem);
     const uint32_t full_bar = smem_base + C::BAR_OFF;
     const uint32_t empty_bar = full_bar + C::STAGES * 8;
-    uint8_t* stage_fill = smem + C::BAR_OFF + 2 * C::STAGES * 8;
-    volatile int* last_flag = reinterpret_cast<volatile int*>(stage_fill + C::STAGES * 4);
+    volatile int* last_flag = reinterpret_cast<volatile int*>(smem + C::BAR_OFF + 2 * C::STAGES * 8);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -146,29 +152,32 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT>::THREADS, 1)
         const uint64_t policy = l2_policy_evict_first();
         for (int base = p_begin; base < p_end; base += 32) {
             const int mine = base + lane;
-            int frame = 0, fill = C::PAGE;
-            if (mine < p_end) {
-                frame = __ldg(p.block_table + mine);
-                if (p.page_fill) fill = __ldg(p.page_fill + mine);
-            }
+            int frame = 0;
+            if (mine < p_end) frame = __ldg(p.block_table + mine);
             const int n = min(32, p_end - base);
             for (int i = 0; i < n; ++i) {
                 const int f = __shfl_sync(0xffffffffu, frame, i);
-                const int fl = __shfl_sync(0xffffffffu, fill, i);
                 if (lane == 0) {
                     const int it = base - p_begin + i;
+                    for (int c = 0; c < C::CHUNKS; ++c) {
 #pragma unroll
-                    for (int part = 0; part < (SPLIT ? 2 : 1); ++part) {
-                        const int j = SPLIT ? 2 * it + part : it;
-                        const int s = j % C::STAGES;
-                        const uint32_t ph = (j / C::STAGES) & 1;
-                        mbar_wait(empty_bar + 8 * s, ph ^ 1);
-                        if (part == 0) stage_fill[s] = static_cast<uint8_t>(fl);
-                        mbar_arrive_expect_tx(full_bar + 8 * s, C::STAGE_BYTES);
-                        const uint32_t dst = smem_base + s * C::STAGE_BYTES;
-                        const int row = f * C::ROWS + part * C::HALF;
-                        tma_load_2d(dst, &kv_map, 0, row, full_bar + 8 * s, policy);
-                        tma_load_2d(dst + C::BOX_BYTES, &kv_map, 64, row, full_bar + 8 * s, policy);
+                        for (int part = 0; part < (SPLIT ? 2 : 1); ++part) {
+                            const int j = SPLIT ? 2 * (it * C::CHUNKS + c) + part : it;
+                            const int s = j % C::STAGES;
+                            const uint32_t ph = (j / C::STAGES) & 1;
+                            mbar_wait(empty_bar + 8 * s, ph ^ 1);
+                            mbar_arrive_expect_tx(full_bar + 8 * s, C::STAGE_BYTES);
+                            const uint32_t dst = smem_base + s * C::STAGE_BYTES;
+                            if constexpr (SPLIT) {
+                                const int z = (f * 2 + part) * HKV;
+                                tma_load_3d(dst, &kv_map, 0, c * 16, z, full_bar + 8 * s, policy);
+                                tma_load_3d(dst + C::BOX_BYTES, &kv_map, 64, c * 16, z, full_bar + 8 * s, policy);
+                            } else {
+                                const int row = f * C::ROWS;
+                                tma_load_2d(dst, &kv_map, 0, row, full_bar + 8 * s, policy);
+                                tma_load_2d(dst + C::BOX_BYTES, &kv_map, 64, row, full_bar + 8 * s, policy);
+                            }
+                        }
                     }
                 }
                 __syncwarp();
@@ -241,6 +250,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT>::THREADS, 1)
 
     int it = 0;
     int pg = p_begin;
+    int fwin = -1, fval = 0;  // page_fill window cache
     while (pg < p_end) {
         while (p.cu_pages[r + 1] <= pg) ++r;  // skip zero-page shards
         const int r_first = p.cu_pages[r];
@@ -275,21 +285,29 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT>::THREADS, 1)
         for (int i = 0; i < 16; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
         float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
 
-        for (; pg < seg_end; ++pg, ++it) {
-            const int jk = SPLIT ? 2 * it : it;      // ring item of the K part
+        for (; pg < seg_end; ++pg, ++it)
+        for (int c = 0; c < C::CHUNKS; ++c) {
+            const int jk = SPLIT ? 2 * (it * C::CHUNKS + c) : it;  // ring item of the K part
             const int s = jk % C::STAGES;
             const uint32_t ph = (jk / C::STAGES) & 1;
             const int sv = SPLIT ? (jk + 1) % C::STAGES : s;
             const uint32_t phv = SPLIT ? ((jk + 1) / C::STAGES) & 1 : ph;
             int fill;
-            if (p.page_fill) {
-                mbar_wait(full_bar + 8 * s, ph);
-                fill = stage_fill[s];
+            if (p.page_fill) {  // per-page fills, fetched 32 pages per coalesced warp load
+                const int w = pg & ~31;
+                if (w != fwin) {
+                    fwin = w;
+                    fval = (w + lane < p_end && w + lane >= p_begin) ? __ldg(p.page_fill + w + lane) : 0;
+                }
+                fill = __shfl_sync(0xffffffffu, fval, pg - w);
             } else {
                 const int64_t rem = len - static_cast<int64_t>(pg - r_first) * C::PAGE;
                 fill = rem < C::PAGE ? static_cast<int>(rem) : C::PAGE;
-                mbar_wait(full_bar + 8 * s, ph);
             }
+            mbar_wait(full_bar + 8 * s, ph);
+            // valid tokens of this 16-token chunk (chunks past the page's fill are fully masked;
+            // chunk 0 always holds >= 1 token, so the running max is finite before any empty chunk)
+            fill = min(16, max(0, fill - 16 * c));
             const uint32_t st = smem_base + s * C::STAGE_BYTES;
             const uint32_t stv = smem_base + sv * C::STAGE_BYTES;
 

@@ -77,6 +77,28 @@ def test_small_shapes(ctx, hq, hkv):
     _check(b, q, pool, out, lse)
 
 
+@pytest.mark.parametrize("page", [32, 64])
+@pytest.mark.parametrize("hq,hkv", [(32, 8), (32, 4)])
+def test_page_sizes(ctx, hq, hkv, page):
+    # ClusterTopology::page_size (types.hpp:92) other than 16: split ring, 16-token chunks
+    rng = np.random.default_rng(page + hkv)
+    lens = [1, 15, 16, 17, page - 1, page, page + 1, 0] + rng.integers(1, 5000, size=12).tolist()
+    b = workload.paged_batch(lens, hq, hkv, page_size=page, frame_order="shuffled", seed=5, spare_frames=9)
+    q, pool = _make(b, 12)
+    out, lse, _ = _run(ctx, b, q, pool)
+    _check(b, q, pool, out, lse)
+    # per-page fills, incl. a non-final partial page and a page holding < 16 tokens
+    fill = np.full(int(b.cu_pages[-1]), page, np.uint8)
+    for r, L in enumerate(lens):
+        if b.cu_pages[r + 1] > b.cu_pages[r]:
+            fill[b.cu_pages[r + 1] - 1] = L - page * (b.cu_pages[r + 1] - b.cu_pages[r] - 1)
+    big = int(np.argmax(lens))
+    fill[b.cu_pages[big]] = 3
+    fill[b.cu_pages[big] + 1] = page - 7
+    out, lse, _ = _run(ctx, b, q, pool, page_fill=fill)
+    _check(b, q, pool, out, lse, page_fill=fill)
+
+
 def test_cross_cta_splits(ctx):
     # enough pages that most shards are cut by several of the 148 page ranges
     rng = np.random.default_rng(7)
