@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             const int ks = 2 * kp + (mi >> 1);
             const int box = ks >> 2;
             const int chunk = ((ks & 3) << 1) | (mi & 1);
-            const int row = h * C::PAGE + nt * 8 + rr;
+            const int row = h * 16 + nt * 8 + rr;
             k_off[nt][kp] = box * C::BOX_BYTES + row * 128 + ((chunk ^ rr) << 4);
         }
 #pragma unroll
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
         const int tok = (mi & 1) * 8 + rr;
         const int dchunk = 2 * np + (mi >> 1);
         const int box = dchunk >> 3, chunk = dchunk & 7;
-        const int row = C::V_ROW + h * C::PAGE + tok;
+        const int row = C::V_ROW + h * 16 + tok;
         v_off[np] = box * C::BOX_BYTES + row * 128 + ((chunk ^ rr) << 4);
     }
 
