@@ -125,6 +125,47 @@ DCP_API int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* args, voi
  * bench's gpu_launches accounting). */
 DCP_API int dcp_attn_launches_per_call(void);
 
+/* ---- K10: MLA split-KV paged decode attention (tcgen05, CTA pairs) ------------
+ *
+ * The DeepSeek-V3 absorbed-latent decode shape of cfg5.  Per
+ * (shard, q-head) the semantics are dcpsim::shard_attention<T>
+ * (attn_merge.hpp:53-82) with keys = the 576-wide cache rows (kv_lora_rank 512
+ * latent | 64 rope) and values = their first 512 columns; the intra-GPU split
+ * combine is lse_merge (hpp:86-100).  The reference does not model MLA
+ * (SPEC.md:381); the shard / page / fill conventions are those of
+ * dcp_splitkv_decode_attn above.
+ *
+ * q:       bf16 [num_shards][128][576]  (absorbed q_nope | q_pe)
+ * kv_pool: bf16 [num_frames][page_size][576]  (c_kv | k_pe), 16-byte aligned
+ * out:     fp32 [num_shards][128][512]  softmax-normalised over the shard
+ * lse:     fp32 [num_shards][128]       natural log
+ * Compiled: num_q_heads 128, kv_lora_rank 512, rope_dim 64, page_size 16/32/64.
+ * workspace: dcp_mla_workspace_bytes(...) bytes, zeroed once before first use;
+ * each call issues 2 kernels (tile scan + the pair kernel). */
+typedef struct dcp_mla_args {
+    int32_t num_shards;
+    int32_t num_q_heads;
+    int32_t kv_lora_rank;
+    int32_t rope_dim;
+    int32_t page_size;
+    int64_t num_frames;
+    const void* q;
+    const void* kv_pool;
+    const int32_t* block_table;
+    const int32_t* cu_pages;
+    const int64_t* shard_len;
+    const uint8_t* page_fill;   /* optional */
+    float scale;                /* softmax scale (DeepSeek-V3: 1/sqrt(192) x yarn mscale^2) */
+    float* out;
+    float* lse;
+    void* workspace;
+    size_t workspace_bytes;
+} dcp_mla_args;
+
+DCP_API size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards);
+DCP_API int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* args, void* stream);
+DCP_API int dcp_mla_launches_per_call(void);
+
 
 /* ---- K6 + K7: the DCP planner on the device ----------------------------------
  *

@@ -227,6 +227,79 @@ int dcpora_paged_decode_attn_f64(int nshards, int hq, int hkv, int d, int page_s
     return rc;
 }
 
+/* MLA decode (K10).  The reference does not model MLA; this is
+ * shard_attention<double> (attn_merge.hpp:53-82, same serial recurrence) with
+ * keys = the dk-wide cache rows and values = their first dv columns, applied
+ * per (shard, head) over a paged pool pool[frame][page_size][dk] (bf16 bits);
+ * q is [nshards][heads][dk].  Zero-token shards give O = 0, LSE = -inf, as
+ * dcp_mla_decode_attn does. */
+int dcpora_shard_attention_kv_f64(const double* q, const double* k, const double* v, int64_t len, int dk,
+                                  int dv, int v_stride, double scale, double* out, double* lse) {
+    if (len < 1) return E_EMPTY; /* hpp:57 */
+    double mx = -INFINITY, den = 0.0;
+    for (int i = 0; i < dv; ++i) out[i] = 0.0;
+    for (int64_t j = 0; j < len; ++j) {
+        const double* kj = k + j * dk;
+        const double* vj = v + j * v_stride;
+        double s = 0.0;
+        for (int i = 0; i < dk; ++i) s += kj[i] * q[i];
+        s *= scale;
+        if (s > mx) {
+            const double shrink = exp(mx - s);
+            den *= shrink;
+            for (int i = 0; i < dv; ++i) out[i] *= shrink;
+            mx = s;
+        }
+        const double w = exp(s - mx);
+        den += w;
+        for (int i = 0; i < dv; ++i) out[i] += w * vj[i];
+    }
+    for (int i = 0; i < dv; ++i) out[i] /= den;
+    *lse = mx + log(den);
+    return 0;
+}
+
+int dcpora_mla_paged_decode_f64(int nshards, int heads, int dk, int dv, int page_size, const uint16_t* q_bf16,
+                                const uint16_t* pool_bf16, const int32_t* block_table, const int32_t* cu_pages,
+                                const int64_t* shard_len, const uint8_t* page_fill, double scale, double* out,
+                                double* lse, int threads) {
+    int rc = 0;
+    for (int r = 0; r < nshards; ++r) {
+        const int p0 = cu_pages[r], p1 = cu_pages[r + 1];
+        int64_t ntok = 0;
+        for (int p = p0; p < p1; ++p) {
+            const int64_t rem = shard_len[r] - (int64_t)(p - p0) * page_size;
+            ntok += page_fill ? page_fill[p] : (rem < page_size ? rem : page_size);
+        }
+        if (ntok == 0) {
+            for (int h = 0; h < heads; ++h) {
+                for (int i = 0; i < dv; ++i) out[((size_t)r * heads + h) * dv + i] = 0.0;
+                lse[(size_t)r * heads + h] = -INFINITY;
+            }
+            continue;
+        }
+        double* kd = malloc(sizeof(double) * (size_t)ntok * dk);
+        int64_t t = 0;
+        for (int p = p0; p < p1; ++p) {
+            const int64_t rem = shard_len[r] - (int64_t)(p - p0) * page_size;
+            const int fill = page_fill ? page_fill[p] : (int)(rem < page_size ? rem : page_size);
+            const uint16_t* kp = pool_bf16 + (size_t)block_table[p] * page_size * dk;
+            for (int s = 0; s < fill; ++s, ++t)
+                for (int i = 0; i < dk; ++i) kd[(size_t)t * dk + i] = bf16_to_f64(kp[(size_t)s * dk + i]);
+        }
+#pragma omp parallel for schedule(dynamic) num_threads(threads > 0 ? threads : 1) reduction(min : rc)
+        for (int h = 0; h < heads; ++h) {
+            double qd[1024];
+            for (int i = 0; i < dk; ++i) qd[i] = bf16_to_f64(q_bf16[((size_t)r * heads + h) * dk + i]);
+            const int e = dcpora_shard_attention_kv_f64(qd, kd, kd, ntok, dk, dv, dk, scale,
+                                                        out + ((size_t)r * heads + h) * dv, lse + (size_t)r * heads + h);
+            rc = e < rc ? e : rc;
+        }
+        free(kd);
+    }
+    return rc;
+}
+
 /* ======================================================================
  * Planner — scheduler.cpp
  * ====================================================================== */

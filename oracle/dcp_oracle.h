@@ -44,6 +44,12 @@ int dcpora_paged_decode_attn_f64(int nshards, int hq, int hkv, int d, int page_s
                                  double* out, double* lse, int threads);
 
 /* ---- planner pieces (scheduler.cpp) ---- */
+int dcpora_shard_attention_kv_f64(const double* q, const double* k, const double* v, int64_t len, int dk,
+                                  int dv, int v_stride, double scale, double* out, double* lse);
+int dcpora_mla_paged_decode_f64(int nshards, int heads, int dk, int dv, int page_size, const uint16_t* q_bf16,
+                                const uint16_t* pool_bf16, const int32_t* block_table, const int32_t* cu_pages,
+                                const int64_t* shard_len, const uint8_t* page_fill, double scale, double* out,
+                                double* lse, int threads);
 int dcpora_water_fill(int n, const int32_t* participants, int64_t seq_len, const int64_t* loads,
                       int64_t* split);
 int dcpora_cp_degree(int64_t seq_len, const int64_t* bucket_len, const int* bucket_deg,

@@ -78,6 +78,17 @@ class AttnArgs(Structure):
     ]
 
 
+class MlaArgs(Structure):
+    _fields_ = [
+        ("num_shards", c_int32), ("num_q_heads", c_int32), ("kv_lora_rank", c_int32),
+        ("rope_dim", c_int32), ("page_size", c_int32), ("num_frames", c_int64),
+        ("q", c_void_p), ("kv_pool", c_void_p), ("block_table", c_void_p),
+        ("cu_pages", c_void_p), ("shard_len", c_void_p), ("page_fill", c_void_p),
+        ("scale", c_float), ("out", c_void_p), ("lse", c_void_p),
+        ("workspace", c_void_p), ("workspace_bytes", c_size_t),
+    ]
+
+
 class PlannerConfig(Structure):
     _fields_ = [
         ("nodes", c_int32), ("instances_per_node", c_int32), ("page_size", c_int64),
@@ -122,6 +133,9 @@ _SIGNATURES = [
     ("dcp_attn_workspace_bytes", c_size_t, [c_void_p, c_int32, c_int32, c_int32]),
     ("dcp_splitkv_decode_attn", c_int, [c_void_p, POINTER(AttnArgs), c_void_p]),
     ("dcp_attn_launches_per_call", c_int, []),
+    ("dcp_mla_workspace_bytes", c_size_t, [c_void_p, c_int32]),
+    ("dcp_mla_decode_attn", c_int, [c_void_p, POINTER(MlaArgs), c_void_p]),
+    ("dcp_mla_launches_per_call", c_int, []),
     ("dcp_planner_create", c_int, [c_void_p, POINTER(PlannerConfig), POINTER(c_void_p)]),
     ("dcp_planner_destroy", c_int, [c_void_p]),
     ("dcp_planner_enqueue", c_int, [c_void_p, c_void_p, c_void_p, c_int32]),

@@ -102,3 +102,64 @@ class DecodeAttention:
         out, lse = self.prepare(*args, **kw)
         self.launch(stream)
         return out, lse
+
+
+class MlaDecodeAttention:
+    """K10 MLA split-KV paged decode attention (dcp_mla_decode_attn), tcgen05 CTA pairs.
+
+    The DeepSeek-V3 absorbed-latent decode shape (cfg5): 128 q-heads share one
+    576-wide cache row per token (512 latent | 64 rope); keys are the whole row,
+    values its first 512 columns.  Per (shard, head) the math is the reference's
+    shard_attention (attn_merge.hpp:53-82); the reference itself does not model
+    MLA (SPEC.md:381).
+
+    kv_pool: bf16 [num_frames, page_size, 576]
+    q:       bf16 [num_shards, 128, 576]
+    Returns (out fp32 [num_shards, 128, 512], lse fp32 [num_shards, 128]).
+    """
+
+    HEADS, LORA, ROPE = 128, 512, 64
+
+    def __init__(self, ctx: DcpContext, page_size: int = 16, max_shards: int = 4096):
+        self.ctx, self.page, self.max_shards = ctx, page_size, max_shards
+        nbytes = _capi.lib().dcp_mla_workspace_bytes(ctx.handle, max_shards)
+        self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=f"cuda:{ctx.device}")
+        self.args = _capi.MlaArgs()
+
+    def prepare(self, q, kv_pool, block_table, cu_pages, shard_len, page_fill=None, scale=None,
+                out=None, lse=None):
+        R = q.shape[0]
+        if R > self.max_shards:
+            raise _capi.DcpInvalidArgument(f"{R} shards > max_shards {self.max_shards}")
+        for name, t, dt in (("q", q, torch.bfloat16), ("kv_pool", kv_pool, torch.bfloat16),
+                            ("block_table", block_table, torch.int32),
+                            ("cu_pages", cu_pages, torch.int32), ("shard_len", shard_len, torch.int64)):
+            if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+                raise _capi.DcpInvalidArgument(f"{name}: need contiguous CUDA {dt}, got {t.dtype}")
+        if out is None:
+            out = torch.empty(R, self.HEADS, self.LORA, dtype=torch.float32, device=q.device)
+        if lse is None:
+            lse = torch.empty(R, self.HEADS, dtype=torch.float32, device=q.device)
+        a = self.args
+        a.num_shards, a.num_q_heads, a.kv_lora_rank, a.rope_dim = R, self.HEADS, self.LORA, self.ROPE
+        a.page_size, a.num_frames = self.page, kv_pool.shape[0]
+        a.q, a.kv_pool = q.data_ptr(), kv_pool.data_ptr()
+        a.block_table, a.cu_pages, a.shard_len = (block_table.data_ptr(), cu_pages.data_ptr(),
+                                                  shard_len.data_ptr())
+        a.page_fill = page_fill.data_ptr() if page_fill is not None else None
+        # DeepSeek-V3 softmax scale: 1/sqrt(qk_nope_head_dim 128 + qk_rope_head_dim 64)
+        a.scale = scale if scale is not None else 1.0 / math.sqrt(192.0)
+        a.out, a.lse = out.data_ptr(), lse.data_ptr()
+        a.workspace, a.workspace_bytes = self.workspace.data_ptr(), self.workspace.numel()
+        self._keep = (q, kv_pool, block_table, cu_pages, shard_len, page_fill, out, lse)
+        return out, lse
+
+    def launch(self, stream=None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.ctx.device)
+        _capi.check(_capi.lib().dcp_mla_decode_attn(self.ctx.handle, ctypes.byref(self.args),
+                                                    ctypes.c_void_p(s.cuda_stream)))
+
+    def __call__(self, *args, stream=None, **kw):
+        out, lse = self.prepare(*args, **kw)
+        self.launch(stream)
+        return out, lse

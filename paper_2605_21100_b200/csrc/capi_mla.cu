@@ -1,0 +1,151 @@
+// SPDX-License-Identifier: Apache-2.0
+// C ABI: K10 MLA split-KV paged decode attention (dcp_capi.h, dcp_mla_*).
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "capi_common.cuh"
+#include "mla_decode.cuh"
+
+namespace dcp {
+
+static PFN_cuTensorMapEncodeTiled_v12000 mla_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// Pairs the persistent kernel runs: one cluster of 2 per TPC that can hold it.
+template <int PAGE>
+static int mla_pairs(dcp_ctx* ctx, int* out) {
+    static int cached[64] = {0};
+    int& c = cached[ctx->device & 63];
+    if (c == 0) {
+        DCP_CUDA_TRY(cudaFuncSetAttribute(mla::mla_decode_kernel<PAGE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          mla::SMEM));
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(ctx->num_sms & ~1);
+        cfg.blockDim = dim3(mla::THREADS);
+        cfg.dynamicSmemBytes = mla::SMEM;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        DCP_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, mla::mla_decode_kernel<PAGE>, &cfg));
+        c = n > 0 ? (n < ctx->num_sms / 2 ? n : ctx->num_sms / 2) : ctx->num_sms / 2;
+    }
+    *out = c;
+    return DCP_OK;
+}
+
+template <int PAGE>
+static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) {
+    auto fn = mla_encode_fn();
+    DCP_REQUIRE(fn != nullptr, DCP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    int pairs = 0;
+    if (int rc = mla_pairs<PAGE>(ctx, &pairs)) return rc;
+
+    CUtensorMap qmap, kvmap;
+    {
+        cuuint64_t dims[2] = {mla::DK, static_cast<cuuint64_t>(a->num_shards) * mla::H};
+        cuuint64_t strides[1] = {mla::DK * 2};
+        cuuint32_t box[2] = {64, 64};
+        cuuint32_t estr[2] = {1, 1};
+        CUresult r = fn(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->q), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        DCP_REQUIRE(r == CUDA_SUCCESS, DCP_E_CUDA, "q tensor map (%d)", static_cast<int>(r));
+    }
+    {
+        cuuint64_t dims[3] = {mla::DK, PAGE, static_cast<cuuint64_t>(a->num_frames)};
+        cuuint64_t strides[2] = {mla::DK * 2, static_cast<cuuint64_t>(PAGE) * mla::DK * 2};
+        cuuint32_t box[3] = {64, 16, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = fn(&kvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->kv_pool), dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        DCP_REQUIRE(r == CUDA_SUCCESS, DCP_E_CUDA, "kv tensor map (%d)", static_cast<int>(r));
+    }
+    mla::MlaParams p{};
+    p.block_table = a->block_table;
+    p.cu_pages = a->cu_pages;
+    p.shard_len = a->shard_len;
+    p.page_fill = a->page_fill;
+    p.out = a->out;
+    p.lse = a->lse;
+    const size_t slots = 2 * static_cast<size_t>(ctx->num_sms / 2);
+    char* ws = static_cast<char*>(a->workspace);
+    p.ws_acc = reinterpret_cast<float*>(ws);
+    ws += slots * mla::H * mla::DL * sizeof(float);
+    p.ws_ml = reinterpret_cast<float*>(ws);
+    ws += slots * mla::H * 2 * sizeof(float);
+    p.counters = reinterpret_cast<int32_t*>(ws);
+    ws += 2 * static_cast<size_t>(a->num_shards) * sizeof(int32_t);
+    p.cu_tiles = reinterpret_cast<int32_t*>(ws);
+    p.num_shards = a->num_shards;
+    p.num_frames = static_cast<int32_t>(a->num_frames);
+    p.scale_log2 = a->scale * 1.4426950408889634f;
+
+    mla::mla_tile_scan_kernel<PAGE><<<1, 1024, 0, stream>>>(p);
+    DCP_CUDA_TRY(cudaGetLastError());
+    mla::mla_decode_kernel<PAGE><<<2 * pairs, mla::THREADS, mla::SMEM, stream>>>(qmap, kvmap, p);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+}  // namespace dcp
+
+using namespace dcp;
+
+extern "C" {
+
+size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards) {
+    if (!ctx || num_shards < 0) return 0;
+    const size_t slots = 2 * static_cast<size_t>(ctx->num_sms / 2);
+    size_t b = slots * mla::H * mla::DL * sizeof(float);          // ws_acc
+    b += slots * mla::H * 2 * sizeof(float);                      // ws_ml
+    b += 2 * static_cast<size_t>(num_shards) * sizeof(int32_t);   // counters
+    b += (static_cast<size_t>(num_shards) + 1) * sizeof(int32_t); // cu_tiles
+    return (b + 255) & ~size_t(255);
+}
+
+int dcp_mla_launches_per_call(void) { return 2; }
+
+int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* a, void* stream) {
+    DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");
+    DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
+    if (a->num_shards == 0) return DCP_OK;
+    DCP_REQUIRE(a->num_q_heads == mla::H && a->kv_lora_rank == mla::DL && a->rope_dim == mla::DR, DCP_E_UNSUPPORTED,
+                "MLA shape (heads %d, kv_lora_rank %d, rope_dim %d); compiled: 128 / 512 / 64", a->num_q_heads,
+                a->kv_lora_rank, a->rope_dim);
+    DCP_REQUIRE(a->page_size == 16 || a->page_size == 32 || a->page_size == 64, DCP_E_UNSUPPORTED,
+                "page_size %d (compiled: 16, 32, 64)", a->page_size);
+    DCP_REQUIRE(a->q && a->kv_pool && a->block_table && a->cu_pages && a->shard_len && a->out && a->lse &&
+                    a->workspace,
+                DCP_E_INVALID_ARG, "NULL device pointer in dcp_mla_args");
+    DCP_REQUIRE((reinterpret_cast<uintptr_t>(a->kv_pool) & 15) == 0 && (reinterpret_cast<uintptr_t>(a->q) & 15) == 0,
+                DCP_E_INVALID_ARG, "q and kv_pool must be 16-byte aligned");
+    DCP_REQUIRE(a->num_frames > 0 && a->num_frames < (int64_t(1) << 31), DCP_E_INVALID_ARG, "num_frames");
+    DCP_REQUIRE(static_cast<int64_t>(a->num_shards) * mla::H < (int64_t(1) << 31), DCP_E_INVALID_ARG,
+                "num_shards too large");
+    const size_t need = dcp_mla_workspace_bytes(ctx, a->num_shards);
+    DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu bytes", a->workspace_bytes,
+                need);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (a->page_size == 16) return mla_launch<16>(ctx, a, s);
+    if (a->page_size == 32) return mla_launch<32>(ctx, a, s);
+    return mla_launch<64>(ctx, a, s);
+}
+
+}  // extern "C"

@@ -55,6 +55,8 @@ def _load(path, prefix):
         sigs["sharded_attention_merge_f32"] = (c_int, [vp, vp, vp, c_int64, c_int, c_float, vp, c_int, vp])
         sigs["world_instance_shards"] = (c_int, [c_void_p, c_int, vp, vp, vp, vp, c_int, c_int])
         sigs["moe_layer_f64"] = (c_int, [c_int] * 5 + [vp] * 7 + [c_int])
+        sigs["mla_paged_decode_f64"] = (c_int, [c_int] * 5 + [vp] * 6 + [c_double, vp, vp, c_int])
+        sigs["shard_attention_kv_f64"] = (c_int, [vp, vp, vp, c_int64, c_int, c_int, c_int, c_double, vp, vp])
     else:
         sigs["sharded_attention_merge_f64"] = (c_int, [vp, vp, vp, c_int64, c_int, c_double, vp, c_int, c_int, vp])
         sigs["sharded_attention_merge_f32"] = (c_int, [vp, vp, vp, c_int64, c_int, c_float, vp, c_int, c_int, vp])
@@ -98,6 +100,22 @@ def paged_decode_f64(batch, q_bits: np.ndarray, pool_bits: np.ndarray, page_fill
         P(np.ascontiguousarray(q_bits)), P(np.ascontiguousarray(pool_bits)),
         P(batch.block_table), P(batch.cu_pages), P(batch.shard_len),
         P(page_fill), sc, P(out), P(lse), th)
+    assert rc == 0, rc
+    return out, lse
+
+
+def mla_decode_f64(batch, q_bits: np.ndarray, pool_bits: np.ndarray, page_fill=None, scale=None,
+                   threads: int = 0):
+    """Oracle fp64 MLA decode over a PagedBatch (pool [frames][page][576] bf16 bits)."""
+    L = port()
+    R = len(batch.shard_len)
+    out = np.zeros((R, 128, 512), np.float64)
+    lse = np.zeros((R, 128), np.float64)
+    sc = scale if scale is not None else 1.0 / np.sqrt(192.0)
+    th = threads or os.cpu_count() or 1
+    rc = L.dcpora_mla_paged_decode_f64(
+        R, 128, 576, 512, batch.page_size, P(np.ascontiguousarray(q_bits)), P(np.ascontiguousarray(pool_bits)),
+        P(batch.block_table), P(batch.cu_pages), P(batch.shard_len), P(page_fill), sc, P(out), P(lse), th)
     assert rc == 0, rc
     return out, lse
 

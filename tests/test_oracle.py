@@ -341,3 +341,35 @@ def test_trace_generator_matches_reference(ref):
         assert [m[2] for m in mine] == sl[:cnt].tolist()
         assert [m[3] for m in mine] == ol[:cnt].tolist()
         assert np.allclose([m[1] for m in mine], arr[:cnt], rtol=0, atol=1e-9)
+
+
+def test_mla_oracle_matches_reference_on_gathered_rows(port, ref):
+    """The MLA fp64 oracle (used to check K10) equals the reference's own
+    shard_attention<double> on the gathered 576-wide cache rows, with values =
+    the rows' first 512 columns zero-padded to 576 (the reference needs equal
+    key / value widths; the padding columns stay exactly 0)."""
+    from paper_2605_21100_b200 import workload
+    rng = np.random.default_rng(12)
+    lens = [1, 20, 0, 77]
+    heads = 128
+    b = workload.paged_batch(lens, heads, 1, 576, 16, frame_order="shuffled", seed=4, spare_frames=5)
+    q = rng.standard_normal((len(lens), heads, 576)).astype(np.float32)
+    pool = rng.standard_normal((b.num_frames, 16, 576)).astype(np.float32)
+    qb = (q.view(np.uint32) >> 16).astype(np.uint16)
+    pb = (pool.view(np.uint32) >> 16).astype(np.uint16)
+    sc = 1 / np.sqrt(192.0)
+    out, lse = oracle_lib.mla_decode_f64(b, qb, pb, scale=sc)
+    widen = lambda x: (x.astype(np.uint32) << 16).view(np.float32).astype(np.float64)  # noqa: E731
+    for r, L in enumerate(lens):
+        if L == 0:
+            assert np.all(np.isneginf(lse[r])) and np.all(out[r] == 0)
+            continue
+        frames = b.block_table[b.cu_pages[r]:b.cu_pages[r + 1]]
+        kk = np.ascontiguousarray(np.concatenate([widen(pb[f]) for f in frames])[:L])
+        vv = kk.copy()
+        vv[:, 512:] = 0.0
+        for h in range(0, heads, 9):
+            qq = np.ascontiguousarray(widen(qb[r, h]))
+            o, l = np.zeros(576), np.zeros(1)
+            assert ref.dcpref_shard_attention_f64(P(qq), P(kk), P(vv), L, 576, sc, P(o), P(l)) == 0
+            assert np.array_equal(o[:512], out[r, h]) and np.all(o[512:] == 0) and l[0] == lse[r, h]
