@@ -140,8 +140,8 @@ DCP_API int dcp_attn_launches_per_call(void);
  * out:     fp32 [num_shards][128][512]  softmax-normalised over the shard
  * lse:     fp32 [num_shards][128]       natural log
  * Compiled: num_q_heads 128, kv_lora_rank 512, rope_dim 64, page_size 16/32/64.
- * workspace: dcp_mla_workspace_bytes(...) bytes, zeroed once before first use;
- * each call issues 2 kernels (tile scan + the pair kernel). */
+ * workspace: dcp_mla_workspace_bytes(...) bytes (no zeroing needed); each call
+ * issues 3 kernels (tile scan, the CTA-pair kernel, the split merge). */
 typedef struct dcp_mla_args {
     int32_t num_shards;
     int32_t num_q_heads;
@@ -165,6 +165,10 @@ typedef struct dcp_mla_args {
 DCP_API size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards);
 DCP_API int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* args, void* stream);
 DCP_API int dcp_mla_launches_per_call(void);
+/* Diagnostics: record globaltimer stamps of CTA pair 0 into a device buffer of
+ * 256 x 8 int64 (per tile: MMA before-QK, after-QK, after-P wait, after-PV;
+ * softmax S-ready / P-published for CTA 0 and CTA 1).  NULL switches it off. */
+DCP_API int dcp_mla_set_trace(void* dev_buf);
 
 
 /* ---- K6 + K7: the DCP planner on the device ----------------------------------

@@ -136,6 +136,7 @@ _SIGNATURES = [
     ("dcp_mla_workspace_bytes", c_size_t, [c_void_p, c_int32]),
     ("dcp_mla_decode_attn", c_int, [c_void_p, POINTER(MlaArgs), c_void_p]),
     ("dcp_mla_launches_per_call", c_int, []),
+    ("dcp_mla_set_trace", c_int, [c_void_p]),
     ("dcp_planner_create", c_int, [c_void_p, POINTER(PlannerConfig), POINTER(c_void_p)]),
     ("dcp_planner_destroy", c_int, [c_void_p]),
     ("dcp_planner_enqueue", c_int, [c_void_p, c_void_p, c_void_p, c_int32]),

@@ -2,12 +2,15 @@
 // C ABI: K10 MLA split-KV paged decode attention (dcp_capi.h, dcp_mla_*).
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "capi_common.cuh"
 #include "mla_decode.cuh"
 
 namespace dcp {
+
+static long long* g_mla_trace = nullptr;
 
 static PFN_cuTensorMapEncodeTiled_v12000 mla_encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -56,7 +59,7 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
     int pairs = 0;
     if (int rc = mla_pairs<PAGE>(ctx, &pairs)) return rc;
 
-    CUtensorMap qmap, kvmap;
+    CUtensorMap qmap, kvq, kvp;
     {
         cuuint64_t dims[2] = {mla::DK, static_cast<cuuint64_t>(a->num_shards) * mla::H};
         cuuint64_t strides[1] = {mla::DK * 2};
@@ -67,13 +70,15 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         DCP_REQUIRE(r == CUDA_SUCCESS, DCP_E_CUDA, "q tensor map (%d)", static_cast<int>(r));
     }
-    {
+    // paged cache as (column, token-in-page, frame); QK boxes take min(PAGE, HT) rows, PV boxes min(PAGE, 32)
+    for (int which = 0; which < 2; ++which) {
+        const cuuint32_t rows = which == 0 ? (PAGE < mla::HT ? PAGE : mla::HT) : (PAGE < 32 ? PAGE : 32);
         cuuint64_t dims[3] = {mla::DK, PAGE, static_cast<cuuint64_t>(a->num_frames)};
         cuuint64_t strides[2] = {mla::DK * 2, static_cast<cuuint64_t>(PAGE) * mla::DK * 2};
-        cuuint32_t box[3] = {64, 16, 1};
+        cuuint32_t box[3] = {64, rows, 1};
         cuuint32_t estr[3] = {1, 1, 1};
-        CUresult r = fn(&kvmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->kv_pool), dims, strides, box,
-                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CUresult r = fn(which == 0 ? &kvq : &kvp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(a->kv_pool),
+                        dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         DCP_REQUIRE(r == CUDA_SUCCESS, DCP_E_CUDA, "kv tensor map (%d)", static_cast<int>(r));
     }
@@ -90,16 +95,19 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
     ws += slots * mla::H * mla::DL * sizeof(float);
     p.ws_ml = reinterpret_cast<float*>(ws);
     ws += slots * mla::H * 2 * sizeof(float);
-    p.counters = reinterpret_cast<int32_t*>(ws);
-    ws += 2 * static_cast<size_t>(a->num_shards) * sizeof(int32_t);
     p.cu_tiles = reinterpret_cast<int32_t*>(ws);
     p.num_shards = a->num_shards;
     p.num_frames = static_cast<int32_t>(a->num_frames);
     p.scale_log2 = a->scale * 1.4426950408889634f;
+    static const int dbg = [] { const char* e = std::getenv("DCP_MLA_DBG"); return e ? std::atoi(e) : 0; }();
+    p.dbg = dbg;
+    p.trace = g_mla_trace;
 
     mla::mla_tile_scan_kernel<PAGE><<<1, 1024, 0, stream>>>(p);
     DCP_CUDA_TRY(cudaGetLastError());
-    mla::mla_decode_kernel<PAGE><<<2 * pairs, mla::THREADS, mla::SMEM, stream>>>(qmap, kvmap, p);
+    mla::mla_decode_kernel<PAGE><<<2 * pairs, mla::THREADS, mla::SMEM, stream>>>(qmap, kvq, kvp, p);
+    DCP_CUDA_TRY(cudaGetLastError());
+    mla::mla_merge_kernel<<<dim3(a->num_shards, mla::H / 16), 512, 0, stream>>>(p, pairs);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
@@ -115,12 +123,17 @@ size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards) {
     const size_t slots = 2 * static_cast<size_t>(ctx->num_sms / 2);
     size_t b = slots * mla::H * mla::DL * sizeof(float);          // ws_acc
     b += slots * mla::H * 2 * sizeof(float);                      // ws_ml
-    b += 2 * static_cast<size_t>(num_shards) * sizeof(int32_t);   // counters
     b += (static_cast<size_t>(num_shards) + 1) * sizeof(int32_t); // cu_tiles
     return (b + 255) & ~size_t(255);
 }
 
-int dcp_mla_launches_per_call(void) { return 2; }
+int dcp_mla_launches_per_call(void) { return 3; }
+
+/* Debug: globaltimer stamps of pair 0 into a device buffer of 256 x 8 int64 (NULL = off). */
+int dcp_mla_set_trace(void* dev_buf) {
+    g_mla_trace = static_cast<long long*>(dev_buf);
+    return DCP_OK;
+}
 
 int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* a, void* stream) {
     DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");

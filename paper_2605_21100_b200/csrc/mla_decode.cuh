@@ -29,7 +29,7 @@
 //     max and rescales O in TMEM only when the max grows by more than 2^8.
 //   * Persistent pairs, stream-K over tiles: every pair streams the same number
 //     of tiles whatever the 1K..512K length skew; cut shards leave partials in
-//     a per-pair slot, the last pair to finish a shard merges (device ticket).
+//     a per-pair slot and a second, fully parallel launch merges them.
 #pragma once
 
 #include <cstdint>
@@ -48,19 +48,24 @@ constexpr int DR = 64;               // rope width
 constexpr int DK = DL + DR;          // 576 = K width
 constexpr int NKB = DK / 64;         // 9 K boxes of 64 columns
 constexpr int TILE = 128;            // tokens per pair tile
-constexpr int CHUNKS = TILE / 16;    // 16-token TMA chunks per tile
+constexpr int HT = TILE / 2;         // tokens per CTA in S = Q K^T
 constexpr int STAGE = 8192;          // ring stage bytes
-constexpr int NS = 15;               // ring stages
+constexpr int NSQ = 10;              // QK ring stages (the HBM stream)
+constexpr int NSV = 5;               // PV ring stages (the L2 re-read stream)
 constexpr int Q_BYTES = NKB * 8192;  // 64 heads x 576 bf16 per CTA
 constexpr int P_BYTES = 2 * 8192;    // 64 heads x 128 tokens bf16 per CTA
 constexpr int OFF_Q = 0;
 constexpr int OFF_P = OFF_Q + Q_BYTES;
-constexpr int OFF_RING = OFF_P + 2 * P_BYTES;
-constexpr int OFF_MISC = OFF_RING + NS * STAGE;
-// misc: barriers then exchange scratch
-constexpr int BAR_FULL = 0;             // [NS] leader: 2 producer arrivals + tx
-constexpr int BAR_EMPTY = BAR_FULL + 8 * NS;  // [NS] each CTA: 1 (MMA commit multicast)
-constexpr int BAR_QFULL = BAR_EMPTY + 8 * NS; // leader: 2 + tx
+constexpr int OFF_RQ = OFF_P + 2 * P_BYTES;
+constexpr int OFF_RV = OFF_RQ + NSQ * STAGE;
+constexpr int OFF_MISC = OFF_RV + NSV * STAGE;
+// misc: barriers then exchange scratch.  Ring "full" barriers live in the leader: 1 arrival
+// (the leader's producer, expecting both CTAs' bytes) + tx; "empty" in each CTA: 1 (MMA commit multicast).
+constexpr int BAR_FULLQ = 0;                      // [NSQ]
+constexpr int BAR_EMPTYQ = BAR_FULLQ + 8 * NSQ;   // [NSQ]
+constexpr int BAR_FULLV = BAR_EMPTYQ + 8 * NSQ;   // [NSV]
+constexpr int BAR_EMPTYV = BAR_FULLV + 8 * NSV;   // [NSV]
+constexpr int BAR_QFULL = BAR_EMPTYV + 8 * NSV;   // leader: 1 + tx
 constexpr int BAR_QEMPTY = BAR_QFULL + 8;     // each: 1
 constexpr int BAR_SFULL = BAR_QEMPTY + 8;     // [2] each: 1
 constexpr int BAR_SEMPTY = BAR_SFULL + 16;    // [2] leader: 8 softmax warps
@@ -68,11 +73,20 @@ constexpr int BAR_PFULL = BAR_SEMPTY + 16;    // [2] leader: 8
 constexpr int BAR_PEMPTY = BAR_PFULL + 16;    // [2] each: 1
 constexpr int BAR_OEMPTY = BAR_PEMPTY + 16;   // leader: 8
 constexpr int TMEM_SLOT = BAR_OEMPTY + 8;
-constexpr int LAST_FLAG = TMEM_SLOT + 4;
 constexpr int RED = 512;                      // float[2][128] exchange scratch
 constexpr int MISC_BYTES = RED + 2 * 128 * 4;
 constexpr int SMEM = 1024 + OFF_MISC + MISC_BYTES;
-constexpr int THREADS = 192;                  // warps 0-3 softmax, 4 producer, 5 MMA
+// Warp roles: 0-3 softmax, 4 QK MMA, 5 PV MMA, then NQW QK-stream and NVW PV-stream TMA
+// issuers.  The two MMA chains touch disjoint TMEM (S vs O) and meet only through the
+// softmax barriers, so they are issued by two warps and run concurrently.  A single
+// thread issues a TMA box only every ~200 cycles (measured, tools/probe/tma_bw.cu), so the
+// 2-KB boxes of 16-token pages are spread over several issuing warps.
+constexpr int NQW = 4;
+constexpr int NVW = 2;
+constexpr int W_MMAQ = 4;                     // issues the S = Q K^T MMAs (leader CTA)
+constexpr int W_MMAV = 5;                     // issues the O += P V MMAs (leader CTA)
+constexpr int W_PROD = 6;
+constexpr int THREADS = 32 * (W_PROD + NQW + NVW);
 constexpr uint32_t TM_S = 0;                  // S buffers: cols [0,64), [64,128)
 constexpr uint32_t TM_O = 256;                // O: chunk j at 256 + 128 j
 constexpr float RESCALE_LOG2 = 8.f;           // rescale O only when the max grows by > 2^8
@@ -89,11 +103,23 @@ struct MlaParams {
     float* lse;                  // [R][128]
     float* ws_acc;               // [2*pairs][128][512]
     float* ws_ml;                // [2*pairs][128][2]
-    int32_t* counters;           // [2R]
     int32_t num_shards;
     int32_t num_frames;
     float scale_log2;
+    int32_t dbg;                 // bottleneck experiments (env DCP_MLA_DBG): 1 = no MMAs, 2 = no softmax math
+    long long* trace;            // optional [256][8] globaltimer stamps of pair 0 (dcp_mla_set_trace)
 };
+
+__device__ __forceinline__ long long gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// trace slot k of pair-0 tile g (one writer per slot)
+#define MLA_TRACE(g, k)                                                                     \
+    do {                                                                                    \
+        if (p.trace && pair == 0 && (g) < 256) p.trace[(g) * 8 + (k)] = gtime();            \
+    } while (0)
 
 __device__ __forceinline__ int pair_of_tile(int64_t t, int64_t T, int64_t np) {
     return static_cast<int>(((t + 1) * np + T - 1) / T - 1);
@@ -166,9 +192,11 @@ struct SegWalk {
 
 template <int PAGE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    mla_decode_kernel(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap kv_map,
-                      const MlaParams p) {
+    mla_decode_kernel(const __grid_constant__ CUtensorMap q_map, const __grid_constant__ CUtensorMap kvq_map,
+                      const __grid_constant__ CUtensorMap kvp_map, const MlaParams p) {
     constexpr int PPT = TILE / PAGE;  // pages per tile
+    constexpr int BQ = PAGE < HT ? PAGE : HT;  // rows per TMA box, QK stages (kvq_map)
+    constexpr int BP = PAGE < 32 ? PAGE : 32;  // rows per TMA box, PV stages (kvp_map)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = smem_u32(smem);
@@ -184,11 +212,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int t_end = static_cast<int>((pair + 1) * T / NP);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(misc + BAR_FULL + 8 * s, 2);
-            mbar_init(misc + BAR_EMPTY + 8 * s, 1);
+        for (int s = 0; s < NSQ; ++s) {
+            mbar_init(misc + BAR_FULLQ + 8 * s, 1);
+            mbar_init(misc + BAR_EMPTYQ + 8 * s, 1);
         }
-        mbar_init(misc + BAR_QFULL, 2);
+        for (int s = 0; s < NSV; ++s) {
+            mbar_init(misc + BAR_FULLV + 8 * s, 1);
+            mbar_init(misc + BAR_EMPTYV + 8 * s, 1);
+        }
+        mbar_init(misc + BAR_QFULL, 1);
         mbar_init(misc + BAR_QEMPTY, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(misc + BAR_SFULL + 8 * b, 1);
@@ -199,9 +231,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         mbar_init(misc + BAR_OEMPTY, 8);
         fence_mbar_init();
     }
-    if (warp == 4 && lane == 0) {
+    if (warp == W_PROD && lane == 0) {
         tma_prefetch_desc(&q_map);
-        tma_prefetch_desc(&kv_map);
+        tma_prefetch_desc(&kvq_map);
+        tma_prefetch_desc(&kvp_map);
     }
     if (warp == 0) tc::tmem_alloc<2>(misc + TMEM_SLOT, 512);
     tc::fence_before_sync();
@@ -211,48 +244,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t lead = tc::mapa(misc, 0);  // leader's misc block (shared::cluster)
 
     if (t_begin < t_end) {
-        if (warp == 4) {
-            // ===================== TMA producer (both CTAs) =====================
+        if (warp >= W_PROD) {
+          if (lane == 0) {
+            // ===================== TMA issuers (both CTAs, one thread per warp) =====================
+            // NQW warps stream Q and the QK stages (ring Q), NVW warps the PV stages (ring V):
+            // PV stages wait for the softmax before they are consumed, and on a separate ring
+            // they never hold back the QK prefetch.  Issuer k of a stream issues boxes k, k+n, ...
+            // of every stage; issuer 0 of the leader posts the stage's expected bytes.
+            // Single-thread loops: every TMA operand is thread-local; frame ids live in
+            // registers, prefetched a tile ahead.
+            const bool is_qk = warp < W_PROD + NQW;
+            const int ik = is_qk ? warp - W_PROD : warp - W_PROD - NQW;  // issuer index
+            const int nk = is_qk ? NQW : NVW;
             const uint64_t pol_first = l2_policy_evict_first();
             const uint64_t pol_norm = tc::l2_policy_evict_normal();
+            const int nst = is_qk ? NSQ : NSV;
+            const uint32_t ring = sbase + (is_qk ? OFF_RQ : OFF_RV);
+            const uint32_t bfull = is_qk ? BAR_FULLQ : BAR_FULLV, bempty = is_qk ? BAR_EMPTYQ : BAR_EMPTYV;
             uint32_t it = 0;  // ring counter
             int seg = 0;
-            auto stage_begin = [&](uint32_t& dst) {
-                const uint32_t s = it % NS;
-                if (lane == 0) {
-                    mbar_wait(misc + BAR_EMPTY + 8 * s, ((it / NS) & 1) ^ 1);
-                    tc::mbar_arrive_expect_tx_cluster(lead + BAR_FULL + 8 * s, STAGE);
-                }
-                dst = sbase + OFF_RING + s * STAGE;
-                return lead + BAR_FULL + 8 * s;
+            const bool skip = !is_qk && (p.dbg & 4);  // experiment: PV stages without their loads
+            auto stage_begin = [&]() {
+                const uint32_t s = it % nst;
+                tc::mbar_wait_sleep(misc + bempty + 8 * s, ((it / nst) & 1) ^ 1);
+                // the leader expects both CTAs' bytes; the peer's TMA completes on it directly
+                if (cta == 0 && ik == 0) mbar_arrive_expect_tx(misc + bfull + 8 * s, skip ? 0 : 2 * STAGE);
+                return s;
             };
-            // QK stage b of a tile: this CTA's 64 tokens (chunks 4c..4c+3) x K box b
-            auto qk_stage = [&](int b, int frame_lane) {
-                uint32_t dst;
-                const uint32_t bar = stage_begin(dst);
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int chunk = 4 * cta + k;
-                    const int f = __shfl_sync(0xffffffffu, frame_lane, (chunk * 16) / PAGE);
-                    if (lane == 0)
-                        tc::tma_load_3d_pair(dst + k * 2048, &kv_map, 64 * b, (chunk * 16) % PAGE, f, bar, pol_norm);
+            // QK stage b of a tile: this CTA's 64 tokens [64c, 64c+64) x K box b, as boxes of
+            // BQ = min(PAGE, 64) rows (one page, or a 64-token part of one)
+            auto qk_stage = [&](int b, const int (&fr)[PPT]) {
+                const uint32_t s = stage_begin();
+                const uint32_t dst = ring + s * STAGE, bar = lead + bfull + 8 * s;
+                for (int k = ik; k < 64 / BQ; k += nk) {
+                    const int u = 64 * static_cast<int>(cta) + k * BQ;  // token within the tile
+                    tc::tma_load_3d_pair(dst + k * BQ * 128, &kvq_map, 64 * b, u % PAGE, fr[u / PAGE], bar, pol_norm);
                 }
                 ++it;
             };
-            // PV stage (j, q): tokens [32q, 32q+32) x dims [256j + 128c, +128) as 2 boxes of 64
-            auto pv_stage = [&](int j, int q, int frame_lane) {
-                uint32_t dst;
-                const uint32_t bar = stage_begin(dst);
-#pragma unroll
-                for (int pg = 0; pg < 2; ++pg) {
-                    const int chunk = 2 * q + pg;
-                    const int f = __shfl_sync(0xffffffffu, frame_lane, (chunk * 16) / PAGE);
-#pragma unroll
-                    for (int bx = 0; bx < 2; ++bx)
-                        if (lane == 0)
-                            tc::tma_load_3d_pair(dst + bx * 4096 + pg * 2048, &kv_map,
-                                                 64 * (4 * j + 2 * static_cast<int>(cta) + bx), (chunk * 16) % PAGE, f,
-                                                 bar, pol_first);
+            // PV stage (j, q): tokens [32q, 32q+32) x dims [256j + 128c, +128) as 2 column boxes of 64,
+            // each in boxes of BP = min(PAGE, 32) rows
+            auto pv_stage = [&](int j, int q, const int (&fr)[PPT]) {
+                const uint32_t s = stage_begin();
+                if (skip) {
+                    ++it;
+                    return;
+                }
+                const uint32_t dst = ring + s * STAGE, bar = lead + bfull + 8 * s;
+                for (int i = ik; i < 2 * (32 / BP); i += nk) {
+                    const int k = i >> 1, bx = i & 1;
+                    const int u = 32 * q + k * BP;
+                    tc::tma_load_3d_pair(dst + bx * 4096 + k * BP * 128, &kvp_map,
+                                         64 * (4 * j + 2 * static_cast<int>(cta) + bx), u % PAGE, fr[u / PAGE], bar,
+                                         pol_first);
                 }
                 ++it;
             };
@@ -262,101 +306,146 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const int r = w.r;
                 const int t0 = w.t, t1 = min(p.cu_tiles[r + 1], w.t_end);
                 const int pg_begin = p.cu_pages[r], pg_end = p.cu_pages[r + 1];
-                // Q rows of this shard (this CTA's 64 heads)
-                if (lane == 0) {
-                    if (seg > 0) mbar_wait(misc + BAR_QEMPTY, (seg - 1) & 1);
-                    tc::mbar_arrive_expect_tx_cluster(lead + BAR_QFULL, Q_BYTES);
+                const int r_first_tile = p.cu_tiles[r];
+                // pages past the shard get an out-of-bounds frame -> TMA zero fill
+                auto load_frames = [&](int t, int (&fr)[PPT]) {
+                    const int pg0 = pg_begin + (t - r_first_tile) * PPT;
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) fr[k] = pg0 + k < pg_end ? __ldg(p.block_table + pg0 + k) : p.num_frames;
+                };
+                int f_cur[PPT], f_next[PPT];
+                load_frames(t0, f_cur);
+                if (is_qk && ik == 0) {  // Q rows of this shard (this CTA's 64 heads)
+                    if (seg > 0) tc::mbar_wait_sleep(misc + BAR_QEMPTY, (seg - 1) & 1);
+                    if (cta == 0) mbar_arrive_expect_tx(misc + BAR_QFULL, 2 * Q_BYTES);
                     for (int b = 0; b < NKB; ++b)
                         tc::tma_load_2d_pair(sbase + OFF_Q + b * 8192, &q_map, 64 * b, r * H + 64 * static_cast<int>(cta),
                                              lead + BAR_QFULL, pol_norm);
                 }
-                __syncwarp();
-                int prev_frames = 0;
                 for (int t = t0; t < t1; ++t) {
-                    const int pg0 = pg_begin + (t - p.cu_tiles[r]) * PPT;
-                    int frames = p.num_frames;  // out of bounds -> TMA zero fill
-                    if (lane < PPT && pg0 + lane < pg_end) frames = __ldg(p.block_table + pg0 + lane);
-                    for (int b = 0; b < NKB; ++b) qk_stage(b, frames);
-                    if (t > t0)
+                    if (t + 1 < t1) load_frames(t + 1, f_next);
+                    if (is_qk) {
+                        for (int b = 0; b < NKB; ++b) qk_stage(b, f_cur);
+                    } else {
                         for (int j = 0; j < 2; ++j)
-                            for (int q = 0; q < 4; ++q) pv_stage(j, q, prev_frames);
-                    prev_frames = frames;
+                            for (int q = 0; q < 4; ++q) pv_stage(j, q, f_cur);
+                    }
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) f_cur[k] = f_next[k];
                 }
-                for (int j = 0; j < 2; ++j)
-                    for (int q = 0; q < 4; ++q) pv_stage(j, q, prev_frames);
                 ++seg;
                 w.t = t1;
                 ++w.r;
             }
-        } else if (warp == 5) {
-            // ===================== MMA issuer (leader CTA, one thread) =====================
-            if (cta == 0 && lane == 0) {
+          }
+        } else if (warp == W_MMAQ || warp == W_MMAV) {
+            // ===================== MMA issuers (leader CTA, whole warp; one elected lane issues) ======
+            if (cta == 0) {
                 constexpr uint32_t ID_QK = tc::idesc_bf16_f32(128, 128, false, false);
                 constexpr uint32_t ID_PV = tc::idesc_bf16_f32(128, 256, false, true);
-                uint32_t it = 0;
-                uint32_t g = 0;  // pair tile counter (S / P buffers)
+                const bool is_qk = warp == W_MMAQ;
+                uint32_t it = 0;  // ring counter
+                uint32_t g = 0;   // pair tile counter (S / P buffers)
                 int seg = 0;
-                auto wait_full = [&]() -> uint32_t {
-                    const uint32_t s = it % NS;
-                    tc::mbar_wait_cluster(misc + BAR_FULL + 8 * s, (it / NS) & 1);
-                    tc::fence_after_sync();
-                    return s;
-                };
-                auto pv = [&](uint32_t gp, bool first) {
-                    const uint32_t pb = gp & 1;
-                    tc::mbar_wait_cluster(misc + BAR_PFULL + 8 * pb, (gp >> 1) & 1);
-                    if (first && seg > 0) tc::mbar_wait_cluster(misc + BAR_OEMPTY, (seg - 1) & 1);
-                    tc::fence_after_sync();
-                    const uint32_t pbase = sbase + OFF_P + pb * P_BYTES;
-                    for (int j = 0; j < 2; ++j)
-                        for (int q = 0; q < 4; ++q) {
-                            const uint32_t s = wait_full();
-                            const uint32_t st = sbase + OFF_RING + s * STAGE;
-#pragma unroll
-                            for (int kk = 0; kk < 2; ++kk) {
-                                const int ks = 2 * q + kk;  // 16-token k-step of the tile
-                                const uint64_t ad = tc::sdesc_sw128(pbase + (ks >> 2) * 8192 + (ks & 3) * 32, 16, 1024);
-                                const uint64_t bd = tc::sdesc_sw128(st + kk * 2048, 4096, 1024);
-                                tc::mma_bf16_ss<2>(tmem + TM_O + 128 * j, ad, bd, ID_PV, !(first && ks == 0));
+                long long wait_ns = 0, n_wait = 0, n_ready = 0;  // diagnostics (trace row 255)
+                const long long t_mma0 = gtime();
+                // Ring waits are polled by lane 0 and the stage index re-broadcast, so every
+                // value feeding a tcgen05.mma stays warp-uniform (uniform datapath, no
+                // per-MMA R2UR / ELECT retry loops).
+                auto wait_full = [&](int nst, uint32_t bfull) -> uint32_t {
+                    const uint32_t s = it % nst;
+                    if (lane == 0) {
+                        if (p.trace) {
+                            if (mbar_try_wait(misc + bfull + 8 * s, (it / nst) & 1)) {
+                                ++n_ready;
+                            } else {
+                                const long long a0 = gtime();
+                                mbar_wait(misc + bfull + 8 * s, (it / nst) & 1);
+                                wait_ns += gtime() - a0;
+                                ++n_wait;
                             }
-                            tc::commit2_mc(misc + BAR_EMPTY + 8 * s, 0x3);
-                            ++it;
+                        } else {
+                            mbar_wait(misc + bfull + 8 * s, (it / nst) & 1);
                         }
-                    tc::commit2_mc(misc + BAR_PEMPTY + 8 * pb, 0x3);
+                    }
+                    __syncwarp();
+                    tc::fence_after_sync();
+                    return __shfl_sync(0xffffffffu, s, 0);
                 };
+                // base descriptors; the 14-bit start-address field never carries (smem < 256 KB)
+                const uint64_t dQ = tc::sdesc_sw128(sbase + OFF_Q, 16, 1024);
+                const uint64_t dRQ = tc::sdesc_sw128(sbase + OFF_RQ, 16, 1024);
+                const uint64_t dP = tc::sdesc_sw128(sbase + OFF_P, 16, 1024);
+                const uint64_t dRV = tc::sdesc_sw128(sbase + OFF_RV, 4096, 1024);
                 SegWalk w(p.cu_tiles, R, t_begin, t_end);
                 while (w.t < w.t_end) {
                     while (p.cu_tiles[w.r + 1] <= w.t) ++w.r;
                     const int t0 = w.t, t1 = min(p.cu_tiles[w.r + 1], w.t_end);
-                    tc::mbar_wait_cluster(misc + BAR_QFULL, seg & 1);
-                    tc::fence_after_sync();
+                    if (is_qk) {
+                        tc::mbar_wait_sleep(misc + BAR_QFULL, seg & 1);
+                        tc::fence_after_sync();
+                    }
                     for (int t = t0; t < t1; ++t, ++g) {
                         const uint32_t sb = g & 1;
-                        if (g >= 2) tc::mbar_wait_cluster(misc + BAR_SEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
-                        tc::fence_after_sync();
-                        for (int b = 0; b < NKB; ++b) {
-                            const uint32_t s = wait_full();
-                            const uint32_t st = sbase + OFF_RING + s * STAGE;
+                        if (is_qk) {
+                            // ---- S[sb] = Q K^T over the 9 K boxes ----
+                            if (lane == 0) MLA_TRACE(g, 0);
+                            if (g >= 2) tc::mbar_wait_sleep(misc + BAR_SEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
+                            tc::fence_after_sync();
+                            for (int b = 0; b < NKB; ++b) {
+                                const uint32_t s = wait_full(NSQ, BAR_FULLQ);
+                                const uint64_t a0 = dQ + ((b * 8192) >> 4), b0 = dRQ + ((s * STAGE) >> 4);
 #pragma unroll
-                            for (int kk = 0; kk < 4; ++kk) {
-                                const uint64_t ad = tc::sdesc_sw128(sbase + OFF_Q + b * 8192 + kk * 32, 16, 1024);
-                                const uint64_t bd = tc::sdesc_sw128(st + kk * 32, 16, 1024);
-                                tc::mma_bf16_ss<2>(tmem + TM_S + 64 * sb, ad, bd, ID_QK, (b | kk) != 0);
+                                for (int kk = 0; kk < 4; ++kk)
+                                    if (!(p.dbg & 1))
+                                        tc::mma2_bf16_ss_warp(tmem + TM_S + 64 * sb, a0 + 2 * kk, b0 + 2 * kk, ID_QK,
+                                                              (b | kk) != 0);
+                                tc::commit2_mc_warp(misc + BAR_EMPTYQ + 8 * s, 0x3);
+                                ++it;
                             }
-                            tc::commit2_mc(misc + BAR_EMPTY + 8 * s, 0x3);
-                            ++it;
+                            tc::commit2_mc_warp(misc + BAR_SFULL + 8 * sb, 0x3);
+                            if (lane == 0) MLA_TRACE(g, 1);
+                            if (t == t1 - 1) tc::commit2_mc_warp(misc + BAR_QEMPTY, 0x3);
+                        } else {
+                            // ---- O += P[sb] V over the 2 latent halves x 4 token quarters ----
+                            const bool first = t == t0;
+                            tc::mbar_wait_sleep(misc + BAR_PFULL + 8 * sb, (g >> 1) & 1);
+                            if (first && seg > 0) tc::mbar_wait_sleep(misc + BAR_OEMPTY, (seg - 1) & 1);
+                            tc::fence_after_sync();
+                            if (lane == 0) MLA_TRACE(g, 2);
+                            const uint64_t pd = dP + ((sb * P_BYTES) >> 4);
+                            for (int j = 0; j < 2; ++j)
+                                for (int q = 0; q < 4; ++q) {
+                                    const uint32_t s = wait_full(NSV, BAR_FULLV);
+                                    const uint64_t b0 = dRV + ((s * STAGE) >> 4);
+#pragma unroll
+                                    for (int kk = 0; kk < 2; ++kk) {
+                                        const int ks = 2 * q + kk;  // 16-token k-step of the tile
+                                        const uint64_t ad = pd + (((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
+                                        if (!(p.dbg & 1))
+                                            tc::mma2_bf16_ss_warp(tmem + TM_O + 128 * j, ad, b0 + ((kk * 2048) >> 4),
+                                                                  ID_PV, !(first && ks == 0));
+                                    }
+                                    tc::commit2_mc_warp(misc + BAR_EMPTYV + 8 * s, 0x3);
+                                    ++it;
+                                }
+                            tc::commit2_mc_warp(misc + BAR_PEMPTY + 8 * sb, 0x3);
+                            if (lane == 0) MLA_TRACE(g, 3);
                         }
-                        tc::commit2_mc(misc + BAR_SFULL + 8 * sb, 0x3);
-                        if (t == t1 - 1) tc::commit2_mc(misc + BAR_QEMPTY, 0x3);
-                        if (t > t0) pv(g - 1, t - 1 == t0);
                     }
-                    pv(g - 1, t1 - 1 == t0);
                     ++seg;
                     w.t = t1;
                     ++w.r;
                 }
+                if (p.trace && pair == 0 && lane == 0) {
+                    const int row = is_qk ? 254 : 255;
+                    p.trace[row * 8 + 0] = gtime() - t_mma0;
+                    p.trace[row * 8 + 1] = wait_ns;
+                    p.trace[row * 8 + 2] = n_wait;
+                    p.trace[row * 8 + 3] = n_ready;
+                }
             }
-        } else {
+        } else if (warp < 4) {
             // ===================== softmax / correction / epilogue (warps 0-3, both CTAs) ==========
             const int tid = threadIdx.x;        // == TMEM lane
             const int hl = tid & 63;            // head within this CTA
@@ -398,8 +487,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             nvalid[k] = min(16, max(0, fill - off));
                         }
                     }
-                    tc::mbar_wait_cluster(sbase + OFF_MISC + BAR_SFULL + 8 * sb, (g >> 1) & 1);
+                    tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_SFULL + 8 * sb, (g >> 1) & 1);
                     tc::fence_after_sync();
+                    if (tid == 0) MLA_TRACE(g, 4 + 2 * static_cast<int>(cta));
+                    if (p.dbg & 2) {  // experiment: pass S / P through without the softmax math
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_SEMPTY + 8 * sb);
+                        if (g >= 2) tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_PFULL + 8 * sb);
+                        m_used = 0.f;
+                        l_run = 1.f;
+                        continue;
+                    }
                     uint32_t sv[2][32];
                     tc::tmem_ld32(tl + TM_S + 64 * sb, sv[0]);
                     tc::tmem_ld32(tl + TM_S + 64 * sb + 32, sv[1]);
@@ -436,7 +536,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     }
                     l_run = l_run * alpha + ps;
                     // P buffer sb is free once PV(g-2) completed
-                    if (g >= 2) tc::mbar_wait_cluster(sbase + OFF_MISC + BAR_PEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
+                    if (g >= 2) tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
                     {
                         uint8_t* prow = smem + OFF_P + sb * P_BYTES + half * 8192 + hl * 128;
 #pragma unroll
@@ -452,7 +552,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     // O *= alpha once PV(g-1) has landed.  tcgen05.ld/st are warp-collective, so the
                     // whole warp waits and rewrites its lanes if any lane needs it (alpha = 1 elsewhere).
                     if (__any_sync(0xffffffffu, rescale)) {
-                        tc::mbar_wait_cluster(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) & 1), ((g - 1) >> 1) & 1);
+                        tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) & 1), ((g - 1) >> 1) & 1);
                         tc::fence_after_sync();
                         for (int c = 0; c < 256; c += 32) {
                             uint32_t ov[32];
@@ -468,9 +568,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     tc::fence_before_sync();
                     __syncwarp();
                     if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_PFULL + 8 * sb);
+                    if (tid == 0) MLA_TRACE(g, 5 + 2 * static_cast<int>(cta));
                 }
                 // ---- epilogue of segment [t0, t1) of shard r ----
-                tc::mbar_wait_cluster(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) & 1), ((g - 1) >> 1) & 1);
+                tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) & 1), ((g - 1) >> 1) & 1);
                 tc::fence_after_sync();
                 red[tid] = l_run;
                 named_bar_sync(1, 128);
@@ -498,66 +599,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_OEMPTY);
                 if (complete) {
                     if (half == 0) p.lse[static_cast<size_t>(r) * H + head] = (m_used + __log2f(l_tot)) * 0.69314718055994530942f;
-                } else {
-                    if (half == 0)
-                        __stcg(reinterpret_cast<float2*>(p.ws_ml) + (static_cast<size_t>(slot) * H + head),
-                               make_float2(m_used, l_tot));
-                    __threadfence();
-                    named_bar_sync(1, 128);
-                    volatile int* last_flag = reinterpret_cast<volatile int*>(smem + OFF_MISC + LAST_FLAG);
-                    if (tid == 0) {
-                        const int a = pair_of_tile(r_first, T, NP);
-                        const int b = pair_of_tile(r_last - 1, T, NP);
-                        int nparts = b - a + 1;
-                        if (T < NP) {
-                            nparts = 0;
-                            for (int k = a; k <= b; ++k) nparts += pair_nonempty(k, T, NP);
-                        }
-                        const int prev = atomicAdd(p.counters + 2 * r + cta, 1);
-                        *last_flag = (prev == nparts - 1) ? 1 : 0;
-                    }
-                    named_bar_sync(1, 128);
-                    if (*last_flag) {
-                        __threadfence();
-                        const int a = pair_of_tile(r_first, T, NP);
-                        const int b = pair_of_tile(r_last - 1, T, NP);
-                        for (int hh = warp; hh < 64; hh += 4) {
-                            const int qh = 64 * static_cast<int>(cta) + hh;
-                            float mmax = -INFINITY;
-                            for (int k = a; k <= b; ++k) {
-                                if (!pair_nonempty(k, T, NP)) continue;
-                                const int sl = (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
-                                mmax = fmaxf(mmax, __ldcg(p.ws_ml + (static_cast<size_t>(sl) * H + qh) * 2));
-                            }
-                            float den = 0.f;
-                            float4 num[4];
-#pragma unroll
-                            for (int v = 0; v < 4; ++v) num[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-                            for (int k = a; k <= b; ++k) {
-                                if (!pair_nonempty(k, T, NP)) continue;
-                                const int sl = (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
-                                const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + (static_cast<size_t>(sl) * H + qh));
-                                const float wk = fast_exp2(ml.x - mmax);
-                                den += wk * ml.y;
-                                const float4* src = reinterpret_cast<const float4*>(p.ws_acc + (static_cast<size_t>(sl) * H + qh) * DL);
-#pragma unroll
-                                for (int v = 0; v < 4; ++v) {
-                                    const float4 x = __ldcg(src + lane + 32 * v);
-                                    num[v].x += wk * x.x;
-                                    num[v].y += wk * x.y;
-                                    num[v].z += wk * x.z;
-                                    num[v].w += wk * x.w;
-                                }
-                            }
-                            const float dinv = 1.f / den;
-                            float4* o = reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL);
-#pragma unroll
-                            for (int v = 0; v < 4; ++v)
-                                o[lane + 32 * v] = make_float4(num[v].x * dinv, num[v].y * dinv, num[v].z * dinv, num[v].w * dinv);
-                            if (lane == 0) p.lse[static_cast<size_t>(r) * H + qh] = (mmax + __log2f(den)) * 0.69314718055994530942f;
-                        }
-                        if (tid == 0) p.counters[2 * r + cta] = 0;  // re-arm
-                    }
+                } else if (half == 0) {  // cut segment: (max, sum) of the partial; mla_merge_kernel combines
+                    __stcg(reinterpret_cast<float2*>(p.ws_ml) + (static_cast<size_t>(slot) * H + head),
+                           make_float2(m_used, l_tot));
                 }
                 ++seg;
                 w.t = t1;
@@ -569,6 +613,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc::fence_before_sync();
     tc::cluster_sync();
     if (warp == 0) tc::tmem_dealloc<2>(tmem, 512);
+}
+
+// Stream-K combine (lse_merge, attn_merge.hpp:86-100, in the log2 domain): every shard cut
+// by a pair-range boundary has one partial per pair that touched it.  One CTA per
+// (shard, 16-head group), one warp per head; uncut shards exit at once.  A separate launch
+// keeps a shard split over many pairs (a 512K request spans ~50) off any one pair's tail.
+__global__ void __launch_bounds__(512) mla_merge_kernel(MlaParams p, int num_pairs) {
+    const int r = blockIdx.x;
+    const int64_t T = p.cu_tiles[p.num_shards];
+    const int64_t NP = num_pairs;
+    const int r_first = p.cu_tiles[r], r_last = p.cu_tiles[r + 1];
+    if (r_first == r_last) return;
+    const int a = pair_of_tile(r_first, T, NP);
+    const int b = pair_of_tile(r_last - 1, T, NP);
+    if (a == b) return;  // one pair covered the whole shard and wrote the final output
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qh = blockIdx.y * 16 + warp;
+    auto slot_of = [&](int k) {
+        return (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
+    };
+    float mmax = -INFINITY;
+    for (int k = a; k <= b; ++k) {
+        if (!pair_nonempty(k, T, NP)) continue;
+        mmax = fmaxf(mmax, __ldcg(p.ws_ml + (static_cast<size_t>(slot_of(k)) * H + qh) * 2));
+    }
+    float den = 0.f;
+    float4 num[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) num[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int k = a; k <= b; ++k) {
+        if (!pair_nonempty(k, T, NP)) continue;
+        const int sl = slot_of(k);
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + (static_cast<size_t>(sl) * H + qh));
+        const float wk = fast_exp2(ml.x - mmax);
+        den += wk * ml.y;
+        const float4* src = reinterpret_cast<const float4*>(p.ws_acc + (static_cast<size_t>(sl) * H + qh) * DL);
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const float4 x = __ldcg(src + lane + 32 * v);
+            num[v].x += wk * x.x;
+            num[v].y += wk * x.y;
+            num[v].z += wk * x.z;
+            num[v].w += wk * x.w;
+        }
+    }
+    const float dinv = 1.f / den;
+    float4* o = reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL);
+#pragma unroll
+    for (int v = 0; v < 4; ++v)
+        o[lane + 32 * v] = make_float4(num[v].x * dinv, num[v].y * dinv, num[v].z * dinv, num[v].w * dinv);
+    if (lane == 0) p.lse[static_cast<size_t>(r) * H + qh] = (mmax + __log2f(den)) * 0.69314718055994530942f;
 }
 
 }  // namespace mla
