@@ -374,6 +374,16 @@ def run_ours(args, ws, rank, local):
             planner = dict(scenario=PLANNER_SCENARIO, **planner_device(ctx))
         except Exception as e:  # reported, not fatal
             planner = {"scenario": PLANNER_SCENARIO, "error": str(e)}
+    mla = None
+    if rank == 0 and ws == 1 and not args.no_mla:
+        # the cfg5 MLA attention shape on tcgen05 CTA pairs (K10), reported beside K1
+        try:
+            import bench_mla
+            keep = ("workload", "requests", "kv_tokens", "ms_per_step", "decode_tok_s", "achieved_gbs", "hbm_frac",
+                    "achieved_tflops", "tensor_frac", "roofline_frac", "peak_kind", "kernel", "gpu_launches_per_step")
+            mla = [{k: r[k] for k in keep} for r in bench_mla.run_all(ctx, dev, steps=min(args.steps, 50), warmup=3)]
+        except Exception as e:  # reported, not fatal
+            mla = {"error": str(e)}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -406,6 +416,7 @@ def run_ours(args, ws, rank, local):
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "planner": planner,
+            "mla": mla,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -425,6 +436,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mla", action="store_true", help="skip the K10 MLA leg (SURVEY §8f #1)")
     args = ap.parse_args()
     ws, rank, local = dist_init()
     if args.impl == "reference":

@@ -9,7 +9,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG
 timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?" >> $OUT/bench_$TAG.err
 timeout 900 python bench_dcp.py --steps 300 > $OUT/bench_dcp_$TAG.json 2> $OUT/bench_dcp_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
-    python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch_bench_$TAG.log 2>&1
+    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-mla > $OUT/ncu_launch_bench_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:splitkv_decode -s 3 -c 1 \
-    -o $OUT/k1_$TAG -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$TAG.log 2>&1
+    -o $OUT/k1_$TAG -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-mla > $OUT/ncu_full_$TAG.log 2>&1
 echo done

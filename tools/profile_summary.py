@@ -2,7 +2,7 @@
 """Summarise an ncu launch list (+ optional --set full report) into profiles/.
 
     python tools/profile_summary.py TAG gpurun_out/launches_TAG.csv [gpurun_out/k1_TAG.ncu-rep] \
-        [--alg-bytes N]
+        [--alg-bytes N] [--kernel SUBSTR (default splitkv)] [--traffic-out k1_traffic.json]
 
 Writes profiles/TAG_launches.csv (our kernels + per-kernel totals) and
 profiles/TAG_ncu_summary.md (speed-of-light, DRAM bytes per launch vs the
@@ -46,6 +46,8 @@ def main():
     alg = None
     if "--alg-bytes" in sys.argv:
         alg = int(sys.argv[sys.argv.index("--alg-bytes") + 1])
+    kern = sys.argv[sys.argv.index("--kernel") + 1] if "--kernel" in sys.argv else "splitkv"
+    tout = sys.argv[sys.argv.index("--traffic-out") + 1] if "--traffic-out" in sys.argv else "k1_traffic.json"
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     L = read_launches(launches)
     tot = {}
@@ -65,7 +67,7 @@ def main():
     if rep:
         for rec in ncu_raw(rep):
             name = rec.get("Kernel Name", ("?", ""))[0]
-            if "splitkv" not in name and "dcp" not in name:
+            if kern not in name:
                 continue
             def g(m):
                 v = rec.get(m)
@@ -102,7 +104,7 @@ def main():
             if alg:
                 md.append(f"- algorithmic bytes/launch {alg / 1e9:.4f} GB; traffic/algorithmic = "
                           f"{summary['dram_bytes_per_launch'] / alg:.4f}")
-            with open(os.path.join(ROOT, "profiles", "k1_traffic.json"), "w") as f:
+            with open(os.path.join(ROOT, "profiles", tout), "w") as f:
                 json.dump(summary, f, indent=1)
     with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.md"), "w") as f:
         f.write("\n".join(md) + "\n")
