@@ -50,44 +50,57 @@ constexpr int NKB = DK / 64;         // 9 K boxes of 64 columns
 constexpr int TILE = 128;            // tokens per pair tile
 constexpr int HT = TILE / 2;         // tokens per CTA in S = Q K^T
 constexpr int STAGE = 8192;          // ring stage bytes
-constexpr int NSQ = 10;              // QK ring stages (the HBM stream)
-constexpr int NSV = 5;               // PV ring stages (the L2 re-read stream)
 constexpr int Q_BYTES = NKB * 8192;  // 64 heads x 576 bf16 per CTA
 constexpr int P_BYTES = 2 * 8192;    // 64 heads x 128 tokens bf16 per CTA
+// Four accumulator chains, each issued by its own MMA warp and fed by its own ring: an
+// accumulating 2-CTA M=128 MMA costs ~120 ns whatever its N, but chains issued by different
+// warps overlap (tools/probe/mma_rate.cu).  S = Q K^T is split over K into two accumulators
+// (boxes 0-4 -> S_A, 5-8 -> S_B; the softmax adds them), O += P V over the two latent halves.
+enum Ring { RQA = 0, RQB = 1, RV0 = 2, RV1 = 3, NRING = 4 };
+constexpr int QA_BOXES = 5;          // K boxes [0, 5) -> S_A, [5, 9) -> S_B
+#ifndef MLA_RS_QA
+#define MLA_RS_QA 5
+#define MLA_RS_QB 4
+#define MLA_RS_V0 3
+#define MLA_RS_V1 3
+#endif
+__host__ __device__ constexpr int ring_stages(int k) {
+    return k == RQA ? MLA_RS_QA : k == RQB ? MLA_RS_QB : k == RV0 ? MLA_RS_V0 : MLA_RS_V1;
+}
+__host__ __device__ constexpr int ring_first(int k) { return k == 0 ? 0 : ring_first(k - 1) + ring_stages(k - 1); }
+constexpr int NSTAGES = ring_first(NRING);  // 15 stages of 8 KB
 constexpr int OFF_Q = 0;
 constexpr int OFF_P = OFF_Q + Q_BYTES;
-constexpr int OFF_RQ = OFF_P + 2 * P_BYTES;
-constexpr int OFF_RV = OFF_RQ + NSQ * STAGE;
-constexpr int OFF_MISC = OFF_RV + NSV * STAGE;
+constexpr int OFF_RING = OFF_P + 2 * P_BYTES;
+constexpr int OFF_MISC = OFF_RING + NSTAGES * STAGE;
 // misc: barriers then exchange scratch.  Ring "full" barriers live in the leader: 1 arrival
-// (the leader's producer, expecting both CTAs' bytes) + tx; "empty" in each CTA: 1 (MMA commit multicast).
-constexpr int BAR_FULLQ = 0;                      // [NSQ]
-constexpr int BAR_EMPTYQ = BAR_FULLQ + 8 * NSQ;   // [NSQ]
-constexpr int BAR_FULLV = BAR_EMPTYQ + 8 * NSQ;   // [NSV]
-constexpr int BAR_EMPTYV = BAR_FULLV + 8 * NSV;   // [NSV]
-constexpr int BAR_QFULL = BAR_EMPTYV + 8 * NSV;   // leader: 1 + tx
-constexpr int BAR_QEMPTY = BAR_QFULL + 8;     // each: 1
-constexpr int BAR_SFULL = BAR_QEMPTY + 8;     // [2] each: 1
-constexpr int BAR_SEMPTY = BAR_SFULL + 16;    // [2] leader: 8 softmax warps
+// (the leader's issuer, expecting both CTAs' bytes) + tx; "empty" in each CTA: 1 (MMA commit multicast).
+constexpr int BAR_FULL = 0;                        // [NSTAGES]
+constexpr int BAR_EMPTY = BAR_FULL + 8 * NSTAGES;  // [NSTAGES]
+constexpr int BAR_QFULL = BAR_EMPTY + 8 * NSTAGES; // leader: 1 + tx
+constexpr int BAR_QEMPTY = BAR_QFULL + 8;     // each: 2 (both QK MMA warps)
+constexpr int BAR_SFULL = BAR_QEMPTY + 8;     // [2 S buffers][A, B] each: 1
+constexpr int BAR_SEMPTY = BAR_SFULL + 32;    // [2] leader: 8 softmax warps
 constexpr int BAR_PFULL = BAR_SEMPTY + 16;    // [2] leader: 8
-constexpr int BAR_PEMPTY = BAR_PFULL + 16;    // [2] each: 1
+constexpr int BAR_PEMPTY = BAR_PFULL + 16;    // [2] each: 2 (both PV MMA warps)
 constexpr int BAR_OEMPTY = BAR_PEMPTY + 16;   // leader: 8
 constexpr int TMEM_SLOT = BAR_OEMPTY + 8;
 constexpr int RED = 512;                      // float[2][128] exchange scratch
 constexpr int MISC_BYTES = RED + 2 * 128 * 4;
 constexpr int SMEM = 1024 + OFF_MISC + MISC_BYTES;
-// Warp roles: 0-3 softmax, 4 QK MMA, 5 PV MMA, then NQW QK-stream and NVW PV-stream TMA
-// issuers.  The two MMA chains touch disjoint TMEM (S vs O) and meet only through the
-// softmax barriers, so they are issued by two warps and run concurrently.  A single
-// thread issues a TMA box only every ~200 cycles (measured, tools/probe/tma_bw.cu), so the
-// 2-KB boxes of 16-token pages are spread over several issuing warps.
-constexpr int NQW = 4;
-constexpr int NVW = 2;
-constexpr int W_MMAQ = 4;                     // issues the S = Q K^T MMAs (leader CTA)
-constexpr int W_MMAV = 5;                     // issues the O += P V MMAs (leader CTA)
-constexpr int W_PROD = 6;
-constexpr int THREADS = 32 * (W_PROD + NQW + NVW);
-constexpr uint32_t TM_S = 0;                  // S buffers: cols [0,64), [64,128)
+// Warp roles: 0-3 softmax (thread t <-> TMEM lane t), 4-7 MMA issuers of rings QA/QB/V0/V1
+// (leader CTA), 8-11 TMA issuers of the same rings (both CTAs; the lanes of a warp issue the
+// boxes of a stage together, since one thread issues a box only every ~200 cycles,
+// tools/probe/tma_bw.cu).
+constexpr int W_MMA = 4;
+constexpr int W_TMA = 8;
+#ifndef MLA_NTW
+#define MLA_NTW 2
+#endif
+constexpr int NTW = MLA_NTW;                  // TMA issuer warps per ring
+constexpr int THREADS = 32 * (W_TMA + NTW * NRING);
+constexpr uint32_t TM_SA = 0;                 // S_A buffers: cols [0,64), [64,128)
+constexpr uint32_t TM_SB = 128;               // S_B buffers: cols [128,192), [192,256)
 constexpr uint32_t TM_O = 256;                // O: chunk j at 256 + 128 j
 constexpr float RESCALE_LOG2 = 8.f;           // rescale O only when the max grows by > 2^8
 
@@ -212,26 +225,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int t_end = static_cast<int>((pair + 1) * T / NP);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSQ; ++s) {
-            mbar_init(misc + BAR_FULLQ + 8 * s, 1);
-            mbar_init(misc + BAR_EMPTYQ + 8 * s, 1);
-        }
-        for (int s = 0; s < NSV; ++s) {
-            mbar_init(misc + BAR_FULLV + 8 * s, 1);
-            mbar_init(misc + BAR_EMPTYV + 8 * s, 1);
+        for (int s = 0; s < NSTAGES; ++s) {
+            mbar_init(misc + BAR_FULL + 8 * s, 1);
+            mbar_init(misc + BAR_EMPTY + 8 * s, 1);
         }
         mbar_init(misc + BAR_QFULL, 1);
-        mbar_init(misc + BAR_QEMPTY, 1);
+        mbar_init(misc + BAR_QEMPTY, 2);
         for (int b = 0; b < 2; ++b) {
-            mbar_init(misc + BAR_SFULL + 8 * b, 1);
+            mbar_init(misc + BAR_SFULL + 16 * b, 1);
+            mbar_init(misc + BAR_SFULL + 16 * b + 8, 1);
             mbar_init(misc + BAR_SEMPTY + 8 * b, 8);
             mbar_init(misc + BAR_PFULL + 8 * b, 8);
-            mbar_init(misc + BAR_PEMPTY + 8 * b, 1);
+            mbar_init(misc + BAR_PEMPTY + 8 * b, 2);
         }
         mbar_init(misc + BAR_OEMPTY, 8);
         fence_mbar_init();
     }
-    if (warp == W_PROD && lane == 0) {
+    if (warp == W_TMA && lane == 0) {
         tma_prefetch_desc(&q_map);
         tma_prefetch_desc(&kvq_map);
         tma_prefetch_desc(&kvp_map);
@@ -244,61 +254,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t lead = tc::mapa(misc, 0);  // leader's misc block (shared::cluster)
 
     if (t_begin < t_end) {
-        if (warp >= W_PROD) {
-          if (lane == 0) {
-            // ===================== TMA issuers (both CTAs, one thread per warp) =====================
-            // NQW warps stream Q and the QK stages (ring Q), NVW warps the PV stages (ring V):
-            // PV stages wait for the softmax before they are consumed, and on a separate ring
-            // they never hold back the QK prefetch.  Issuer k of a stream issues boxes k, k+n, ...
-            // of every stage; issuer 0 of the leader posts the stage's expected bytes.
-            // Single-thread loops: every TMA operand is thread-local; frame ids live in
-            // registers, prefetched a tile ahead.
-            const bool is_qk = warp < W_PROD + NQW;
-            const int ik = is_qk ? warp - W_PROD : warp - W_PROD - NQW;  // issuer index
-            const int nk = is_qk ? NQW : NVW;
+        if (warp >= W_TMA) {
+            // ===================== TMA issuers (both CTAs, one warp per ring) =====================
+            // Ring k streams its stages in tile order; lane 0 waits for the slot and (leader)
+            // posts both CTAs' bytes, then lanes 0..n-1 issue the stage's n boxes together.
+            // Frame ids: lane i holds page i of the tile, prefetched a tile ahead.
+            const int rk = (warp - W_TMA) / NTW, ik = (warp - W_TMA) % NTW;  // ring, issuer within it
+            const int nst = ring_stages(rk), s0 = ring_first(rk);
+            const uint32_t ring = sbase + OFF_RING + s0 * STAGE;
+            const int bi = ik + NTW * lane;  // the box of a stage this lane issues
             const uint64_t pol_first = l2_policy_evict_first();
             const uint64_t pol_norm = tc::l2_policy_evict_normal();
-            const int nst = is_qk ? NSQ : NSV;
-            const uint32_t ring = sbase + (is_qk ? OFF_RQ : OFF_RV);
-            const uint32_t bfull = is_qk ? BAR_FULLQ : BAR_FULLV, bempty = is_qk ? BAR_EMPTYQ : BAR_EMPTYV;
-            uint32_t it = 0;  // ring counter
+            uint32_t it = 0;
             int seg = 0;
-            const bool skip = !is_qk && (p.dbg & 4);  // experiment: PV stages without their loads
             auto stage_begin = [&]() {
                 const uint32_t s = it % nst;
-                tc::mbar_wait_sleep(misc + bempty + 8 * s, ((it / nst) & 1) ^ 1);
-                // the leader expects both CTAs' bytes; the peer's TMA completes on it directly
-                if (cta == 0 && ik == 0) mbar_arrive_expect_tx(misc + bfull + 8 * s, skip ? 0 : 2 * STAGE);
+                if (lane == 0) {
+                    tc::mbar_wait_sleep(misc + BAR_EMPTY + 8 * (s0 + s), ((it / nst) & 1) ^ 1);
+                    if (cta == 0 && ik == 0) mbar_arrive_expect_tx(misc + BAR_FULL + 8 * (s0 + s), 2 * STAGE);
+                }
+                __syncwarp();
+                ++it;
                 return s;
-            };
-            // QK stage b of a tile: this CTA's 64 tokens [64c, 64c+64) x K box b, as boxes of
-            // BQ = min(PAGE, 64) rows (one page, or a 64-token part of one)
-            auto qk_stage = [&](int b, const int (&fr)[PPT]) {
-                const uint32_t s = stage_begin();
-                const uint32_t dst = ring + s * STAGE, bar = lead + bfull + 8 * s;
-                for (int k = ik; k < 64 / BQ; k += nk) {
-                    const int u = 64 * static_cast<int>(cta) + k * BQ;  // token within the tile
-                    tc::tma_load_3d_pair(dst + k * BQ * 128, &kvq_map, 64 * b, u % PAGE, fr[u / PAGE], bar, pol_norm);
-                }
-                ++it;
-            };
-            // PV stage (j, q): tokens [32q, 32q+32) x dims [256j + 128c, +128) as 2 column boxes of 64,
-            // each in boxes of BP = min(PAGE, 32) rows
-            auto pv_stage = [&](int j, int q, const int (&fr)[PPT]) {
-                const uint32_t s = stage_begin();
-                if (skip) {
-                    ++it;
-                    return;
-                }
-                const uint32_t dst = ring + s * STAGE, bar = lead + bfull + 8 * s;
-                for (int i = ik; i < 2 * (32 / BP); i += nk) {
-                    const int k = i >> 1, bx = i & 1;
-                    const int u = 32 * q + k * BP;
-                    tc::tma_load_3d_pair(dst + bx * 4096 + k * BP * 128, &kvp_map,
-                                         64 * (4 * j + 2 * static_cast<int>(cta) + bx), u % PAGE, fr[u / PAGE], bar,
-                                         pol_first);
-                }
-                ++it;
             };
             SegWalk w(p.cu_tiles, R, t_begin, t_end);
             while (w.t < w.t_end) {
@@ -308,75 +285,98 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const int pg_begin = p.cu_pages[r], pg_end = p.cu_pages[r + 1];
                 const int r_first_tile = p.cu_tiles[r];
                 // pages past the shard get an out-of-bounds frame -> TMA zero fill
-                auto load_frames = [&](int t, int (&fr)[PPT]) {
-                    const int pg0 = pg_begin + (t - r_first_tile) * PPT;
-#pragma unroll
-                    for (int k = 0; k < PPT; ++k) fr[k] = pg0 + k < pg_end ? __ldg(p.block_table + pg0 + k) : p.num_frames;
+                auto tile_frame = [&](int t) {
+                    const int pg = pg_begin + (t - r_first_tile) * PPT + lane;
+                    return (lane < PPT && pg < pg_end) ? __ldg(p.block_table + pg) : p.num_frames;
                 };
-                int f_cur[PPT], f_next[PPT];
-                load_frames(t0, f_cur);
-                if (is_qk && ik == 0) {  // Q rows of this shard (this CTA's 64 heads)
-                    if (seg > 0) tc::mbar_wait_sleep(misc + BAR_QEMPTY, (seg - 1) & 1);
-                    if (cta == 0) mbar_arrive_expect_tx(misc + BAR_QFULL, 2 * Q_BYTES);
-                    for (int b = 0; b < NKB; ++b)
-                        tc::tma_load_2d_pair(sbase + OFF_Q + b * 8192, &q_map, 64 * b, r * H + 64 * static_cast<int>(cta),
-                                             lead + BAR_QFULL, pol_norm);
+                int f_cur = tile_frame(t0);
+                if (rk == RQA && ik == 0) {  // Q rows of this shard (this CTA's 64 heads), 9 boxes issued by lanes 0-8
+                    if (lane == 0) {
+                        if (seg > 0) tc::mbar_wait_sleep(misc + BAR_QEMPTY, (seg - 1) & 1);
+                        if (cta == 0) mbar_arrive_expect_tx(misc + BAR_QFULL, 2 * Q_BYTES);
+                    }
+                    __syncwarp();
+                    if (lane < NKB)
+                        tc::tma_load_2d_pair(sbase + OFF_Q + lane * 8192, &q_map, 64 * lane,
+                                             r * H + 64 * static_cast<int>(cta), lead + BAR_QFULL, pol_norm);
                 }
                 for (int t = t0; t < t1; ++t) {
-                    if (t + 1 < t1) load_frames(t + 1, f_next);
-                    if (is_qk) {
-                        for (int b = 0; b < NKB; ++b) qk_stage(b, f_cur);
+                    const int f_next = (t + 1 < t1) ? tile_frame(t + 1) : 0;
+                    if (rk == RQA || rk == RQB) {
+                        // QK stage b: this CTA's HT tokens x K box b, as boxes of BQ = min(PAGE, HT) rows
+                        const int b_lo = rk == RQA ? 0 : QA_BOXES, b_hi = rk == RQA ? QA_BOXES : NKB;
+                        for (int b = b_lo; b < b_hi; ++b) {
+                            const uint32_t s = stage_begin();
+                            const int u = HT * static_cast<int>(cta) + bi * BQ;  // this lane's box
+                            const int f = __shfl_sync(0xffffffffu, f_cur, (u / PAGE) & 31);
+                            if (bi < HT / BQ)
+                                tc::tma_load_3d_pair(ring + s * STAGE + bi * BQ * 128, &kvq_map, 64 * b, u % PAGE, f,
+                                                     lead + BAR_FULL + 8 * (s0 + s), pol_norm);
+                        }
                     } else {
-                        for (int j = 0; j < 2; ++j)
-                            for (int q = 0; q < 4; ++q) pv_stage(j, q, f_cur);
+                        // PV stage q of latent half j: tokens [32q, 32q+32) x dims [256j + 128c, +128),
+                        // 2 column boxes of 64 x (32 / BP) row boxes of BP = min(PAGE, 32)
+                        const int j = rk - RV0;
+                        for (int q = 0; q < TILE / 32; ++q) {
+                            const uint32_t s = stage_begin();
+                            const int k = bi >> 1, bx = bi & 1;
+                            const int u = 32 * q + k * BP;
+                            const int f = __shfl_sync(0xffffffffu, f_cur, (u / PAGE) & 31);
+                            if (bi < 2 * (32 / BP))
+                                tc::tma_load_3d_pair(ring + s * STAGE + bx * 4096 + k * BP * 128, &kvp_map,
+                                                     64 * (4 * j + 2 * static_cast<int>(cta) + bx), u % PAGE, f,
+                                                     lead + BAR_FULL + 8 * (s0 + s), pol_first);
+                        }
                     }
-#pragma unroll
-                    for (int k = 0; k < PPT; ++k) f_cur[k] = f_next[k];
+                    f_cur = f_next;
                 }
                 ++seg;
                 w.t = t1;
                 ++w.r;
             }
-          }
-        } else if (warp == W_MMAQ || warp == W_MMAV) {
+        } else if (warp >= W_MMA) {
             // ===================== MMA issuers (leader CTA, whole warp; one elected lane issues) ======
+            // Warp W_MMA + k drains ring k: QA / QB accumulate S_A / S_B, V0 / V1 the two latent
+            // halves of O.  Ring waits are polled by lane 0 and the slot re-broadcast, so every
+            // value feeding a tcgen05.mma stays warp-uniform.
             if (cta == 0) {
+                const int rk = warp - W_MMA;
+                const int nst = ring_stages(rk), s0 = ring_first(rk);
                 constexpr uint32_t ID_QK = tc::idesc_bf16_f32(128, 128, false, false);
                 constexpr uint32_t ID_PV = tc::idesc_bf16_f32(128, 256, false, true);
-                const bool is_qk = warp == W_MMAQ;
-                uint32_t it = 0;  // ring counter
-                uint32_t g = 0;   // pair tile counter (S / P buffers)
+                uint32_t it = 0;
+                uint32_t g = 0;  // pair tile counter (S / P buffers)
                 int seg = 0;
-                long long wait_ns = 0, n_wait = 0, n_ready = 0;  // diagnostics (trace row 255)
+                long long wait_ns = 0, n_wait = 0, n_ready = 0;  // diagnostics (trace rows 252-255)
                 const long long t_mma0 = gtime();
-                // Ring waits are polled by lane 0 and the stage index re-broadcast, so every
-                // value feeding a tcgen05.mma stays warp-uniform (uniform datapath, no
-                // per-MMA R2UR / ELECT retry loops).
-                auto wait_full = [&](int nst, uint32_t bfull) -> uint32_t {
+                auto wait_full = [&]() -> uint32_t {
                     const uint32_t s = it % nst;
                     if (lane == 0) {
+                        const uint32_t bar = misc + BAR_FULL + 8 * (s0 + s), par = (it / nst) & 1;
                         if (p.trace) {
-                            if (mbar_try_wait(misc + bfull + 8 * s, (it / nst) & 1)) {
+                            if (mbar_try_wait(bar, par)) {
                                 ++n_ready;
                             } else {
                                 const long long a0 = gtime();
-                                mbar_wait(misc + bfull + 8 * s, (it / nst) & 1);
+                                mbar_wait(bar, par);
                                 wait_ns += gtime() - a0;
                                 ++n_wait;
                             }
                         } else {
-                            mbar_wait(misc + bfull + 8 * s, (it / nst) & 1);
+                            mbar_wait(bar, par);
                         }
                     }
                     __syncwarp();
                     tc::fence_after_sync();
+                    ++it;
                     return __shfl_sync(0xffffffffu, s, 0);
                 };
                 // base descriptors; the 14-bit start-address field never carries (smem < 256 KB)
                 const uint64_t dQ = tc::sdesc_sw128(sbase + OFF_Q, 16, 1024);
-                const uint64_t dRQ = tc::sdesc_sw128(sbase + OFF_RQ, 16, 1024);
+                const uint64_t dR = tc::sdesc_sw128(sbase + OFF_RING + s0 * STAGE, 16, 1024);
+                const uint64_t dRV = tc::sdesc_sw128(sbase + OFF_RING + s0 * STAGE, 4096, 1024);
                 const uint64_t dP = tc::sdesc_sw128(sbase + OFF_P, 16, 1024);
-                const uint64_t dRV = tc::sdesc_sw128(sbase + OFF_RV, 4096, 1024);
+                const bool is_qk = rk == RQA || rk == RQB;
                 SegWalk w(p.cu_tiles, R, t_begin, t_end);
                 while (w.t < w.t_end) {
                     while (p.cu_tiles[w.r + 1] <= w.t) ++w.r;
@@ -388,49 +388,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     for (int t = t0; t < t1; ++t, ++g) {
                         const uint32_t sb = g & 1;
                         if (is_qk) {
-                            // ---- S[sb] = Q K^T over the 9 K boxes ----
-                            if (lane == 0) MLA_TRACE(g, 0);
+                            // ---- S_A / S_B [sb] = Q K^T over this chain's K boxes ----
+                            if (lane == 0 && rk == RQA) MLA_TRACE(g, 0);
                             if (g >= 2) tc::mbar_wait_sleep(misc + BAR_SEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
                             tc::fence_after_sync();
-                            for (int b = 0; b < NKB; ++b) {
-                                const uint32_t s = wait_full(NSQ, BAR_FULLQ);
-                                const uint64_t a0 = dQ + ((b * 8192) >> 4), b0 = dRQ + ((s * STAGE) >> 4);
+                            const int b_lo = rk == RQA ? 0 : QA_BOXES, b_hi = rk == RQA ? QA_BOXES : NKB;
+                            const uint32_t dst = tmem + (rk == RQA ? TM_SA : TM_SB) + 64 * sb;
+                            for (int b = b_lo; b < b_hi; ++b) {
+                                const uint32_t s = wait_full();
+                                const uint64_t a0 = dQ + ((b * 8192) >> 4), b0 = dR + ((s * STAGE) >> 4);
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
                                     if (!(p.dbg & 1))
-                                        tc::mma2_bf16_ss_warp(tmem + TM_S + 64 * sb, a0 + 2 * kk, b0 + 2 * kk, ID_QK,
-                                                              (b | kk) != 0);
-                                tc::commit2_mc_warp(misc + BAR_EMPTYQ + 8 * s, 0x3);
-                                ++it;
+                                        tc::mma2_bf16_ss_warp(dst, a0 + 2 * kk, b0 + 2 * kk, ID_QK, ((b - b_lo) | kk) != 0);
+                                tc::commit2_mc_warp(misc + BAR_EMPTY + 8 * (s0 + s), 0x3);
                             }
-                            tc::commit2_mc_warp(misc + BAR_SFULL + 8 * sb, 0x3);
-                            if (lane == 0) MLA_TRACE(g, 1);
+                            tc::commit2_mc_warp(misc + BAR_SFULL + 16 * sb + 8 * rk, 0x3);
+                            if (lane == 0 && rk == RQA) MLA_TRACE(g, 1);
                             if (t == t1 - 1) tc::commit2_mc_warp(misc + BAR_QEMPTY, 0x3);
                         } else {
-                            // ---- O += P[sb] V over the 2 latent halves x 4 token quarters ----
+                            // ---- O[j] += P[sb] V[j] over 4 token quarters ----
+                            const int j = rk - RV0;
                             const bool first = t == t0;
                             tc::mbar_wait_sleep(misc + BAR_PFULL + 8 * sb, (g >> 1) & 1);
                             if (first && seg > 0) tc::mbar_wait_sleep(misc + BAR_OEMPTY, (seg - 1) & 1);
                             tc::fence_after_sync();
-                            if (lane == 0) MLA_TRACE(g, 2);
+                            if (lane == 0 && rk == RV0) MLA_TRACE(g, 2);
                             const uint64_t pd = dP + ((sb * P_BYTES) >> 4);
-                            for (int j = 0; j < 2; ++j)
-                                for (int q = 0; q < 4; ++q) {
-                                    const uint32_t s = wait_full(NSV, BAR_FULLV);
-                                    const uint64_t b0 = dRV + ((s * STAGE) >> 4);
+                            for (int q = 0; q < TILE / 32; ++q) {
+                                const uint32_t s = wait_full();
+                                const uint64_t b0 = dRV + ((s * STAGE) >> 4);
 #pragma unroll
-                                    for (int kk = 0; kk < 2; ++kk) {
-                                        const int ks = 2 * q + kk;  // 16-token k-step of the tile
-                                        const uint64_t ad = pd + (((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
-                                        if (!(p.dbg & 1))
-                                            tc::mma2_bf16_ss_warp(tmem + TM_O + 128 * j, ad, b0 + ((kk * 2048) >> 4),
-                                                                  ID_PV, !(first && ks == 0));
-                                    }
-                                    tc::commit2_mc_warp(misc + BAR_EMPTYV + 8 * s, 0x3);
-                                    ++it;
+                                for (int kk = 0; kk < 2; ++kk) {
+                                    const int ks = 2 * q + kk;  // 16-token k-step of the tile
+                                    const uint64_t ad = pd + (((ks >> 2) * 8192 + (ks & 3) * 32) >> 4);
+                                    if (!(p.dbg & 1))
+                                        tc::mma2_bf16_ss_warp(tmem + TM_O + 128 * j, ad, b0 + ((kk * 2048) >> 4), ID_PV,
+                                                              !(first && ks == 0));
                                 }
+                                tc::commit2_mc_warp(misc + BAR_EMPTY + 8 * (s0 + s), 0x3);
+                            }
                             tc::commit2_mc_warp(misc + BAR_PEMPTY + 8 * sb, 0x3);
-                            if (lane == 0) MLA_TRACE(g, 3);
+                            if (lane == 0 && rk == RV0) MLA_TRACE(g, 3);
                         }
                     }
                     ++seg;
@@ -438,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     ++w.r;
                 }
                 if (p.trace && pair == 0 && lane == 0) {
-                    const int row = is_qk ? 254 : 255;
+                    const int row = 252 + rk;
                     p.trace[row * 8 + 0] = gtime() - t_mma0;
                     p.trace[row * 8 + 1] = wait_ns;
                     p.trace[row * 8 + 2] = n_wait;
@@ -487,7 +486,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             nvalid[k] = min(16, max(0, fill - off));
                         }
                     }
-                    tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_SFULL + 8 * sb, (g >> 1) & 1);
+                    tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_SFULL + 16 * sb, (g >> 1) & 1);
+                    tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_SFULL + 16 * sb + 8, (g >> 1) & 1);
                     tc::fence_after_sync();
                     if (tid == 0) MLA_TRACE(g, 4 + 2 * static_cast<int>(cta));
                     if (p.dbg & 2) {  // experiment: pass S / P through without the softmax math
@@ -500,21 +500,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         l_run = 1.f;
                         continue;
                     }
-                    uint32_t sv[2][32];
-                    tc::tmem_ld32(tl + TM_S + 64 * sb, sv[0]);
-                    tc::tmem_ld32(tl + TM_S + 64 * sb + 32, sv[1]);
-                    tc::tmem_wait_ld();
-                    tc::fence_before_sync();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_SEMPTY + 8 * sb);
                     float s[64];
                     float mx = -INFINITY;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        const bool ok = (j & 15) < nvalid[j >> 4];
-                        s[j] = ok ? __uint_as_float(sv[j >> 5][j & 31]) * p.scale_log2 : -INFINITY;
-                        mx = fmaxf(mx, s[j]);
+                    for (int c = 0; c < 2; ++c) {  // S = S_A + S_B, 32 columns at a time
+                        uint32_t va[32], vb[32];
+                        tc::tmem_ld32(tl + TM_SA + 64 * sb + 32 * c, va);
+                        tc::tmem_ld32(tl + TM_SB + 64 * sb + 32 * c, vb);
+                        tc::tmem_wait_ld();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int j = 32 * c + i;
+                            const bool ok = (j & 15) < nvalid[j >> 4];
+                            s[j] = ok ? (__uint_as_float(va[i]) + __uint_as_float(vb[i])) * p.scale_log2 : -INFINITY;
+                            mx = fmaxf(mx, s[j]);
+                        }
                     }
+                    tc::fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_SEMPTY + 8 * sb);
                     red[tid] = mx;
                     named_bar_sync(1, 128);
                     mx = fmaxf(mx, red[partner]);

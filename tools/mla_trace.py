@@ -33,9 +33,9 @@ att.launch()
 torch.cuda.synchronize()
 _capi.lib().dcp_mla_set_trace(None)
 t = tr.cpu().numpy()
-for row, nm in ((254, "QK"), (255, "PV")):
+for row, nm in ((252, "QK-A"), (253, "QK-B"), (254, "PV-0"), (255, "PV-1")):
     print(f"{nm} MMA warp: total ns", t[row, 0], "waiting on full ring ns", t[row, 1], "waits", t[row, 2], "ready", t[row, 3])
-t[254:] = 0
+t[252:] = 0
 n = int((t[:, 0] > 0).sum())
 t0 = t[0, 0]
 t = t[:n].astype(np.int64) - t0
