@@ -112,3 +112,14 @@ def test_mla_page_sizes(ctx, page):
     b, q, pool = _case([1, 100, 2000, 5000], page=page, seed=page)
     out, lse = _run(ctx, b, q, pool)
     _check(b, q, pool, out, lse)
+
+
+def test_mla_many_shards(ctx):
+    """1,100 shards (the tile scan's carry across 1,024-shard chunks), mostly 1-3 tiles each,
+    zero-token shards interleaved, several segments per pair."""
+    rng = np.random.default_rng(21)
+    lens = rng.integers(1, 400, size=1100)
+    lens[::97] = 0
+    b, q, pool = _case(lens.tolist(), seed=21, spare=3)
+    out, lse = _run(ctx, b, q, pool)
+    _check(b, q, pool, out, lse)
