@@ -1,0 +1,133 @@
+"""K4/K5 MoE dispatch / combine bench (the cfg4 / cfg5 EP exchange).
+
+W DP-EP instances are emulated on one GPU: every instance's pools are mapped into the
+others with dcp_moe_set_peer_local, so each cross-instance store is a local HBM store
+(on a multi-GPU node the same kernels store over NVLink into CUDA-IPC peer pools).
+The expert FFN between receive and combine is out of scope (library GEMMs); here it
+is the identity (y_rows = x_rows, untimed), so the combine returns each token's
+hidden state once per destination rank.
+
+One step = every instance: K4 (layout + dispatch), then K5a (receive), then K5b
+(combine_put), then K5c (combine_reduce).  Reported per phase: device time (CUDA events
+around each instance's call, summed over instances = the time W GPUs would each
+spend, max-over-instances would be the per-GPU critical path) and bytes moved; plus
+the algorithmic cross-instance bytes of the step (2 x sum over tokens of
+distinct remote destination ranks x hidden x 2 B).
+
+python bench_moe.py [--steps K]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "cfg4 Qwen3-30B-A3B layer (hidden 2048, 128 experts top-8, W=8)": dict(H=2048, E=128, k=8, W=8, M=128),
+    "cfg5 DeepSeek-V3 layer (hidden 7168, 256 experts top-8, W=8)": dict(H=7168, E=256, k=8, W=8, M=128),
+}
+
+
+def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup):
+    import torch
+    from paper_2605_21100_b200.moe import MoeInstance
+    inst = [MoeInstance(ctx, W, s, H, k, E, M) for s in range(W)]
+    for s in range(W):
+        for t in range(W):
+            inst[s].set_peer_local(t, inst[t])
+        inst[s].commit()
+    g = torch.Generator(device=dev).manual_seed(5)
+    toks = []
+    for s in range(W):
+        x = torch.randn(M, H, generator=g, device=dev).to(torch.bfloat16)
+        logits = torch.randn(M, E, generator=g, device=dev)
+        top = torch.topk(logits, k, dim=-1)
+        toks.append((x, top.indices.to(torch.int32).contiguous(), torch.softmax(top.values, -1).float().contiguous()))
+    per = E // W
+    ranks = [(toks[s][1] // per).cpu().numpy() for s in range(W)]
+    distinct = [np.array([len(set(r.tolist())) for r in rk]) for rk in ranks]
+    remote = sum(int(sum(len(set(r.tolist()) - {s}) for r in ranks[s])) for s in range(W))
+    alg_xfer = 2 * remote * H * 2
+    rows_total = int(sum(d.sum() for d in distinct))
+    stream = torch.cuda.current_stream(dev)
+    from paper_2605_21100_b200 import _capi
+    import ctypes
+    E_ = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # host-known receive counts (the gating decides them); m_count set once, outside the steps
+    R = [int(sum(int((ranks[s2] == d).any(axis=1).sum()) for s2 in range(W))) for d in range(W)]
+    mcnt = [torch.full((1,), M, dtype=torch.int32, device=dev) for _ in range(W)]
+    phases = {"dispatch": [], "receive": [], "combine_put": [], "combine_reduce": []}
+    for it in range(warmup + steps):
+        ev = {p: [(E_(), E_()) for _ in range(W)] for p in phases}
+        # a device sleep gates the step so the events below time device work, not host launch gaps
+        _capi.lib().dcp_device_sleep(ctx.handle, 3000, ctypes.c_void_p(stream.cuda_stream))
+        for s in range(W):
+            ev["dispatch"][s][0].record(stream)
+            inst[s].dispatch(*toks[s], m_count_ptr=mcnt[s].data_ptr())
+            ev["dispatch"][s][1].record(stream)
+        for s in range(W):
+            ev["receive"][s][0].record(stream)
+            inst[s].receive_async()
+            ev["receive"][s][1].record(stream)
+        for s in range(W):  # identity "experts" (untimed)
+            inst[s].y_rows[:R[s]].copy_(inst[s].x_rows[:R[s]])
+        for s in range(W):
+            ev["combine_put"][s][0].record(stream)
+            inst[s].combine_put()
+            ev["combine_put"][s][1].record(stream)
+        for s in range(W):
+            ev["combine_reduce"][s][0].record(stream)
+            inst[s].combine_reduce()
+            ev["combine_reduce"][s][1].record(stream)
+        torch.cuda.synchronize(dev)
+        if it >= warmup:
+            for p in phases:
+                phases[p].append([a.elapsed_time(b) * 1e3 for a, b in ev[p]])
+    # correctness of the identity round trip: out[t] = (#distinct ranks of t) * x[t]
+    for s in range(W):
+        ref = toks[s][0].float() * torch.from_numpy(distinct[s]).to(dev)[:, None].float()
+        assert torch.allclose(inst[s].out[:M], ref, rtol=1e-2, atol=1e-2), f"instance {s} combine mismatch"
+    res = {"workload": name, "instances": W, "tokens_per_instance": M, "hidden": H, "experts": E, "topk": k,
+           "rows_dispatched": rows_total, "cross_instance_bytes_per_step": alg_xfer}
+    moved = {"dispatch": rows_total * H * 2, "receive": 2 * rows_total * H * 2,
+             "combine_put": rows_total * H * 2, "combine_reduce": rows_total * H * 2 + W * M * H * 4}
+    tot_sum = 0.0
+    for p, v in phases.items():
+        a = np.array(v)  # [steps][W] us
+        s_sum = float(np.median(a.sum(axis=1)))
+        tot_sum += s_sum
+        res[p] = {"us_sum_over_instances": s_sum, "us_max_instance": float(np.median(a.max(axis=1))),
+                  "bytes": moved[p], "gbs": moved[p] / (s_sum * 1e-6) / 1e9}
+    res["us_per_instance_step"] = tot_sum / W
+    res["note"] = ("single GPU: cross-instance stores are local HBM stores; expert FFN = identity, untimed; "
+                   "each step gated behind a device sleep so CUDA events time device work only")
+    for i in inst:
+        i.close()
+    return res
+
+
+def run_all(ctx, dev, steps=20, warmup=3):
+    return [run_config(ctx, dev, n, steps=steps, warmup=warmup, **c) for n, c in CONFIGS.items()]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    args = ap.parse_args()
+    import torch
+    from paper_2605_21100_b200.attention import DcpContext
+    dev = torch.device("cuda", 0)
+    ctx = DcpContext(0)
+    for r in run_all(ctx, dev, args.steps, args.warmup):
+        print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -403,6 +403,10 @@ DCP_API int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* top
  * copies the per-source counts to host `counts` and returns the row count. */
 DCP_API int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* counts,
                                 void* stream);
+/* K5a without the host read-back (stream-ordered, graph-capturable): the per-source
+ * counts stay on the device at dcp_moe_recv_counts_dev(x) (int32 [world]). */
+DCP_API int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* stream);
+DCP_API const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x);
 /* K5b: y_rows bf16 [R][hidden] (same row order as receive) back to each token's home. */
 DCP_API int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream);
 /* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */

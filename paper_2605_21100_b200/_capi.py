@@ -191,6 +191,8 @@ _SIGNATURES = [
     ("dcp_moe_meta_width", c_int32, [c_void_p]),
     ("dcp_moe_dispatch", c_int, [c_void_p] + [c_void_p] * 5),
     ("dcp_moe_receive", c_int32, [c_void_p] + [c_void_p] * 4),
+    ("dcp_moe_receive_async", c_int, [c_void_p] + [c_void_p] * 3),
+    ("dcp_moe_recv_counts_dev", c_void_p, [c_void_p]),
     ("dcp_moe_combine_put", c_int, [c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_combine_reduce", c_int, [c_void_p, c_void_p, c_void_p]),
 ]

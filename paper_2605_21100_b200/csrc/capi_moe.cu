@@ -11,7 +11,7 @@ struct dcp_moe {
     dcp_ctx* ctx = nullptr;
     dcp_moe_config cfg{};
     char* pool = nullptr;
-    size_t off_x = 0, off_meta = 0, off_flag = 0, off_cnt = 0, off_cntf = 0, off_cb = 0, off_cbf = 0;
+    size_t off_x = 0, off_meta = 0, off_flag = 0, off_cnt = 0, off_cb = 0, off_cbf = 0;
     char* local = nullptr;
     MoePeers host{};
     MoePeers* dev = nullptr;
@@ -31,7 +31,6 @@ void fill(dcp_moe* x, int peer, char* base) {
     x->host.rx_meta[peer] = reinterpret_cast<int32_t*>(base + x->off_meta);
     x->host.rx_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_flag);
     x->host.rx_count[peer] = reinterpret_cast<int32_t*>(base + x->off_cnt);
-    x->host.rx_count_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_cntf);
     x->host.cb_y[peer] = reinterpret_cast<__nv_bfloat16*>(base + x->off_cb);
     x->host.cb_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_cbf);
 }
@@ -56,11 +55,10 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     size_t o = 0;
     x->off_x = o;    o = al(o + W * m * H * 2);
     x->off_meta = o; o = al(o + W * m * meta * 4);
-    x->off_flag = o; o = al(o + W * m * 4);
+    x->off_flag = o; o = al(o + W * 4);
     x->off_cnt = o;  o = al(o + W * 4);
-    x->off_cntf = o; o = al(o + W * 4);
     x->off_cb = o;   o = al(o + m * W * H * 2);
-    x->off_cbf = o;  o = al(o + m * W * 4);
+    x->off_cbf = o;  o = al(o + W * 4);
     DCP_CUDA_TRY(cudaMalloc(&x->pool, o));
     DCP_CUDA_TRY(cudaMemset(x->pool, 0, o));
     size_t l = 0;
@@ -69,6 +67,8 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     const size_t o_slot = l; l = al(l + m * W * 4);
     const size_t o_src = l;  l = al(l + W * m * 4);
     const size_t o_cnt = l;  l = al(l + W * 4);
+    const size_t o_dd = l;   l = al(l + W * 4);
+    const size_t o_cd = l;   l = al(l + W * 4);
     DCP_CUDA_TRY(cudaMalloc(&x->local, l));
     DCP_CUDA_TRY(cudaMemset(x->local, 0, l));
     x->epoch = reinterpret_cast<uint32_t*>(x->local + o_ep);
@@ -84,6 +84,9 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     x->host.m_max = c->m_max;
     x->host.meta = (int32_t)meta;
     x->host.epoch = x->epoch;
+    x->host.disp_done = reinterpret_cast<int32_t*>(x->local + o_dd);
+    x->host.cb_done = reinterpret_cast<int32_t*>(x->local + o_cd);
+    x->host.chunks = static_cast<int32_t>(m < 32 ? m : 32);
     fill(x, c->self, x->pool);
     *out = x;
     return DCP_OK;
@@ -157,18 +160,36 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
     DCP_REQUIRE(x && m_count, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
-    moe_layout_kernel<<<1, 1024, 0, s>>>(x->dev, idx, m_count, x->slot_tbl);
-    moe_dispatch_kernel<<<x->cfg.m_max, 128, 0, s>>>(x->dev, static_cast<const __nv_bfloat16*>(x_local), idx, w,
-                                                      m_count, x->slot_tbl);
+    moe_dispatch_kernel<<<dim3(x->host.chunks, x->cfg.world), 128, 0, s>>>(
+        x->dev, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, x->slot_tbl);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
 
+int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* stream) {
+    DCP_REQUIRE(x && x_rows && meta_rows, DCP_E_INVALID_ARG, "NULL argument");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int rows = x->cfg.world * x->cfg.m_max;
+    int grid = (rows + 7) / 8;
+    if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
+    moe_receive_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
+                                            x->counts);
+    DCP_CUDA_TRY(cudaGetLastError());
+    x->meta_rows = meta_rows;
+    return DCP_OK;
+}
+
+const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x) { return x ? x->counts : nullptr; }
+
 int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* counts, void* stream) {
     DCP_REQUIRE(x && x_rows && meta_rows, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    moe_receive_kernel<<<1, 1024, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
-                                           x->counts);
+    // one warp per received row, at most W * m_max rows
+    const int rows = x->cfg.world * x->cfg.m_max;
+    int grid = (rows + 7) / 8;
+    if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
+    moe_receive_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
+                                            x->counts);
     DCP_CUDA_TRY(cudaGetLastError());
     x->meta_rows = meta_rows;
     int32_t c[PL_MAXW];
@@ -184,15 +205,16 @@ int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* c
 
 int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream) {
     DCP_REQUIRE(x && y_rows && x->meta_rows, DCP_E_INVALID_ARG, "call dcp_moe_receive first");
-    moe_combine_put_kernel<<<x->cfg.world * x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, static_cast<const __nv_bfloat16*>(y_rows), x->meta_rows, x->row_src, x->counts);
+    moe_combine_put_kernel<<<dim3(x->host.chunks, x->cfg.world), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+        x->dev, static_cast<const __nv_bfloat16*>(y_rows), x->meta_rows, x->counts);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
 
 int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {
     DCP_REQUIRE(x && out && x->m_count_dev, DCP_E_INVALID_ARG, "call dcp_moe_dispatch first");
-    moe_combine_reduce_kernel<<<x->cfg.m_max, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    const int groups = x->cfg.hidden / 4;  // hidden % 8 == 0
+    moe_combine_reduce_kernel<<<dim3(x->cfg.m_max, (groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
         x->dev, x->m_count_dev, x->slot_tbl, out);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;

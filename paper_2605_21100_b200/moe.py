@@ -72,6 +72,12 @@ class MoeInstance:
             _capi.check(R)
         return int(R), counts
 
+    def receive_async(self, stream=None):
+        """K5a without the host count read-back (counts stay on the device)."""
+        _capi.check(_capi.lib().dcp_moe_receive_async(self.h, ctypes.c_void_p(self.x_rows.data_ptr()),
+                                                      ctypes.c_void_p(self.meta_rows.data_ptr()),
+                                                      _s(stream, self.ctx.device)))
+
     def expert_stage(self, R, w_gate, w_up, w_down):
         """Library-GEMM expert FFN over the R received rows (local experts
         w_*[e - first_local_expert])."""
