@@ -444,7 +444,7 @@ int dcp_binding_config(dcp_ctx* ctx, int32_t n, const int64_t* ids, const int32_
     DCP_CUDA_TRY(cudaMemcpy(st.k, k, n * 4, cudaMemcpyHostToDevice));
     DCP_CUDA_TRY(cudaMemcpy(st.moe, moe, n * 4, cudaMemcpyHostToDevice));
     DCP_CUDA_TRY(cudaMemcpy(st.kv, kv, (size_t)n * PL_MAXK * 4, cudaMemcpyHostToDevice));
-    routing_rows_kernel<<<1, 1024>>>(st, ro);
+    DCP_CUDA_TRY(launch_routing_rows(st, ro, nullptr));
     DCP_CUDA_TRY(cudaGetLastError());
     int32_t status = 0;
     DCP_CUDA_TRY(cudaMemcpy(&status, ro.status, 4, cudaMemcpyDeviceToHost));

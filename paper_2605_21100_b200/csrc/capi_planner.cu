@@ -562,7 +562,7 @@ int64_t dcp_planner_dump_page_table(dcp_planner* pl, char* buf, int64_t cap) {
 int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
     DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
     set_stream(pl, stream);
-    routing_rows_kernel<<<1, 1024, 0, pl->stream>>>(pl->st, pl->ro);
+    DCP_CUDA_TRY(launch_routing_rows(pl->st, pl->ro, pl->stream));
     const dim3 wide(pl->st.W, RT_SPLIT);
     routing_count_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
     routing_scan_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);

@@ -142,6 +142,157 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerSta
     if (tid == 0) *ro.status = 0;
 }
 
+// routing_rows_kernel with the sort and the per-active data in shared memory (the common
+// case: max_slots <= ROWS_SMEM_MAX).  The global-memory sort above does ~80 barrier-separated
+// passes over HBM; here each pass is a few hundred cycles, and the W row-building warps scan
+// (kv membership mask, moe) from shared memory instead of chasing st.k / st.kv per request.
+constexpr int ROWS_SMEM_MAX = 8192;
+constexpr size_t rows_smem_bytes(int np2) { return (size_t)np2 * (8 + 4 + 4 + 4); }
+
+static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(PlannerState st, RoutingOut ro, int np2cap) {
+    extern __shared__ __align__(16) uint8_t rsm[];
+    int64_t* key = reinterpret_cast<int64_t*>(rsm);
+    int32_t* val = reinterpret_cast<int32_t*>(key + np2cap);
+    uint32_t* kvm = reinterpret_cast<uint32_t*>(val + np2cap);
+    int32_t* moe = reinterpret_cast<int32_t*>(kvm + np2cap);
+    __shared__ int32_t s_n;
+    __shared__ int32_t s_bad;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int S = st.max_slots, W = st.W;
+    if (tid == 0) {
+        s_n = 0;
+        s_bad = 0;
+    }
+    __syncthreads();
+    for (int sl = tid; sl < S; sl += blockDim.x) {
+        if (st.state[sl] != ST_ACTIVE) continue;
+        const int i = atomicAdd(&s_n, 1);
+        key[i] = st.id[sl];
+        val[i] = sl;
+    }
+    __syncthreads();
+    const int n = s_n;
+    int np2 = 1;
+    while (np2 < n) np2 <<= 1;
+    for (int i = n + tid; i < np2; i += blockDim.x) {
+        key[i] = INT64_MAX;
+        val[i] = -1;
+    }
+    __syncthreads();
+    for (int size = 2; size <= np2; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < np2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                if ((key[lo] > key[hi]) == ((lo & size) == 0)) {
+                    const int64_t tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
+                    const int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
+                }
+            }
+            __syncthreads();
+        }
+    for (int a = tid; a < n; a += blockDim.x) {
+        const int sl = val[a];
+        const int k = st.k[sl], m_r = st.moe[sl];
+        uint32_t mask = 0;
+        bool holds = false;  // InconsistentPlacement check (routing.cpp:19-21)
+        for (int m = 0; m < k; ++m) {
+            const int sp = st.kv[sl * PL_MAXK + m];
+            mask |= 1u << sp;
+            holds |= sp == m_r;
+        }
+        kvm[a] = mask;
+        moe[a] = m_r;
+        if (!holds) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) {
+        if (tid == 0) *ro.status = -4;
+        return;
+    }
+    // Q warps per instance (32 / W, at least 1): warp q of instance s takes actives
+    // [q n / Q, (q+1) n / Q); pass 1 counts its N / M members, pass 2 writes them after the
+    // counts of the lower segments.
+    const int Q = W <= 32 ? (32 / W) : 1;
+    __shared__ int32_t seg_n[32], seg_m[32];
+    const int s = warp / Q, q = warp % Q;
+    const bool active_warp = warp < W * Q;
+    const int a0 = (int)((int64_t)q * n / Q), a1 = (int)((int64_t)(q + 1) * n / Q);
+    if (active_warp) {
+        int cn = 0, cm = 0;
+        for (int c = a0; c < a1; c += 32) {
+            const int a = c + lane;
+            cn += __popc(__ballot_sync(0xffffffffu, a < a1 && ((kvm[a] >> s) & 1u)));
+            cm += __popc(__ballot_sync(0xffffffffu, a < a1 && moe[a] == s));
+        }
+        if (lane == 0) {
+            seg_n[warp] = cn;
+            seg_m[warp] = cm;
+        }
+    }
+    __syncthreads();
+    if (active_warp) {
+        int nrow = 0, mrow = 0;
+        for (int j = 0; j < q; ++j) {
+            nrow += seg_n[s * Q + j];
+            mrow += seg_m[s * Q + j];
+        }
+        for (int c = a0; c < a1; c += 32) {
+            const int a = c + lane;
+            const bool inN = a < a1 && ((kvm[a] >> s) & 1u);
+            const bool inM = a < a1 && moe[a] == s;
+            const unsigned bn = __ballot_sync(0xffffffffu, inN);
+            const unsigned bm = __ballot_sync(0xffffffffu, inM);
+            const unsigned lt = (1u << lane) - 1u;
+            if (inN) {
+                const int sl = val[a];
+                const int row = nrow + __popc(bn & lt);
+                const size_t r = (size_t)s * S + row;
+                ro.n_id[r] = key[a];
+                ro.n_slot[r] = sl;
+                ro.n_moe[r] = moe[a];
+                uint8_t* qr = ro.q_route + r * W;
+                for (int c2 = 0; c2 < W; ++c2) qr[c2] = (c2 == moe[a]) ? 1 : 0;
+                ro.shard_len[r] = st.shard_tokens[(size_t)sl * W + s];
+                ro.slot_nrow[(size_t)sl * W + s] = row;
+            }
+            if (inM) {
+                const int sl = val[a];
+                const int row = mrow + __popc(bm & lt);
+                const size_t r = (size_t)s * S + row;
+                ro.m_id[r] = key[a];
+                ro.m_slot[r] = sl;
+                uint8_t* qr = ro.res_route + r * W;
+                for (int c2 = 0; c2 < W; ++c2) qr[c2] = (kvm[a] >> c2) & 1u;
+                ro.slot_mrow[sl] = row;
+            }
+            nrow += __popc(bn);
+            mrow += __popc(bm);
+        }
+        if (lane == 0 && q == Q - 1) {
+            ro.n_count[s] = nrow;
+            ro.m_count[s] = mrow;
+            bucket_shape_default_d(mrow, nrow, ro.bucket + 2 * s);
+        }
+    }
+    if (tid == 0) *ro.status = 0;
+}
+
+// Host: routing rows for the planner's active set, shared-memory sort when it fits.
+static inline cudaError_t launch_routing_rows(const PlannerState& st, const RoutingOut& ro, cudaStream_t stream) {
+    int np2 = 1;
+    while (np2 < st.max_slots) np2 <<= 1;
+    if (np2 <= ROWS_SMEM_MAX) {
+        const size_t sm = rows_smem_bytes(np2);
+        cudaError_t e = cudaFuncSetAttribute(routing_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+        routing_rows_smem_kernel<<<1, 1024, sm, stream>>>(st, ro, np2);
+    } else {
+        routing_rows_kernel<<<1, 1024, 0, stream>>>(st, ro);
+    }
+    return cudaGetLastError();
+}
+
 // One CTA per instance: block table + fill + cu_pages for its N rows.
 static __global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerState st, RoutingOut ro) {
     __shared__ int64_t part[1024];
@@ -229,6 +380,11 @@ static __global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerS
 // The same output as routing_blocks_kernel, spread over gridDim.y CTAs per
 // instance so a long shard's thousands of pages are not walked by one CTA.
 constexpr int RT_SPLIT = 16;
+// Rows with more than RT_LONG pages (a 512K-token request has 32K) are spread over a whole
+// CTA (256 pages per step, block-wide counts) instead of one warp, so one long request does
+// not serialise the block-table build; short rows keep one warp each.
+constexpr int RT_LONG = 256;
+
 static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState st, RoutingOut ro) {
     const int s = blockIdx.x;
     const int lane = threadIdx.x & 31;
@@ -237,19 +393,42 @@ static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState 
     const int S = st.max_slots, W = st.W;
     const int rows = ro.n_count[s];
     int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
-    for (int row = gw; row < rows; row += nw) {
+    for (int row = gw; row < rows; row += nw) {  // short rows: one warp each
         const int sl = ro.n_slot[(size_t)s * S + row];
-        const int64_t off = st.page_off[sl];
         const int np = st.page_cnt[sl];
+        if (lane == 0) ro.n_mrow[(size_t)s * S + row] = ro.slot_mrow[sl];
+        if (np > RT_LONG) continue;
+        const int64_t off = st.page_off[sl];
         int c = 0;
-        for (int t = lane; t - lane < np; t += 32) {
-            const bool on = t < np && st.pg_inst[off + t] == s;
-            c += __popc(__ballot_sync(0xffffffffu, on));
+        for (int base = 0; base < np; base += 4 * 32) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = base + 32 * u + lane;
+                v[u] = t < np ? st.pg_inst[off + t] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c += __popc(__ballot_sync(0xffffffffu, v[u] == s));
         }
-        if (lane == 0) {
-            cu[row + 1] = c;
-            ro.n_mrow[(size_t)s * S + row] = ro.slot_mrow[sl];
+        if (lane == 0) cu[row + 1] = c;
+    }
+    for (int row = blockIdx.y; row < rows; row += gridDim.y) {  // long rows: one CTA each
+        const int sl = ro.n_slot[(size_t)s * S + row];
+        const int np = st.page_cnt[sl];
+        if (np <= RT_LONG) continue;
+        const int64_t off = st.page_off[sl];
+        int c = 0;
+        for (int base = 0; base < np; base += 4 * 256) {
+            int v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = base + u * 256 + threadIdx.x;
+                v[u] = t < np ? st.pg_inst[off + t] : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c += __syncthreads_count(v[u] == s);
         }
+        if (threadIdx.x == 0) cu[row + 1] = c;
     }
     const int mrows = ro.m_count[s];
     const int gt = blockIdx.y * blockDim.x + threadIdx.x;
@@ -293,29 +472,82 @@ static __global__ void __launch_bounds__(1024) routing_scan_kernel(PlannerState 
 }
 
 static __global__ void __launch_bounds__(256) routing_scatter_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int32_t wsum[32];
     const int s = blockIdx.x;
-    const int lane = threadIdx.x & 31;
-    const int gw = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gw = blockIdx.y * (blockDim.x >> 5) + warp;
     const int nw = gridDim.y * (blockDim.x >> 5);
     const int S = st.max_slots;
     const int rows = ro.n_count[s];
     const int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
     int32_t* bt = ro.block_table + (size_t)s * st.capacity;
     uint8_t* pf = ro.page_fill + (size_t)s * st.capacity;
-    for (int row = gw; row < rows; row += nw) {
+    for (int row = gw; row < rows; row += nw) {  // short rows: one warp each
         const int sl = ro.n_slot[(size_t)s * S + row];
-        const int64_t off = st.page_off[sl];
         const int np = st.page_cnt[sl];
+        if (np > RT_LONG) continue;
+        const int64_t off = st.page_off[sl];
         int pos = cu[row];
-        for (int t = lane; t - lane < np; t += 32) {
-            const bool on = t < np && st.pg_inst[off + t] == s;
-            const unsigned b = __ballot_sync(0xffffffffu, on);
-            if (on) {
-                const int p = pos + __popc(b & ((1u << lane) - 1u));
-                bt[p] = st.pg_frame[off + t];
-                pf[p] = st.pg_fill[off + t];
+        for (int base = 0; base < np; base += 4 * 32) {
+            int v[4], fr[4], fi[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = base + 32 * u + lane;
+                v[u] = t < np ? st.pg_inst[off + t] : -1;
+                fr[u] = t < np ? st.pg_frame[off + t] : 0;
+                fi[u] = t < np ? st.pg_fill[off + t] : 0;
             }
-            pos += __popc(b);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned b = __ballot_sync(0xffffffffu, v[u] == s);
+                if (v[u] == s) {
+                    const int p = pos + __popc(b & ((1u << lane) - 1u));
+                    bt[p] = fr[u];
+                    pf[p] = static_cast<uint8_t>(fi[u]);
+                }
+                pos += __popc(b);
+            }
+        }
+    }
+    for (int row = blockIdx.y; row < rows; row += gridDim.y) {  // long rows: one CTA each
+        const int sl = ro.n_slot[(size_t)s * S + row];
+        const int np = st.page_cnt[sl];
+        if (np <= RT_LONG) continue;
+        const int64_t off = st.page_off[sl];
+        int pos = cu[row];
+        for (int base = 0; base < np; base += 4 * 256) {
+            // 4 sub-chunks of 256 pages in flight per step (page order: sub-chunk, warp, lane)
+            int inst[4], frame[4], fill[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = base + u * 256 + threadIdx.x;
+                inst[u] = t < np ? st.pg_inst[off + t] : -1;
+                frame[u] = t < np ? st.pg_frame[off + t] : 0;
+                fill[u] = t < np ? st.pg_fill[off + t] : 0;
+            }
+            unsigned b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                b[u] = __ballot_sync(0xffffffffu, inst[u] == s);
+                if (lane == 0) wsum[u * 8 + warp] = __popc(b[u]);
+            }
+            __syncthreads();
+            int run = pos;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                int p = run;
+                for (int w = 0; w < 8; ++w) {
+                    if (w < warp) p += wsum[u * 8 + w];
+                    run += wsum[u * 8 + w];
+                }
+                if (inst[u] == s) {
+                    p += __popc(b[u] & ((1u << lane) - 1u));
+                    bt[p] = frame[u];
+                    pf[p] = static_cast<uint8_t>(fill[u]);
+                }
+            }
+            pos = run;
+            __syncthreads();
         }
     }
 }
