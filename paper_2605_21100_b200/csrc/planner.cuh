@@ -140,16 +140,39 @@ struct SmemPlace {
 };
 
 // water_fill (scheduler.cpp:70-102) with one lane per participant (lanes < n).
+// The level -- the minimal integer P with sum_i max(0, P - K_i) >= len, which the reference
+// finds by binary search (cpp:74-86) -- is computed in closed form: with the K_i sorted
+// ascending, the first j whose candidate P_j = ceil((len + K_(0) + .. + K_(j-1)) / j) does not
+// exceed K_(j) (or j = n) is the piece of the convex f(P) where f first reaches len.  Same
+// integer, no ~log2(K + len) warp reductions.
 __device__ __forceinline__ int64_t warp_water_fill(int lane, int n, int64_t len, int64_t K) {
     const bool part = lane < n;
-    int64_t lo = 0;
-    int64_t hi = warp_max_i64(part ? K : 0) + len;
-    while (lo < hi) {
-        const int64_t mid = lo + (hi - lo) / 2;
-        const int64_t cap = warp_sum_i64(part && mid > K ? mid - K : 0);
-        if (cap >= len) hi = mid; else lo = mid + 1;
+    int64_t level;
+    if (n == 1) {
+        level = __shfl_sync(0xffffffffu, K, 0) + len;
+    } else {
+        int64_t ks[16];  // n <= instances_per_node <= 16
+        int m = 0;
+        for (int j = 0; j < n; ++j) {  // every lane: the participants' K, insertion-sorted
+            const int64_t v = __shfl_sync(0xffffffffu, K, j);
+            int i = m++;
+            while (i > 0 && ks[i - 1] > v) {
+                ks[i] = ks[i - 1];
+                --i;
+            }
+            ks[i] = v;
+        }
+        int64_t prefix = 0;
+        level = 0;
+        for (int j = 1; j <= n; ++j) {
+            prefix += ks[j - 1];
+            const int64_t pj = (len + prefix + j - 1) / j;
+            if (j == n || pj <= ks[j]) {
+                level = pj;
+                break;
+            }
+        }
     }
-    const int64_t level = lo;
     int64_t s = part && level - 1 - K > 0 ? level - 1 - K : 0;
     const int64_t rem = len - warp_sum_i64(s);
     const bool elig = part && (K + s < level);
@@ -439,7 +462,7 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
                         const int s = pl.kv[m];
                         si.nfree[s] -= pl.need_off[m + 1] - pl.need_off[m];
                         si.K[s] += pl.split[m];
-                        st.shard_tokens[(int64_t)sl * W + s] += pl.split[m];
+                        st.shard_tokens[(int64_t)sl * W + s] = pl.split[m];  // zeroed above; kv members are distinct
                         if (pl.split[m] > 0) {
                             const int64_t r = pl.split[m] % st.page;
                             trailing = r == 0 ? st.page : r;
