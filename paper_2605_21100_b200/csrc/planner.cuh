@@ -151,7 +151,7 @@ __device__ __forceinline__ int64_t warp_water_fill(int lane, int n, int64_t len,
     if (n == 1) {
         level = __shfl_sync(0xffffffffu, K, 0) + len;
     } else {
-        int64_t ks[16];  // n <= instances_per_node <= 16
+        int64_t ks[32];  // n <= 32 (dcp_water_fill); the planner uses n <= instances_per_node <= 16
         int m = 0;
         for (int j = 0; j < n; ++j) {  // every lane: the participants' K, insertion-sorted
             const int64_t v = __shfl_sync(0xffffffffu, K, j);
