@@ -467,33 +467,62 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 const int a = cta_of_page(r_first, P, grid);
                 const int b = cta_of_page(r_last - 1, P, grid);
                 const float ln2 = 0.69314718055994530942f;
+                // lane j handles parts a + j, a + j + 32, ... for (max, sum); the numerator walks the
+                // parts with 4 partial rows in flight (a shard spread over many CTAs -- a long
+                // request's shard on one instance spans ~20 -- would otherwise be a serial tail).
+                auto slot_of = [&](int k) {
+                    return (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
+                };
                 for (int row = 0; row < G; ++row) {
                     const int qh = h * G + row;
-                    float mmax = -INFINITY;
-                    for (int k = a; k <= b; ++k) {
-                        if (!cta_nonempty(k, P, grid)) continue;
-                        const int sl = (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
-                        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
-                                                 (static_cast<size_t>(sl) * C::HQ + qh));
-                        mmax = fmaxf(mmax, ml.x);
-                    }
+                    float mloc = -INFINITY;
+                    for (int k = a + lane; k <= b; k += 32)
+                        if (cta_nonempty(k, P, grid))
+                            mloc = fmaxf(mloc, __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
+                                                      (static_cast<size_t>(slot_of(k)) * C::HQ + qh)).x);
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+                    const float mmax = mloc;
                     float den = 0.f;
                     float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (int k = a; k <= b; ++k) {
-                        if (!cta_nonempty(k, P, grid)) continue;
-                        const int sl = (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
-                        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
-                                                 (static_cast<size_t>(sl) * C::HQ + qh));
-                        const float w = fast_exp2(ml.x - mmax);
-                        den += w * ml.y;
-                        const float4 v = __ldcg(reinterpret_cast<const float4*>(
-                                                    p.ws_acc + (static_cast<size_t>(sl) * C::HQ + qh) * C::D) +
-                                                lane);
-                        num.x += w * v.x;
-                        num.y += w * v.y;
-                        num.z += w * v.z;
-                        num.w += w * v.w;
+                    for (int base = a; base <= b; base += 32) {
+                        const int k = base + lane;
+                        float w = 0.f;
+                        int sl = -1;
+                        if (k <= b && cta_nonempty(k, P, grid)) {
+                            sl = slot_of(k);
+                            const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
+                                                     (static_cast<size_t>(sl) * C::HQ + qh));
+                            w = fast_exp2(ml.x - mmax);
+                            den += w * ml.y;
+                        }
+                        const int cnt = min(32, b - base + 1);
+                        for (int j = 0; j < cnt; j += 4) {
+                            float4 v[4];
+                            float wj[4];
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                const int jj = min(j + u, 31);
+                                wj[u] = __shfl_sync(0xffffffffu, w, jj);
+                                const int slj = __shfl_sync(0xffffffffu, sl, jj);
+                                v[u] = (j + u < cnt && slj >= 0)
+                                           ? __ldcg(reinterpret_cast<const float4*>(
+                                                        p.ws_acc + (static_cast<size_t>(slj) * C::HQ + qh) * C::D) +
+                                                    lane)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                                if (j + u >= cnt) wj[u] = 0.f;
+                            }
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                num.x += wj[u] * v[u].x;
+                                num.y += wj[u] * v[u].y;
+                                num.z += wj[u] * v[u].z;
+                                num.w += wj[u] * v[u].w;
+                            }
+                        }
                     }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
                     const float inv = 1.f / den;
                     float* o = row_out(p, r, C::HQ, C::D) + qh * C::D;
                     reinterpret_cast<float4*>(o)[lane] =
