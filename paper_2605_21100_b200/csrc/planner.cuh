@@ -327,28 +327,90 @@ static __device__ void cta_bitonic_sort(int64_t* k1, int64_t* k2, int32_t* val, 
 // zeroed): the given slots, or every ACTIVE slot when slots == nullptr.
 // (cp_degree, id) order: CP=1 first (m_r pinned, parallel histogram), then the
 // CP>=2 requests sequentially with a warp argmin over P_r.
+// The CP >= 2 requests (a few percent of the actives) are gathered with their kv membership
+// mask into shared memory, sorted there, and assigned by warp 0 without global round trips;
+// more than RB_SMEM of them fall back to the global-memory sort.
+constexpr int RB_SMEM = 512;
+
 static __device__ void rebalance_core(const PlannerState& st, SmemInst& si, int32_t& s_n2, const int32_t* slots,
                                int n) {
+    __shared__ int64_t rb_id[RB_SMEM];
+    __shared__ int32_t rb_k[RB_SMEM], rb_sl[RB_SMEM];
+    __shared__ uint32_t rb_mask[RB_SMEM];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = st.max_slots;
     const int lim = slots ? n : S;
     for (int j = tid; j < lim; j += blockDim.x) {
         const int sl = slots ? slots[j] : j;
         if (!slots && st.state[sl] != ST_ACTIVE) continue;
-        if (st.k[sl] == 1) {
+        const int kk = st.k[sl];
+        if (kk == 1) {
             const int s = st.kv[sl * PL_MAXK];
             st.moe[sl] = s;
             atomicAdd(&si.B[s], 1);
         } else {
             const int i = atomicAdd(&s_n2, 1);
-            st.sk1[i] = st.k[sl];
+            st.sk1[i] = kk;
             st.sk2[i] = st.id[sl];
             st.sval[i] = sl;
+            if (i < RB_SMEM) {
+                uint32_t mask = 0;
+                for (int m = 0; m < kk; ++m) mask |= 1u << st.kv[sl * PL_MAXK + m];
+                rb_k[i] = kk;
+                rb_id[i] = st.id[sl];
+                rb_sl[i] = sl;
+                rb_mask[i] = mask;
+            }
         }
     }
     __syncthreads();
     const int n2 = s_n2;
-    if (n2 > 1) cta_bitonic_sort(st.sk1, st.sk2, st.sval, n2);
+    if (n2 <= RB_SMEM) {
+        // bitonic sort by (cp_degree, id) in shared memory
+        int np2 = 1;
+        while (np2 < n2) np2 <<= 1;
+        for (int i = n2 + tid; i < np2; i += blockDim.x) {
+            rb_k[i] = 0x7fffffff;
+            rb_id[i] = INT64_MAX;
+        }
+        __syncthreads();
+        for (int size = 2; size <= np2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = tid; i < np2 / 2; i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    const bool gt = rb_k[lo] > rb_k[hi] || (rb_k[lo] == rb_k[hi] && rb_id[lo] > rb_id[hi]);
+                    if (gt == ((lo & size) == 0)) {
+                        const int tk = rb_k[lo]; rb_k[lo] = rb_k[hi]; rb_k[hi] = tk;
+                        const int64_t ti = rb_id[lo]; rb_id[lo] = rb_id[hi]; rb_id[hi] = ti;
+                        const int ts = rb_sl[lo]; rb_sl[lo] = rb_sl[hi]; rb_sl[hi] = ts;
+                        const uint32_t tm = rb_mask[lo]; rb_mask[lo] = rb_mask[hi]; rb_mask[hi] = tm;
+                    }
+                }
+                __syncthreads();
+            }
+        if (warp == 0) {
+            for (int i = 0; i < n2; ++i) {
+                // argmin over P_r of B, ties to the lowest instance id (cpp:54-59); lane = instance
+                const bool mem = lane < st.W && ((rb_mask[i] >> lane) & 1u);
+                int64_t bv = mem ? (int64_t)si.B[lane] : INT64_MAX;
+                int bs = mem ? lane : 0x7fffffff;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                    const int os = __shfl_xor_sync(0xffffffffu, bs, o);
+                    if (ov < bv || (ov == bv && os < bs)) { bv = ov; bs = os; }
+                }
+                if (lane == 0) {
+                    st.moe[rb_sl[i]] = bs;
+                    si.B[bs] += 1;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        return;
+    }
+    cta_bitonic_sort(st.sk1, st.sk2, st.sval, n2);
     __syncthreads();
     if (warp == 0) {
         for (int i = 0; i < n2; ++i) {
