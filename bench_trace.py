@@ -3,7 +3,9 @@
 
 The simengine-equivalent metrics driver of SURVEY §8(f)#3 over real GPU steps
 (SPEC.md:432-460 metrics: per-step latency P50/P99, TPOT, SLO attainment,
-HoL events, CP histogram).  Requests arrive from the reference's gen_trace
+HoL events, CP histogram, attention reduction potential, KV-load and batch
+imbalance, share of active requests at CP > 1; the formulas are in
+paper_2605_21100_b200/metrics.py).  Requests arrive from the reference's gen_trace
 (ShareGPT-4o short mix + GitHub-Issue long mix, workload.cpp:73-106); every
 n_sched iterations the device planner (K6) admits arrivals; every iteration
 each active request decodes one token: append_token (K6), routing (K7), the
@@ -13,6 +15,11 @@ are timed alone; the iteration's attention latency is the max over
 instances, and the simulated clock advances by layers x that latency.
 
     python bench_trace.py [--instances 8] [--rate 8] [--duration 20] [--long-ratio 0.01]
+    python bench_trace.py --sweep-rates 8,16,32,64 --long-ratio 0.05 --slo-ms 20   (P99-TPOT sweep)
+
+TPOT here counts the attention layers only (no expert FFN / MoE time), so an
+SLO passed with --slo-ms is an attention-share budget, not the paper's
+whole-model 50 ms.
 """
 from __future__ import annotations
 
@@ -37,6 +44,7 @@ def gate(ctx, us=3000):
 
 def run(policy, trace, args, ctx, pools):
     import torch
+    from paper_2605_21100_b200 import metrics
     from paper_2605_21100_b200.dcp_step import DcpInstance
     from paper_2605_21100_b200.planner import DevicePlanner
     from paper_2605_21100_b200._capi import device_to_numpy
@@ -59,6 +67,7 @@ def run(policy, trace, args, ctx, pools):
     queued = set()
     active, remaining, start, out_len = [], {}, {}, {}
     step_ms, tpot, cp_of, hol, sched_ms = [], [], {}, 0, []
+    red_attn, kv_imb, b_imb, cp_frac = [], [], [], []
     finished = 0
     while it < args.max_iters:
         if it % args.n_sched == 0:
@@ -94,6 +103,10 @@ def run(policy, trace, args, ctx, pools):
             it += 1
             continue
         pl.append_many(active)
+        ins = pl.instances()
+        kv_imb.append(metrics.imbalance_metrics(ins["kv_load"])[0])
+        b_imb.append(metrics.imbalance_metrics(ins["moe_batch"])[0])
+        cp_frac.append(sum(1 for r in active if cp_of[r] > 1) / len(active))
         pl.build_routing()
         views = [pl.instance_view(s) for s in range(W)]
         for s in range(W):
@@ -116,6 +129,7 @@ def run(policy, trace, args, ctx, pools):
             per[s] += a.elapsed_time(b)
         lat = max(per)
         step_ms.append(lat)
+        red_attn.append(metrics.imbalance_metrics(per)[1])
         t_ms += args.layers * lat
         done = []
         for rid in active:
@@ -139,9 +153,15 @@ def run(policy, trace, args, ctx, pools):
         "step_ms_p50": float(np.percentile(st, 50)), "step_ms_p99": float(np.percentile(st, 99)),
         "step_ms_max": float(st.max()),
         "tpot_ms_mean": float(tp.mean()), "tpot_ms_p99": float(np.percentile(tp, 99)),
-        "slo_attainment": float((tp <= args.slo_ms).mean()),
+        "slo_attainment": metrics.slo_attainment(tpot, args.slo_ms),
         "hol_events": hol, "cp_histogram": {str(k): ks.count(k) for k in sorted(set(ks))},
         "planner_step_ms_mean": float(np.mean(sched_ms)) if sched_ms else None,
+        # SPEC.md:432-439 formulas over the per-iteration per-instance values (AC5, AC6, AC8)
+        "attn_reduction_potential_pct_mean": float(np.mean(red_attn)) if red_attn else 0.0,
+        "kv_load_imbalance_pct_mean": float(np.mean(kv_imb)) if kv_imb else 0.0,
+        "batch_imbalance_pct_mean": float(np.mean(b_imb)) if b_imb else 0.0,
+        "cp_gt1_active_frac_max": float(max(cp_frac)) if cp_frac else 0.0,
+        "cp_gt1_active_frac_mean": float(np.mean(cp_frac)) if cp_frac else 0.0,
         "sim_time_s": t_ms / 1e3,
     }
 
@@ -162,34 +182,56 @@ def main():
     ap.add_argument("--max-iters", type=int, default=4000)
     ap.add_argument("--uniform-degree", type=int, default=8)
     ap.add_argument("--policies", default="dcp,least_batch,least_cache,uniform")
+    ap.add_argument("--sweep-rates", default="",
+                    help="comma-separated ascending rates: P99-TPOT sweep + max sustainable rate (SPEC.md:449-455)")
     args = ap.parse_args()
     import torch
-    from paper_2605_21100_b200 import workload
+    from paper_2605_21100_b200 import metrics, workload
     from paper_2605_21100_b200.attention import DcpContext
-    trace = workload.gen_trace(args.seed, args.long_ratio, args.rate, args.duration, poisson=True,
-                               output_len=(args.out_min, args.out_max))
     ctx = DcpContext(0)
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(1)
     pools = [torch.randn(args.capacity, 2, 8, 16, 128, generator=g, device=dev, dtype=torch.bfloat16)
              for _ in range(args.instances)]
-    longs = sum(1 for r in trace if r[2] >= 100000)
-    print(json.dumps({"trace": {"requests": len(trace), "long": longs, "rate_per_s": args.rate,
-                                "duration_s": args.duration, "long_ratio": args.long_ratio,
-                                "max_len": max(r[2] for r in trace)},
-                      "setup": f"{args.instances} instances (single-GPU emulation), GQA 32q/8kv d128 bf16, "
-                               f"{args.layers} layers/iteration, SLO {args.slo_ms} ms TPOT"}), flush=True)
-    results = []
-    for pol in args.policies.split(","):
-        r = run(pol, trace, args, ctx, pools)
-        results.append(r)
-        print(json.dumps(r), flush=True)
-    dcp = next(r for r in results if r["policy"] == "dcp")
-    base = [r for r in results if r["policy"] != "dcp"]
-    if base:
-        best = min(base, key=lambda r: r["step_ms_p99"])
-        print(json.dumps({"p99_step_dcp_vs_best_baseline": best["step_ms_p99"] / dcp["step_ms_p99"],
-                          "best_baseline": best["policy"]}), flush=True)
+    setup = (f"{args.instances} instances (single-GPU emulation), GQA 32q/8kv d128 bf16, "
+             f"{args.layers} layers/iteration, SLO {args.slo_ms} ms TPOT (attention layers only)")
+    rates = [float(x) for x in args.sweep_rates.split(",") if x] or [args.rate]
+    by_policy = {}
+    for rate in rates:
+        trace = workload.gen_trace(args.seed, args.long_ratio, rate, args.duration, poisson=True,
+                                   output_len=(args.out_min, args.out_max))
+        longs = sum(1 for r in trace if r[2] >= 100000)
+        print(json.dumps({"trace": {"requests": len(trace), "long": longs, "rate_per_s": rate,
+                                    "duration_s": args.duration, "long_ratio": args.long_ratio,
+                                    "max_len": max(r[2] for r in trace)}, "setup": setup}), flush=True)
+        results = []
+        for pol in args.policies.split(","):
+            r = run(pol, trace, args, ctx, pools)
+            r["rate_per_s"] = rate
+            results.append(r)
+            by_policy.setdefault(r["policy"], []).append(r)
+            print(json.dumps(r), flush=True)
+        dcp = next((r for r in results if r["policy"] == "dcp"), None)
+        base = [r for r in results if r["policy"] != "dcp"]
+        if dcp and base:
+            best = min(base, key=lambda r: r["step_ms_p99"])
+            print(json.dumps({"rate_per_s": rate, "p99_step_dcp_vs_best_baseline": best["step_ms_p99"] / dcp["step_ms_p99"],
+                              "best_baseline": best["policy"]}), flush=True)
+    if len(rates) > 1:
+        summary = {"sweep": "P99 TPOT (ms) per rate and max sustainable rate at SLO "
+                            f"{args.slo_ms} ms / 99% (SPEC.md:449-455, monotone truncation)", "rates": rates}
+        for pol, rs in by_policy.items():
+            att = {r["rate_per_s"]: r["slo_attainment"] for r in rs}
+            best, _ = metrics.slo_sweep(att.__getitem__, rates)
+            summary[pol] = {"tpot_ms_p99": [r["tpot_ms_p99"] for r in rs],
+                            "step_ms_p99": [r["step_ms_p99"] for r in rs],
+                            "slo_attainment": [r["slo_attainment"] for r in rs],
+                            "hol_events": [r["hol_events"] for r in rs],
+                            "attn_reduction_potential_pct": [round(r["attn_reduction_potential_pct_mean"], 1) for r in rs],
+                            "kv_load_imbalance_pct": [round(r["kv_load_imbalance_pct_mean"], 1) for r in rs],
+                            "batch_imbalance_pct": [round(r["batch_imbalance_pct_mean"], 1) for r in rs],
+                            "max_sustainable_rate": best}
+        print(json.dumps(summary), flush=True)
 
 
 if __name__ == "__main__":

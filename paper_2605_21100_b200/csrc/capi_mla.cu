@@ -107,7 +107,7 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
     DCP_CUDA_TRY(cudaGetLastError());
     mla::mla_decode_kernel<PAGE><<<2 * pairs, mla::THREADS, mla::SMEM, stream>>>(qmap, kvq, kvp, p);
     DCP_CUDA_TRY(cudaGetLastError());
-    mla::mla_merge_kernel<<<dim3(a->num_shards, mla::H / 16), 512, 0, stream>>>(p, pairs);
+    mla::mla_merge_kernel<<<dim3(a->num_shards, mla::H / 16, mla::MERGE_QUARTERS), 512, 0, stream>>>(p, pairs);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }

@@ -141,7 +141,7 @@ __device__ __forceinline__ bool pair_nonempty(int64_t k, int64_t T, int64_t np) 
     return T >= np || (k * T / np) < ((k + 1) * T / np);
 }
 
-// cu_tiles[r] = sum_{s<r} ceil(pages_s / pages_per_tile); zero-token shards get O = 0, LSE = -inf.
+// cu_tiles[r] = sum_{s<r} ceil(pages_s / pages_per_tile).
 template <int PAGE>
 __global__ void __launch_bounds__(1024) mla_tile_scan_kernel(MlaParams p) {
     constexpr int PPT = TILE / PAGE;
@@ -179,13 +179,6 @@ __global__ void __launch_bounds__(1024) mla_tile_scan_kernel(MlaParams p) {
         __syncthreads();
     }
     if (threadIdx.x == 0) const_cast<int32_t*>(p.cu_tiles)[R] = carry;
-    // zero-token shards
-    for (int r = 0; r < R; ++r) {
-        if (p.cu_pages[r + 1] != p.cu_pages[r]) continue;
-        float4* o = reinterpret_cast<float4*>(p.out + static_cast<size_t>(r) * H * DL);
-        for (int i = threadIdx.x; i < H * DL / 4; i += 1024) o[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (threadIdx.x < H) p.lse[static_cast<size_t>(r) * H + threadIdx.x] = -INFINITY;
-    }
 }
 
 // Segment walk shared by every role: the pair's tile range [t_begin, t_end)
@@ -621,53 +614,107 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
 // Stream-K combine (lse_merge, attn_merge.hpp:86-100, in the log2 domain): every shard cut
 // by a pair-range boundary has one partial per pair that touched it.  One CTA per
-// (shard, 16-head group), one warp per head; uncut shards exit at once.  A separate launch
-// keeps a shard split over many pairs (a 512K request spans ~50) off any one pair's tail.
-__global__ void __launch_bounds__(512) mla_merge_kernel(MlaParams p, int num_pairs) {
+// (shard, 16-head group, column quarter), one warp per head.  A shard cut over at most
+// MERGE_SHORT pairs (the common case: a boundary or two) is merged whole by its quarter-0 CTA,
+// all 512 columns per warp; a longer one (a 512K request spans ~50 pairs) spreads its columns
+// over four CTAs, so 32 SMs share it.  Uncut shards exit at once; zero-token shards write
+// O = 0, LSE = -inf.  A separate launch keeps long shards off any one pair's tail.
+constexpr int MERGE_QUARTERS = 4;
+constexpr int MERGE_SHORT = 8;
+// One warp merges head qh's columns [4*col4, +4*32*NV) over slots a..b.  Slot weights live in
+// lanes (32 slots per chunk, read once) and are broadcast by shuffle, so the main loop only
+// streams the partial rows: U slots x NV float4 per lane in flight.
+template <int NV, int U>
+__device__ __forceinline__ void merge_cols(const MlaParams& p, int a, int b, int r_first, int64_t T, int64_t NP,
+                                          int r, int qh, int col4, float mmax, bool write_lse) {
+    auto slot_of = [&](int k) {
+        return (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
+    };
+    const int lane = threadIdx.x & 31;
+    float den = 0.f;
+    float4 num[NV];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) num[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int c0 = a; c0 <= b; c0 += 32) {
+        const int kl = c0 + lane;
+        float w = 0.f;
+        int sl_l = slot_of(a);
+        if (kl <= b && pair_nonempty(kl, T, NP)) {
+            sl_l = slot_of(kl);
+            const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + (static_cast<size_t>(sl_l) * H + qh));
+            w = fast_exp2(ml.x - mmax);
+            den += w * ml.y;
+        }
+        const int n = min(32, b - c0 + 1);
+        for (int j0 = 0; j0 < n; j0 += U) {
+            float wj[U];
+            float4 x[U][NV];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = (j0 + u) & 31;  // lanes past n hold w = 0 and a valid slot
+                wj[u] = __shfl_sync(0xffffffffu, w, j);
+                if (j0 + u >= 32) wj[u] = 0.f;  // the last round of a full chunk wraps
+                const int sl = __shfl_sync(0xffffffffu, sl_l, j);
+                const float4* src =
+                    reinterpret_cast<const float4*>(p.ws_acc + (static_cast<size_t>(sl) * H + qh) * DL) + col4;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) x[u][v] = __ldcg(src + lane + 32 * v);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    num[v].x += wj[u] * x[u][v].x;
+                    num[v].y += wj[u] * x[u][v].y;
+                    num[v].z += wj[u] * x[u][v].z;
+                    num[v].w += wj[u] * x[u][v].w;
+                }
+        }
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) den += __shfl_xor_sync(0xffffffffu, den, s);
+    const float dinv = 1.f / den;
+    float4* o = reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL) + col4;
+#pragma unroll
+    for (int v = 0; v < NV; ++v)
+        o[lane + 32 * v] = make_float4(num[v].x * dinv, num[v].y * dinv, num[v].z * dinv, num[v].w * dinv);
+    if (write_lse && lane == 0)
+        p.lse[static_cast<size_t>(r) * H + qh] = (mmax + __log2f(den)) * 0.69314718055994530942f;
+}
+
+__global__ void __launch_bounds__(512, 2) mla_merge_kernel(MlaParams p, int num_pairs) {
     const int r = blockIdx.x;
     const int64_t T = p.cu_tiles[p.num_shards];
     const int64_t NP = num_pairs;
     const int r_first = p.cu_tiles[r], r_last = p.cu_tiles[r + 1];
-    if (r_first == r_last) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int qh = blockIdx.y * 16 + warp;
+    constexpr int QV = DL / 4 / MERGE_QUARTERS;  // float4 columns per quarter (32)
+    if (r_first == r_last) {  // zero-token shard: O = 0, LSE = -inf (its merge weight is 0)
+        reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL)[blockIdx.z * QV + lane] =
+            make_float4(0.f, 0.f, 0.f, 0.f);
+        if (blockIdx.z == 0 && lane == 0) p.lse[static_cast<size_t>(r) * H + qh] = -INFINITY;
+        return;
+    }
     const int a = pair_of_tile(r_first, T, NP);
     const int b = pair_of_tile(r_last - 1, T, NP);
     if (a == b) return;  // one pair covered the whole shard and wrote the final output
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int qh = blockIdx.y * 16 + warp;
+    const bool short_span = b - a < MERGE_SHORT;
+    if (short_span && blockIdx.z != 0) return;
     auto slot_of = [&](int k) {
         return (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
     };
     float mmax = -INFINITY;
-    for (int k = a; k <= b; ++k) {
+    for (int k = a + lane; k <= b; k += 32) {
         if (!pair_nonempty(k, T, NP)) continue;
         mmax = fmaxf(mmax, __ldcg(p.ws_ml + (static_cast<size_t>(slot_of(k)) * H + qh) * 2));
     }
-    float den = 0.f;
-    float4 num[4];
 #pragma unroll
-    for (int v = 0; v < 4; ++v) num[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int k = a; k <= b; ++k) {
-        if (!pair_nonempty(k, T, NP)) continue;
-        const int sl = slot_of(k);
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + (static_cast<size_t>(sl) * H + qh));
-        const float wk = fast_exp2(ml.x - mmax);
-        den += wk * ml.y;
-        const float4* src = reinterpret_cast<const float4*>(p.ws_acc + (static_cast<size_t>(sl) * H + qh) * DL);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const float4 x = __ldcg(src + lane + 32 * v);
-            num[v].x += wk * x.x;
-            num[v].y += wk * x.y;
-            num[v].z += wk * x.z;
-            num[v].w += wk * x.w;
-        }
-    }
-    const float dinv = 1.f / den;
-    float4* o = reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL);
-#pragma unroll
-    for (int v = 0; v < 4; ++v)
-        o[lane + 32 * v] = make_float4(num[v].x * dinv, num[v].y * dinv, num[v].z * dinv, num[v].w * dinv);
-    if (lane == 0) p.lse[static_cast<size_t>(r) * H + qh] = (mmax + __log2f(den)) * 0.69314718055994530942f;
+    for (int s = 16; s > 0; s >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, s));
+    if (short_span)
+        merge_cols<MERGE_QUARTERS, 2>(p, a, b, r_first, T, NP, r, qh, 0, mmax, true);
+    else
+        merge_cols<1, 6>(p, a, b, r_first, T, NP, r, qh, blockIdx.z * QV, mmax, blockIdx.z == 0);
 }
 
 }  // namespace mla
