@@ -129,6 +129,9 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     DCP_REQUIRE(c->capacity_pages >= 0 && c->capacity_pages < (1LL << 31), DCP_E_UNSUPPORTED,
                 "capacity_pages out of range");
     DCP_REQUIRE(c->max_requests >= 1, DCP_E_INVALID_ARG, "max_requests < 1");
+    // B_s sums stay below 2^22, which the planner's packed warp argmin relies on (planner.cuh)
+    DCP_REQUIRE(c->max_requests <= (1 << 22) / PL_MAXW, DCP_E_INVALID_ARG, "max_requests %d > %d", c->max_requests,
+                (1 << 22) / PL_MAXW);
     DCP_REQUIRE(c->policy >= 0 && c->policy <= 3, DCP_E_CONFIG, "unknown policy %d", c->policy);
     DCP_REQUIRE(c->n_bucket >= 0 && c->n_bucket <= 16, DCP_E_UNSUPPORTED, "n_bucket > 16");
     DCP_CUDA_TRY(cudaSetDevice(ctx->device));
@@ -226,6 +229,8 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     rc |= dalloc(&st.res_slots, 3 * S, o);
     rc |= dalloc(&st.res_counts, 4, o);
     rc |= dalloc(&st.res_hol, 1, o);
+    rc |= dalloc(&st.recs, S, o);
+    rc |= dalloc(&st.res_pages, 1, o);
     rc |= dalloc(&st.sk1, sort_cap, o);
     rc |= dalloc(&st.sk2, sort_cap, o);
     rc |= dalloc(&st.sval, sort_cap, o);
@@ -328,7 +333,9 @@ int dcp_planner_step(dcp_planner* pl, void* stream) {
     }
     planner_step_kernel<<<1, PL_THREADS, 0, pl->stream>>>(pl->st);
     DCP_CUDA_TRY(cudaGetLastError());
-    pl->last_launches += 1;
+    planner_pages_kernel<<<pl->ctx->num_sms * 2, 256, 0, pl->stream>>>(pl->st);
+    DCP_CUDA_TRY(cudaGetLastError());
+    pl->last_launches += 2;
     pl->routing_valid = false;
     // conservative bound until the result is read back
     pl->arena_top_host += pl->waiting_pages_bound;

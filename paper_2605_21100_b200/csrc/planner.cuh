@@ -76,6 +76,8 @@ struct PlannerState {
     int32_t* res_slots;    // [3][S]: committed, deferred, unschedulable (slot ids)
     int32_t* res_counts;   // [4]: n_committed, n_deferred, n_unsched, status
     int64_t* res_hol;      // [1]
+    struct PageRec* recs;  // [S] frame pops of the step's commits, in commit order
+    int64_t* res_pages;    // [1] pages popped by the step (sum over recs)
     // ---- scratch
     int64_t* sk1;          // [sort_cap]
     int64_t* sk2;
@@ -108,8 +110,23 @@ __device__ __forceinline__ int warp_argmin_i64(int64_t v, int idx) {
     return idx;
 }
 
+// argmin over lanes of small non-negative counts (< 2^22, the B_s batch counts and their node
+// sums; dcp_planner_create bounds max_requests), ties to the lowest lane: one redux.sync on the
+// packed key (value, lane) instead of five shuffle rounds.
+__device__ __forceinline__ int warp_argmin_small(uint32_t v, bool valid, int lane) {
+    const uint32_t key = valid ? (v << 5) | static_cast<uint32_t>(lane) : 0xffffffffu;
+    return static_cast<int>(__reduce_min_sync(0xffffffffu, key) & 31u);
+}
+
+// ceil(tokens / page) (types.hpp:100-102); a power-of-two page (16 by default) takes a shift
+// instead of a 64-bit division, which is a ~100-instruction call on the admission path.
 __device__ __forceinline__ int64_t pages_for_d(int64_t tokens, int64_t page) {
+    if ((page & (page - 1)) == 0) return (tokens + page - 1) >> (__ffsll(page) - 1);
     return (tokens + page - 1) / page;
+}
+__device__ __forceinline__ int64_t page_rem_d(int64_t tokens, int64_t page) {
+    if ((page & (page - 1)) == 0) return tokens & (page - 1);
+    return tokens % page;
 }
 
 __device__ __forceinline__ int bucket_lookup_d(const PlannerState& st, int64_t len) {
@@ -137,6 +154,17 @@ struct SmemPlace {
     int64_t need_off[PL_MAXK + 1];  // page prefix over members
     int32_t ok;                     // can_allocate
     int32_t unsched;
+};
+
+// One commit's frame pops; planner_pages_kernel copies them after the step.
+struct PageRec {
+    int64_t base;                   // pages of the step's earlier commits
+    int64_t off;                    // arena segment start
+    int32_t k;
+    int32_t kv[PL_MAXK];
+    int64_t top[PL_MAXK];           // nfree of each member before the pops
+    int64_t split[PL_MAXK];
+    int64_t need_off[PL_MAXK + 1];
 };
 
 // water_fill (scheduler.cpp:70-102) with one lane per participant (lanes < n).
@@ -188,16 +216,14 @@ static __device__ void place_request(const PlannerState& st, const SmemInst& si,
     const int W = st.W, ipn = st.ipn;
     if (st.kind == KIND_DCP) {
         // node = argmin_n sum_{s in n} B_s, ties by node id (scheduler.cpp:133-141)
-        int64_t bn = INT64_MAX;
-        if (lane < st.nodes) {
-            bn = 0;
+        uint32_t bn = 0;
+        if (lane < st.nodes)
             for (int s = lane * ipn; s < (lane + 1) * ipn; ++s) bn += si.B[s];
-        }
-        const int node = warp_argmin_i64(bn, lane);
+        const int node = st.nodes == 1 ? 0 : warp_argmin_small(bn, lane < st.nodes, lane);
         const int k = cp_degree_d(st, L);
         const int nb = node * ipn;
         // m_r = min_batch_instance over the node, ties to lowest id (cpp:118-126)
-        const int moe = nb + warp_argmin_i64(lane < ipn ? (int64_t)si.B[nb + lane] : INT64_MAX, lane);
+        const int moe = nb + warp_argmin_small(lane < ipn ? si.B[nb + lane] : 0u, lane < ipn, lane);
         // SelectSmallestKV: node minus m_r by (K, id) (cpp:148-156) -> rank per lane
         if (lane < ipn) {
             const int s = nb + lane;
@@ -216,9 +242,13 @@ static __device__ void place_request(const PlannerState& st, const SmemInst& si,
             pl.k = k;
         }
         __syncwarp();
-        const int64_t Kl = lane < k ? si.K[pl.kv[lane]] : 0;
-        const int64_t s = warp_water_fill(lane, k, L, Kl);
-        if (lane < k) pl.split[lane] = s;
+        if (k == 1) {  // water_fill over one participant: the whole request (cpp:70-102)
+            if (lane == 0) pl.split[0] = L;
+        } else {
+            const int64_t Kl = lane < k ? si.K[pl.kv[lane]] : 0;
+            const int64_t s = warp_water_fill(lane, k, L, Kl);
+            if (lane < k) pl.split[lane] = s;
+        }
     } else if (st.kind == KIND_LEAST_BATCH || st.kind == KIND_LEAST_CACHE) {
         // argmin over all instances, first minimum (cpp:172-187)
         int64_t v = INT64_MAX;
@@ -263,12 +293,14 @@ static __device__ void place_request(const PlannerState& st, const SmemInst& si,
         ok = si.nfree[pl.kv[lane]] >= need;
     }
     const bool all_ok = __all_sync(0xffffffffu, ok);
-    // inclusive scan of need over lanes
+    // inclusive scan of need over the k <= 16 member lanes
     int64_t incl = need;
+    if (k > 1) {
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += u;
+        for (int o = 1; o < PL_MAXK; o <<= 1) {
+            const int64_t u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+        }
     }
     if (lane < k) pl.need_off[lane + 1] = incl;
     if (lane == 0) {
@@ -464,6 +496,26 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
     }
     __syncthreads();
 
+#ifdef DCP_PLANNER_PROF
+    long long prof_t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(prof_t0));
+#define PL_PROF(tag)                                                                  \
+    do {                                                                              \
+        long long t_;                                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                        \
+        if (tid == 0) printf("planner_step %s %lld ns\n", tag, t_ - prof_t0);          \
+    } while (0)
+    long long plp[5] = {0, 0, 0, 0, 0}, plp_last = 0;
+#define PLP_MARK(k)                                         \
+    do {                                                    \
+        const long long c_ = clock64();                     \
+        if ((k) > 0) plp[k] += c_ - plp_last;               \
+        plp_last = c_;                                      \
+    } while (0)
+#else
+#define PL_PROF(tag) do {} while (0)
+#define PLP_MARK(k) do {} while (0)
+#endif
     // ---- Alg. 1 line 1: recompute B (scheduler.cpp:250-261) ----
     if (st.kind == KIND_DCP) {
         rebalance_core(st, si, s_n2, nullptr, 0);
@@ -472,61 +524,78 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
             if (st.state[sl] == ST_ACTIVE) atomicAdd(&si.B[st.moe[sl]], 1);
     }
     __syncthreads();
+    PL_PROF("rebalance");
 
     // ---- FIFO admission (scheduler.cpp:263-304) ----
+    // Warp 0 walks the queue alone (warp argmin / water_fill / can_allocate with one lane per
+    // instance, no CTA barrier per request) and records each commit's frame pops; the copy of
+    // the popped frame ids runs afterwards over the whole GPU (planner_pages_kernel).  The pops
+    // can be deferred because admission only moves each stack's top (nfree), never its contents.
+    __shared__ int32_t s_wq, s_i;
     const int nw = *st.nwait;
-    int wq = 0;              // entries kept so far == the reference's `scan`
-    bool head_recorded = false;
-    int i = 0;
-    for (; i < nw; ++i) {
-        const int sl = st.waiting[i];
-        const int64_t L = st.seq_len[sl];
-        if (never_fits_d(st, L)) {  // -> unschedulable, erased
-            if (tid == 0) st.res_slots[2 * S + s_cnt[2]++] = sl;
-            __syncthreads();
-            continue;
-        }
-        if (warp == 0) place_request(st, si, pl, lane, L);
-        __syncthreads();
-        if (pl.ok) {
-            // GlobalPageTable::allocate (page_table.cpp:9-49)
-            const int k = pl.k;
-            const int64_t np = pl.need_off[k];
-            const int64_t cap = np + st.reserve_pages;
-            const int64_t off = s_arena_top;
-            if (L < 1 || off + cap > st.arena_cap) {
-                if (tid == 0) s_status = L < 1 ? PL_E_FRAMES : PL_E_ARENA;
-                __syncthreads();
-                break;
+    if (warp == 0) {
+        int wq = 0;              // entries kept so far == the reference's `scan`
+        bool head_recorded = false;
+        int i = 0;
+        int64_t arena_top = s_arena_top;
+        int64_t pbase = 0;
+        int32_t q_sl = 0;        // lane j holds queue entry i0 + j (prefetched 32 at a time)
+        int64_t q_len = 0;
+        int i0 = -64;
+        for (; i < nw; ++i) {
+            if (i - i0 >= 32) {
+                i0 = i;
+                if (i + lane < nw) {
+                    q_sl = st.waiting[i + lane];
+                    q_len = st.seq_len[q_sl];
+                }
             }
-            for (int64_t t = tid; t < np; t += blockDim.x) {
-                int m = 0;
-                while (pl.need_off[m + 1] <= t) ++m;
-                const int s = pl.kv[m];
-                const int64_t j = t - pl.need_off[m];
-                st.pg_inst[off + t] = s;
-                st.pg_frame[off + t] = st.stack[(int64_t)s * st.capacity + si.nfree[s] - 1 - j];
-                const int64_t rem = pl.split[m] - j * st.page;
-                st.pg_fill[off + t] = (uint8_t)(rem < st.page ? rem : st.page);
+            PLP_MARK(0);
+            const int sl = __shfl_sync(0xffffffffu, q_sl, i - i0);
+            const int64_t L = __shfl_sync(0xffffffffu, q_len, i - i0);
+            PLP_MARK(1);
+            if (never_fits_d(st, L)) {  // -> unschedulable, erased
+                if (lane == 0) st.res_slots[2 * S + s_cnt[2]++] = sl;
+                continue;
             }
-            __syncthreads();
-            if (warp == 0) {
+            PLP_MARK(2);
+            place_request(st, si, pl, lane, L);
+            PLP_MARK(3);
+            if (pl.ok) {
+                // GlobalPageTable::allocate (page_table.cpp:9-49)
+                const int k = pl.k;
+                const int64_t np = pl.need_off[k];
+                const int64_t cap = np + st.reserve_pages;
+                const int64_t off = arena_top;
+                if (L < 1 || off + cap > st.arena_cap) {
+                    if (lane == 0) s_status = L < 1 ? PL_E_FRAMES : PL_E_ARENA;
+                    break;
+                }
+                PageRec& rc = st.recs[s_cnt[0]];
                 if (lane < k) {
                     const int s = pl.kv[lane];
+                    rc.kv[lane] = s;
+                    rc.top[lane] = si.nfree[s];
+                    rc.split[lane] = pl.split[lane];
+                    rc.need_off[lane + 1] = pl.need_off[lane + 1];
                     st.kv[sl * PL_MAXK + lane] = s;
                     st.split[sl * PL_MAXK + lane] = pl.split[lane];
                 }
                 for (int s = lane; s < W; s += 32) st.shard_tokens[(int64_t)sl * W + s] = 0;
                 __syncwarp();
                 if (lane == 0) {
+                    rc.need_off[0] = 0;
+                    rc.k = k;
+                    rc.off = off;
+                    rc.base = pbase;
                     int64_t trailing = 0;
                     for (int m = 0; m < k; ++m) {  // members in order: allocate() mutations
                         const int s = pl.kv[m];
                         si.nfree[s] -= pl.need_off[m + 1] - pl.need_off[m];
                         si.K[s] += pl.split[m];
-                        st.shard_tokens[(int64_t)sl * W + s] = pl.split[m];  // zeroed above; kv members are distinct
+                        st.shard_tokens[(int64_t)sl * W + s] = pl.split[m];  // zeroed above; members distinct
                         if (pl.split[m] > 0) {
-                            const int64_t r = pl.split[m] % st.page;
+                            const int64_t r = page_rem_d(pl.split[m], st.page);
                             trailing = r == 0 ? st.page : r;
                         }
                         si.shards[s] += 1;
@@ -539,48 +608,55 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
                     st.page_cap[sl] = (int32_t)cap;
                     st.trailing_fill[sl] = trailing;
                     si.B[pl.moe] += 1;
-                    s_arena_top = off + cap;
                     st.res_slots[s_cnt[0]++] = sl;
                 }
+                arena_top = off + cap;
+                pbase += np;
+                __syncwarp();
+                PLP_MARK(4);
+                continue;
             }
-            __syncthreads();
-            continue;
-        }
-        // deferred (cpp:296-303)
-        if (warp == 0) {
+            // deferred (cpp:296-303)
             const int64_t tf = warp_sum_i64(lane < W ? si.nfree[lane] : 0);
             if (lane == 0) {
                 st.res_slots[S + s_cnt[1]++] = sl;
                 if (wq == 0 && !head_recorded) {
                     if (tf >= pages_for_d(L, st.page)) s_hol += 1;
                 }
+                st.waiting[wq] = sl;
+            }
+            head_recorded = head_recorded || (wq == 0);
+            ++wq;
+            if (st.hol_strict) {
+                ++i;
+                break;
             }
         }
-        head_recorded = head_recorded || (wq == 0);
-        __syncthreads();
-        if (tid == 0) st.waiting[wq] = sl;
-        __syncthreads();
-        ++wq;
-        if (st.hol_strict) {
-            ++i;
-            break;
-        }
-    }
-    // keep the untouched tail of the queue in order
-    __syncthreads();
-    if (s_status == PL_OK) {
-        for (int j = i; j < nw; ++j) {
-            if (tid == 0) st.waiting[wq] = st.waiting[j];
-            ++wq;
-        }
-    } else {
-        // allocation failure: stop like the reference's exception, keep the rest queued
-        for (int j = i; j < nw; ++j) {
-            if (tid == 0) st.waiting[wq] = st.waiting[j];
-            ++wq;
+        if (lane == 0) {
+            s_arena_top = arena_top;
+            *st.res_pages = pbase;
+            s_wq = wq;
+            s_i = i;
         }
     }
     __syncthreads();
+    PL_PROF("admission");
+#ifdef DCP_PLANNER_PROF
+    if (tid == 0) printf("sections(cycles): prefetch %lld nf %lld place %lld commit %lld\n", plp[1], plp[2], plp[3], plp[4]);
+#endif
+    int wq = s_wq;
+    const int i = s_i;
+    // keep the untouched tail of the queue in order (wq <= i: a downward move, chunk by chunk)
+    for (int c = 0; c < nw - i; c += blockDim.x) {
+        const int j = i + c + tid;
+        const int32_t v = j < nw ? st.waiting[j] : 0;
+        __syncthreads();
+        if (j < nw) st.waiting[wq + c + tid] = v;
+        __syncthreads();
+    }
+    wq += nw - i;
+    __syncthreads();
+    PL_PROF("tail");
     if (tid < W) {
         st.kv_load[tid] = si.K[tid];
         st.nfree[tid] = si.nfree[tid];
@@ -595,6 +671,51 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
         st.res_counts[2] = s_cnt[2];
         st.res_counts[3] = s_status;
         *st.res_hol = s_hol;
+    }
+}
+
+// The frame pops of the step's commits (page_table.cpp:30-45): page g of the step's commit
+// list -> (commit, member, page j of that member) -> the member's stack entry top - 1 - j.
+// Grid-stride over every page the step popped, UP pages per thread per round, loads first.
+static __global__ void __launch_bounds__(256) planner_pages_kernel(PlannerState st) {
+    const int64_t ptot = *st.res_pages;
+    const int nrec = st.res_counts[0];
+    constexpr int UP = 4;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g0 < ptot; g0 += UP * stride) {
+        int32_t fr[UP];
+        int rs[UP], ms[UP];
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            const int64_t g = g0 + u * stride;
+            int r = 0, m = 0;
+            if (g < ptot) {
+                int hi = nrec - 1;  // last commit with base <= g
+                while (r < hi) {
+                    const int mid = (r + hi + 1) >> 1;
+                    if (st.recs[mid].base <= g) r = mid; else hi = mid - 1;
+                }
+                const PageRec& rc = st.recs[r];
+                const int64_t t = g - rc.base;
+                while (rc.need_off[m + 1] <= t) ++m;
+                fr[u] = st.stack[(int64_t)rc.kv[m] * st.capacity + rc.top[m] - 1 - (t - rc.need_off[m])];
+            }
+            rs[u] = r;
+            ms[u] = m;
+        }
+#pragma unroll
+        for (int u = 0; u < UP; ++u) {
+            const int64_t g = g0 + u * stride;
+            if (g >= ptot) break;
+            const PageRec& rc = st.recs[rs[u]];
+            const int m = ms[u];
+            const int64_t t = g - rc.base;
+            const int64_t j = t - rc.need_off[m];
+            st.pg_inst[rc.off + t] = rc.kv[m];
+            st.pg_frame[rc.off + t] = fr[u];
+            const int64_t rem = rc.split[m] - j * st.page;
+            st.pg_fill[rc.off + t] = (uint8_t)(rem < st.page ? rem : st.page);
+        }
     }
 }
 
@@ -968,7 +1089,7 @@ static __global__ void __launch_bounds__(PL_THREADS, 1)
             st.kv[sl * PL_MAXK + m] = s;
             st.split[sl * PL_MAXK + m] = split[m];
             if (split[m] > 0) {
-                const int64_t r = split[m] % st.page;
+                const int64_t r = page_rem_d(split[m], st.page);
                 trailing = r == 0 ? st.page : r;
             }
         }
