@@ -165,9 +165,10 @@ typedef struct dcp_mla_args {
 DCP_API size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards);
 DCP_API int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* args, void* stream);
 DCP_API int dcp_mla_launches_per_call(void);
-/* Diagnostics: record globaltimer stamps of CTA pair 0 into a device buffer of
- * 256 x 8 int64 (per tile: MMA before-QK, after-QK, after-P wait, after-PV;
- * softmax S-ready / P-published for CTA 0 and CTA 1).  NULL switches it off. */
+/* Diagnostics: record globaltimer stamps into a device buffer of 2048 + 3 x 256
+ * int64: [0, 2048) = 256 x 8 for CTA pair 0 (per tile: MMA before-QK, after-QK,
+ * after-P wait, after-PV; softmax S-ready / P-published for CTA 0 and CTA 1),
+ * then per pair (start, end, SM id).  NULL switches it off. */
 DCP_API int dcp_mla_set_trace(void* dev_buf);
 
 

@@ -120,7 +120,7 @@ struct MlaParams {
     int32_t num_frames;
     float scale_log2;
     int32_t dbg;                 // bottleneck experiments (env DCP_MLA_DBG): 1 = no MMAs, 2 = no softmax math
-    long long* trace;            // optional [256][8] globaltimer stamps of pair 0 (dcp_mla_set_trace)
+    long long* trace;            // optional [256][8] globaltimer stamps of pair 0 + [256][3] per pair (dcp_mla_set_trace)
 };
 
 __device__ __forceinline__ long long gtime() {
@@ -245,6 +245,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc::fence_after_sync();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_MISC + TMEM_SLOT);
     const uint32_t lead = tc::mapa(misc, 0);  // leader's misc block (shared::cluster)
+    // trace tail (dcp_mla_set_trace): per pair start, end and SM at [2048 + 3 pair + 0..2]
+    if (p.trace && cta == 0 && threadIdx.x == 0 && pair < 256) {
+        uint32_t smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[2048 + 3 * pair] = gtime();
+        p.trace[2048 + 3 * pair + 2] = smid;
+    }
 
     if (t_begin < t_end) {
         if (warp >= W_TMA) {
@@ -609,6 +616,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
     tc::fence_before_sync();
     tc::cluster_sync();
+    if (p.trace && cta == 0 && threadIdx.x == 0 && pair < 256) p.trace[2048 + 3 * pair + 1] = gtime();
     if (warp == 0) tc::tmem_dealloc<2>(tmem, 512);
 }
 

@@ -27,12 +27,24 @@ att.prepare(q, pool, torch.from_numpy(b.block_table).to(dev), torch.from_numpy(b
             torch.from_numpy(b.shard_len).to(dev))
 for _ in range(3):
     att.launch()
-tr = torch.zeros(256, 8, dtype=torch.int64, device=dev)
+tr = torch.zeros(2048 + 3 * 256, dtype=torch.int64, device=dev)
 _capi.lib().dcp_mla_set_trace(ctypes.c_void_p(tr.data_ptr()))
 att.launch()
 torch.cuda.synchronize()
 _capi.lib().dcp_mla_set_trace(None)
-t = tr.cpu().numpy()
+allt = tr.cpu().numpy()
+t = allt[:2048].reshape(256, 8).copy()
+pt = allt[2048:].reshape(256, 3)
+npair = int((pt[:, 1] > 0).sum())
+pt = pt[:npair]
+st0 = pt[:, 0].min()
+ends = (pt[:, 1] - st0) / 1e3
+starts = (pt[:, 0] - st0) / 1e3
+print(f"pairs {npair}: start us min/max {starts.min():.1f}/{starts.max():.1f}; end us min/median/max "
+      f"{ends.min():.1f}/{np.median(ends):.1f}/{ends.max():.1f}")
+order = np.argsort(ends)
+print("slowest pairs (pair, sm, end us):", [(int(i), int(pt[i, 2]), round(float(ends[i]), 1)) for i in order[-8:]])
+print("fastest pairs (pair, sm, end us):", [(int(i), int(pt[i, 2]), round(float(ends[i]), 1)) for i in order[:8]])
 for row, nm in ((252, "QK-A"), (253, "QK-B"), (254, "PV-0"), (255, "PV-1")):
     print(f"{nm} MMA warp: total ns", t[row, 0], "waiting on full ring ns", t[row, 1], "waits", t[row, 2], "ready", t[row, 3])
 t[252:] = 0
