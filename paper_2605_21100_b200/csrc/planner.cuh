@@ -156,11 +156,12 @@ struct SmemPlace {
     int32_t unsched;
 };
 
-// One commit's frame pops; planner_pages_kernel copies them after the step.
-struct PageRec {
+// One commit: its frame pops and its slot fields.  Warp 0 of the step records it; planner_pages_kernel
+// writes the slot's placement / page-table fields and copies the popped frame ids afterwards.
+struct alignas(16) PageRec {
     int64_t base;                   // pages of the step's earlier commits
     int64_t off;                    // arena segment start
-    int32_t k;
+    int32_t k, sl, moe, cap;        // members, slot, m_r, reserved pages of the segment
     int32_t kv[PL_MAXK];
     int64_t top[PL_MAXK];           // nfree of each member before the pops
     int64_t split[PL_MAXK];
@@ -212,7 +213,7 @@ __device__ __forceinline__ int64_t warp_water_fill(int lane, int n, int64_t len,
 
 // Placement decision for one request (warp 0).  Writes *pl.
 static __device__ void place_request(const PlannerState& st, const SmemInst& si, SmemPlace& pl, int lane,
-                              int64_t L) {
+                              int64_t L, int k_dcp) {
     const int W = st.W, ipn = st.ipn;
     if (st.kind == KIND_DCP) {
         // node = argmin_n sum_{s in n} B_s, ties by node id (scheduler.cpp:133-141)
@@ -220,10 +221,24 @@ static __device__ void place_request(const PlannerState& st, const SmemInst& si,
         if (lane < st.nodes)
             for (int s = lane * ipn; s < (lane + 1) * ipn; ++s) bn += si.B[s];
         const int node = st.nodes == 1 ? 0 : warp_argmin_small(bn, lane < st.nodes, lane);
-        const int k = cp_degree_d(st, L);
+        const int k = k_dcp;
         const int nb = node * ipn;
         // m_r = min_batch_instance over the node, ties to lowest id (cpp:118-126)
         const int moe = nb + warp_argmin_small(lane < ipn ? si.B[nb + lane] : 0u, lane < ipn, lane);
+        if (k == 1) {  // P_r = [m_r], water_fill of one participant = the whole request, can_allocate
+            if (lane == 0) {
+                const int64_t need = pages_for_d(L, st.page);
+                pl.kv[0] = moe;
+                pl.moe = moe;
+                pl.k = 1;
+                pl.split[0] = L;
+                pl.need_off[0] = 0;
+                pl.need_off[1] = need;
+                pl.ok = si.nfree[moe] >= need ? 1 : 0;
+            }
+            __syncwarp();
+            return;
+        }
         // SelectSmallestKV: node minus m_r by (K, id) (cpp:148-156) -> rank per lane
         if (lane < ipn) {
             const int s = nb + lane;
@@ -311,12 +326,12 @@ static __device__ void place_request(const PlannerState& st, const SmemInst& si,
 }
 
 // never_fits (scheduler.cpp:225-243): uses the first instance's capacity.
-__device__ __forceinline__ bool never_fits_d(const PlannerState& st, int64_t L) {
+__device__ __forceinline__ bool never_fits_d(const PlannerState& st, int64_t L, int k_dcp) {
     const int64_t demand = pages_for_d(L, st.page);
     const int64_t per = st.capacity;
     int64_t reach;
     if (st.kind == KIND_DCP) {
-        const int k = cp_degree_d(st, L);
+        const int k = k_dcp;
         reach = per * k - (k - 1);
     } else if (st.kind == KIND_UNIFORM) {
         reach = per * st.udeg - (st.udeg - 1);
@@ -372,26 +387,44 @@ static __device__ void rebalance_core(const PlannerState& st, SmemInst& si, int3
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = st.max_slots;
     const int lim = slots ? n : S;
-    for (int j = tid; j < lim; j += blockDim.x) {
-        const int sl = slots ? slots[j] : j;
-        if (!slots && st.state[sl] != ST_ACTIVE) continue;
-        const int kk = st.k[sl];
-        if (kk == 1) {
-            const int s = st.kv[sl * PL_MAXK];
-            st.moe[sl] = s;
-            atomicAdd(&si.B[s], 1);
-        } else {
-            const int i = atomicAdd(&s_n2, 1);
-            st.sk1[i] = kk;
-            st.sk2[i] = st.id[sl];
-            st.sval[i] = sl;
-            if (i < RB_SMEM) {
-                uint32_t mask = 0;
-                for (int m = 0; m < kk; ++m) mask |= 1u << st.kv[sl * PL_MAXK + m];
-                rb_k[i] = kk;
-                rb_id[i] = st.id[sl];
-                rb_sl[i] = sl;
-                rb_mask[i] = mask;
+    constexpr int RU = 8;  // slots per thread per round: every dependent load level issued together
+    for (int j0 = tid; j0 < lim; j0 += RU * blockDim.x) {
+        int sls[RU], kks[RU], s1[RU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int j = j0 + u * blockDim.x;
+            sls[u] = j < lim ? (slots ? slots[j] : j) : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u)
+            if (sls[u] >= 0 && !slots && st.state[sls[u]] != ST_ACTIVE) sls[u] = -1;
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            kks[u] = sls[u] >= 0 ? st.k[sls[u]] : 0;
+            s1[u] = sls[u] >= 0 ? st.kv[sls[u] * PL_MAXK] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int sl = sls[u];
+            if (sl < 0) continue;
+            const int kk = kks[u];
+            if (kk == 1) {
+                const int s = s1[u];
+                st.moe[sl] = s;
+                atomicAdd(&si.B[s], 1);
+            } else {
+                const int i = atomicAdd(&s_n2, 1);
+                st.sk1[i] = kk;
+                st.sk2[i] = st.id[sl];
+                st.sval[i] = sl;
+                if (i < RB_SMEM) {
+                    uint32_t mask = 0;
+                    for (int m = 0; m < kk; ++m) mask |= 1u << st.kv[sl * PL_MAXK + m];
+                    rb_k[i] = kk;
+                    rb_id[i] = st.id[sl];
+                    rb_sl[i] = sl;
+                    rb_mask[i] = mask;
+                }
             }
         }
     }
@@ -554,12 +587,13 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
             const int sl = __shfl_sync(0xffffffffu, q_sl, i - i0);
             const int64_t L = __shfl_sync(0xffffffffu, q_len, i - i0);
             PLP_MARK(1);
-            if (never_fits_d(st, L)) {  // -> unschedulable, erased
+            const int k_dcp = st.kind == KIND_DCP ? cp_degree_d(st, L) : 1;
+            if (never_fits_d(st, L, k_dcp)) {  // -> unschedulable, erased
                 if (lane == 0) st.res_slots[2 * S + s_cnt[2]++] = sl;
                 continue;
             }
             PLP_MARK(2);
-            place_request(st, si, pl, lane, L);
+            place_request(st, si, pl, lane, L, k_dcp);
             PLP_MARK(3);
             if (pl.ok) {
                 // GlobalPageTable::allocate (page_table.cpp:9-49)
@@ -572,41 +606,20 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
                     break;
                 }
                 PageRec& rc = st.recs[s_cnt[0]];
-                if (lane < k) {
+                if (lane < k) {  // one lane per member (members are distinct instances)
                     const int s = pl.kv[lane];
                     rc.kv[lane] = s;
                     rc.top[lane] = si.nfree[s];
                     rc.split[lane] = pl.split[lane];
                     rc.need_off[lane + 1] = pl.need_off[lane + 1];
-                    st.kv[sl * PL_MAXK + lane] = s;
-                    st.split[sl * PL_MAXK + lane] = pl.split[lane];
+                    si.nfree[s] -= pl.need_off[lane + 1] - pl.need_off[lane];
+                    si.K[s] += pl.split[lane];
+                    si.shards[s] += 1;
                 }
-                for (int s = lane; s < W; s += 32) st.shard_tokens[(int64_t)sl * W + s] = 0;
-                __syncwarp();
                 if (lane == 0) {
                     rc.need_off[0] = 0;
-                    rc.k = k;
-                    rc.off = off;
-                    rc.base = pbase;
-                    int64_t trailing = 0;
-                    for (int m = 0; m < k; ++m) {  // members in order: allocate() mutations
-                        const int s = pl.kv[m];
-                        si.nfree[s] -= pl.need_off[m + 1] - pl.need_off[m];
-                        si.K[s] += pl.split[m];
-                        st.shard_tokens[(int64_t)sl * W + s] = pl.split[m];  // zeroed above; members distinct
-                        if (pl.split[m] > 0) {
-                            const int64_t r = page_rem_d(pl.split[m], st.page);
-                            trailing = r == 0 ? st.page : r;
-                        }
-                        si.shards[s] += 1;
-                    }
-                    st.k[sl] = k;
-                    st.moe[sl] = pl.moe;
-                    st.state[sl] = ST_ACTIVE;
-                    st.page_off[sl] = off;
-                    st.page_cnt[sl] = (int32_t)np;
-                    st.page_cap[sl] = (int32_t)cap;
-                    st.trailing_fill[sl] = trailing;
+                    *reinterpret_cast<longlong2*>(&rc.base) = make_longlong2(pbase, off);
+                    *reinterpret_cast<int4*>(&rc.k) = make_int4(k, sl, pl.moe, (int32_t)cap);
                     si.B[pl.moe] += 1;
                     st.res_slots[s_cnt[0]++] = sl;
                 }
@@ -680,6 +693,33 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
 static __global__ void __launch_bounds__(256) planner_pages_kernel(PlannerState st) {
     const int64_t ptot = *st.res_pages;
     const int nrec = st.res_counts[0];
+    // the commits' slot fields (allocate(), page_table.cpp:9-49; Request::placement / state)
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nrec; c += gridDim.x * blockDim.x) {
+        const PageRec& rc = st.recs[c];
+        const int sl = rc.sl, k = rc.k;
+        int64_t trailing = 0;
+        for (int m = 0; m < k; ++m) {
+            st.kv[sl * PL_MAXK + m] = rc.kv[m];
+            st.split[sl * PL_MAXK + m] = rc.split[m];
+            if (rc.split[m] > 0) {  // the last member with tokens holds the trailing page
+                const int64_t r = page_rem_d(rc.split[m], st.page);
+                trailing = r == 0 ? st.page : r;
+            }
+        }
+        for (int s = 0; s < st.W; ++s) {
+            int64_t v = 0;
+            for (int m = 0; m < k; ++m)
+                if (rc.kv[m] == s) v = rc.split[m];
+            st.shard_tokens[(int64_t)sl * st.W + s] = v;
+        }
+        st.k[sl] = k;
+        st.moe[sl] = rc.moe;
+        st.state[sl] = ST_ACTIVE;
+        st.page_off[sl] = rc.off;
+        st.page_cnt[sl] = (int32_t)rc.need_off[k];
+        st.page_cap[sl] = rc.cap;
+        st.trailing_fill[sl] = trailing;
+    }
     constexpr int UP = 4;
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t g0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g0 < ptot; g0 += UP * stride) {
