@@ -293,97 +293,33 @@ static inline cudaError_t launch_routing_rows(const PlannerState& st, const Rout
     return cudaGetLastError();
 }
 
-// One CTA per instance: block table + fill + cu_pages for its N rows.
-static __global__ void __launch_bounds__(1024, 1) routing_blocks_kernel(PlannerState st, RoutingOut ro) {
-    __shared__ int64_t part[1024];
-    const int s = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int nw = blockDim.x >> 5;
-    const int S = st.max_slots;
-    const int rows = ro.n_count[s];
-    int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
-    // (a) pages of each row on this instance
-    for (int row = warp; row < rows; row += nw) {
-        const int sl = ro.n_slot[(size_t)s * S + row];
-        const int64_t off = st.page_off[sl];
-        const int np = st.page_cnt[sl];
-        int c = 0;
-        for (int t = lane; t - lane < np; t += 32) {
-            const bool on = t < np && st.pg_inst[off + t] == s;
-            c += __popc(__ballot_sync(0xffffffffu, on));
-        }
-        if (lane == 0) cu[row + 1] = c;
-    }
-    __syncthreads();
-    // (b) exclusive scan of counts -> cu_pages
-    const int per = (rows + blockDim.x - 1) / blockDim.x;
-    int64_t sum = 0;
-    for (int j = tid * per; j < min(rows, (tid + 1) * per); ++j) sum += cu[j + 1];
-    part[tid] = sum;
-    __syncthreads();
-    if (tid == 0) {
-        int64_t run = 0;
-        for (int t = 0; t < (int)blockDim.x; ++t) {
-            const int64_t v = part[t];
-            part[t] = run;
-            run += v;
-        }
-        cu[0] = 0;
-    }
-    __syncthreads();
-    int64_t run = part[tid];
-    for (int j = tid * per; j < min(rows, (tid + 1) * per); ++j) {
-        run += cu[j + 1];
-        cu[j + 1] = (int32_t)run;
-    }
-    __syncthreads();
-    // (c0) exchange maps for this instance's N and M rows
-    for (int row = tid; row < rows; row += blockDim.x)
-        ro.n_mrow[(size_t)s * S + row] = ro.slot_mrow[ro.n_slot[(size_t)s * S + row]];
-    const int mrows = ro.m_count[s];
-    const int W = st.W;
-    for (int row = tid; row < mrows; row += blockDim.x) {
-        const int sl = ro.m_slot[(size_t)s * S + row];
-        const int k = st.k[sl];
-        ro.m_k[(size_t)s * S + row] = k;
-        int32_t* dst = ro.m_nrow + ((size_t)s * S + row) * W;
-        for (int c = 0; c < W; ++c) dst[c] = -1;
-        for (int m = 0; m < k; ++m) {
-            const int sp = st.kv[sl * PL_MAXK + m];
-            ro.m_kv[((size_t)s * S + row) * PL_MAXK + m] = sp;
-            dst[sp] = ro.slot_nrow[(size_t)sl * W + sp];
-        }
-    }
-    // (c) scatter frames in logical page order
-    int32_t* bt = ro.block_table + (size_t)s * st.capacity;
-    uint8_t* pf = ro.page_fill + (size_t)s * st.capacity;
-    for (int row = warp; row < rows; row += nw) {
-        const int sl = ro.n_slot[(size_t)s * S + row];
-        const int64_t off = st.page_off[sl];
-        const int np = st.page_cnt[sl];
-        int pos = cu[row];
-        for (int t = lane; t - lane < np; t += 32) {
-            const bool on = t < np && st.pg_inst[off + t] == s;
-            const unsigned b = __ballot_sync(0xffffffffu, on);
-            if (on) {
-                const int p = pos + __popc(b & ((1u << lane) - 1u));
-                bt[p] = st.pg_frame[off + t];
-                pf[p] = st.pg_fill[off + t];
-            }
-            pos += __popc(b);
-        }
-    }
-}
-
-
 // ------------------------------------------------------------------ K7 (wide): count / scan / scatter
-// The same output as routing_blocks_kernel, spread over gridDim.y CTAs per
-// instance so a long shard's thousands of pages are not walked by one CTA.
-constexpr int RT_SPLIT = 16;
-// Rows with more than RT_LONG pages (a 512K-token request has 32K) are spread over a whole
-// CTA (256 pages per step, block-wide counts) instead of one warp, so one long request does
-// not serialise the block-table build; short rows keep one warp each.
+// Block tables per instance, spread over gridDim.y CTAs per instance.  allocate() lays a
+// request's pages out member by member in kv order (page_table.cpp:30-45), so instance s's
+// pages of a row are its own allocation segment -- pages_for(split) of each earlier member
+// in -- followed by whatever append_token grew at the end of the list on s
+// (page_table.cpp:86-121).  Only that appended tail is scanned; the segment is a plain copy.
+constexpr int RT_SPLIT = 48;
+// Segments longer than RT_LONG pages (a 512K-token request has 32K / CP) are copied by a
+// whole CTA; shorter ones and every tail by one warp.
 constexpr int RT_LONG = 256;
+
+// Row (sl, s): s's allocation segment [seg0, seg1) and the start of the appended tail.
+__device__ __forceinline__ void row_segment(const PlannerState& st, int sl, int s, int64_t& seg0, int64_t& seg1,
+                                            int64_t& tail0) {
+    const int k = st.k[sl];
+    int64_t acc = 0;
+    seg0 = seg1 = 0;
+    for (int m = 0; m < k; ++m) {
+        const int64_t need = pages_for_d(st.split[sl * PL_MAXK + m], st.page);
+        if (st.kv[sl * PL_MAXK + m] == s) {
+            seg0 = acc;
+            seg1 = acc + need;
+        }
+        acc += need;
+    }
+    tail0 = acc;
+}
 
 static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState st, RoutingOut ro) {
     const int s = blockIdx.x;
@@ -393,42 +329,17 @@ static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState 
     const int S = st.max_slots, W = st.W;
     const int rows = ro.n_count[s];
     int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
-    for (int row = gw; row < rows; row += nw) {  // short rows: one warp each
+    for (int row = gw; row < rows; row += nw) {  // one warp per row: segment length + tail count
         const int sl = ro.n_slot[(size_t)s * S + row];
-        const int np = st.page_cnt[sl];
         if (lane == 0) ro.n_mrow[(size_t)s * S + row] = ro.slot_mrow[sl];
-        if (np > RT_LONG) continue;
-        const int64_t off = st.page_off[sl];
-        int c = 0;
-        for (int base = 0; base < np; base += 4 * 32) {
-            int v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = base + 32 * u + lane;
-                v[u] = t < np ? st.pg_inst[off + t] : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) c += __popc(__ballot_sync(0xffffffffu, v[u] == s));
-        }
-        if (lane == 0) cu[row + 1] = c;
-    }
-    for (int row = blockIdx.y; row < rows; row += gridDim.y) {  // long rows: one CTA each
-        const int sl = ro.n_slot[(size_t)s * S + row];
+        int64_t seg0, seg1, tail0;
+        row_segment(st, sl, s, seg0, seg1, tail0);
         const int np = st.page_cnt[sl];
-        if (np <= RT_LONG) continue;
         const int64_t off = st.page_off[sl];
         int c = 0;
-        for (int base = 0; base < np; base += 4 * 256) {
-            int v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = base + u * 256 + threadIdx.x;
-                v[u] = t < np ? st.pg_inst[off + t] : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) c += __syncthreads_count(v[u] == s);
-        }
-        if (threadIdx.x == 0) cu[row + 1] = c;
+        for (int64_t t = tail0 + lane; t - lane < np; t += 32)
+            c += __popc(__ballot_sync(0xffffffffu, t < np && st.pg_inst[off + t] == s));
+        if (lane == 0) cu[row + 1] = static_cast<int>(seg1 - seg0) + c;
     }
     const int mrows = ro.m_count[s];
     const int gt = blockIdx.y * blockDim.x + threadIdx.x;
@@ -472,7 +383,6 @@ static __global__ void __launch_bounds__(1024) routing_scan_kernel(PlannerState 
 }
 
 static __global__ void __launch_bounds__(256) routing_scatter_kernel(PlannerState st, RoutingOut ro) {
-    __shared__ int32_t wsum[32];
     const int s = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.y * (blockDim.x >> 5) + warp;
@@ -482,72 +392,69 @@ static __global__ void __launch_bounds__(256) routing_scatter_kernel(PlannerStat
     const int32_t* cu = ro.cu_pages + (size_t)s * (S + 1);
     int32_t* bt = ro.block_table + (size_t)s * st.capacity;
     uint8_t* pf = ro.page_fill + (size_t)s * st.capacity;
-    for (int row = gw; row < rows; row += nw) {  // short rows: one warp each
+    for (int row = gw; row < rows; row += nw) {  // one warp per row: short segment + the tail
         const int sl = ro.n_slot[(size_t)s * S + row];
+        int64_t seg0, seg1, tail0;
+        row_segment(st, sl, s, seg0, seg1, tail0);
         const int np = st.page_cnt[sl];
-        if (np > RT_LONG) continue;
         const int64_t off = st.page_off[sl];
+        const int segn = static_cast<int>(seg1 - seg0);
         int pos = cu[row];
-        for (int base = 0; base < np; base += 4 * 32) {
-            int v[4], fr[4], fi[4];
+        if (segn <= RT_LONG) {
+            for (int j0 = 0; j0 < segn; j0 += 4 * 32) {
+                int fr[4], fi[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = base + 32 * u + lane;
-                v[u] = t < np ? st.pg_inst[off + t] : -1;
-                fr[u] = t < np ? st.pg_frame[off + t] : 0;
-                fi[u] = t < np ? st.pg_fill[off + t] : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const unsigned b = __ballot_sync(0xffffffffu, v[u] == s);
-                if (v[u] == s) {
-                    const int p = pos + __popc(b & ((1u << lane) - 1u));
-                    bt[p] = fr[u];
-                    pf[p] = static_cast<uint8_t>(fi[u]);
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 32 * u + lane;
+                    fr[u] = j < segn ? st.pg_frame[off + seg0 + j] : 0;
+                    fi[u] = j < segn ? st.pg_fill[off + seg0 + j] : 0;
                 }
-                pos += __popc(b);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 32 * u + lane;
+                    if (j < segn) {
+                        bt[pos + j] = fr[u];
+                        pf[pos + j] = static_cast<uint8_t>(fi[u]);
+                    }
+                }
             }
         }
+        pos += segn;
+        for (int64_t t = tail0 + lane; t - lane < np; t += 32) {
+            const bool on = t < np && st.pg_inst[off + t] == s;
+            const unsigned b = __ballot_sync(0xffffffffu, on);
+            if (on) {
+                const int p = pos + __popc(b & ((1u << lane) - 1u));
+                bt[p] = st.pg_frame[off + t];
+                pf[p] = st.pg_fill[off + t];
+            }
+            pos += __popc(b);
+        }
     }
-    for (int row = blockIdx.y; row < rows; row += gridDim.y) {  // long rows: one CTA each
+    for (int row = blockIdx.y; row < rows; row += gridDim.y) {  // long segments: one CTA each, plain copy
         const int sl = ro.n_slot[(size_t)s * S + row];
-        const int np = st.page_cnt[sl];
-        if (np <= RT_LONG) continue;
-        const int64_t off = st.page_off[sl];
-        int pos = cu[row];
-        for (int base = 0; base < np; base += 4 * 256) {
-            // 4 sub-chunks of 256 pages in flight per step (page order: sub-chunk, warp, lane)
-            int inst[4], frame[4], fill[4];
+        int64_t seg0, seg1, tail0;
+        row_segment(st, sl, s, seg0, seg1, tail0);
+        const int segn = static_cast<int>(seg1 - seg0);
+        if (segn <= RT_LONG) continue;
+        const int64_t src = st.page_off[sl] + seg0;
+        const int pos = cu[row];
+        for (int j0 = threadIdx.x; j0 < segn; j0 += 4 * blockDim.x) {
+            int fr[4], fi[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const int t = base + u * 256 + threadIdx.x;
-                inst[u] = t < np ? st.pg_inst[off + t] : -1;
-                frame[u] = t < np ? st.pg_frame[off + t] : 0;
-                fill[u] = t < np ? st.pg_fill[off + t] : 0;
+                const int j = j0 + u * blockDim.x;
+                fr[u] = j < segn ? st.pg_frame[src + j] : 0;
+                fi[u] = j < segn ? st.pg_fill[src + j] : 0;
             }
-            unsigned b[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                b[u] = __ballot_sync(0xffffffffu, inst[u] == s);
-                if (lane == 0) wsum[u * 8 + warp] = __popc(b[u]);
-            }
-            __syncthreads();
-            int run = pos;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                int p = run;
-                for (int w = 0; w < 8; ++w) {
-                    if (w < warp) p += wsum[u * 8 + w];
-                    run += wsum[u * 8 + w];
-                }
-                if (inst[u] == s) {
-                    p += __popc(b[u] & ((1u << lane) - 1u));
-                    bt[p] = frame[u];
-                    pf[p] = static_cast<uint8_t>(fill[u]);
+                const int j = j0 + u * blockDim.x;
+                if (j < segn) {
+                    bt[pos + j] = fr[u];
+                    pf[pos + j] = static_cast<uint8_t>(fi[u]);
                 }
             }
-            pos = run;
-            __syncthreads();
         }
     }
 }
