@@ -199,7 +199,7 @@ def _random_world_script(rng):
         b1 = int(rng.integers(16, 2000))
         bucket = [[b1, 1], [b1 * 3, 2], [b1 * 9, 4], [I64MAX, 8]]
     cap = int(rng.integers(8, 400))
-    page = int(rng.choice([1, 4, 16, 16, 16]))
+    page = int(rng.choice([1, 3, 4, 12, 16, 16, 16]))  # non-powers of two take the division path
     ev = []
     nid = 0
     live = []
