@@ -149,6 +149,78 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerSta
 constexpr int ROWS_SMEM_MAX = 8192;
 constexpr size_t rows_smem_bytes(int np2) { return (size_t)np2 * (8 + 4 + 4 + 4); }
 
+// Bitonic sort of np2 (key, val) pairs in shared memory, ascending by key, with blockDim.x
+// threads each holding E = np2 / blockDim.x consecutive elements in registers: strides below
+// E stay in the thread, strides below 32 E go through warp shuffles, and only the strides of
+// 32 E and more take a shared-memory pass and a CTA barrier (15 of the 78 stages at 4,096).
+template <int E>
+__device__ void bitonic_sort_regs(int64_t* key, int32_t* val, int np2) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int base = tid * E;
+    constexpr int WSPAN = 32 * E;  // contiguous elements of one warp
+    auto reg_phase = [&](int size_lo, int size_hi) {  // sizes [size_lo, size_hi], strides < WSPAN
+        int64_t k[E];
+        int32_t v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            k[j] = key[base + j];
+            v[j] = val[base + j];
+        }
+        for (int size = size_lo; size <= size_hi; size <<= 1) {
+            for (int stride = min(size >> 1, WSPAN >> 1); stride >= E; stride >>= 1) {  // across lanes
+                const int ls = stride / E;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int i = base + j;
+                    const int64_t pk = __shfl_xor_sync(0xffffffffu, k[j], ls);
+                    const int32_t pv = __shfl_xor_sync(0xffffffffu, v[j], ls);
+                    const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
+                    if (keep_min ? (pk < k[j]) : (pk > k[j])) {
+                        k[j] = pk;
+                        v[j] = pv;
+                    }
+                }
+            }
+#pragma unroll
+            for (int st = E / 2; st > 0; st >>= 1) {  // within the thread (compile-time indices)
+                if (st > (size >> 1)) continue;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    if (j & st) continue;
+                    const int jh = j | st;
+                    const bool asc = ((base + j) & size) == 0;
+                    if ((k[j] > k[jh]) == asc) {
+                        const int64_t tk = k[j]; k[j] = k[jh]; k[jh] = tk;
+                        const int32_t tv = v[j]; v[j] = v[jh]; v[jh] = tv;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            key[base + j] = k[j];
+            val[base + j] = v[j];
+        }
+        (void)lane;
+    };
+    reg_phase(2, min(np2, WSPAN));
+    __syncthreads();
+    for (int size = 2 * WSPAN; size <= np2; size <<= 1) {
+        for (int stride = size >> 1; stride >= WSPAN; stride >>= 1) {
+            for (int i = tid; i < np2 / 2; i += blockDim.x) {
+                const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                if ((key[lo] > key[hi]) == ((lo & size) == 0)) {
+                    const int64_t tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
+                    const int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
+                }
+            }
+            __syncthreads();
+        }
+        reg_phase(size, size);
+        __syncthreads();
+    }
+}
+
 static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(PlannerState st, RoutingOut ro, int np2cap) {
     extern __shared__ __align__(16) uint8_t rsm[];
     int64_t* key = reinterpret_cast<int64_t*>(rsm);
@@ -179,17 +251,23 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
         val[i] = -1;
     }
     __syncthreads();
-    for (int size = 2; size <= np2; size <<= 1)
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = tid; i < np2 / 2; i += blockDim.x) {
-                const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-                if ((key[lo] > key[hi]) == ((lo & size) == 0)) {
-                    const int64_t tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
-                    const int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
+    if (np2 == 4 * static_cast<int>(blockDim.x)) {
+        bitonic_sort_regs<4>(key, val, np2);
+    } else if (np2 == 8 * static_cast<int>(blockDim.x)) {
+        bitonic_sort_regs<8>(key, val, np2);
+    } else {
+        for (int size = 2; size <= np2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = tid; i < np2 / 2; i += blockDim.x) {
+                    const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                    if ((key[lo] > key[hi]) == ((lo & size) == 0)) {
+                        const int64_t tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
+                        const int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
+                    }
                 }
+                __syncthreads();
             }
-            __syncthreads();
-        }
+    }
     for (int a = tid; a < n; a += blockDim.x) {
         const int sl = val[a];
         const int k = st.k[sl], m_r = st.moe[sl];

@@ -123,6 +123,27 @@ def test_block_tables_match_page_table(ctx, page):
             assert int(fill[cu[row]:cu[row + 1]].sum()) == int(slen[row])
 
 
+@pytest.mark.parametrize("max_requests", [4096, 8192])
+def test_routing_large_active_sets(ctx, max_requests):
+    """K7's row sort keeps its elements in registers at 4 and 8 slots per thread (the
+    shared-memory kernel at max_requests 4096 / 8192): routing and page-table CSVs equal
+    the oracle's for a few thousand actives with shuffled ids."""
+    from paper_2605_21100_b200.planner import DevicePlanner
+    rng = np.random.default_rng(max_requests)
+    n = max_requests - max_requests // 5
+    bucket = [[3000, 1], [12000, 2], [2**63 - 1, 4]]
+    w = DevicePlanner(ctx, 1, 8, 16, 1 << 17, "dcp", bucket, max_requests=max_requests)
+    o = World(oracle_lib.port(), "dcpora_", 1, 8, 16, 1 << 17, "dcp", bucket)
+    ids = rng.permutation(10 * n)[:n].tolist()
+    lens = rng.integers(1, 20000, size=n).tolist()
+    for i, L in zip(ids, lens):
+        w.enqueue(i, L)
+        o.enqueue(i, L)
+    assert w.step() == o.step()
+    assert w.routing_csv() == o.routing_csv()
+    assert w.page_table_csv() == o.page_table_csv()
+
+
 def _d2h(ptr, n, dtype):
     from paper_2605_21100_b200._capi import device_to_numpy
     return device_to_numpy(ptr, n, dtype)
