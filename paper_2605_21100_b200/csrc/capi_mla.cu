@@ -96,6 +96,11 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
     p.ws_ml = reinterpret_cast<float*>(ws);
     ws += slots * mla::H * 2 * sizeof(float);
     p.cu_tiles = reinterpret_cast<int32_t*>(ws);
+    ws += (static_cast<size_t>(a->num_shards) + 1) * sizeof(int32_t);
+    p.pair_t0 = reinterpret_cast<int32_t*>(ws);
+    p.num_pairs = pairs;
+    static const int seg_tiles = [] { const char* e = std::getenv("DCP_MLA_SEG_TILES"); return e ? std::atoi(e) : 4; }();
+    p.seg_tiles = seg_tiles;
     p.num_shards = a->num_shards;
     p.num_frames = static_cast<int32_t>(a->num_frames);
     p.scale_log2 = a->scale * 1.4426950408889634f;
@@ -124,6 +129,7 @@ size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards) {
     size_t b = slots * mla::H * mla::DL * sizeof(float);          // ws_acc
     b += slots * mla::H * 2 * sizeof(float);                      // ws_ml
     b += (static_cast<size_t>(num_shards) + 1) * sizeof(int32_t); // cu_tiles
+    b += (slots / 2 + 1) * sizeof(int32_t);                       // pair_t0
     return (b + 255) & ~size_t(255);
 }
 

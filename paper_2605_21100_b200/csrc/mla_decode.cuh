@@ -112,6 +112,9 @@ struct MlaParams {
     const int64_t* shard_len;    // [R]
     const uint8_t* page_fill;    // [P] or nullptr
     const int32_t* cu_tiles;     // [R+1] (workspace, from mla_tile_scan_kernel)
+    int32_t* pair_t0;            // [pairs+1] first tile of each pair (workspace, from mla_tile_scan_kernel)
+    int32_t num_pairs;
+    int32_t seg_tiles;           // stream-K weight of a shard start, in tiles (pipeline drain + Q load + O epilogue)
     float* out;                  // [R][128][512]
     float* lse;                  // [R][128]
     float* ws_acc;               // [2*pairs][128][512]
@@ -134,12 +137,20 @@ __device__ __forceinline__ long long gtime() {
         if (p.trace && pair == 0 && (g) < 256) p.trace[(g) * 8 + (k)] = gtime();            \
     } while (0)
 
-__device__ __forceinline__ int pair_of_tile(int64_t t, int64_t T, int64_t np) {
-    return static_cast<int>(((t + 1) * np + T - 1) / T - 1);
+// Weighted stream-K: pair k streams tiles [pair_t0[k], pair_t0[k+1]).  The split is even in
+// work = tiles + seg_tiles per shard, because every shard a pair starts costs it a pipeline
+// drain, a Q load and an O epilogue (at equal tile counts, pairs with 2-3 segments were the
+// slowest: profiles/r1_k10_trace_pairs.txt).  seg_tiles = 4 (env DCP_MLA_SEG_TILES) measured
+// best: long mix 0.327 -> 0.309 ms, cfg2-shaped unchanged (its spread is mostly SM speed).
+__device__ __forceinline__ int pair_of_tile(const int32_t* pair_t0, int np, int t) {
+    int lo = 0, hi = np - 1;  // last pair k with pair_t0[k] <= t (the non-empty one holding t)
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (pair_t0[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
 }
-__device__ __forceinline__ bool pair_nonempty(int64_t k, int64_t T, int64_t np) {
-    return T >= np || (k * T / np) < ((k + 1) * T / np);
-}
+__device__ __forceinline__ bool pair_nonempty(const int32_t* pair_t0, int k) { return pair_t0[k] < pair_t0[k + 1]; }
 
 // cu_tiles[r] = sum_{s<r} ceil(pages_s / pages_per_tile).
 template <int PAGE>
@@ -179,6 +190,27 @@ __global__ void __launch_bounds__(1024) mla_tile_scan_kernel(MlaParams p) {
         __syncthreads();
     }
     if (threadIdx.x == 0) const_cast<int32_t*>(p.cu_tiles)[R] = carry;
+    __syncthreads();
+    // pair_t0[k]: the tile at work unit floor(k W / NP), W = T + seg_tiles R, shard r spanning
+    // work [cu_tiles[r] + seg_tiles r, +seg_tiles + tiles_r) with its start cost first
+    const int64_t T = carry, X = p.seg_tiles, NP = p.num_pairs;
+    const int64_t Wt = T + X * R;
+    for (int k = threadIdx.x; k <= NP; k += blockDim.x) {
+        const int64_t U = k * Wt / NP;
+        int t;
+        if (k == NP) {
+            t = static_cast<int>(T);
+        } else {
+            int lo = 0, hi = R;  // last r with cu_work[r] <= U
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.cu_tiles[mid] + X * mid <= U) lo = mid; else hi = mid - 1;
+            }
+            const int64_t off = U - (p.cu_tiles[lo] + X * lo);
+            t = lo >= R ? static_cast<int>(T) : p.cu_tiles[lo] + static_cast<int>(off > X ? off - X : 0);
+        }
+        p.pair_t0[k] = t;
+    }
 }
 
 // Segment walk shared by every role: the pair's tile range [t_begin, t_end)
@@ -212,10 +244,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int lane = threadIdx.x & 31;
     const int R = p.num_shards;
     const int64_t T = p.cu_tiles[R];
-    const int64_t NP = gridDim.x >> 1;
     const int pair = blockIdx.x >> 1;
-    const int t_begin = static_cast<int>(pair * T / NP);
-    const int t_end = static_cast<int>((pair + 1) * T / NP);
+    const int t_begin = p.pair_t0[pair];
+    const int t_end = p.pair_t0[pair + 1];
+    (void)T;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGES; ++s) {
@@ -633,11 +665,9 @@ constexpr int MERGE_SHORT = 8;
 // lanes (32 slots per chunk, read once) and are broadcast by shuffle, so the main loop only
 // streams the partial rows: U slots x NV float4 per lane in flight.
 template <int NV, int U>
-__device__ __forceinline__ void merge_cols(const MlaParams& p, int a, int b, int r_first, int64_t T, int64_t NP,
-                                          int r, int qh, int col4, float mmax, bool write_lse) {
-    auto slot_of = [&](int k) {
-        return (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
-    };
+__device__ __forceinline__ void merge_cols(const MlaParams& p, int a, int b, int r_first, int r, int qh, int col4,
+                                          float mmax, bool write_lse) {
+    auto slot_of = [&](int k) { return (k == a && r_first != p.pair_t0[k]) ? 2 * k + 1 : 2 * k; };
     const int lane = threadIdx.x & 31;
     float den = 0.f;
     float4 num[NV];
@@ -647,7 +677,7 @@ __device__ __forceinline__ void merge_cols(const MlaParams& p, int a, int b, int
         const int kl = c0 + lane;
         float w = 0.f;
         int sl_l = slot_of(a);
-        if (kl <= b && pair_nonempty(kl, T, NP)) {
+        if (kl <= b && pair_nonempty(p.pair_t0, kl)) {
             sl_l = slot_of(kl);
             const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) + (static_cast<size_t>(sl_l) * H + qh));
             w = fast_exp2(ml.x - mmax);
@@ -692,8 +722,6 @@ __device__ __forceinline__ void merge_cols(const MlaParams& p, int a, int b, int
 
 __global__ void __launch_bounds__(512, 2) mla_merge_kernel(MlaParams p, int num_pairs) {
     const int r = blockIdx.x;
-    const int64_t T = p.cu_tiles[p.num_shards];
-    const int64_t NP = num_pairs;
     const int r_first = p.cu_tiles[r], r_last = p.cu_tiles[r + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qh = blockIdx.y * 16 + warp;
@@ -704,25 +732,23 @@ __global__ void __launch_bounds__(512, 2) mla_merge_kernel(MlaParams p, int num_
         if (blockIdx.z == 0 && lane == 0) p.lse[static_cast<size_t>(r) * H + qh] = -INFINITY;
         return;
     }
-    const int a = pair_of_tile(r_first, T, NP);
-    const int b = pair_of_tile(r_last - 1, T, NP);
+    const int a = pair_of_tile(p.pair_t0, num_pairs, r_first);
+    const int b = pair_of_tile(p.pair_t0, num_pairs, r_last - 1);
     if (a == b) return;  // one pair covered the whole shard and wrote the final output
     const bool short_span = b - a < MERGE_SHORT;
     if (short_span && blockIdx.z != 0) return;
-    auto slot_of = [&](int k) {
-        return (k == a && r_first != static_cast<int>(k * T / NP)) ? 2 * k + 1 : 2 * k;
-    };
+    auto slot_of = [&](int k) { return (k == a && r_first != p.pair_t0[k]) ? 2 * k + 1 : 2 * k; };
     float mmax = -INFINITY;
     for (int k = a + lane; k <= b; k += 32) {
-        if (!pair_nonempty(k, T, NP)) continue;
+        if (!pair_nonempty(p.pair_t0, k)) continue;
         mmax = fmaxf(mmax, __ldcg(p.ws_ml + (static_cast<size_t>(slot_of(k)) * H + qh) * 2));
     }
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, s));
     if (short_span)
-        merge_cols<MERGE_QUARTERS, 2>(p, a, b, r_first, T, NP, r, qh, 0, mmax, true);
+        merge_cols<MERGE_QUARTERS, 2>(p, a, b, r_first, r, qh, 0, mmax, true);
     else
-        merge_cols<1, 6>(p, a, b, r_first, T, NP, r, qh, blockIdx.z * QV, mmax, blockIdx.z == 0);
+        merge_cols<1, 6>(p, a, b, r_first, r, qh, blockIdx.z * QV, mmax, blockIdx.z == 0);
 }
 
 }  // namespace mla
