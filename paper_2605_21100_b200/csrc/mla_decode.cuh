@@ -57,7 +57,8 @@ constexpr int P_BYTES = 2 * 8192;    // 64 heads x 128 tokens bf16 per CTA
 // warps overlap (tools/probe/mma_rate.cu).  S = Q K^T is split over K into two accumulators
 // (boxes 0-4 -> S_A, 5-8 -> S_B; the softmax adds them), O += P V over the two latent halves.
 enum Ring { RQA = 0, RQB = 1, RV0 = 2, RV1 = 3, NRING = 4 };
-constexpr int QA_BOXES = 5;          // K boxes [0, 5) -> S_A, [5, 9) -> S_B
+constexpr int QA_BOXES = 5;          // K boxes [0, 5) -> S_A, [5, 9) -> S_B ...
+constexpr int QB_SHARE = 2;          // ... except box 4's last 2 k-steps, issued by the S_B chain: 18 + 18 MMAs
 #ifndef MLA_RS_QA
 #define MLA_RS_QA 5
 #define MLA_RS_QB 4
@@ -68,6 +69,8 @@ __host__ __device__ constexpr int ring_stages(int k) {
     return k == RQA ? MLA_RS_QA : k == RQB ? MLA_RS_QB : k == RV0 ? MLA_RS_V0 : MLA_RS_V1;
 }
 __host__ __device__ constexpr int ring_first(int k) { return k == 0 ? 0 : ring_first(k - 1) + ring_stages(k - 1); }
+// The S_B chain reads box 4 from the QA ring's stage 4, which therefore always holds box 4.
+static_assert(MLA_RS_QA == QA_BOXES, "the QA ring has one stage per QA box");
 constexpr int NSTAGES = ring_first(NRING);  // 15 stages of 8 KB
 constexpr int OFF_Q = 0;
 constexpr int OFF_P = OFF_Q + Q_BYTES;
@@ -252,7 +255,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGES; ++s) {
             mbar_init(misc + BAR_FULL + 8 * s, 1);
-            mbar_init(misc + BAR_EMPTY + 8 * s, 1);
+            // QA stage 4 (box 4) is released by both QK chains
+            mbar_init(misc + BAR_EMPTY + 8 * s, s == ring_first(RQA) + QA_BOXES - 1 ? 2 : 1);
         }
         mbar_init(misc + BAR_QFULL, 1);
         mbar_init(misc + BAR_QEMPTY, 2);
@@ -406,6 +410,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 // base descriptors; the 14-bit start-address field never carries (smem < 256 KB)
                 const uint64_t dQ = tc::sdesc_sw128(sbase + OFF_Q, 16, 1024);
                 const uint64_t dR = tc::sdesc_sw128(sbase + OFF_RING + s0 * STAGE, 16, 1024);
+                const uint64_t dRA = tc::sdesc_sw128(sbase + OFF_RING + ring_first(RQA) * STAGE, 16, 1024);
                 const uint64_t dRV = tc::sdesc_sw128(sbase + OFF_RING + s0 * STAGE, 4096, 1024);
                 const uint64_t dP = tc::sdesc_sw128(sbase + OFF_P, 16, 1024);
                 const bool is_qk = rk == RQA || rk == RQB;
@@ -426,13 +431,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             tc::fence_after_sync();
                             const int b_lo = rk == RQA ? 0 : QA_BOXES, b_hi = rk == RQA ? QA_BOXES : NKB;
                             const uint32_t dst = tmem + (rk == RQA ? TM_SA : TM_SB) + 64 * sb;
+                            constexpr int SB4 = QA_BOXES - 1;  // the shared box / QA stage
+                            if (rk == RQB) {  // S_B starts with box 4's last QB_SHARE k-steps
+                                if (lane == 0) mbar_wait(misc + BAR_FULL + 8 * (ring_first(RQA) + SB4), g & 1);
+                                __syncwarp();
+                                tc::fence_after_sync();
+                                const uint64_t a0 = dQ + ((SB4 * 8192) >> 4), b0 = dRA + ((SB4 * STAGE) >> 4);
+#pragma unroll
+                                for (int kk = 4 - QB_SHARE; kk < 4; ++kk)
+                                    if (!(p.dbg & 1))
+                                        tc::mma2_bf16_ss_warp(dst, a0 + 2 * kk, b0 + 2 * kk, ID_QK, kk != 4 - QB_SHARE);
+                                tc::commit2_mc_warp(misc + BAR_EMPTY + 8 * (ring_first(RQA) + SB4), 0x3);
+                            }
                             for (int b = b_lo; b < b_hi; ++b) {
                                 const uint32_t s = wait_full();
                                 const uint64_t a0 = dQ + ((b * 8192) >> 4), b0 = dR + ((s * STAGE) >> 4);
+                                const int kk_hi = b == SB4 ? 4 - QB_SHARE : 4;
 #pragma unroll
                                 for (int kk = 0; kk < 4; ++kk)
-                                    if (!(p.dbg & 1))
-                                        tc::mma2_bf16_ss_warp(dst, a0 + 2 * kk, b0 + 2 * kk, ID_QK, ((b - b_lo) | kk) != 0);
+                                    if (kk < kk_hi && !(p.dbg & 1))
+                                        tc::mma2_bf16_ss_warp(dst, a0 + 2 * kk, b0 + 2 * kk, ID_QK,
+                                                              rk == RQB || ((b - b_lo) | kk) != 0);
                                 tc::commit2_mc_warp(misc + BAR_EMPTY + 8 * (s0 + s), 0x3);
                             }
                             tc::commit2_mc_warp(misc + BAR_SFULL + 16 * sb + 8 * rk, 0x3);

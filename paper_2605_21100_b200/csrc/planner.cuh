@@ -616,6 +616,7 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
                     si.K[s] += pl.split[lane];
                     si.shards[s] += 1;
                 }
+                __syncwarp();  // every lane has read s_cnt[0] / pl before lane 0 advances them
                 if (lane == 0) {
                     rc.need_off[0] = 0;
                     *reinterpret_cast<longlong2*>(&rc.base) = make_longlong2(pbase, off);
@@ -645,6 +646,7 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
                 break;
             }
         }
+        __syncwarp();  // the lanes' initial read of s_arena_top precedes lane 0's write
         if (lane == 0) {
             s_arena_top = arena_top;
             *st.res_pages = pbase;
