@@ -222,6 +222,18 @@ __device__ void bitonic_sort_regs(int64_t* key, int32_t* val, int np2) {
 }
 
 static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(PlannerState st, RoutingOut ro, int np2cap) {
+#ifdef DCP_PLANNER_PROF
+    long long rt_ts[6];
+    int rt_n = 0;
+#define RT_STAMP()                                                   \
+    do {                                                             \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(rt_ts[rt_n])); \
+        ++rt_n;                                                      \
+    } while (0)
+    RT_STAMP();
+#else
+#define RT_STAMP() do {} while (0)
+#endif
     extern __shared__ __align__(16) uint8_t rsm[];
     int64_t* key = reinterpret_cast<int64_t*>(rsm);
     int32_t* val = reinterpret_cast<int32_t*>(key + np2cap);
@@ -243,6 +255,7 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
         val[i] = sl;
     }
     __syncthreads();
+    RT_STAMP();
     const int n = s_n;
     int np2 = 1;
     while (np2 < n) np2 <<= 1;
@@ -268,6 +281,7 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
                 __syncthreads();
             }
     }
+    RT_STAMP();
     for (int a = tid; a < n; a += blockDim.x) {
         const int sl = val[a];
         const int k = st.k[sl], m_r = st.moe[sl];
@@ -287,6 +301,7 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
         if (tid == 0) *ro.status = -4;
         return;
     }
+    RT_STAMP();
     // Q warps per instance (32 / W, at least 1): warp q of instance s takes actives
     // [q n / Q, (q+1) n / Q); pass 1 counts its N / M members, pass 2 writes them after the
     // counts of the lower segments.
@@ -308,6 +323,7 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
         }
     }
     __syncthreads();
+    RT_STAMP();
     if (active_warp) {
         int nrow = 0, mrow = 0;
         for (int j = 0; j < q; ++j) {
@@ -352,6 +368,14 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
             bucket_shape_default_d(mrow, nrow, ro.bucket + 2 * s);
         }
     }
+#ifdef DCP_PLANNER_PROF
+    __syncthreads();
+    RT_STAMP();
+    if (tid == 0)
+        printf("routing_rows us: collect %.1f sort %.1f kvm %.1f count %.1f write %.1f\n", (rt_ts[1] - rt_ts[0]) / 1e3,
+               (rt_ts[2] - rt_ts[1]) / 1e3, (rt_ts[3] - rt_ts[2]) / 1e3, (rt_ts[4] - rt_ts[3]) / 1e3,
+               (rt_ts[5] - rt_ts[4]) / 1e3);
+#endif
     if (tid == 0) *ro.status = 0;
 }
 
