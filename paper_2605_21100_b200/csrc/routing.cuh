@@ -149,6 +149,20 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerSta
 constexpr int ROWS_SMEM_MAX = 8192;
 constexpr size_t rows_smem_bytes(int np2) { return (size_t)np2 * (8 + 4 + 4 + 4); }
 
+// One uint8 route row (RouteTable, routing.hpp:27-40): byte c = bit c of `mask`.  Rows are
+// W bytes at r * W, so for W % 4 == 0 they go out as 32-bit words (4 bytes per store).
+__device__ __forceinline__ void store_route_row(uint8_t* row, int W, uint32_t mask) {
+    if ((W & 3) == 0) {
+        for (int c = 0; c < W; c += 4) {
+            const uint32_t b = mask >> c;
+            reinterpret_cast<uint32_t*>(row)[c >> 2] =
+                (b & 1u) | ((b >> 1) & 1u) << 8 | ((b >> 2) & 1u) << 16 | ((b >> 3) & 1u) << 24;
+        }
+    } else {
+        for (int c = 0; c < W; ++c) row[c] = (mask >> c) & 1u;
+    }
+}
+
 // Bitonic sort of np2 (key, val) pairs in shared memory, ascending by key, with blockDim.x
 // threads each holding E = np2 / blockDim.x consecutive elements in registers: strides below
 // E stay in the thread, strides below 32 E go through warp shuffles, and only the strides of
@@ -330,37 +344,46 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
             nrow += seg_n[s * Q + j];
             mrow += seg_m[s * Q + j];
         }
-        for (int c = a0; c < a1; c += 32) {
-            const int a = c + lane;
-            const bool inN = a < a1 && ((kvm[a] >> s) & 1u);
-            const bool inM = a < a1 && moe[a] == s;
-            const unsigned bn = __ballot_sync(0xffffffffu, inN);
-            const unsigned bm = __ballot_sync(0xffffffffu, inM);
-            const unsigned lt = (1u << lane) - 1u;
-            if (inN) {
-                const int sl = val[a];
-                const int row = nrow + __popc(bn & lt);
-                const size_t r = (size_t)s * S + row;
-                ro.n_id[r] = key[a];
-                ro.n_slot[r] = sl;
-                ro.n_moe[r] = moe[a];
-                uint8_t* qr = ro.q_route + r * W;
-                for (int c2 = 0; c2 < W; ++c2) qr[c2] = (c2 == moe[a]) ? 1 : 0;
-                ro.shard_len[r] = st.shard_tokens[(size_t)sl * W + s];
-                ro.slot_nrow[(size_t)sl * W + s] = row;
+        constexpr int CU = 4;  // four 32-entry chunks per round: their shard_tokens loads issue together
+        for (int c0 = a0; c0 < a1; c0 += 32 * CU) {
+            bool inN[CU], inM[CU];
+            int64_t len[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+                const int a = c0 + 32 * u + lane;
+                inN[u] = a < a1 && ((kvm[a] >> s) & 1u);
+                inM[u] = a < a1 && moe[a] == s;
+                len[u] = inN[u] ? st.shard_tokens[(size_t)val[a] * W + s] : 0;
             }
-            if (inM) {
-                const int sl = val[a];
-                const int row = mrow + __popc(bm & lt);
-                const size_t r = (size_t)s * S + row;
-                ro.m_id[r] = key[a];
-                ro.m_slot[r] = sl;
-                uint8_t* qr = ro.res_route + r * W;
-                for (int c2 = 0; c2 < W; ++c2) qr[c2] = (kvm[a] >> c2) & 1u;
-                ro.slot_mrow[sl] = row;
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+                const int a = c0 + 32 * u + lane;
+                const unsigned bn = __ballot_sync(0xffffffffu, inN[u]);
+                const unsigned bm = __ballot_sync(0xffffffffu, inM[u]);
+                const unsigned lt = (1u << lane) - 1u;
+                if (inN[u]) {
+                    const int sl = val[a];
+                    const int row = nrow + __popc(bn & lt);
+                    const size_t r = (size_t)s * S + row;
+                    ro.n_id[r] = key[a];
+                    ro.n_slot[r] = sl;
+                    ro.n_moe[r] = moe[a];
+                    store_route_row(ro.q_route + r * W, W, 1u << moe[a]);
+                    ro.shard_len[r] = len[u];
+                    ro.slot_nrow[(size_t)sl * W + s] = row;
+                }
+                if (inM[u]) {
+                    const int sl = val[a];
+                    const int row = mrow + __popc(bm & lt);
+                    const size_t r = (size_t)s * S + row;
+                    ro.m_id[r] = key[a];
+                    ro.m_slot[r] = sl;
+                    store_route_row(ro.res_route + r * W, W, kvm[a]);
+                    ro.slot_mrow[sl] = row;
+                }
+                nrow += __popc(bn);
+                mrow += __popc(bm);
             }
-            nrow += __popc(bn);
-            mrow += __popc(bm);
         }
         if (lane == 0 && q == Q - 1) {
             ro.n_count[s] = nrow;
