@@ -176,9 +176,18 @@ __device__ void bitonic_sort_regs(int64_t* key, int32_t* val, int np2) {
         int64_t k[E];
         int32_t v[E];
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            k[j] = key[base + j];
-            v[j] = val[base + j];
+        for (int j = 0; j < E; j += 2) {  // 16-byte accesses: 2 keys, then 4 vals
+            const longlong2 kk = *reinterpret_cast<const longlong2*>(key + base + j);
+            k[j] = kk.x;
+            k[j + 1] = kk.y;
+        }
+#pragma unroll
+        for (int j = 0; j < E; j += 4) {
+            const int4 vv = *reinterpret_cast<const int4*>(val + base + j);
+            v[j] = vv.x;
+            v[j + 1] = vv.y;
+            v[j + 2] = vv.z;
+            v[j + 3] = vv.w;
         }
         for (int size = size_lo; size <= size_hi; size <<= 1) {
             for (int stride = min(size >> 1, WSPAN >> 1); stride >= E; stride >>= 1) {  // across lanes
@@ -211,10 +220,11 @@ __device__ void bitonic_sort_regs(int64_t* key, int32_t* val, int np2) {
             }
         }
 #pragma unroll
-        for (int j = 0; j < E; ++j) {
-            key[base + j] = k[j];
-            val[base + j] = v[j];
-        }
+        for (int j = 0; j < E; j += 2)
+            *reinterpret_cast<longlong2*>(key + base + j) = make_longlong2(k[j], k[j + 1]);
+#pragma unroll
+        for (int j = 0; j < E; j += 4)
+            *reinterpret_cast<int4*>(val + base + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         (void)lane;
     };
     reg_phase(2, min(np2, WSPAN));
