@@ -246,11 +246,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int R = p.num_shards;
-    const int64_t T = p.cu_tiles[R];
     const int pair = blockIdx.x >> 1;
     const int t_begin = p.pair_t0[pair];
     const int t_end = p.pair_t0[pair + 1];
-    (void)T;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGES; ++s) {
