@@ -438,6 +438,7 @@ int dcp_binding_config(dcp_ctx* ctx, int32_t n, const int64_t* ids, const int32_
     rc |= dalloc_tmp(&ro.slot_nrow, (size_t)n * W, tf.v);
     rc |= dalloc_tmp(&ro.slot_mrow, n, tf.v);
     rc |= dalloc_tmp(&ro.status, 1, tf.v);
+    rc |= dalloc_tmp(&ro.n_active, 1, tf.v);
     if (rc) return DCP_E_CUDA;
     DCP_CUDA_TRY(cudaMemcpy(st.state, active.data(), n * 4, cudaMemcpyHostToDevice));
     DCP_CUDA_TRY(cudaMemcpy(st.id, ids, n * 8, cudaMemcpyHostToDevice));

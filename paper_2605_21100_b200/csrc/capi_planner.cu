@@ -240,6 +240,7 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     rc |= dalloc(&pl->d_io_out, S, o);
     RoutingOut& ro = pl->ro;
     rc |= dalloc(&ro.n_count, W, o);
+    rc |= dalloc(&ro.n_active, 1, o);
     rc |= dalloc(&ro.m_count, W, o);
     rc |= dalloc(&ro.n_id, (size_t)W * S, o);
     rc |= dalloc(&ro.n_slot, (size_t)W * S, o);
@@ -575,7 +576,7 @@ int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
     routing_scan_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);
     routing_scatter_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
     DCP_CUDA_TRY(cudaGetLastError());
-    pl->last_launches = 4;
+    pl->last_launches = ROWS_SMEM_MAX >= pl->st.max_slots ? 6 : 4;
     pl->routing_valid = true;
     return DCP_OK;
 }

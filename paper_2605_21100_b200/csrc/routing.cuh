@@ -39,6 +39,7 @@ struct RoutingOut {
     int32_t* block_table; // [W][capacity]
     uint8_t* page_fill;   // [W][capacity]
     int32_t* status;      // [1]
+    int32_t* n_active;    // [1] actives compacted by routing_collect_kernel
     // exchange maps (K2/K3 destinations)
     int32_t* slot_nrow;   // [S][W] row of a slot in instance s's N list
     int32_t* slot_mrow;   // [S]    row of a slot in m_r's M list
@@ -163,86 +164,48 @@ __device__ __forceinline__ void store_route_row(uint8_t* row, int W, uint32_t ma
     }
 }
 
-// Bitonic sort of np2 (key, val) pairs in shared memory, ascending by key, with blockDim.x
-// threads each holding E = np2 / blockDim.x consecutive elements in registers: strides below
-// E stay in the thread, strides below 32 E go through warp shuffles, and only the strides of
-// 32 E and more take a shared-memory pass and a CTA barrier (15 of the 78 stages at 4,096).
-template <int E>
-__device__ void bitonic_sort_regs(int64_t* key, int32_t* val, int np2) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int base = tid * E;
-    constexpr int WSPAN = 32 * E;  // contiguous elements of one warp
-    auto reg_phase = [&](int size_lo, int size_hi) {  // sizes [size_lo, size_hi], strides < WSPAN
-        int64_t k[E];
-        int32_t v[E];
-#pragma unroll
-        for (int j = 0; j < E; j += 2) {  // 16-byte accesses: 2 keys, then 4 vals
-            const longlong2 kk = *reinterpret_cast<const longlong2*>(key + base + j);
-            k[j] = kk.x;
-            k[j + 1] = kk.y;
-        }
-#pragma unroll
-        for (int j = 0; j < E; j += 4) {
-            const int4 vv = *reinterpret_cast<const int4*>(val + base + j);
-            v[j] = vv.x;
-            v[j + 1] = vv.y;
-            v[j + 2] = vv.z;
-            v[j + 3] = vv.w;
-        }
-        for (int size = size_lo; size <= size_hi; size <<= 1) {
-            for (int stride = min(size >> 1, WSPAN >> 1); stride >= E; stride >>= 1) {  // across lanes
-                const int ls = stride / E;
-#pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    const int i = base + j;
-                    const int64_t pk = __shfl_xor_sync(0xffffffffu, k[j], ls);
-                    const int32_t pv = __shfl_xor_sync(0xffffffffu, v[j], ls);
-                    const bool keep_min = ((i & stride) == 0) == ((i & size) == 0);
-                    if (keep_min ? (pk < k[j]) : (pk > k[j])) {
-                        k[j] = pk;
-                        v[j] = pv;
-                    }
-                }
-            }
-#pragma unroll
-            for (int st = E / 2; st > 0; st >>= 1) {  // within the thread (compile-time indices)
-                if (st > (size >> 1)) continue;
-#pragma unroll
-                for (int j = 0; j < E; ++j) {
-                    if (j & st) continue;
-                    const int jh = j | st;
-                    const bool asc = ((base + j) & size) == 0;
-                    if ((k[j] > k[jh]) == asc) {
-                        const int64_t tk = k[j]; k[j] = k[jh]; k[jh] = tk;
-                        const int32_t tv = v[j]; v[j] = v[jh]; v[jh] = tv;
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < E; j += 2)
-            *reinterpret_cast<longlong2*>(key + base + j) = make_longlong2(k[j], k[j + 1]);
-#pragma unroll
-        for (int j = 0; j < E; j += 4)
-            *reinterpret_cast<int4*>(val + base + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        (void)lane;
-    };
-    reg_phase(2, min(np2, WSPAN));
+// Row order = request id order (build_binding_config sorts by id, routing.cpp:9-32).  The ids
+// are ranked on the whole GPU instead of sorted in one CTA: routing_collect_kernel compacts the
+// active slots (id -> sk2, slot -> sval, rank sk1 = 0), routing_rank_kernel counts for every
+// active how many ids are smaller (equal ids, which the planner never has, rank by collection
+// order), split over RK_SPLIT CTAs per 256 actives,
+// and the rows kernel scatters each active to its rank.  (A one-CTA bitonic sort of 4,096
+// keys took ~35 us, issue-bound on that one SM.)
+constexpr int RK_SPLIT = 8;
+
+static __global__ void __launch_bounds__(1024) routing_collect_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int32_t s_n;
+    if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
-    for (int size = 2 * WSPAN; size <= np2; size <<= 1) {
-        for (int stride = size >> 1; stride >= WSPAN; stride >>= 1) {
-            for (int i = tid; i < np2 / 2; i += blockDim.x) {
-                const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-                if ((key[lo] > key[hi]) == ((lo & size) == 0)) {
-                    const int64_t tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
-                    const int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
-                }
-            }
-            __syncthreads();
-        }
-        reg_phase(size, size);
+    for (int sl = threadIdx.x; sl < st.max_slots; sl += blockDim.x) {
+        if (st.state[sl] != ST_ACTIVE) continue;
+        const int i = atomicAdd(&s_n, 1);
+        st.sk2[i] = st.id[sl];
+        st.sval[i] = sl;
+        st.sk1[i] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *ro.n_active = s_n;
+}
+
+static __global__ void __launch_bounds__(256) routing_rank_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int64_t tile[256];
+    const int n = *ro.n_active;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (static_cast<int>(blockIdx.x * blockDim.x) >= n) return;
+    const int64_t ki = i < n ? st.sk2[i] : 0;
+    const int j0 = static_cast<int>(static_cast<int64_t>(blockIdx.y) * n / gridDim.y);
+    const int j1 = static_cast<int>(static_cast<int64_t>(blockIdx.y + 1) * n / gridDim.y);
+    unsigned long long cnt = 0;
+    for (int t = j0; t < j1; t += blockDim.x) {
+        const int j = t + threadIdx.x;
+        tile[threadIdx.x] = j < j1 ? st.sk2[j] : INT64_MAX;
+        __syncthreads();
+        const int m = min(static_cast<int>(blockDim.x), j1 - t);
+        for (int u = 0; u < m; ++u) cnt += tile[u] < ki || (tile[u] == ki && t + u < i);  // ties: a permutation
         __syncthreads();
     }
+    if (i < n && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(st.sk1 + i), cnt);
 }
 
 static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(PlannerState st, RoutingOut ro, int np2cap) {
@@ -263,49 +226,21 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
     int32_t* val = reinterpret_cast<int32_t*>(key + np2cap);
     uint32_t* kvm = reinterpret_cast<uint32_t*>(val + np2cap);
     int32_t* moe = reinterpret_cast<int32_t*>(kvm + np2cap);
-    __shared__ int32_t s_n;
     __shared__ int32_t s_bad;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int S = st.max_slots, W = st.W;
-    if (tid == 0) {
-        s_n = 0;
-        s_bad = 0;
-    }
+    if (tid == 0) s_bad = 0;
     __syncthreads();
-    for (int sl = tid; sl < S; sl += blockDim.x) {
-        if (st.state[sl] != ST_ACTIVE) continue;
-        const int i = atomicAdd(&s_n, 1);
-        key[i] = st.id[sl];
-        val[i] = sl;
+    // actives in id order: each to its rank (routing_rank_kernel)
+    const int n = *ro.n_active;
+    for (int i = tid; i < n; i += blockDim.x) {
+        const int r = static_cast<int>(st.sk1[i]);
+        key[r] = st.sk2[i];
+        val[r] = st.sval[i];
     }
     __syncthreads();
     RT_STAMP();
-    const int n = s_n;
-    int np2 = 1;
-    while (np2 < n) np2 <<= 1;
-    for (int i = n + tid; i < np2; i += blockDim.x) {
-        key[i] = INT64_MAX;
-        val[i] = -1;
-    }
-    __syncthreads();
-    if (np2 == 4 * static_cast<int>(blockDim.x)) {
-        bitonic_sort_regs<4>(key, val, np2);
-    } else if (np2 == 8 * static_cast<int>(blockDim.x)) {
-        bitonic_sort_regs<8>(key, val, np2);
-    } else {
-        for (int size = 2; size <= np2; size <<= 1)
-            for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                for (int i = tid; i < np2 / 2; i += blockDim.x) {
-                    const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-                    if ((key[lo] > key[hi]) == ((lo & size) == 0)) {
-                        const int64_t tk = key[lo]; key[lo] = key[hi]; key[hi] = tk;
-                        const int32_t tv = val[lo]; val[lo] = val[hi]; val[hi] = tv;
-                    }
-                }
-                __syncthreads();
-            }
-    }
-    RT_STAMP();
+    RT_STAMP();  // (was: the one-CTA sort)
     for (int a = tid; a < n; a += blockDim.x) {
         const int sl = val[a];
         const int k = st.k[sl], m_r = st.moe[sl];
@@ -421,6 +356,8 @@ static inline cudaError_t launch_routing_rows(const PlannerState& st, const Rout
         cudaError_t e = cudaFuncSetAttribute(routing_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sm));
         if (e != cudaSuccess) return e;
+        routing_collect_kernel<<<1, 1024, 0, stream>>>(st, ro);
+        routing_rank_kernel<<<dim3((st.max_slots + 255) / 256, RK_SPLIT), 256, 0, stream>>>(st, ro);
         routing_rows_smem_kernel<<<1, 1024, sm, stream>>>(st, ro, np2);
     } else {
         routing_rows_kernel<<<1, 1024, 0, stream>>>(st, ro);
