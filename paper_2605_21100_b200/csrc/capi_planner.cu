@@ -576,7 +576,7 @@ int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
     routing_scan_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);
     routing_scatter_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
     DCP_CUDA_TRY(cudaGetLastError());
-    pl->last_launches = ROWS_SMEM_MAX >= pl->st.max_slots ? 6 : 4;
+    pl->last_launches = ROWS_SMEM_MAX >= pl->st.max_slots ? 7 : 4;
     pl->routing_valid = true;
     return DCP_OK;
 }

@@ -227,8 +227,7 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
     uint32_t* kvm = reinterpret_cast<uint32_t*>(val + np2cap);
     int32_t* moe = reinterpret_cast<int32_t*>(kvm + np2cap);
     __shared__ int32_t s_bad;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int S = st.max_slots, W = st.W;
+    const int tid = threadIdx.x;
     if (tid == 0) s_bad = 0;
     __syncthreads();
     // actives in id order: each to its rank (routing_rank_kernel)
@@ -260,91 +259,91 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
         if (tid == 0) *ro.status = -4;
         return;
     }
-    RT_STAMP();
-    // Q warps per instance (32 / W, at least 1): warp q of instance s takes actives
-    // [q n / Q, (q+1) n / Q); pass 1 counts its N / M members, pass 2 writes them after the
-    // counts of the lower segments.
-    const int Q = W <= 32 ? (32 / W) : 1;
-    __shared__ int32_t seg_n[32], seg_m[32];
-    const int s = warp / Q, q = warp % Q;
-    const bool active_warp = warp < W * Q;
-    const int a0 = (int)((int64_t)q * n / Q), a1 = (int)((int64_t)(q + 1) * n / Q);
-    if (active_warp) {
-        int cn = 0, cm = 0;
-        for (int c = a0; c < a1; c += 32) {
-            const int a = c + lane;
-            cn += __popc(__ballot_sync(0xffffffffu, a < a1 && ((kvm[a] >> s) & 1u)));
-            cm += __popc(__ballot_sync(0xffffffffu, a < a1 && moe[a] == s));
-        }
-        if (lane == 0) {
-            seg_n[warp] = cn;
-            seg_m[warp] = cm;
-        }
-    }
-    __syncthreads();
-    RT_STAMP();
-    if (active_warp) {
-        int nrow = 0, mrow = 0;
-        for (int j = 0; j < q; ++j) {
-            nrow += seg_n[s * Q + j];
-            mrow += seg_m[s * Q + j];
-        }
-        constexpr int CU = 4;  // four 32-entry chunks per round: their shard_tokens loads issue together
-        for (int c0 = a0; c0 < a1; c0 += 32 * CU) {
-            bool inN[CU], inM[CU];
-            int64_t len[CU];
-#pragma unroll
-            for (int u = 0; u < CU; ++u) {
-                const int a = c0 + 32 * u + lane;
-                inN[u] = a < a1 && ((kvm[a] >> s) & 1u);
-                inM[u] = a < a1 && moe[a] == s;
-                len[u] = inN[u] ? st.shard_tokens[(size_t)val[a] * W + s] : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < CU; ++u) {
-                const int a = c0 + 32 * u + lane;
-                const unsigned bn = __ballot_sync(0xffffffffu, inN[u]);
-                const unsigned bm = __ballot_sync(0xffffffffu, inM[u]);
-                const unsigned lt = (1u << lane) - 1u;
-                if (inN[u]) {
-                    const int sl = val[a];
-                    const int row = nrow + __popc(bn & lt);
-                    const size_t r = (size_t)s * S + row;
-                    ro.n_id[r] = key[a];
-                    ro.n_slot[r] = sl;
-                    ro.n_moe[r] = moe[a];
-                    store_route_row(ro.q_route + r * W, W, 1u << moe[a]);
-                    ro.shard_len[r] = len[u];
-                    ro.slot_nrow[(size_t)sl * W + s] = row;
-                }
-                if (inM[u]) {
-                    const int sl = val[a];
-                    const int row = mrow + __popc(bm & lt);
-                    const size_t r = (size_t)s * S + row;
-                    ro.m_id[r] = key[a];
-                    ro.m_slot[r] = sl;
-                    store_route_row(ro.res_route + r * W, W, kvm[a]);
-                    ro.slot_mrow[sl] = row;
-                }
-                nrow += __popc(bn);
-                mrow += __popc(bm);
-            }
-        }
-        if (lane == 0 && q == Q - 1) {
-            ro.n_count[s] = nrow;
-            ro.m_count[s] = mrow;
-            bucket_shape_default_d(mrow, nrow, ro.bucket + 2 * s);
-        }
+    // the id-ordered actives for routing_write_kernel: id -> sk2, slot -> sval, (P_r mask, m_r) -> sk1
+    for (int a = tid; a < n; a += blockDim.x) {
+        st.sk2[a] = key[a];
+        st.sval[a] = val[a];
+        st.sk1[a] = static_cast<int64_t>((static_cast<uint64_t>(kvm[a]) << 32) | static_cast<uint32_t>(moe[a]));
     }
 #ifdef DCP_PLANNER_PROF
     __syncthreads();
     RT_STAMP();
+    RT_STAMP();
+    RT_STAMP();
     if (tid == 0)
-        printf("routing_rows us: collect %.1f sort %.1f kvm %.1f count %.1f write %.1f\n", (rt_ts[1] - rt_ts[0]) / 1e3,
-               (rt_ts[2] - rt_ts[1]) / 1e3, (rt_ts[3] - rt_ts[2]) / 1e3, (rt_ts[4] - rt_ts[3]) / 1e3,
-               (rt_ts[5] - rt_ts[4]) / 1e3);
+        printf("routing_rows us: rank-scatter %.1f kvm %.1f\n", (rt_ts[1] - rt_ts[0]) / 1e3, (rt_ts[3] - rt_ts[2]) / 1e3);
 #endif
     if (tid == 0) *ro.status = 0;
+}
+
+// M / N rows of instance blockIdx.x (build_binding_config + derive_routing_tables,
+// routing.cpp:9-63): 32 warps split the id-ordered actives; pass 1 counts each warp's N / M
+// members, pass 2 writes them after the counts of the lower warps.
+static __global__ void __launch_bounds__(1024) routing_write_kernel(PlannerState st, RoutingOut ro) {
+    __shared__ int32_t seg_n[32], seg_m[32];
+    if (*ro.status != 0) return;
+    const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int S = st.max_slots, W = st.W;
+    const int n = *ro.n_active;
+    const int nw = blockDim.x >> 5;
+    const int a0 = (int)((int64_t)warp * n / nw), a1 = (int)((int64_t)(warp + 1) * n / nw);
+    auto kvm_of = [&](int a) { return static_cast<uint32_t>(static_cast<uint64_t>(st.sk1[a]) >> 32); };
+    auto moe_of = [&](int a) { return static_cast<int>(static_cast<uint32_t>(st.sk1[a])); };
+    int cn = 0, cm = 0;
+    for (int c = a0; c < a1; c += 32) {
+        const int a = c + lane;
+        const bool ok = a < a1;
+        const int64_t pk = ok ? st.sk1[a] : 0;
+        cn += __popc(__ballot_sync(0xffffffffu, ok && ((static_cast<uint64_t>(pk) >> (32 + s)) & 1u)));
+        cm += __popc(__ballot_sync(0xffffffffu, ok && static_cast<int>(static_cast<uint32_t>(pk)) == s));
+    }
+    if (lane == 0) {
+        seg_n[warp] = cn;
+        seg_m[warp] = cm;
+    }
+    __syncthreads();
+    int nrow = 0, mrow = 0;
+    for (int j = 0; j < warp; ++j) {
+        nrow += seg_n[j];
+        mrow += seg_m[j];
+    }
+    for (int c = a0; c < a1; c += 32) {
+        const int a = c + lane;
+        const bool ok = a < a1;
+        const uint32_t km = ok ? kvm_of(a) : 0u;
+        const int mo = ok ? moe_of(a) : -1;
+        const bool inN = ok && ((km >> s) & 1u);
+        const bool inM = ok && mo == s;
+        const int sl = ok ? st.sval[a] : 0;
+        const unsigned bn = __ballot_sync(0xffffffffu, inN);
+        const unsigned bm = __ballot_sync(0xffffffffu, inM);
+        const unsigned lt = (1u << lane) - 1u;
+        if (inN) {
+            const int row = nrow + __popc(bn & lt);
+            const size_t r = (size_t)s * S + row;
+            ro.n_id[r] = st.sk2[a];
+            ro.n_slot[r] = sl;
+            ro.n_moe[r] = mo;
+            store_route_row(ro.q_route + r * W, W, 1u << mo);
+            ro.shard_len[r] = st.shard_tokens[(size_t)sl * W + s];
+            ro.slot_nrow[(size_t)sl * W + s] = row;
+        }
+        if (inM) {
+            const int row = mrow + __popc(bm & lt);
+            const size_t r = (size_t)s * S + row;
+            ro.m_id[r] = st.sk2[a];
+            ro.m_slot[r] = sl;
+            store_route_row(ro.res_route + r * W, W, km);
+            ro.slot_mrow[sl] = row;
+        }
+        nrow += __popc(bn);
+        mrow += __popc(bm);
+    }
+    if (lane == 0 && warp == nw - 1) {
+        ro.n_count[s] = nrow;
+        ro.m_count[s] = mrow;
+        bucket_shape_default_d(mrow, nrow, ro.bucket + 2 * s);
+    }
 }
 
 // Host: routing rows for the planner's active set, shared-memory sort when it fits.
@@ -359,6 +358,7 @@ static inline cudaError_t launch_routing_rows(const PlannerState& st, const Rout
         routing_collect_kernel<<<1, 1024, 0, stream>>>(st, ro);
         routing_rank_kernel<<<dim3((st.max_slots + 255) / 256, RK_SPLIT), 256, 0, stream>>>(st, ro);
         routing_rows_smem_kernel<<<1, 1024, sm, stream>>>(st, ro, np2);
+        routing_write_kernel<<<st.W, 1024, 0, stream>>>(st, ro);
     } else {
         routing_rows_kernel<<<1, 1024, 0, stream>>>(st, ro);
     }
