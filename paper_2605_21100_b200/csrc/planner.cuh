@@ -457,14 +457,7 @@ static __device__ void rebalance_core(const PlannerState& st, SmemInst& si, int3
             for (int i = 0; i < n2; ++i) {
                 // argmin over P_r of B, ties to the lowest instance id (cpp:54-59); lane = instance
                 const bool mem = lane < st.W && ((rb_mask[i] >> lane) & 1u);
-                int64_t bv = mem ? (int64_t)si.B[lane] : INT64_MAX;
-                int bs = mem ? lane : 0x7fffffff;
-#pragma unroll
-                for (int o = 16; o; o >>= 1) {
-                    const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                    const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-                    if (ov < bv || (ov == bv && os < bs)) { bv = ov; bs = os; }
-                }
+                const int bs = warp_argmin_small(static_cast<uint32_t>(si.B[lane]), mem, lane);
                 if (lane == 0) {
                     st.moe[rb_sl[i]] = bs;
                     si.B[bs] += 1;
@@ -481,16 +474,9 @@ static __device__ void rebalance_core(const PlannerState& st, SmemInst& si, int3
         for (int i = 0; i < n2; ++i) {
             const int sl = st.sval[i];
             const int kk = st.k[sl];
-            const int s = lane < kk ? st.kv[sl * PL_MAXK + lane] : 0x7fffffff;
-            int64_t bv = lane < kk ? (int64_t)si.B[s] : INT64_MAX;
-            int bs = s;
-            // argmin over P_r of B, ties to the lowest instance id (cpp:54-59)
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const int64_t ov = __shfl_xor_sync(0xffffffffu, bv, o);
-                const int os = __shfl_xor_sync(0xffffffffu, bs, o);
-                if (ov < bv || (ov == bv && os < bs)) { bv = ov; bs = os; }
-            }
+            const int s = lane < kk ? st.kv[sl * PL_MAXK + lane] : 0;
+            // argmin over P_r of B, ties to the lowest instance id (cpp:54-59): key (B_s, s)
+            const int bs = warp_argmin_small(static_cast<uint32_t>(si.B[s]), lane < kk, s);
             if (lane == 0) {
                 st.moe[sl] = bs;
                 si.B[bs] += 1;
