@@ -18,14 +18,17 @@ def _bits(t):
     return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
-@pytest.mark.parametrize("W,E,k,H,I", [(4, 8, 2, 256, 64), (2, 16, 4, 512, 128), (8, 32, 8, 256, 32)])
-def test_dispatch_combine_matches_oracle(W, E, k, H, I):
+@pytest.mark.parametrize("W,E,k,H,I,m_max", [
+    (4, 8, 2, 256, 64, 64), (2, 16, 4, 512, 128, 64), (8, 32, 8, 256, 32, 64),
+    # the exchange at cfg4 / cfg5 widths (Qwen3-30B-A3B: hidden 2048, 128 experts top-8;
+    # DeepSeek-V3: hidden 7168, 256 experts top-8), narrow experts to keep the fp64 oracle short
+    (8, 128, 8, 2048, 16, 16), (8, 256, 8, 7168, 16, 8)])
+def test_dispatch_combine_matches_oracle(W, E, k, H, I, m_max):
     from paper_2605_21100_b200.attention import DcpContext
     from paper_2605_21100_b200.moe import MoeInstance
     ctx = DcpContext(0)
     dev = torch.device("cuda:0")
     g = torch.Generator(device=dev).manual_seed(W * 100 + E)
-    m_max = 64
     inst = [MoeInstance(ctx, W, s, H, k, E, m_max) for s in range(W)]
     for s in range(W):
         for t in range(W):
