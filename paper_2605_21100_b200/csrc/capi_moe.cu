@@ -3,6 +3,7 @@
 #include <cstring>
 
 #include "capi_common.cuh"
+#include <cstdlib>
 #include "moe.cuh"
 
 using namespace dcp;
@@ -86,7 +87,8 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     x->host.epoch = x->epoch;
     x->host.disp_done = reinterpret_cast<int32_t*>(x->local + o_dd);
     x->host.cb_done = reinterpret_cast<int32_t*>(x->local + o_cd);
-    x->host.chunks = static_cast<int32_t>(m < 32 ? m : 32);
+    static const int max_chunks = [] { const char* e = std::getenv("DCP_MOE_CHUNKS"); return e ? std::atoi(e) : 128; }();
+    x->host.chunks = static_cast<int32_t>(m < max_chunks ? m : max_chunks);
     fill(x, c->self, x->pool);
     *out = x;
     return DCP_OK;
