@@ -172,7 +172,7 @@ int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* st
     DCP_REQUIRE(x && x_rows && meta_rows, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int rows = x->cfg.world * x->cfg.m_max;
-    int grid = (rows + 7) / 8;
+    int grid = rows;  // up to one CTA per received row (warp groups per row, moe.cuh)
     if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
     moe_receive_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
                                             x->counts);
@@ -186,9 +186,9 @@ const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x) { return x ? x->counts 
 int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* counts, void* stream) {
     DCP_REQUIRE(x && x_rows && meta_rows, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // one warp per received row, at most W * m_max rows
+    // one CTA per received row, at most W * m_max rows
     const int rows = x->cfg.world * x->cfg.m_max;
-    int grid = (rows + 7) / 8;
+    int grid = rows;  // up to one CTA per received row (warp groups per row, moe.cuh)
     if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
     moe_receive_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
                                             x->counts);

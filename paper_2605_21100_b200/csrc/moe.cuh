@@ -153,8 +153,8 @@ static __global__ void __launch_bounds__(128) moe_dispatch_kernel(const MoePeers
 }
 
 // K5a: wait for every source, compact received rows in (source, slot) order.  Grid-wide:
-// every CTA derives the per-source offsets from the published counts, then its warps copy
-// rows r = warp_global, warp_global + total_warps, ... (one warp per 16-byte-vector row).
+// every CTA derives the per-source offsets from the published counts, then its warp groups
+// copy rows r = group_global, + total_groups, ...
 static __global__ void __launch_bounds__(256) moe_receive_kernel(const MoePeers* __restrict__ mp,
                                                                  __nv_bfloat16* __restrict__ x_rows,
                                                                  int32_t* __restrict__ meta_rows,
@@ -177,25 +177,32 @@ static __global__ void __launch_bounds__(256) moe_receive_kernel(const MoePeers*
     }
     __syncthreads();
     const int R = off[W];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int r = blockIdx.x * nw + warp; r < R; r += gridDim.x * nw) {
+    // a group of wpr warps per row, wpr ~ vectors / 128 (capped at the CTA's 8 warps): a
+    // 7,168-wide row (896 vectors) takes the whole CTA and is in flight at once, a 2,048-wide
+    // row two warps (one warp per row took H / 1,024 dependent load rounds)
+    const int nvec = H / 8;
+    const int wpr = nvec > 512 ? 8 : nvec > 256 ? 4 : nvec > 128 ? 2 : 1;
+    const int gsz = 32 * wpr, groups = (blockDim.x >> 5) / wpr;
+    const int grp = (threadIdx.x >> 5) / wpr, gt = threadIdx.x % gsz;
+    for (int r = blockIdx.x * groups + grp; r < R; r += gridDim.x * groups) {
         int s = 0;
         while (off[s + 1] <= r) ++s;
         const int slot = r - off[s];
         const size_t row = (size_t)s * p.m_max + slot;
         const uint4* src = reinterpret_cast<const uint4*>(p.rx_x[p.self] + row * H);
         uint4* dst = reinterpret_cast<uint4*>(x_rows + (size_t)r * H);
-        for (int base = lane; base < H / 8; base += 4 * 32) {
+        for (int base = gt; base < nvec; base += 4 * gsz) {
             uint4 v[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (base + 32 * u < H / 8) v[u] = __ldcg(src + base + 32 * u);
+                if (base + gsz * u < nvec) v[u] = __ldcg(src + base + gsz * u);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                if (base + 32 * u < H / 8) dst[base + 32 * u] = v[u];
+                if (base + gsz * u < nvec) dst[base + gsz * u] = v[u];
         }
-        for (int i = lane; i < p.meta; i += 32) meta_rows[(size_t)r * p.meta + i] = __ldcg(p.rx_meta[p.self] + row * p.meta + i);
-        if (lane == 0) row_src[r] = s;
+        for (int i = gt; i < p.meta; i += gsz)
+            meta_rows[(size_t)r * p.meta + i] = __ldcg(p.rx_meta[p.self] + row * p.meta + i);
+        if (gt == 0) row_src[r] = s;
     }
 }
 
