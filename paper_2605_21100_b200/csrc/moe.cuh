@@ -101,6 +101,7 @@ static __global__ void __launch_bounds__(128) moe_dispatch_kernel(const MoePeers
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) n_mine = 0;
+    __syncthreads();  // the scan loop below holds the other barriers, and it is empty when M == 0
     int carry = 0;
     for (int t0 = 0; t0 < M; t0 += blockDim.x) {
         const int t = t0 + threadIdx.x;
