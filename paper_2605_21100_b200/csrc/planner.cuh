@@ -627,6 +627,7 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
             }
             head_recorded = head_recorded || (wq == 0);
             ++wq;
+            __syncwarp();  // every lane has read pl before the next placement rewrites it
             if (st.hol_strict) {
                 ++i;
                 break;
