@@ -1,5 +1,6 @@
 #!/bin/bash
-# gpurun: K1 tests, then small-step / DCP / trace timing for several K1 stream-K floors (DCP_K1_MIN_PAGES).
+# gpurun: K1 tests, then small-step / DCP timing for several K1 stream-K floors (DCP_K1_MIN_PAGES: an
+# experiment build only -- the knob was not kept).
 set -u
 mkdir -p gpurun_out
 timeout 900 python -m pytest -m gpu -q -x tests/test_attention_gpu.py tests/test_dcp_step_gpu.py tests/test_step_graph_gpu.py tests/test_cfg1_gpu.py tests/test_cfg3_gpu.py > gpurun_out/pytest_k1min.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_k1min.log
