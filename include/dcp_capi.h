@@ -320,6 +320,10 @@ DCP_API int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* st
 DCP_API int dcp_planner_set_policy(dcp_planner* pl, int32_t policy, int32_t n_bucket,
                                    const int64_t* bucket_len, const int32_t* bucket_deg,
                                    int32_t uniform_degree, int32_t hol_strict);
+/* UniformCP round-robin counters (Scheduler::ucp_round_robin_, scheduler.hpp:88):
+ * dir 0 uploads rr[0..n) (resizing the device vector), dir 1 reads them back.  The
+ * C++ drop-in keeps them per Scheduler and pushes / pulls them around each step. */
+DCP_API int dcp_planner_ucp_rr(dcp_planner* pl, int32_t* rr, int32_t n, int32_t dir);
 /* Make the device waiting queue exactly `ids` (FIFO order).  Unknown ids are
  * admitted as new waiting requests with seq_lens[i]; known ids must be waiting.
  * Waiting requests not listed are dropped. */

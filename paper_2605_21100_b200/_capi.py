@@ -165,6 +165,7 @@ _SIGNATURES = [
     ("dcp_merge_partials", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
     ("dcp_planner_set_policy", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32, c_int32]),
     ("dcp_planner_set_queue", c_int, [c_void_p, c_void_p, c_void_p, c_int32]),
+    ("dcp_planner_ucp_rr", c_int, [c_void_p, c_void_p, c_int32, c_int32]),
     ("dcp_planner_allocate", c_int, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_int32]),
     ("dcp_planner_pages", c_int64, [c_void_p, c_int64, c_void_p, c_void_p, c_int64]),
     ("dcp_planner_active_moe", c_int32, [c_void_p, c_void_p, c_void_p, c_int32]),

@@ -154,6 +154,30 @@ int dcp_planner_set_policy(dcp_planner* pl, int32_t policy, int32_t n_bucket, co
     return DCP_OK;
 }
 
+int dcp_planner_ucp_rr(dcp_planner* pl, int32_t* rr, int32_t n, int32_t dir) {
+    DCP_REQUIRE(pl && (n == 0 || rr) && n >= 0 && (dir == 0 || dir == 1), DCP_E_INVALID_ARG, "bad argument");
+    PlannerState& st = pl->st;
+    if (dir == 0) {
+        if (n != st.n_groups || !st.ucp_rr) {
+            if (st.ucp_rr) {
+                DCP_CUDA_TRY(cudaFree(st.ucp_rr));
+                auto it = std::find(pl->owned.begin(), pl->owned.end(), static_cast<void*>(st.ucp_rr));
+                if (it != pl->owned.end()) pl->owned.erase(it);
+            }
+            void* q = nullptr;
+            DCP_CUDA_TRY(cudaMalloc(&q, std::max(n, 1) * sizeof(int32_t)));
+            pl->owned.push_back(q);
+            st.ucp_rr = static_cast<int32_t*>(q);
+            st.n_groups = n;
+        }
+        if (n) DCP_CUDA_TRY(cudaMemcpy(st.ucp_rr, rr, n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    } else {
+        DCP_REQUIRE(n == st.n_groups, DCP_E_INVALID_ARG, "rr size %d != %d groups", n, st.n_groups);
+        if (n) DCP_CUDA_TRY(cudaMemcpy(rr, st.ucp_rr, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
+    return DCP_OK;
+}
+
 int dcp_planner_set_queue(dcp_planner* pl, const int64_t* ids, const int64_t* lens, int32_t n) {
     DCP_REQUIRE(pl && (n == 0 || (ids && lens)), DCP_E_INVALID_ARG, "NULL argument");
     std::vector<int32_t> state;
@@ -223,8 +247,12 @@ int dcp_planner_allocate(dcp_planner* pl, int64_t id, int64_t seq_len, int32_t k
                          const int64_t* split, int32_t moe) {
     DCP_REQUIRE(pl && kv && split, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(k >= 1 && k <= PL_MAXK, DCP_E_UNSUPPORTED, "cp_degree %d", k);
-    for (int m = 0; m < k; ++m)
+    for (int m = 0; m < k; ++m) {
         DCP_REQUIRE(kv[m] >= 0 && kv[m] < pl->st.W, DCP_E_INVALID_ARG, "instance %d out of range", kv[m]);
+        // the device allocator pops every member's frames from the same pre-pop stack top
+        for (int j = 0; j < m; ++j)
+            DCP_REQUIRE(kv[j] != kv[m], DCP_E_INCONSISTENT, "instance %d listed twice in kv_binding", kv[m]);
+    }
     std::vector<int32_t> state;
     if (int rc = planner_states(pl, state)) return rc;
     int sl;

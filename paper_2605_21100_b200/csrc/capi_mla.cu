@@ -104,8 +104,11 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
     p.num_shards = a->num_shards;
     p.num_frames = static_cast<int32_t>(a->num_frames);
     p.scale_log2 = a->scale * 1.4426950408889634f;
-    static const int dbg = [] { const char* e = std::getenv("DCP_MLA_DBG"); return e ? std::atoi(e) : 0; }();
-    p.dbg = dbg;
+#ifdef DCP_MLA_DBG
+    p.dbg = DCP_MLA_DBG;  // bottleneck experiments only: a -DDCP_MLA_DBG=n build produces wrong results
+#else
+    p.dbg = 0;
+#endif
     p.trace = g_mla_trace;
 
     mla::mla_tile_scan_kernel<PAGE><<<1, 1024, 0, stream>>>(p);

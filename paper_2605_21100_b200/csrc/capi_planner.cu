@@ -126,6 +126,8 @@ int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* c, dcp_planner** 
     DCP_REQUIRE(c->instances_per_node <= PL_MAXK, DCP_E_UNSUPPORTED, "instances_per_node %d > %d",
                 c->instances_per_node, PL_MAXK);
     DCP_REQUIRE(c->page_size >= 1, DCP_E_CONFIG, "page_size < 1");
+    // per-page fills are stored in 8 bits (pg_fill, routing page_fill)
+    DCP_REQUIRE(c->page_size <= 255, DCP_E_UNSUPPORTED, "page_size %lld > 255", (long long)c->page_size);
     DCP_REQUIRE(c->capacity_pages >= 0 && c->capacity_pages < (1LL << 31), DCP_E_UNSUPPORTED,
                 "capacity_pages out of range");
     DCP_REQUIRE(c->max_requests >= 1, DCP_E_INVALID_ARG, "max_requests < 1");

@@ -125,7 +125,7 @@ struct MlaParams {
     int32_t num_shards;
     int32_t num_frames;
     float scale_log2;
-    int32_t dbg;                 // bottleneck experiments (env DCP_MLA_DBG): 1 = no MMAs, 2 = no softmax math
+    int32_t dbg;                 // bottleneck experiments (compile-time -DDCP_MLA_DBG=n only): 1 = no MMAs, 2 = no softmax math
     long long* trace;            // optional [256][8] globaltimer stamps of pair 0 + [256][3] per pair (dcp_mla_set_trace)
 };
 

@@ -141,6 +141,34 @@ StepResult Scheduler::step(std::deque<std::size_t>& waiting, std::span<Request> 
                            std::span<const std::size_t> active, ClusterState& cluster) {
     auto& dev = bound_planner(cluster);
     push_policy(dev, policy_);
+    // The device recomputes B over its own active set (every committed, unfinished request);
+    // the reference recomputes it over `active` (scheduler.cpp:250-261).  They must agree.
+    {
+        const int acap = static_cast<int>(active.size()) + 1;
+        std::vector<std::int64_t> aid(acap);
+        std::vector<std::int32_t> amoe(acap);
+        const int n = dcp_planner_active_moe(dev.handle, aid.data(), amoe.data(), acap);
+        if (n < 0) device::check(n);
+        bool same = n == static_cast<int>(active.size());
+        if (same) {
+            std::vector<std::int64_t> want;
+            for (std::size_t idx : active) want.push_back(requests[idx].id);
+            std::sort(want.begin(), want.end());
+            std::sort(aid.begin(), aid.begin() + n);
+            same = std::equal(want.begin(), want.end(), aid.begin());
+        }
+        if (!same)
+            throw InconsistentPlacement("Scheduler::step: `active` differs from the requests committed and not "
+                                        "released on this cluster (the device recomputes B over that set)");
+    }
+    // UniformCP round-robin state belongs to this Scheduler (scheduler.hpp:88), not to the cluster:
+    // push it before the round, read it back after (place_uniform, scheduler.cpp:189-222).
+    const bool uniform = policy_.kind == PolicyKind::UniformCP;
+    if (uniform) {
+        const int groups = (cluster.topo.instances_per_node / policy_.uniform_degree) * cluster.topo.nodes;
+        if (static_cast<int>(ucp_round_robin_.size()) != groups) ucp_round_robin_.assign(groups, 0);
+        device::check(dcp_planner_ucp_rr(dev.handle, ucp_round_robin_.data(), groups, 0));
+    }
     // 1. the device queue mirrors the caller's FIFO queue
     std::vector<std::int64_t> ids, lens;
     std::unordered_map<std::int64_t, std::size_t> index_of;
@@ -163,6 +191,9 @@ StepResult Scheduler::step(std::deque<std::size_t>& waiting, std::span<Request> 
     res.deferred.assign(d.begin(), d.begin() + nd);
     res.unschedulable.assign(u.begin(), u.begin() + nu);
     res.hol_events = hol;
+    if (uniform)
+        device::check(dcp_planner_ucp_rr(dev.handle, ucp_round_robin_.data(),
+                                         static_cast<int>(ucp_round_robin_.size()), 1));
     // 3. rebalanced MoE bindings of the active set (DCP) / sticky otherwise
     if (policy_.kind == PolicyKind::DualBalancedDCP && !active.empty()) {
         const int acap = static_cast<int>(active.size() + res.committed.size()) + 1024;

@@ -105,3 +105,14 @@ def test_cpp_api_matches_oracle_on_random_scripts(driver):
         p = subprocess.run([driver], input=_script_text(sc), capture_output=True, text=True, timeout=300)
         assert p.returncode == 0, p.stderr
         assert p.stdout == _oracle_text(sc), f"trial {trial}"
+
+
+def test_two_schedulers_share_a_cluster():
+    """UniformCP round-robin state is per Scheduler (reference scheduler.hpp:88): two
+    Schedulers (plus a LeastBatch one) interleaved on one cluster print exactly what the
+    reference printed for the same program (tests/golden/two_schedulers.txt)."""
+    exe = _compile("dropin_two_schedulers")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert p.returncode == 0, p.stderr
+    with open(os.path.join(ROOT, "tests", "golden", "two_schedulers.txt")) as f:
+        assert p.stdout == f.read()

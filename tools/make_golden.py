@@ -119,7 +119,25 @@ def scenarios(L):
     return sc
 
 
+def two_schedulers():
+    """tests/cpp/dropin_two_schedulers.cpp compiled against the reference headers and the
+    reference library (-Ddcpsim=dcpsim_ref); its stdout is the drop-in's expected output."""
+    import subprocess
+    import tempfile
+    ref = "/root/reference/proj"
+    with tempfile.TemporaryDirectory() as td:
+        exe = os.path.join(td, "two")
+        lib = os.path.join(ROOT, "oracle", "_ref")
+        subprocess.run(["/usr/bin/g++", "-std=c++20", "-O1", "-Ddcpsim=dcpsim_ref", f"-I{ref}/include",
+                        os.path.join(ROOT, "tests", "cpp", "dropin_two_schedulers.cpp"), "-o", exe, f"-L{lib}",
+                        "-ldcpsim_ref", f"-Wl,-rpath,{lib}", "-fopenmp"], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    with open(os.path.join(OUT, "two_schedulers.txt"), "w") as f:
+        f.write(out)
+
+
 def main():
+    two_schedulers()
     L = oracle_lib.reference()
     if L is None:
         raise SystemExit("build oracle/_ref first: make -C oracle")
