@@ -266,11 +266,8 @@ def run_ours(args, ws, rank, local):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     ctx = DcpContext(local)
-    lens = workload.cfg2_lengths()
-    b = workload.paged_batch(lens, HQ, HKV, D, PAGE)
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    pool = torch.randn(b.num_frames, 2, HKV, PAGE, D, generator=g, device=dev, dtype=torch.bfloat16)
-    q = torch.randn(64, HQ, D, generator=g, device=dev, dtype=torch.bfloat16)
+    # the exact tensors tests/test_attention_gpu.py::test_cfg2_full_size_all_shards checks
+    b, pool, q = workload.cfg2_bench_inputs(dev, seed=1234 + rank)
     bt = torch.from_numpy(b.block_table).to(dev)
     cu = torch.from_numpy(b.cu_pages).to(dev)
     sl = torch.from_numpy(b.shard_len).to(dev)

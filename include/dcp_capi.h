@@ -48,7 +48,8 @@ enum {
     DCP_E_CONFIG = -7,               /* dcpsim::ConfigError          */
     DCP_E_INVALID_ARG = -8,          /* bad pointer / size at the ABI */
     DCP_E_UNSUPPORTED = -9,          /* shape not compiled in         */
-    DCP_E_CUDA = -10                 /* CUDA runtime / driver failure  */
+    DCP_E_CUDA = -10,                /* CUDA runtime / driver failure  */
+    DCP_E_TIMEOUT = -11              /* an exchange flag wait timed out (peer lost / out of step) */
 };
 
 DCP_API const char* dcp_last_error(void);
@@ -120,6 +121,14 @@ typedef struct dcp_attn_args {
 DCP_API size_t dcp_attn_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards, int32_t num_q_heads,
                                 int32_t head_dim);
 DCP_API int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* args, void* stream);
+
+/* K1-f32: the same call in fp32 — the reference's production precision
+ * (shard_attention<float> / lse_merge<float>, attn_merge.cpp:64-77; SPEC.md:380
+ * rel <= 1e-5).  q fp32 [num_shards][num_q_heads][128], kv_pool fp32
+ * [frames][2][num_kv_heads][page_size][128] (16-byte aligned); any page_size
+ * 1..255; num_kv_heads <= 8, group in {1, 2, 4, 8}.  CUDA-core fp32 FMAs and
+ * expf / logf throughout (no reduced-precision step).  Same workspace. */
+DCP_API int dcp_splitkv_decode_attn_f32(dcp_ctx* ctx, const dcp_attn_args* args, void* stream);
 
 /* Number of kernel launches the last dcp_splitkv_decode_attn issued (for the
  * bench's gpu_launches accounting). */
@@ -276,20 +285,35 @@ DCP_API int dcp_planner_last_launches(const dcp_planner* pl);
  * the Res-route put fused into its epilogue (dcp_decode_attn_routed), 4 LSE
  * merge at the MoE binding (dcp_merge_partials; math of lse_merge,
  * attn_merge.hpp:86-100, in kv_binding order, zero-token shards weight 0).
- * Pools per instance (one allocation, exported by CUDA IPC for peers):
- *   q_recv [n_max][HQ][D] bf16 + flags, res [m_max][W][HQ][D] fp32 + LSE + flags.
- * Local buffers: q_local [m_max][HQ][D] bf16 (queries of the requests
- * MoE-bound here, in M-row order), out [m_max][HQ][D] fp32 + out_lse.
- * Flags carry a per-step epoch (dcp_xchg_begin_step), so graph replay needs no
- * reset.  All instances must call begin_step once per step. */
+ * Pools per instance (one allocation, exported by CUDA IPC for peers), each
+ * buffer twice (selected by the step epoch's parity):
+ *   q_recv [n_max][HQ][q_dim] (bf16 or fp32) + flags,
+ *   res [m_max][W][HQ][o_dim] fp32 + LSE [m_max][W][HQ] + flags, and a "done" word.
+ * Local buffers: q_local [m_max][HQ][q_dim] (queries of the requests MoE-bound
+ * here, in M-row order), out [m_max][HQ][o_dim] fp32 + out_lse.
+ * Step protocol: flags carry a per-step epoch, so graph replay needs no reset.
+ * All instances call dcp_xchg_begin_step once per step; it waits (on the
+ * device) until every peer has begun the previous step, so no instance runs
+ * more than one step ahead and the parity buffers are never overwritten while
+ * a peer still reads them.  Every flag wait is bounded by timeout_ms: a lost or
+ * mis-epoched flag leaves an error in the instance (kernels still terminate)
+ * that dcp_xchg_status reports as DCP_E_TIMEOUT.
+ * Widths: bf16 GQA/MHA (q_dim = o_dim = head_dim, q_elem_bytes 2), fp32
+ * (q_elem_bytes 4, dcp_decode_attn_routed_f32), MLA (q_dim 576, o_dim 512,
+ * dcp_mla_decode_attn_routed).  hq * q_dim * q_elem_bytes must be a multiple
+ * of 16 and o_dim a multiple of 32. */
 typedef struct dcp_xchg dcp_xchg;
 typedef struct dcp_xchg_config {
     int32_t world;
     int32_t self;
     int32_t num_q_heads;
     int32_t head_dim;
-    int32_t n_max;   /* ShapeSpace n_max (routing.hpp:62-63) */
-    int32_t m_max;   /* ShapeSpace m_max */
+    int32_t n_max;        /* ShapeSpace n_max (routing.hpp:62-63) */
+    int32_t m_max;        /* ShapeSpace m_max */
+    int32_t q_dim;        /* Q width per head; 0 = head_dim */
+    int32_t o_dim;        /* partial-O width per head; 0 = head_dim */
+    int32_t q_elem_bytes; /* 2 (bf16) or 4 (fp32); 0 = 2 */
+    int32_t timeout_ms;   /* flag-wait bound; 0 = 10000 */
 } dcp_xchg_config;
 
 DCP_API int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* cfg, dcp_xchg** out);
@@ -311,7 +335,15 @@ DCP_API int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream);
  * q/out/lse/shard arrays are ignored. */
 DCP_API int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
                                    const dcp_attn_args* a, void* stream);
+/* K1-f32 routed: the fp32 variant of dcp_decode_attn_routed over an exchange
+ * created with q_elem_bytes 4 (fp32 Q rows); kv_pool fp32 as dcp_splitkv_decode_attn_f32. */
+DCP_API int dcp_decode_attn_routed_f32(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
+                                       const dcp_attn_args* a, void* stream);
 DCP_API int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream);
+/* Synchronizes the device and reports the exchange error word: DCP_OK, or
+ * DCP_E_TIMEOUT with info[0..3] = {code, where (site << 24 | peer << 16 | row),
+ * wanted flag value, last value seen}; the word is cleared.  info may be NULL. */
+DCP_API int dcp_xchg_status(dcp_xchg* x, uint32_t* info);
 
 /* ---- entry points backing the dcpsim C++ drop-in (include/dcpsim/) ---------- */
 /* Replace the active policy (SchedulerPolicy, scheduler.hpp:31-39).  The
@@ -388,8 +420,12 @@ typedef struct dcp_moe_config {
     int32_t topk;         /* <= 16 */
     int32_t num_experts;  /* multiple of world */
     int32_t m_max;        /* max tokens per instance (<= 1024) */
+    int32_t timeout_ms;   /* flag-wait bound; 0 = 10000 */
 } dcp_moe_config;
 
+/* Pools are double-buffered by step parity and fenced like dcp_xchg (every instance
+ * calls dcp_moe_begin_step once per step; no instance runs more than one step ahead);
+ * waits are bounded, a timeout is reported by dcp_moe_status as DCP_E_TIMEOUT. */
 DCP_API int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* cfg, dcp_moe** out);
 DCP_API int dcp_moe_destroy(dcp_moe* x);
 DCP_API int dcp_moe_ipc_handle(dcp_moe* x, void* handle64);
@@ -397,23 +433,35 @@ DCP_API int dcp_moe_open_peer_ipc(dcp_moe* x, int32_t peer, const void* handle64
 DCP_API int dcp_moe_set_peer_local(dcp_moe* x, int32_t peer, const dcp_moe* other);
 DCP_API int dcp_moe_commit(dcp_moe* x);
 DCP_API int dcp_moe_begin_step(dcp_moe* x, void* stream);
+DCP_API int dcp_moe_status(dcp_moe* x, uint32_t* info);
 /* int32 per received row of meta_rows: src token, n_local, (expert, weight bits) * topk */
 DCP_API int32_t dcp_moe_meta_width(const dcp_moe* x);
-/* K4: x_local bf16 [M][hidden], topk_idx int32 [M][topk], topk_w fp32 [M][topk]
- * (device); *m_count_dev = M (e.g. dcp_instance_view.m_count_all + self). */
+/* K4: x_local bf16 [M][hidden] in M-row order, topk_idx int32 [M][topk], topk_w fp32
+ * [M][topk] (device); *m_count_dev = M, e.g. dcp_instance_view.m_count_all + self (K7's
+ * device M count, so the step needs no host round trip). */
 DCP_API int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* topk_idx,
                              const float* topk_w, const int32_t* m_count_dev, void* stream);
-/* K5a: wait for all sources; compact received rows into x_rows (bf16
- * [world*m_max][hidden]) and meta_rows (int32 [world*m_max][meta_width]);
- * copies the per-source counts to host `counts` and returns the row count. */
+/* K5a, region mode (the fast path): wait for every source; the received rows stay in
+ * this instance's pool, source s's rows at x_region[s * m_max + j], j < count[s]
+ * (meta likewise), for the expert stage to read in place.  Per-source counts and
+ * offsets stay on the device (dcp_moe_recv_counts_dev).  Graph-capturable. */
+DCP_API int dcp_moe_receive_regions(dcp_moe* x, void* stream);
+/* Parity of the current step (host mirror of the epoch) and the region pointers of a
+ * parity: bf16 [world][m_max][hidden], int32 [world][m_max][meta_width]. */
+DCP_API int32_t dcp_moe_parity(const dcp_moe* x);
+DCP_API int dcp_moe_regions(dcp_moe* x, int32_t parity, void** x_region, int32_t** meta_region);
+/* K5a, compact mode: wait, then copy the received rows into x_rows (bf16
+ * [world*m_max][hidden]) and meta_rows in (source, slot) order; returns the row count
+ * and copies the per-source counts to host `counts`. */
 DCP_API int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* counts,
                                 void* stream);
-/* K5a without the host read-back (stream-ordered, graph-capturable): the per-source
- * counts stay on the device at dcp_moe_recv_counts_dev(x) (int32 [world]). */
+/* compact mode without the host read-back (stream-ordered, graph-capturable) */
 DCP_API int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* stream);
 DCP_API const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x);
-/* K5b: y_rows bf16 [R][hidden] (same row order as receive) back to each token's home. */
+/* K5b: y rows back to each token's home; y_rows bf16 [R][hidden] in compact order, or
+ * y_region bf16 [world][m_max][hidden] in region order. */
 DCP_API int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream);
+DCP_API int dcp_moe_combine_put_regions(dcp_moe* x, const void* y_region, void* stream);
 /* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */
 DCP_API int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream);
 

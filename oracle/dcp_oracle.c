@@ -178,53 +178,97 @@ static double bf16_to_f64(uint16_t x) {
 /* shard_attention<double> (hpp:53-82) applied per (shard, q-head) to the keys
  * of a paged KV layout: the shard's tokens are the valid slots of its pages in
  * logical page order (page_table.cpp:9-49 lays pages out in token order). */
+/* Paged decode over a pool whose elements are bf16 (elem_bytes 2, widened exactly) or fp32
+ * (elem_bytes 4, the reference's production precision, attn_merge.cpp:64-77): per (shard,
+ * q-head) the reference's shard_attention<double> over the shard's tokens in page order. */
+static double elem_f64(const void* base, size_t i, int elem_bytes) {
+    if (elem_bytes == 4) return (double)((const float*)base)[i];
+    return bf16_to_f64(((const uint16_t*)base)[i]);
+}
+
+int dcpora_paged_decode_attn_any_f64(int nshards, int hq, int hkv, int d, int page_size, int elem_bytes,
+                                     const void* q_in, const void* pool_in, const int32_t* block_table,
+                                     const int32_t* cu_pages, const int64_t* shard_len, const uint8_t* page_fill,
+                                     double scale, double* out, double* lse, int threads) {
+    /* Streams the shard's pages instead of gathering them: per (shard, kv-head) every token's
+     * K and V rows are widened once and fed to the recurrence of each of the group's q-heads
+     * in token order -- per q-head the exact arithmetic sequence of shard_attention<double>
+     * (attn_merge.hpp:62-80, dcpora_shard_attention_f64), so results are bit-identical. */
+    const int group = hq / hkv;
+    const size_t head_elems = (size_t)page_size * d;
+    const size_t frame_elems = 2 * (size_t)hkv * head_elems;
+#pragma omp parallel for schedule(dynamic) num_threads(threads > 0 ? threads : 1)
+    for (int64_t w = 0; w < (int64_t)nshards * hkv; ++w) {
+        const int r = (int)(w / hkv), j = (int)(w % hkv);
+        const int p0 = cu_pages[r], p1 = cu_pages[r + 1];
+        double* qd = malloc(sizeof(double) * (size_t)group * d);
+        double* kd = malloc(sizeof(double) * d);
+        double* vd = malloc(sizeof(double) * d);
+        double* mx = malloc(sizeof(double) * group);
+        double* den = malloc(sizeof(double) * group);
+        for (int g = 0; g < group; ++g) {
+            const int h = j * group + g;
+            for (int i = 0; i < d; ++i) qd[(size_t)g * d + i] = elem_f64(q_in, ((size_t)r * hq + h) * d + i, elem_bytes);
+            double* o = out + ((size_t)r * hq + h) * d;
+            for (int i = 0; i < d; ++i) o[i] = 0.0;
+            mx[g] = -INFINITY;
+            den[g] = 0.0;
+        }
+        int64_t ntok = 0;
+        for (int p = p0; p < p1; ++p) {
+            const int64_t rem = shard_len[r] - (int64_t)(p - p0) * page_size;
+            const int fill = page_fill ? page_fill[p] : (int)(rem < page_size ? rem : page_size);
+            const size_t kp = (size_t)block_table[p] * frame_elems + (size_t)j * head_elems;
+            const size_t vp = kp + (size_t)hkv * head_elems;
+            for (int t = 0; t < fill; ++t, ++ntok) {
+                for (int i = 0; i < d; ++i) {
+                    kd[i] = elem_f64(pool_in, kp + (size_t)t * d + i, elem_bytes);
+                    vd[i] = elem_f64(pool_in, vp + (size_t)t * d + i, elem_bytes);
+                }
+                for (int g = 0; g < group; ++g) {
+                    const double* q = qd + (size_t)g * d;
+                    double* o = out + ((size_t)r * hq + j * group + g) * d;
+                    double sc = 0.0;
+                    for (int i = 0; i < d; ++i) sc += kd[i] * q[i];
+                    sc *= scale;
+                    if (sc > mx[g]) {
+                        const double shrink = exp(mx[g] - sc);
+                        den[g] *= shrink;
+                        for (int i = 0; i < d; ++i) o[i] *= shrink;
+                        mx[g] = sc;
+                    }
+                    const double wt = exp(sc - mx[g]);
+                    den[g] += wt;
+                    for (int i = 0; i < d; ++i) o[i] += wt * vd[i];
+                }
+            }
+        }
+        for (int g = 0; g < group; ++g) {
+            const int h = j * group + g;
+            double* o = out + ((size_t)r * hq + h) * d;
+            if (ntok == 0) {  /* zero-token shard: O = 0, LSE = -inf (weight 0 in any merge) */
+                lse[(size_t)r * hq + h] = -INFINITY;
+                continue;
+            }
+            for (int i = 0; i < d; ++i) o[i] /= den[g];
+            lse[(size_t)r * hq + h] = mx[g] + log(den[g]);
+        }
+        free(qd);
+        free(kd);
+        free(vd);
+        free(mx);
+        free(den);
+    }
+    return 0;
+}
+
 int dcpora_paged_decode_attn_f64(int nshards, int hq, int hkv, int d, int page_size,
                                  const uint16_t* q_bf16, const uint16_t* pool_bf16,
                                  const int32_t* block_table, const int32_t* cu_pages,
                                  const int64_t* shard_len, const uint8_t* page_fill, double scale,
                                  double* out, double* lse, int threads) {
-    const int group = hq / hkv;
-    const size_t head_elems = (size_t)page_size * d;
-    const size_t frame_elems = 2 * (size_t)hkv * head_elems;
-    int rc = 0;
-#pragma omp parallel for schedule(dynamic) num_threads(threads > 0 ? threads : 1) reduction(min : rc)
-    for (int64_t w = 0; w < (int64_t)nshards * hq; ++w) {
-        const int r = (int)(w / hq), h = (int)(w % hq), j = h / group;
-        double* o = out + ((size_t)r * hq + h) * d;
-        const int p0 = cu_pages[r], p1 = cu_pages[r + 1];
-        int64_t ntok = 0;
-        for (int p = p0; p < p1; ++p) {
-            const int64_t rem = shard_len[r] - (int64_t)(p - p0) * page_size;
-            ntok += page_fill ? page_fill[p] : (rem < page_size ? rem : page_size);
-        }
-        if (ntok == 0) {
-            for (int i = 0; i < d; ++i) o[i] = 0.0;
-            lse[(size_t)r * hq + h] = -INFINITY;
-            continue;
-        }
-        double* qd = malloc(sizeof(double) * d);
-        double* kd = malloc(sizeof(double) * (size_t)ntok * d);
-        double* vd = malloc(sizeof(double) * (size_t)ntok * d);
-        for (int i = 0; i < d; ++i) qd[i] = bf16_to_f64(q_bf16[((size_t)r * hq + h) * d + i]);
-        int64_t t = 0;
-        for (int p = p0; p < p1; ++p) {
-            const int64_t rem = shard_len[r] - (int64_t)(p - p0) * page_size;
-            const int fill = page_fill ? page_fill[p] : (int)(rem < page_size ? rem : page_size);
-            const uint16_t* kp = pool_bf16 + (size_t)block_table[p] * frame_elems + (size_t)j * head_elems;
-            const uint16_t* vp = kp + (size_t)hkv * head_elems;
-            for (int s = 0; s < fill; ++s, ++t)
-                for (int i = 0; i < d; ++i) {
-                    kd[(size_t)t * d + i] = bf16_to_f64(kp[(size_t)s * d + i]);
-                    vd[(size_t)t * d + i] = bf16_to_f64(vp[(size_t)s * d + i]);
-                }
-        }
-        const int e = dcpora_shard_attention_f64(qd, kd, vd, ntok, d, scale, o, lse + (size_t)r * hq + h);
-        rc = e < rc ? e : rc;
-        free(qd);
-        free(kd);
-        free(vd);
-    }
-    return rc;
+    return dcpora_paged_decode_attn_any_f64(nshards, hq, hkv, d, page_size, 2, q_bf16, pool_bf16, block_table,
+                                            cu_pages, shard_len, page_fill, scale, out, lse, threads);
 }
 
 /* MLA decode (K10).  The reference does not model MLA; this is

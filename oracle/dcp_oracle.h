@@ -79,6 +79,12 @@ int dcpora_world_dump_routing(void* h, char* buf, int64_t cap);
 int dcpora_world_instance_shards(void* h, int inst, int64_t* ids, int32_t* cu, int32_t* frames,
                                  int64_t* tokens, int cap_shards, int cap_frames);
 
+/* Same over bf16 (elem_bytes 2) or fp32 (elem_bytes 4) q / pool. */
+int dcpora_paged_decode_attn_any_f64(int nshards, int hq, int hkv, int d, int page_size, int elem_bytes,
+                                     const void* q, const void* pool, const int32_t* block_table,
+                                     const int32_t* cu_pages, const int64_t* shard_len, const uint8_t* page_fill,
+                                     double scale, double* out, double* lse, int threads);
+
 /* MoE layer oracle (no reference implementation exists: parity unpinned vs the
  * reference; this restatement is the definition the device K4/K5 path is
  * checked against).  Per token t:

@@ -60,10 +60,14 @@ class DcpCudaError(RuntimeError):
     pass
 
 
+class ExchangeTimeout(RuntimeError):
+    """A peer flag wait of the exchange / MoE pools timed out (DCP_E_TIMEOUT)."""
+
+
 _CODES = {
     -1: InsufficientFrames, -2: UnknownRequest, -3: UnknownPage, -4: InconsistentPlacement,
     -5: ShapeOverflow, -6: EmptyShard, -7: ConfigError, -8: DcpInvalidArgument,
-    -9: DcpUnsupported, -10: DcpCudaError,
+    -9: DcpUnsupported, -10: DcpCudaError, -11: ExchangeTimeout,
 }
 
 
@@ -111,12 +115,13 @@ class InstanceView(Structure):
 
 class MoeConfig(Structure):
     _fields_ = [("world", c_int32), ("self", c_int32), ("hidden", c_int32), ("topk", c_int32),
-                ("num_experts", c_int32), ("m_max", c_int32)]
+                ("num_experts", c_int32), ("m_max", c_int32), ("timeout_ms", c_int32)]
 
 
 class XchgConfig(Structure):
     _fields_ = [("world", c_int32), ("self", c_int32), ("num_q_heads", c_int32), ("head_dim", c_int32),
-                ("n_max", c_int32), ("m_max", c_int32)]
+                ("n_max", c_int32), ("m_max", c_int32), ("q_dim", c_int32), ("o_dim", c_int32),
+                ("q_elem_bytes", c_int32), ("timeout_ms", c_int32)]
 
 
 _lib = None
@@ -133,6 +138,7 @@ _SIGNATURES = [
     ("dcp_attn_workspace_bytes", c_size_t, [c_void_p, c_int32, c_int32, c_int32]),
     ("dcp_splitkv_decode_attn", c_int, [c_void_p, POINTER(AttnArgs), c_void_p]),
     ("dcp_attn_launches_per_call", c_int, []),
+    ("dcp_splitkv_decode_attn_f32", c_int, [c_void_p, POINTER(AttnArgs), c_void_p]),
     ("dcp_mla_workspace_bytes", c_size_t, [c_void_p, c_int32]),
     ("dcp_mla_decode_attn", c_int, [c_void_p, POINTER(MlaArgs), c_void_p]),
     ("dcp_mla_launches_per_call", c_int, []),
@@ -162,7 +168,9 @@ _SIGNATURES = [
     ("dcp_xchg_write_queries", c_int, [c_void_p, c_void_p, c_int32, c_void_p]),
     ("dcp_route_q", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
     ("dcp_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
+    ("dcp_decode_attn_routed_f32", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
     ("dcp_merge_partials", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
+    ("dcp_xchg_status", c_int, [c_void_p, c_void_p]),
     ("dcp_planner_set_policy", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32, c_int32]),
     ("dcp_planner_set_queue", c_int, [c_void_p, c_void_p, c_void_p, c_int32]),
     ("dcp_planner_ucp_rr", c_int, [c_void_p, c_void_p, c_int32, c_int32]),
@@ -189,6 +197,11 @@ _SIGNATURES = [
     ("dcp_moe_set_peer_local", c_int, [c_void_p, c_int32, c_void_p]),
     ("dcp_moe_commit", c_int, [c_void_p]),
     ("dcp_moe_begin_step", c_int, [c_void_p, c_void_p]),
+    ("dcp_moe_status", c_int, [c_void_p, c_void_p]),
+    ("dcp_moe_receive_regions", c_int, [c_void_p, c_void_p]),
+    ("dcp_moe_parity", c_int32, [c_void_p]),
+    ("dcp_moe_regions", c_int, [c_void_p, c_int32, POINTER(c_void_p), POINTER(c_void_p)]),
+    ("dcp_moe_combine_put_regions", c_int, [c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_meta_width", c_int32, [c_void_p]),
     ("dcp_moe_dispatch", c_int, [c_void_p] + [c_void_p] * 5),
     ("dcp_moe_receive", c_int32, [c_void_p] + [c_void_p] * 4),

@@ -56,8 +56,11 @@ class DecodeAttention:
     """
 
     def __init__(self, ctx: DcpContext, num_q_heads: int, num_kv_heads: int, head_dim: int = 128,
-                 page_size: int = 16, max_shards: int = 4096):
-        self.ctx = ctx
+                 page_size: int = 16, max_shards: int = 4096, dtype: str = "bf16"):
+        if dtype not in ("bf16", "f32"):
+            raise ValueError(f"dtype {dtype!r}")
+        self.ctx, self.dtype = ctx, dtype
+        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
         self.hq, self.hkv, self.d, self.page = num_q_heads, num_kv_heads, head_dim, page_size
         self.max_shards = max_shards
         nbytes = _capi.lib().dcp_attn_workspace_bytes(ctx.handle, max_shards, num_q_heads, head_dim)
@@ -70,7 +73,7 @@ class DecodeAttention:
         R = q.shape[0]
         if R > self.max_shards:
             raise _capi.DcpInvalidArgument(f"{R} shards > max_shards {self.max_shards}")
-        for name, t, dt in (("q", q, torch.bfloat16), ("kv_pool", kv_pool, torch.bfloat16),
+        for name, t, dt in (("q", q, self.tdtype), ("kv_pool", kv_pool, self.tdtype),
                             ("block_table", block_table, torch.int32),
                             ("cu_pages", cu_pages, torch.int32), ("shard_len", shard_len, torch.int64)):
             if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
@@ -95,8 +98,9 @@ class DecodeAttention:
 
     def launch(self, stream=None):
         s = stream if stream is not None else torch.cuda.current_stream(self.ctx.device)
-        _capi.check(_capi.lib().dcp_splitkv_decode_attn(self.ctx.handle, ctypes.byref(self.args),
-                                                        ctypes.c_void_p(s.cuda_stream)))
+        L = _capi.lib()
+        fn = L.dcp_splitkv_decode_attn if self.dtype == "bf16" else L.dcp_splitkv_decode_attn_f32
+        _capi.check(fn(self.ctx.handle, ctypes.byref(self.args), ctypes.c_void_p(s.cuda_stream)))
 
     def __call__(self, *args, stream=None, **kw):
         out, lse = self.prepare(*args, **kw)

@@ -7,6 +7,7 @@
 
 #include "capi_common.cuh"
 #include "splitkv_decode.cuh"
+#include "splitkv_decode_f32.cuh"
 #include "xchg_internal.cuh"
 
 namespace dcp {
@@ -282,8 +283,9 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     DCP_REQUIRE(v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW, "N %d > n_max %d", v->n_rows, x->cfg.n_max);
     DCP_REQUIRE(a->head_dim == 128 && (a->page_size == 16 || a->page_size == 32 || a->page_size == 64),
                 DCP_E_UNSUPPORTED, "head_dim/page_size");
-    DCP_REQUIRE(a->num_q_heads == x->cfg.num_q_heads && a->head_dim == x->cfg.head_dim, DCP_E_INVALID_ARG,
-                "exchange pool shape differs from the attention shape");
+    DCP_REQUIRE(a->num_q_heads == x->cfg.num_q_heads && a->head_dim == x->cfg.q_dim &&
+                    a->head_dim == x->cfg.o_dim && x->cfg.q_elem_bytes == 2,
+                DCP_E_INVALID_ARG, "exchange pool shape differs from the bf16 attention shape");
     DCP_REQUIRE(a->kv_pool && a->workspace && a->num_frames > 0, DCP_E_INVALID_ARG, "kv_pool/workspace");
     DCP_REQUIRE(a->num_kv_heads > 0 && a->num_q_heads % a->num_kv_heads == 0, DCP_E_INVALID_ARG, "heads");
     const size_t need = dcp_attn_workspace_bytes(ctx, x->cfg.n_max, a->num_q_heads, a->head_dim);
@@ -293,7 +295,7 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     int rc = kv_tensor_map(ctx, a->kv_pool, a->num_frames, a->num_kv_heads, a->head_dim, &map, split, a->page_size);
     if (rc) return rc;
     AttnParams prm{};
-    prm.q = reinterpret_cast<const __nv_bfloat16*>(x->pool + x->off_qrecv);
+    prm.q = nullptr;  // from the receive pool, by epoch parity
     prm.block_table = v->block_table;
     prm.cu_pages = v->cu_pages;
     prm.shard_len = v->shard_len;
@@ -312,10 +314,92 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     prm.xp = x->dev;
     prm.n_mrow = v->n_mrow;
     prm.n_moe = v->n_moe;
-    prm.q_flag = reinterpret_cast<const uint32_t*>(x->pool + x->off_qflag);
     prm.num_shards_ptr = v->n_count_dev;
     return dispatch_decode(ctx, map, prm, a->num_kv_heads, a->num_q_heads / a->num_kv_heads,
                            static_cast<cudaStream_t>(stream), a->page_size);
+}
+
+// ---- K1-f32 ------------------------------------------------------------------------------
+
+static int launch_f32(dcp_ctx* ctx, const AttnF32Params& prm, int G, cudaStream_t s) {
+    const dim3 block(prm.hkv * 32);
+    switch (G) {
+        case 1: splitkv_decode_f32_kernel<1><<<ctx->num_sms, block, 0, s>>>(prm); break;
+        case 2: splitkv_decode_f32_kernel<2><<<ctx->num_sms, block, 0, s>>>(prm); break;
+        case 4: splitkv_decode_f32_kernel<4><<<ctx->num_sms, block, 0, s>>>(prm); break;
+        case 8: splitkv_decode_f32_kernel<8><<<ctx->num_sms, block, 0, s>>>(prm); break;
+        default: set_error("fp32 path: group %d (compiled 1, 2, 4, 8)", G); return DCP_E_UNSUPPORTED;
+    }
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+static int f32_common(dcp_ctx* ctx, const dcp_attn_args* a, AttnF32Params& prm) {
+    DCP_REQUIRE(a->head_dim == 128, DCP_E_UNSUPPORTED, "head_dim %d (compiled: 128)", a->head_dim);
+    DCP_REQUIRE(a->num_kv_heads >= 1 && a->num_kv_heads <= 8 && a->num_q_heads % a->num_kv_heads == 0,
+                DCP_E_UNSUPPORTED, "fp32 path: num_kv_heads %d (1..8), num_q_heads %d", a->num_kv_heads,
+                a->num_q_heads);
+    DCP_REQUIRE(a->page_size >= 1 && a->page_size <= 255, DCP_E_UNSUPPORTED, "page_size %d", a->page_size);
+    DCP_REQUIRE(a->kv_pool && a->workspace && a->num_frames > 0, DCP_E_INVALID_ARG, "kv_pool/workspace");
+    DCP_REQUIRE((reinterpret_cast<uintptr_t>(a->kv_pool) & 15) == 0, DCP_E_INVALID_ARG,
+                "kv_pool must be 16-byte aligned");
+    prm.kv = static_cast<const float*>(a->kv_pool);
+    char* ws = static_cast<char*>(a->workspace);
+    const size_t slots = 2 * static_cast<size_t>(ctx->num_sms);
+    prm.ws_acc = reinterpret_cast<float*>(ws);
+    ws += slots * a->num_q_heads * a->head_dim * sizeof(float);
+    prm.ws_ml = reinterpret_cast<float*>(ws);
+    ws += slots * a->num_q_heads * 2 * sizeof(float);
+    prm.counters = reinterpret_cast<int32_t*>(ws);
+    prm.hkv = a->num_kv_heads;
+    prm.page = a->page_size;
+    prm.scale = a->scale;
+    return DCP_OK;
+}
+
+int dcp_splitkv_decode_attn_f32(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) {
+    DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");
+    DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
+    if (a->num_shards == 0) return DCP_OK;
+    DCP_REQUIRE(a->q && a->block_table && a->cu_pages && a->shard_len && a->out && a->lse, DCP_E_INVALID_ARG,
+                "NULL device pointer in dcp_attn_args");
+    const size_t need = dcp_attn_workspace_bytes(ctx, a->num_shards, a->num_q_heads, a->head_dim);
+    DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu bytes", a->workspace_bytes,
+                need);
+    AttnF32Params prm{};
+    if (int rc = f32_common(ctx, a, prm)) return rc;
+    prm.q = static_cast<const float*>(a->q);
+    prm.block_table = a->block_table;
+    prm.cu_pages = a->cu_pages;
+    prm.shard_len = a->shard_len;
+    prm.page_fill = a->page_fill;
+    prm.out = a->out;
+    prm.lse = a->lse;
+    prm.num_shards = a->num_shards;
+    return launch_f32(ctx, prm, a->num_q_heads / a->num_kv_heads, static_cast<cudaStream_t>(stream));
+}
+
+int dcp_decode_attn_routed_f32(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
+                               void* stream) {
+    DCP_REQUIRE(ctx && x && v && a, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    DCP_REQUIRE(v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW, "N %d > n_max %d", v->n_rows, x->cfg.n_max);
+    DCP_REQUIRE(a->num_q_heads == x->cfg.num_q_heads && a->head_dim == x->cfg.q_dim && a->head_dim == x->cfg.o_dim &&
+                    x->cfg.q_elem_bytes == 4,
+                DCP_E_INVALID_ARG, "exchange pool shape differs from the fp32 attention shape");
+    const size_t need = dcp_attn_workspace_bytes(ctx, x->cfg.n_max, a->num_q_heads, a->head_dim);
+    DCP_REQUIRE(a->workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu", a->workspace_bytes, need);
+    AttnF32Params prm{};
+    if (int rc = f32_common(ctx, a, prm)) return rc;
+    prm.block_table = v->block_table;
+    prm.cu_pages = v->cu_pages;
+    prm.shard_len = v->shard_len;
+    prm.page_fill = v->page_fill;
+    prm.xp = x->dev;
+    prm.n_mrow = v->n_mrow;
+    prm.n_moe = v->n_moe;
+    prm.num_shards_ptr = v->n_count_dev;
+    return launch_f32(ctx, prm, a->num_q_heads / a->num_kv_heads, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -12,29 +12,20 @@ struct dcp_moe {
     dcp_ctx* ctx = nullptr;
     dcp_moe_config cfg{};
     char* pool = nullptr;
-    size_t off_x = 0, off_meta = 0, off_flag = 0, off_cnt = 0, off_cb = 0, off_cbf = 0;
     char* local = nullptr;
     MoePeers host{};
     MoePeers* dev = nullptr;
     uint32_t* epoch = nullptr;
-    int32_t* slot_tbl = nullptr;
-    int32_t* row_src = nullptr;
-    int32_t* counts = nullptr;
+    uint32_t* err = nullptr;
+    uint32_t host_epoch = 0;           // mirror of the device epoch (begin_step calls)
     const int32_t* m_count_dev = nullptr;
-    const int32_t* meta_rows = nullptr;
+    bool received = false;
     void* opened[PL_MAXW] = {};
 };
 
 namespace {
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
-void fill(dcp_moe* x, int peer, char* base) {
-    x->host.rx_x[peer] = reinterpret_cast<__nv_bfloat16*>(base + x->off_x);
-    x->host.rx_meta[peer] = reinterpret_cast<int32_t*>(base + x->off_meta);
-    x->host.rx_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_flag);
-    x->host.rx_count[peer] = reinterpret_cast<int32_t*>(base + x->off_cnt);
-    x->host.cb_y[peer] = reinterpret_cast<__nv_bfloat16*>(base + x->off_cb);
-    x->host.cb_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_cbf);
-}
+size_t dispatch_smem(const dcp_moe* x) { return (size_t)x->cfg.m_max * (x->cfg.world + 1) * 4; }
 }  // namespace
 
 extern "C" {
@@ -48,48 +39,66 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     DCP_REQUIRE(c->num_experts >= c->world && c->num_experts % c->world == 0, DCP_E_CONFIG,
                 "num_experts must be a multiple of world");
     DCP_REQUIRE(c->m_max >= 1 && c->m_max <= 1024, DCP_E_UNSUPPORTED, "m_max %d (<= 1024)", c->m_max);
+    DCP_REQUIRE(c->timeout_ms >= 0, DCP_E_INVALID_ARG, "timeout_ms");
     DCP_CUDA_TRY(cudaSetDevice(ctx->device));
     auto* x = new dcp_moe();
     x->ctx = ctx;
     x->cfg = *c;
+    if (x->cfg.timeout_ms == 0) x->cfg.timeout_ms = 10000;
     const size_t W = c->world, H = c->hidden, m = c->m_max, meta = 2 + 2 * c->topk;
+    MoePeers& h = x->host;
+    h.sz_rx_x = al(W * m * H * 2);
+    h.sz_rx_meta = al(W * m * meta * 4);
+    h.sz_rx_cnt = al(W * 16);
+    h.sz_rx_arr = al(W * 4);
+    h.sz_cb_y = al(m * W * H * 2);
+    h.sz_cb_arr = al(W * 4);
     size_t o = 0;
-    x->off_x = o;    o = al(o + W * m * H * 2);
-    x->off_meta = o; o = al(o + W * m * meta * 4);
-    x->off_flag = o; o = al(o + W * 4);
-    x->off_cnt = o;  o = al(o + W * 4);
-    x->off_cb = o;   o = al(o + m * W * H * 2);
-    x->off_cbf = o;  o = al(o + W * 4);
+    h.off_rx_x = o;    o += 2 * h.sz_rx_x;
+    h.off_rx_meta = o; o += 2 * h.sz_rx_meta;
+    h.off_rx_cnt = o;  o += 2 * h.sz_rx_cnt;
+    h.off_rx_arr = o;  o += 2 * h.sz_rx_arr;
+    h.off_cb_y = o;    o += 2 * h.sz_cb_y;
+    h.off_cb_arr = o;  o += 2 * h.sz_cb_arr;
+    h.off_done = o;    o += 256;
     DCP_CUDA_TRY(cudaMalloc(&x->pool, o));
     DCP_CUDA_TRY(cudaMemset(x->pool, 0, o));
     size_t l = 0;
     const size_t o_ep = l;   l = al(l + 4);
+    const size_t o_err = l;  l = al(l + 16);
     const size_t o_dev = l;  l = al(l + sizeof(MoePeers));
     const size_t o_slot = l; l = al(l + m * W * 4);
-    const size_t o_src = l;  l = al(l + W * m * 4);
+    const size_t o_cs = l;   l = al(l + 2 * W * 4);
+    const size_t o_ct = l;   l = al(l + 2 * W * 4);
     const size_t o_cnt = l;  l = al(l + W * 4);
-    const size_t o_dd = l;   l = al(l + W * 4);
-    const size_t o_cd = l;   l = al(l + W * 4);
+    const size_t o_off = l;  l = al(l + (W + 1) * 4);
     DCP_CUDA_TRY(cudaMalloc(&x->local, l));
     DCP_CUDA_TRY(cudaMemset(x->local, 0, l));
     x->epoch = reinterpret_cast<uint32_t*>(x->local + o_ep);
+    x->err = reinterpret_cast<uint32_t*>(x->local + o_err);
     x->dev = reinterpret_cast<MoePeers*>(x->local + o_dev);
-    x->slot_tbl = reinterpret_cast<int32_t*>(x->local + o_slot);
-    x->row_src = reinterpret_cast<int32_t*>(x->local + o_src);
-    x->counts = reinterpret_cast<int32_t*>(x->local + o_cnt);
-    x->host.W = c->world;
-    x->host.self = c->self;
-    x->host.H = c->hidden;
-    x->host.topk = c->topk;
-    x->host.e_per_rank = c->num_experts / c->world;
-    x->host.m_max = c->m_max;
-    x->host.meta = (int32_t)meta;
-    x->host.epoch = x->epoch;
-    x->host.disp_done = reinterpret_cast<int32_t*>(x->local + o_dd);
-    x->host.cb_done = reinterpret_cast<int32_t*>(x->local + o_cd);
-    static const int max_chunks = [] { const char* e = std::getenv("DCP_MOE_CHUNKS"); return e ? std::atoi(e) : 128; }();
-    x->host.chunks = static_cast<int32_t>(m < max_chunks ? m : max_chunks);
-    fill(x, c->self, x->pool);
+    h.W = c->world;
+    h.self = c->self;
+    h.H = c->hidden;
+    h.topk = c->topk;
+    h.e_per_rank = c->num_experts / c->world;
+    h.m_max = c->m_max;
+    h.meta = (int32_t)meta;
+    h.epoch = x->epoch;
+    h.wc.err = x->err;
+    h.wc.timeout_ns = static_cast<uint64_t>(x->cfg.timeout_ms) * 1000000ull;
+    h.slot_tbl = reinterpret_cast<int32_t*>(x->local + o_slot);
+    h.cum_sent = reinterpret_cast<uint32_t*>(x->local + o_cs);
+    h.cb_target = reinterpret_cast<uint32_t*>(x->local + o_ct);
+    h.counts = reinterpret_cast<int32_t*>(x->local + o_cnt);
+    h.offs = reinterpret_cast<int32_t*>(x->local + o_off);
+    // one wave of CTAs for K4 / K5b (a CTA per token / per received row beyond that)
+    h.chunks = ctx->num_sms;
+    h.base[c->self] = x->pool;
+    const size_t sm = dispatch_smem(x);
+    if (sm > 48 * 1024)
+        DCP_CUDA_TRY(cudaFuncSetAttribute(moe_dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(sm)));
     *out = x;
     return DCP_OK;
 }
@@ -114,19 +123,21 @@ int dcp_moe_ipc_handle(dcp_moe* x, void* h64) {
 
 int dcp_moe_open_peer_ipc(dcp_moe* x, int32_t peer, const void* h64) {
     DCP_REQUIRE(x && h64 && peer >= 0 && peer < x->cfg.world && peer != x->cfg.self, DCP_E_INVALID_ARG, "peer");
+    DCP_CUDA_TRY(cudaSetDevice(x->ctx->device));
     cudaIpcMemHandle_t h;
     std::memcpy(&h, h64, 64);
     void* base = nullptr;
     DCP_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
     x->opened[peer] = base;
-    fill(x, peer, static_cast<char*>(base));
+    x->host.base[peer] = static_cast<char*>(base);
     return DCP_OK;
 }
 
 int dcp_moe_set_peer_local(dcp_moe* x, int32_t peer, const dcp_moe* other) {
     DCP_REQUIRE(x && other && peer >= 0 && peer < x->cfg.world, DCP_E_INVALID_ARG, "peer");
     DCP_REQUIRE(x->cfg.hidden == other->cfg.hidden && x->cfg.topk == other->cfg.topk &&
-                    x->cfg.m_max == other->cfg.m_max && x->cfg.world == other->cfg.world,
+                    x->cfg.m_max == other->cfg.m_max && x->cfg.world == other->cfg.world &&
+                    x->cfg.num_experts == other->cfg.num_experts,
                 DCP_E_INVALID_ARG, "peer pool shapes differ");
     if (other->ctx->device != x->ctx->device) {
         cudaError_t e = cudaDeviceEnablePeerAccess(other->ctx->device, 0);
@@ -136,25 +147,51 @@ int dcp_moe_set_peer_local(dcp_moe* x, int32_t peer, const dcp_moe* other) {
         }
         cudaGetLastError();
     }
-    fill(x, peer, other->pool);
+    x->host.base[peer] = other->pool;
     return DCP_OK;
 }
 
 int dcp_moe_commit(dcp_moe* x) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    for (int s = 0; s < x->cfg.world; ++s) DCP_REQUIRE(x->host.rx_x[s], DCP_E_INVALID_ARG, "peer %d not set", s);
+    for (int s = 0; s < x->cfg.world; ++s) DCP_REQUIRE(x->host.base[s], DCP_E_INVALID_ARG, "peer %d not set", s);
     DCP_CUDA_TRY(cudaMemcpy(x->dev, &x->host, sizeof(MoePeers), cudaMemcpyHostToDevice));
     return DCP_OK;
 }
 
 int dcp_moe_begin_step(dcp_moe* x, void* stream) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    epoch_bump_kernel_moe<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(x->epoch);
+    moe_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->dev);
     DCP_CUDA_TRY(cudaGetLastError());
+    ++x->host_epoch;
+    x->received = false;
     return DCP_OK;
 }
 
+int dcp_moe_status(dcp_moe* x, uint32_t* info) {
+    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_CUDA_TRY(cudaSetDevice(x->ctx->device));
+    DCP_CUDA_TRY(cudaDeviceSynchronize());
+    uint32_t e[4];
+    DCP_CUDA_TRY(cudaMemcpy(e, x->err, sizeof(e), cudaMemcpyDeviceToHost));
+    if (info) std::memcpy(info, e, sizeof(e));
+    if (e[0] == XERR_NONE) return DCP_OK;
+    DCP_CUDA_TRY(cudaMemset(x->err, 0, sizeof(e)));
+    set_error("MoE exchange wait timed out: site %u peer %u row %u, wanted %u, saw %u", e[1] >> 24,
+              (e[1] >> 16) & 0xff, e[1] & 0xffff, e[2], e[3]);
+    return DCP_E_TIMEOUT;
+}
+
 int32_t dcp_moe_meta_width(const dcp_moe* x) { return x ? 2 + 2 * x->cfg.topk : 0; }
+
+int32_t dcp_moe_parity(const dcp_moe* x) { return x ? static_cast<int32_t>(x->host_epoch & 1) : 0; }
+
+int dcp_moe_regions(dcp_moe* x, int32_t parity, void** x_region, int32_t** meta_region) {
+    DCP_REQUIRE(x && (parity == 0 || parity == 1), DCP_E_INVALID_ARG, "bad argument");
+    if (x_region) *x_region = x->pool + x->host.off_rx_x + parity * x->host.sz_rx_x;
+    if (meta_region)
+        *meta_region = reinterpret_cast<int32_t*>(x->pool + x->host.off_rx_meta + parity * x->host.sz_rx_meta);
+    return DCP_OK;
+}
 
 int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const float* w, const int32_t* m_count,
                      void* stream) {
@@ -162,9 +199,17 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
     DCP_REQUIRE(x && m_count, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
-    moe_dispatch_kernel<<<dim3(x->host.chunks, x->cfg.world), 128, 0, s>>>(
-        x->dev, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, x->slot_tbl);
+    moe_dispatch_kernel<<<x->host.chunks, MOE_THREADS, dispatch_smem(x), s>>>(
+        x->dev, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count);
     DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+int dcp_moe_receive_regions(dcp_moe* x, void* stream) {
+    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
+    moe_receive_counts_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->dev);
+    DCP_CUDA_TRY(cudaGetLastError());
+    x->received = true;
     return DCP_OK;
 }
 
@@ -174,28 +219,19 @@ int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* st
     const int rows = x->cfg.world * x->cfg.m_max;
     int grid = rows;  // up to one CTA per received row (warp groups per row, moe.cuh)
     if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
-    moe_receive_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
-                                            x->counts);
+    moe_receive_compact_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows);
     DCP_CUDA_TRY(cudaGetLastError());
-    x->meta_rows = meta_rows;
+    x->received = true;
     return DCP_OK;
 }
 
-const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x) { return x ? x->counts : nullptr; }
+const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x) { return x ? x->host.counts : nullptr; }
 
 int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* counts, void* stream) {
-    DCP_REQUIRE(x && x_rows && meta_rows, DCP_E_INVALID_ARG, "NULL argument");
+    if (int rc = dcp_moe_receive_async(x, x_rows, meta_rows, stream)) return rc;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    // one CTA per received row, at most W * m_max rows
-    const int rows = x->cfg.world * x->cfg.m_max;
-    int grid = rows;  // up to one CTA per received row (warp groups per row, moe.cuh)
-    if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
-    moe_receive_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows, x->row_src,
-                                            x->counts);
-    DCP_CUDA_TRY(cudaGetLastError());
-    x->meta_rows = meta_rows;
     int32_t c[PL_MAXW];
-    DCP_CUDA_TRY(cudaMemcpyAsync(c, x->counts, x->cfg.world * 4, cudaMemcpyDeviceToHost, s));
+    DCP_CUDA_TRY(cudaMemcpyAsync(c, x->host.counts, x->cfg.world * 4, cudaMemcpyDeviceToHost, s));
     DCP_CUDA_TRY(cudaStreamSynchronize(s));
     int32_t R = 0;
     for (int i = 0; i < x->cfg.world; ++i) {
@@ -205,19 +241,25 @@ int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* c
     return R;
 }
 
-int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream) {
-    DCP_REQUIRE(x && y_rows && x->meta_rows, DCP_E_INVALID_ARG, "call dcp_moe_receive first");
-    moe_combine_put_kernel<<<dim3(x->host.chunks, x->cfg.world), 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, static_cast<const __nv_bfloat16*>(y_rows), x->meta_rows, x->counts);
+static int combine_put(dcp_moe* x, const void* y, int region, void* stream) {
+    DCP_REQUIRE(x && y && x->received, DCP_E_INVALID_ARG, "call a dcp_moe_receive* first");
+    moe_combine_put_kernel<<<x->host.chunks, MOE_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+        x->dev, static_cast<const __nv_bfloat16*>(y), region);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
+}
+
+int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream) { return combine_put(x, y_rows, 0, stream); }
+
+int dcp_moe_combine_put_regions(dcp_moe* x, const void* y_region, void* stream) {
+    return combine_put(x, y_region, 1, stream);
 }
 
 int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {
     DCP_REQUIRE(x && out && x->m_count_dev, DCP_E_INVALID_ARG, "call dcp_moe_dispatch first");
     const int groups = x->cfg.hidden / 4;  // hidden % 8 == 0
     moe_combine_reduce_kernel<<<dim3(x->cfg.m_max, (groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, x->m_count_dev, x->slot_tbl, out);
+        x->dev, x->m_count_dev, out);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }

@@ -12,43 +12,54 @@ namespace {
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-void fill_peer(dcp_xchg* x, int peer, char* base) {
-    x->host.qrecv[peer] = reinterpret_cast<__nv_bfloat16*>(base + x->off_qrecv);
-    x->host.qflag[peer] = reinterpret_cast<uint32_t*>(base + x->off_qflag);
-    x->host.res_o[peer] = reinterpret_cast<float*>(base + x->off_res_o);
-    x->host.res_lse[peer] = reinterpret_cast<float*>(base + x->off_res_lse);
-    x->host.res_flag[peer] = reinterpret_cast<uint32_t*>(base + x->off_res_flag);
-}
-
 }  // namespace
 
 extern "C" {
 
-int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c, dcp_xchg** out) {
-    DCP_REQUIRE(ctx && c && out, DCP_E_INVALID_ARG, "NULL argument");
-    DCP_REQUIRE(c->world >= 1 && c->world <= PL_MAXW, DCP_E_UNSUPPORTED, "world %d", c->world);
-    DCP_REQUIRE(c->self >= 0 && c->self < c->world, DCP_E_INVALID_ARG, "self %d", c->self);
-    DCP_REQUIRE(c->head_dim % 32 == 0 && c->num_q_heads > 0, DCP_E_UNSUPPORTED, "head_dim %d", c->head_dim);
-    DCP_REQUIRE(c->n_max > 0 && c->m_max > 0, DCP_E_INVALID_ARG, "n_max/m_max");
+int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c0, dcp_xchg** out) {
+    DCP_REQUIRE(ctx && c0 && out, DCP_E_INVALID_ARG, "NULL argument");
+    dcp_xchg_config c = *c0;
+    if (c.q_dim == 0) c.q_dim = c.head_dim;
+    if (c.o_dim == 0) c.o_dim = c.head_dim;
+    if (c.q_elem_bytes == 0) c.q_elem_bytes = 2;
+    if (c.timeout_ms == 0) c.timeout_ms = 10000;
+    DCP_REQUIRE(c.world >= 1 && c.world <= PL_MAXW, DCP_E_UNSUPPORTED, "world %d", c.world);
+    DCP_REQUIRE(c.self >= 0 && c.self < c.world, DCP_E_INVALID_ARG, "self %d", c.self);
+    DCP_REQUIRE(c.num_q_heads > 0 && c.q_dim > 0 && c.o_dim > 0 && c.o_dim % 32 == 0, DCP_E_UNSUPPORTED,
+                "o_dim %d (multiple of 32)", c.o_dim);
+    DCP_REQUIRE(c.q_elem_bytes == 2 || c.q_elem_bytes == 4, DCP_E_UNSUPPORTED, "q_elem_bytes %d", c.q_elem_bytes);
+    DCP_REQUIRE((size_t)c.num_q_heads * c.q_dim * c.q_elem_bytes % 16 == 0, DCP_E_UNSUPPORTED,
+                "query rows must be a multiple of 16 bytes");
+    DCP_REQUIRE(c.n_max > 0 && c.m_max > 0, DCP_E_INVALID_ARG, "n_max/m_max");
+    DCP_REQUIRE(c.timeout_ms > 0, DCP_E_INVALID_ARG, "timeout_ms");
     DCP_CUDA_TRY(cudaSetDevice(ctx->device));
     auto* x = new dcp_xchg();
     x->ctx = ctx;
-    x->cfg = *c;
-    const size_t W = c->world, hq = c->num_q_heads, d = c->head_dim, n = c->n_max, m = c->m_max;
+    x->cfg = c;
+    const size_t W = c.world, hq = c.num_q_heads, n = c.n_max, m = c.m_max;
+    const size_t qrow = hq * c.q_dim * c.q_elem_bytes;
+    XchgPeers& h = x->host;
+    h.sz_qrecv = align256(n * qrow);
+    h.sz_qflag = align256(n * 4);
+    h.sz_res_o = align256(m * W * hq * c.o_dim * 4);
+    h.sz_res_lse = align256(m * W * hq * 4);
+    h.sz_res_flag = align256(m * W * 4);
     size_t o = 0;
-    x->off_qrecv = o;    o = align256(o + n * hq * d * 2);
-    x->off_qflag = o;    o = align256(o + n * 4);
-    x->off_res_o = o;    o = align256(o + m * W * hq * d * 4);
-    x->off_res_lse = o;  o = align256(o + m * W * hq * 4);
-    x->off_res_flag = o; o = align256(o + m * W * 4);
+    h.off_qrecv = o;    o += 2 * h.sz_qrecv;
+    h.off_qflag = o;    o += 2 * h.sz_qflag;
+    h.off_res_o = o;    o += 2 * h.sz_res_o;
+    h.off_res_lse = o;  o += 2 * h.sz_res_lse;
+    h.off_res_flag = o; o += 2 * h.sz_res_flag;
+    h.off_done = o;     o += 256;
     x->pool_bytes = o;
     DCP_CUDA_TRY(cudaMalloc(&x->pool, x->pool_bytes));
     DCP_CUDA_TRY(cudaMemset(x->pool, 0, x->pool_bytes));
     size_t lb = 0;
-    const size_t off_q = lb;   lb = align256(lb + m * hq * d * 2);
-    const size_t off_out = lb; lb = align256(lb + m * hq * d * 4);
+    const size_t off_q = lb;   lb = align256(lb + m * qrow);
+    const size_t off_out = lb; lb = align256(lb + m * hq * c.o_dim * 4);
     const size_t off_lse = lb; lb = align256(lb + m * hq * 4);
     const size_t off_ep = lb;  lb = align256(lb + 4);
+    const size_t off_err = lb; lb = align256(lb + 16);
     const size_t off_dev = lb; lb = align256(lb + sizeof(XchgPeers));
     DCP_CUDA_TRY(cudaMalloc(&x->local, lb));
     DCP_CUDA_TRY(cudaMemset(x->local, 0, lb));
@@ -56,15 +67,20 @@ int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c, dcp_xchg** out) {
     x->out = reinterpret_cast<float*>(x->local + off_out);
     x->out_lse = reinterpret_cast<float*>(x->local + off_lse);
     x->epoch = reinterpret_cast<uint32_t*>(x->local + off_ep);
+    x->err = reinterpret_cast<uint32_t*>(x->local + off_err);
     x->dev = reinterpret_cast<XchgPeers*>(x->local + off_dev);
-    x->host.W = c->world;
-    x->host.self = c->self;
-    x->host.hq = c->num_q_heads;
-    x->host.d = c->head_dim;
-    x->host.n_max = c->n_max;
-    x->host.m_max = c->m_max;
-    x->host.epoch = x->epoch;
-    fill_peer(x, c->self, x->pool);
+    h.W = c.world;
+    h.self = c.self;
+    h.hq = c.num_q_heads;
+    h.q_dim = c.q_dim;
+    h.o_dim = c.o_dim;
+    h.q_bytes = c.q_elem_bytes;
+    h.n_max = c.n_max;
+    h.m_max = c.m_max;
+    h.epoch = x->epoch;
+    h.wc.err = x->err;
+    h.wc.timeout_ns = static_cast<uint64_t>(c.timeout_ms) * 1000000ull;
+    h.base[c.self] = x->pool;
     *out = x;
     return DCP_OK;
 }
@@ -91,19 +107,22 @@ int dcp_xchg_ipc_handle(dcp_xchg* x, void* handle64) {
 int dcp_xchg_open_peer_ipc(dcp_xchg* x, int32_t peer, const void* handle64) {
     DCP_REQUIRE(x && handle64, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(peer >= 0 && peer < x->cfg.world && peer != x->cfg.self, DCP_E_INVALID_ARG, "peer %d", peer);
+    DCP_CUDA_TRY(cudaSetDevice(x->ctx->device));
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle64, 64);
     void* base = nullptr;
     DCP_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
     x->opened[peer] = base;
-    fill_peer(x, peer, static_cast<char*>(base));
+    x->host.base[peer] = static_cast<char*>(base);
     return DCP_OK;
 }
 
 int dcp_xchg_set_peer_local(dcp_xchg* x, int32_t peer, const dcp_xchg* other) {
     DCP_REQUIRE(x && other, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(peer >= 0 && peer < x->cfg.world, DCP_E_INVALID_ARG, "peer %d", peer);
-    DCP_REQUIRE(std::memcmp(&x->cfg.num_q_heads, &other->cfg.num_q_heads, 4 * sizeof(int32_t)) == 0 &&
+    DCP_REQUIRE(x->cfg.num_q_heads == other->cfg.num_q_heads && x->cfg.n_max == other->cfg.n_max &&
+                    x->cfg.m_max == other->cfg.m_max && x->cfg.q_dim == other->cfg.q_dim &&
+                    x->cfg.o_dim == other->cfg.o_dim && x->cfg.q_elem_bytes == other->cfg.q_elem_bytes &&
                     x->cfg.world == other->cfg.world,
                 DCP_E_INVALID_ARG, "peer pool shapes differ");
     if (other->ctx->device != x->ctx->device) {
@@ -114,29 +133,43 @@ int dcp_xchg_set_peer_local(dcp_xchg* x, int32_t peer, const dcp_xchg* other) {
         }
         cudaGetLastError();
     }
-    fill_peer(x, peer, other->pool);
+    x->host.base[peer] = other->pool;
     return DCP_OK;
 }
 
 int dcp_xchg_commit(dcp_xchg* x) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
     for (int s = 0; s < x->cfg.world; ++s)
-        DCP_REQUIRE(x->host.qrecv[s] != nullptr, DCP_E_INVALID_ARG, "peer %d not set", s);
+        DCP_REQUIRE(x->host.base[s] != nullptr, DCP_E_INVALID_ARG, "peer %d not set", s);
     DCP_CUDA_TRY(cudaMemcpy(x->dev, &x->host, sizeof(XchgPeers), cudaMemcpyHostToDevice));
     return DCP_OK;
 }
 
 int dcp_xchg_begin_step(dcp_xchg* x, void* stream) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    epoch_bump_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(x->epoch);
+    xchg_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->dev);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
+}
+
+int dcp_xchg_status(dcp_xchg* x, uint32_t* info) {
+    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_CUDA_TRY(cudaSetDevice(x->ctx->device));
+    DCP_CUDA_TRY(cudaDeviceSynchronize());
+    uint32_t e[4];
+    DCP_CUDA_TRY(cudaMemcpy(e, x->err, sizeof(e), cudaMemcpyDeviceToHost));
+    if (info) std::memcpy(info, e, sizeof(e));
+    if (e[0] == XERR_NONE) return DCP_OK;
+    DCP_CUDA_TRY(cudaMemset(x->err, 0, sizeof(e)));
+    set_error("exchange flag wait timed out: site %u peer %u row %u, wanted %u, saw %u", e[1] >> 24,
+              (e[1] >> 16) & 0xff, e[1] & 0xffff, e[2], e[3]);
+    return DCP_E_TIMEOUT;
 }
 
 int dcp_xchg_buffers(dcp_xchg* x, void** q_local, void** q_recv, float** out, float** out_lse) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
     if (q_local) *q_local = x->q_local;
-    if (q_recv) *q_recv = x->pool + x->off_qrecv;
+    if (q_recv) *q_recv = x->pool + x->host.off_qrecv;  // parity 0
     if (out) *out = x->out;
     if (out_lse) *out_lse = x->out_lse;
     return DCP_OK;
@@ -146,7 +179,7 @@ int dcp_xchg_write_queries(dcp_xchg* x, const void* q_rows, int32_t rows, void* 
     DCP_REQUIRE(x && (rows == 0 || q_rows), DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(rows >= 0 && rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "rows %d > m_max %d", rows,
                 x->cfg.m_max);
-    const size_t bytes = (size_t)rows * x->cfg.num_q_heads * x->cfg.head_dim * 2;
+    const size_t bytes = (size_t)rows * x->cfg.num_q_heads * x->cfg.q_dim * x->cfg.q_elem_bytes;
     if (bytes)
         DCP_CUDA_TRY(cudaMemcpyAsync(x->q_local, q_rows, bytes, cudaMemcpyDeviceToDevice,
                                      static_cast<cudaStream_t>(stream)));
@@ -161,8 +194,8 @@ int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
     DCP_REQUIRE(v->m_rows <= x->cfg.m_max && v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW,
                 "execution shape (%d,%d) exceeds the exchange pools (%d,%d)", v->m_rows, v->n_rows, x->cfg.m_max,
                 x->cfg.n_max);
-    q_route_put_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, static_cast<const __nv_bfloat16*>(x->q_local), v->m_count_all, v->m_nrow);
+    q_route_put_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(x->dev, x->q_local,
+                                                                                  v->m_count_all, v->m_nrow);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
@@ -199,9 +232,8 @@ int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
         const int mh = std::min(g->m_hat[i], x->cfg.m_max);
         cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
         if (e == cudaSuccess) {
-            epoch_bump_kernel<<<1, 1, 0, cs>>>(x->epoch);
-            q_route_put_kernel<<<mh, 128, 0, cs>>>(x->dev, static_cast<const __nv_bfloat16*>(x->q_local),
-                                                  v->m_count_all, v->m_nrow);
+            xchg_begin_step_kernel<<<1, 32, 0, cs>>>(x->dev);
+            q_route_put_kernel<<<mh, 128, 0, cs>>>(x->dev, x->q_local, v->m_count_all, v->m_nrow);
             rc = dcp_decode_attn_routed(ctx, x, v, a, cs);
             lse_merge_kernel<<<mh, 128, 0, cs>>>(x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
             e = cudaStreamEndCapture(cs, &g->graph[i]);

@@ -5,58 +5,75 @@
 
 namespace dcp {
 
-static __global__ void epoch_bump_kernel(uint32_t* epoch) { *epoch += 1; }
+// begin_step: the step fence of exchange.cuh, then the epoch bump.  One warp.
+static __global__ void __launch_bounds__(32) xchg_begin_step_kernel(const XchgPeers* __restrict__ xp) {
+    const XchgPeers& x = *xp;
+    step_fence(x.epoch, [&](int s) { return xdone(x, s); }, x.W, x.self, x.wc);
+}
 
-// K2: grid = m_max (graph-stable), block = 128.  q_local: [m_max][hq][d] bf16
-// in M-row order; m_nrow: [M][W] destination rows (-1 = not in P_r).
+// K2: grid = m_max (graph-stable), block = 128.  q_local: [m_max][hq][q_dim] x q_bytes
+// in M-row order; m_nrow: [M][W] destination rows (-1 = not in P_r).  The payload is
+// moved as 16-byte vectors whatever its element type (bf16 Q, fp32 Q, MLA's 576-wide Q).
 static __global__ void __launch_bounds__(128) q_route_put_kernel(const XchgPeers* __restrict__ xp,
-                                                          const __nv_bfloat16* __restrict__ q_local,
-                                                          const int32_t* __restrict__ m_count,
-                                                          const int32_t* __restrict__ m_nrow) {
+                                                                 const void* __restrict__ q_local,
+                                                                 const int32_t* __restrict__ m_count,
+                                                                 const int32_t* __restrict__ m_nrow) {
     const int r = blockIdx.x;
     const XchgPeers& x = *xp;
     if (r >= m_count[x.self]) return;
     const uint32_t ep = *x.epoch;
     const int W = x.W;
-    const int vecs = x.hq * x.d / 8;  // 16-byte vectors per query row
-    const uint4* src = reinterpret_cast<const uint4*>(q_local + (size_t)r * x.hq * x.d);
+    const size_t row_bytes = (size_t)x.hq * x.q_dim * x.q_bytes;
+    const int vecs = static_cast<int>(row_bytes / 16);
+    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(q_local) + r * row_bytes);
+    constexpr int U = 4;
     for (int s = 0; s < W; ++s) {
         const int row = m_nrow[(size_t)r * W + s];
         if (row < 0) continue;
-        uint4* dst = reinterpret_cast<uint4*>(x.qrecv[s] + (size_t)row * x.hq * x.d);
-        for (int i = threadIdx.x; i < vecs; i += blockDim.x) dst[i] = __ldg(src + i);
+        uint4* dst = reinterpret_cast<uint4*>(xq_recv(x, s, ep) + row * row_bytes);
+        for (int b = threadIdx.x; b < vecs; b += U * blockDim.x) {
+            uint4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b + u * blockDim.x < vecs) v[u] = __ldg(src + b + u * blockDim.x);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (b + u * blockDim.x < vecs) dst[b + u * blockDim.x] = v[u];
+        }
         __syncthreads();
-        if (threadIdx.x == 0) st_release_sys(x.qflag[s] + row, ep);
+        if (threadIdx.x == 0) st_release_sys(xq_flag(x, s, ep) + row, ep);
     }
 }
 
-// K3 merge: grid = m_max, block = 128.  m_k / m_kv: P_r of each M row in
-// kv_binding order.  out: [m_max][hq][d] fp32, out_lse: [m_max][hq].
+// K3 merge: grid = m_max, block = 128.  m_k / m_kv: P_r of each M row in kv_binding
+// order.  out: [m_max][hq][o_dim] fp32, out_lse: [m_max][hq].  Weights follow lse_merge
+// (attn_merge.hpp:86-100): w_k = exp(lse_k - max lse), out = sum w_k o_k / sum w_k, folded
+// in kv_binding order; an empty shard (lse = -inf) has weight 0.
 static __global__ void __launch_bounds__(128) lse_merge_kernel(const XchgPeers* __restrict__ xp,
-                                                        const int32_t* __restrict__ m_count,
-                                                        const int32_t* __restrict__ m_k,
-                                                        const int32_t* __restrict__ m_kv,
-                                                        float* __restrict__ out,
-                                                        float* __restrict__ out_lse) {
+                                                               const int32_t* __restrict__ m_count,
+                                                               const int32_t* __restrict__ m_k,
+                                                               const int32_t* __restrict__ m_kv,
+                                                               float* __restrict__ out,
+                                                               float* __restrict__ out_lse) {
     const int r = blockIdx.x;
     const XchgPeers& x = *xp;
     if (r >= m_count[x.self]) return;
     const uint32_t ep = *x.epoch;
-    const int W = x.W, hq = x.hq, d = x.d;
+    const int W = x.W, hq = x.hq, d = x.o_dim;
     const int k = m_k[r];
     __shared__ int32_t parts[PL_MAXK];
     if (threadIdx.x < k) {
         const int s = m_kv[(size_t)r * PL_MAXK + threadIdx.x];
         parts[threadIdx.x] = s;
-        wait_flag(x.res_flag[x.self] + (size_t)r * W + s, ep);
+        wait_flag(xres_flag(x, x.self, ep) + (size_t)r * W + s, ep, x.wc,
+                  (SITE_K3_RES << 24) | (s << 16) | (r & 0xffff));
     }
     __syncthreads();
-    const float* po = x.res_o[x.self] + (size_t)r * W * hq * d;
-    const float* pl = x.res_lse[x.self] + (size_t)r * W * hq;
-    const float L2E = 1.4426950408889634f;
-    const int quarters = d / 32;  // 32 floats per work item
-    for (int w = threadIdx.x; w < hq * quarters; w += blockDim.x) {
-        const int h = w / quarters, q0 = (w % quarters) * 32;
+    const float* po = xres_o(x, x.self, ep) + (size_t)r * W * hq * d;
+    const float* pl = xres_lse(x, x.self, ep) + (size_t)r * W * hq;
+    const int chunks = d / 32;  // 32 floats per work item
+    for (int w = threadIdx.x; w < hq * chunks; w += blockDim.x) {
+        const int h = w / chunks, q0 = (w % chunks) * 32;
         float mx = -INFINITY;
         for (int i = 0; i < k; ++i) mx = fmaxf(mx, __ldcg(pl + (size_t)parts[i] * hq + h));
         float acc[32];
@@ -66,7 +83,7 @@ static __global__ void __launch_bounds__(128) lse_merge_kernel(const XchgPeers* 
         for (int i = 0; i < k; ++i) {
             const int s = parts[i];
             const float l = __ldcg(pl + (size_t)s * hq + h);
-            const float wgt = l == -INFINITY ? 0.f : exp2f((l - mx) * L2E);
+            const float wgt = l == -INFINITY ? 0.f : expf(l - mx);
             den += wgt;
             const float4* v = reinterpret_cast<const float4*>(po + ((size_t)s * hq + h) * d + q0);
 #pragma unroll

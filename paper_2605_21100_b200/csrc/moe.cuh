@@ -9,22 +9,34 @@
 // known a priori from the gating, so there is no runtime handshake
 // (PAPER.md:869).
 //
-//   K4  moe_dispatch   CTAs (chunk, destination rank): a block-wide ballot prefix
-//                      over the tokens gives each (token, rank) its slot in the
-//                      peer's per-source region; 16-byte stores of the hidden
-//                      states routed to that rank (+ expert ids / weights); the
-//                      last chunk CTA of a destination publishes the count and one
-//                      (source -> destination) flag (st.release.sys = epoch) after
-//                      every chunk's system fence: W flags per instance and step.
-//   K5a moe_receive    wait for counts and slots from every source, compact the
-//                      received rows (source order, slot order) for the expert
-//                      GEMMs.
-//   K5b combine_put    CTAs (chunk, home rank): each expert rank returns the
-//                      gate-weighted sum over its local experts (bf16) to the
-//                      token's home slot [t][rank]; one (rank -> home) flag per
-//                      home, published like K4b's.
-//   K5c combine_reduce at home: wait for every rank's flag, sum the per-rank
-//                      partials in ascending rank (= ascending expert) order into fp32.
+//   K4  moe_dispatch   every CTA derives the layout (each token's destination
+//                      ranks, its slot in each destination's per-source region)
+//                      from the gating in shared memory; CTA c then sends tokens
+//                      c, c + C, ...: the hidden state is loaded ONCE into
+//                      registers and stored to every destination rank it is
+//                      routed to (16-byte vectors, remote NVLink stores on a
+//                      multi-GPU node).  Completion: each CTA adds the rows it
+//                      landed at a destination to that destination's arrival
+//                      counter with one red.release.sys per (CTA, destination);
+//                      CTA 0 publishes the count record {epoch, count} and the
+//                      cumulative row target.  No ticket, no per-row flag, no
+//                      system fence chain.
+//   K5a moe_receive    wait, per source, for the count record and for the
+//                      arrival counter to reach its target; the rows stay in
+//                      the pool's per-source regions [W][m_max][H] (the expert
+//                      stage reads them there), or are compacted (legacy
+//                      dcp_moe_receive).
+//   K5b combine_put    CTAs over the received rows return y rows (gate-weighted
+//                      sums over this rank's experts) to the token's home slot
+//                      [t][rank]; arrival counted like K4.
+//   K5c combine_reduce at home: wait for every rank's counter to reach the rows it
+//                      owes (known from the home's own gating), sum the per-rank
+//                      partials in ascending rank (= ascending expert) order, fp32.
+//
+// Counters are cumulative per (parity, source) and never reset: a waiter compares
+// against a cumulative target in serial-number order, so any number of CTAs can
+// wait on them.  Buffers are double-buffered by the step epoch's parity and the
+// step fence of exchange.cuh keeps every instance within one step of its peers.
 #pragma once
 
 #include <cstdint>
@@ -36,161 +48,238 @@
 namespace dcp {
 
 constexpr int MOE_MAXK = 16;
+constexpr int MOE_THREADS = 256;
 
 struct MoePeers {
     int32_t W, self, H, topk, e_per_rank, m_max, meta;  // meta = 2 + 2*topk int32 per row
     uint32_t* epoch;
-    __nv_bfloat16* rx_x[PL_MAXW];      // [W src][m_max][H]
-    int32_t* rx_meta[PL_MAXW];         // [W src][m_max][meta]: src token, n_local, (expert, weight bits)*
-    uint32_t* rx_flag[PL_MAXW];        // [W src]: all of src's rows for this rank have landed
-    int32_t* rx_count[PL_MAXW];        // [W src]
-    __nv_bfloat16* cb_y[PL_MAXW];      // [m_max][W dst][H]
-    uint32_t* cb_flag[PL_MAXW];        // [W dst]: all of dst's partials for this home have landed
-    int32_t* disp_done;                // [W dst] local: dispatch chunk CTAs finished (self-resetting)
-    int32_t* cb_done;                  // [W home] local: combine chunk CTAs finished (self-resetting)
-    int32_t chunks;                    // CTAs per destination / home rank
+    WaitCtl wc;
+    char* base[PL_MAXW];
+    // pool layout, per parity p (at off_* + p * sz_*):
+    //   rx_x     [W src][m_max][H] bf16
+    //   rx_meta  [W src][m_max][meta] int32: src token, n_local, (expert, weight bits) * n_local
+    //   rx_cnt   [W src][2] u64: {epoch << 32 | count}, cumulative row target
+    //   rx_arr   [W src] u32 cumulative rows landed
+    //   cb_y     [m_max][W rank][H] bf16
+    //   cb_arr   [W rank] u32 cumulative rows landed
+    //   done     u32 (step fence)
+    uint64_t off_rx_x, off_rx_meta, off_rx_cnt, off_rx_arr, off_cb_y, off_cb_arr, off_done;
+    uint64_t sz_rx_x, sz_rx_meta, sz_rx_cnt, sz_rx_arr, sz_cb_y, sz_cb_arr;
+    // local
+    int32_t* slot_tbl;     // [m_max][W] home: token t's slot at rank d, -1 = not routed there
+    uint32_t* cum_sent;    // [2][W] rows sent to each destination, per parity (cumulative)
+    uint32_t* cb_target;   // [2][W] rows each rank owes this home, per parity (cumulative)
+    int32_t* counts;       // [W] rows received from each source this step
+    int32_t* offs;         // [W + 1] exclusive prefix of counts
+    int32_t chunks;        // CTAs of K4 / K5b
 };
 
-// Copy one row of `nvec` 16-byte vectors with the block, UNROLL loads in flight per thread
-// before their stores (a row copy is latency-bound otherwise).
-template <int UNROLL = 4, bool CG = false>
-__device__ __forceinline__ void copy_row(uint4* __restrict__ dst, const uint4* __restrict__ src, int nvec) {
-    for (int base = threadIdx.x; base < nvec; base += UNROLL * blockDim.x) {
-        uint4 v[UNROLL];
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const int i = base + u * blockDim.x;
-            if (i < nvec) v[u] = CG ? __ldcg(src + i) : __ldg(src + i);
-        }
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) {
-            const int i = base + u * blockDim.x;
-            if (i < nvec) dst[i] = v[u];
-        }
-    }
+template <class T>
+__device__ __forceinline__ T* mp_at(const MoePeers& p, int s, uint64_t off, uint64_t sz, uint32_t ep) {
+    return reinterpret_cast<T*>(p.base[s] + off + (ep & 1) * sz);
+}
+__device__ __forceinline__ __nv_bfloat16* rx_x(const MoePeers& p, int s, uint32_t ep) {
+    return mp_at<__nv_bfloat16>(p, s, p.off_rx_x, p.sz_rx_x, ep);
+}
+__device__ __forceinline__ int32_t* rx_meta(const MoePeers& p, int s, uint32_t ep) {
+    return mp_at<int32_t>(p, s, p.off_rx_meta, p.sz_rx_meta, ep);
+}
+__device__ __forceinline__ unsigned long long* rx_cnt(const MoePeers& p, int s, uint32_t ep) {
+    return mp_at<unsigned long long>(p, s, p.off_rx_cnt, p.sz_rx_cnt, ep);
+}
+__device__ __forceinline__ uint32_t* rx_arr(const MoePeers& p, int s, uint32_t ep) {
+    return mp_at<uint32_t>(p, s, p.off_rx_arr, p.sz_rx_arr, ep);
+}
+__device__ __forceinline__ __nv_bfloat16* cb_y(const MoePeers& p, int s, uint32_t ep) {
+    return mp_at<__nv_bfloat16>(p, s, p.off_cb_y, p.sz_cb_y, ep);
+}
+__device__ __forceinline__ uint32_t* cb_arr(const MoePeers& p, int s, uint32_t ep) {
+    return mp_at<uint32_t>(p, s, p.off_cb_arr, p.sz_cb_arr, ep);
+}
+__device__ __forceinline__ uint32_t* moe_done(const MoePeers& p, int s) {
+    return reinterpret_cast<uint32_t*>(p.base[s] + p.off_done);
 }
 
-// Chunk CTA epilogue: after this CTA's stores, the last of `chunks` CTAs publishes `flag`.
-// Every CTA fences system-wide before its ticket, so the last one's release covers all.
-__device__ __forceinline__ void moe_chunk_done(int32_t* done, int chunks, uint32_t* flag, uint32_t ep) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        if (atomicAdd(done, 1) == chunks - 1) {
-            atomicExch(done, 0);
-            st_release_sys(flag, ep);
-        }
-    }
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
-// K4: CTA (chunk c, destination d).  Every CTA of destination d scans the tokens (block-wide
-// ballot prefix) for their slots in d's region; chunk c sends tokens t = c, c + chunks, ...
-// routed to d; the last chunk CTA publishes the count and one (source -> d) flag.  Chunk 0
-// also records the slot table for the combine.
-static __global__ void __launch_bounds__(128) moe_dispatch_kernel(const MoePeers* __restrict__ mp,
-                                                                  const __nv_bfloat16* __restrict__ x,
-                                                                  const int32_t* __restrict__ topk_idx,
-                                                                  const float* __restrict__ topk_w,
-                                                                  const int32_t* __restrict__ m_count,
-                                                                  int32_t* __restrict__ slot_tbl) {
-    __shared__ int32_t wsum[4];
-    __shared__ int16_t mine_t[1024], mine_s[1024];
-    __shared__ int32_t n_mine;
+// Wait for source s's count record of epoch ep and for all of its rows; returns the count.
+__device__ __forceinline__ int moe_wait_source(const MoePeers& p, int s, uint32_t ep) {
+    const unsigned long long* rec = rx_cnt(p, p.self, ep) + 2 * s;
+    const uint32_t where = (SITE_MOE_RX << 24) | (s << 16);
+    unsigned long long a = 0;
+    wait_until(
+        [&](uint32_t& seen) {
+            a = ld_acquire_sys_u64(rec);
+            seen = static_cast<uint32_t>(a >> 32);
+            return seen == ep;
+        },
+        ep, p.wc, where);
+    const uint32_t target = static_cast<uint32_t>(__ldcg(rec + 1));
+    wait_flag(rx_arr(p, p.self, ep) + s, target, p.wc, where | 0x8000u, true);
+    return static_cast<int>(a & 0xffffffffu);
+}
+
+static __global__ void __launch_bounds__(32) moe_begin_step_kernel(const MoePeers* __restrict__ mp) {
     const MoePeers& p = *mp;
-    const int d = blockIdx.y, c = blockIdx.x, M = *m_count;
+    step_fence(p.epoch, [&](int s) { return moe_done(p, s); }, p.W, p.self, p.wc);
+}
+
+// K4.  grid = chunks, block = MOE_THREADS; dynamic smem = m_max * (W + 1) * 4 bytes.
+static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const MoePeers* __restrict__ mp,
+                                                                          const __nv_bfloat16* __restrict__ x,
+                                                                          const int32_t* __restrict__ topk_idx,
+                                                                          const float* __restrict__ topk_w,
+                                                                          const int32_t* __restrict__ m_count) {
+    extern __shared__ int32_t sm[];
+    const MoePeers& p = *mp;
+    const int W = p.W, H = p.H, K = p.topk, M = *m_count;
+    int32_t* s_mask = sm;               // [M] destination-rank bitmask of each token
+    int32_t* s_slot = sm + p.m_max;     // [M][W] slot at each destination (-1 = not routed)
+    __shared__ int32_t s_count[PL_MAXW], s_sent[PL_MAXW];
     const uint32_t ep = *p.epoch;
-    const int W = p.W, H = p.H, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) n_mine = 0;
-    __syncthreads();  // the scan loop below holds the other barriers, and it is empty when M == 0
-    int carry = 0;
-    for (int t0 = 0; t0 < M; t0 += blockDim.x) {
-        const int t = t0 + threadIdx.x;
-        bool routed = false;
-        if (t < M)
-            for (int j = 0; j < p.topk; ++j) routed |= topk_idx[t * p.topk + j] / p.e_per_rank == d;
-        const unsigned bal = __ballot_sync(0xffffffffu, routed);
-        if (lane == 0) wsum[warp] = __popc(bal);
-        __syncthreads();
-        int base = carry;
-        for (int w = 0; w < warp; ++w) base += wsum[w];
-        const int slot = base + __popc(bal & ((1u << lane) - 1u));
-        if (t < M && c == 0) slot_tbl[t * W + d] = routed ? slot : -1;
-        if (routed && t % p.chunks == c) {
-            const int k = atomicAdd(&n_mine, 1);
-            mine_t[k] = static_cast<int16_t>(t);
-            mine_s[k] = static_cast<int16_t>(slot);
-        }
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) carry += wsum[w];
-        __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int NW = MOE_THREADS / 32;
+    for (int t = tid; t < M; t += MOE_THREADS) {
+        uint32_t m = 0;
+        for (int j = 0; j < K; ++j) m |= 1u << (__ldg(topk_idx + t * K + j) / p.e_per_rank);
+        s_mask[t] = static_cast<int32_t>(m);
     }
-    for (int k = 0; k < n_mine; ++k) {
-        const int t = mine_t[k], slot = mine_s[k];
-        const size_t row = (size_t)p.self * p.m_max + slot;
-        copy_row(reinterpret_cast<uint4*>(p.rx_x[d] + row * H), reinterpret_cast<const uint4*>(x + (size_t)t * H), H / 8);
-        if (threadIdx.x == 0) {
-            int32_t* meta = p.rx_meta[d] + row * p.meta;
+    if (tid < PL_MAXW) s_sent[tid] = 0;
+    __syncthreads();
+    // slots: warp d scans the tokens for destination d (ballot prefix, ascending token order)
+    for (int d = warp; d < W; d += NW) {
+        int carry = 0;
+        for (int t0 = 0; t0 < M; t0 += 32) {
+            const int t = t0 + lane;
+            const bool r = t < M && ((s_mask[t] >> d) & 1);
+            const unsigned b = __ballot_sync(0xffffffffu, r);
+            if (t < M) s_slot[t * W + d] = r ? carry + __popc(b & ((1u << lane) - 1u)) : -1;
+            carry += __popc(b);
+        }
+        if (lane == 0) s_count[d] = carry;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0) {
+        for (int i = tid; i < M * W; i += MOE_THREADS) p.slot_tbl[i] = s_slot[i];
+        if (tid < W) {
+            const int d = tid, c = s_count[d];
+            // the home expects c combine rows back from rank d (K5c); rank d gets c rows from us
+            p.cb_target[(ep & 1) * W + d] += c;
+            const uint32_t cum = (p.cum_sent[(ep & 1) * W + d] += c);
+            unsigned long long* rec = rx_cnt(p, d, ep) + 2 * p.self;
+            __stcg(rec + 1, static_cast<unsigned long long>(cum));
+            st_release_sys_u64(rec, (static_cast<unsigned long long>(ep) << 32) | static_cast<uint32_t>(c));
+        }
+    }
+    // rows: CTA c sends tokens c, c + C, ...; each token's hidden state is read once and
+    // stored to all of its destination ranks.
+    const int nvec = H / 8;
+    constexpr int VPT = 4;  // 16-byte vectors in registers per thread per pass (4 x 256 x 16 B = 16 KB)
+    for (int t = blockIdx.x; t < M; t += gridDim.x) {
+        const uint32_t mask = static_cast<uint32_t>(s_mask[t]);
+        const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * H);
+        for (int v0 = 0; v0 < nvec; v0 += VPT * MOE_THREADS) {
+            uint4 v[VPT];
+#pragma unroll
+            for (int u = 0; u < VPT; ++u) {
+                const int i = v0 + u * MOE_THREADS + tid;
+                if (i < nvec) v[u] = __ldg(src + i);
+            }
+            for (uint32_t mm = mask; mm; mm &= mm - 1) {
+                const int d = __ffs(mm) - 1;
+                const size_t row = (size_t)p.self * p.m_max + s_slot[t * W + d];
+                uint4* dst = reinterpret_cast<uint4*>(rx_x(p, d, ep) + row * H);
+#pragma unroll
+                for (int u = 0; u < VPT; ++u) {
+                    const int i = v0 + u * MOE_THREADS + tid;
+                    if (i < nvec) dst[i] = v[u];
+                }
+            }
+        }
+        // meta rows: lane d of warp 0 writes destination d's
+        if (tid < W && ((mask >> tid) & 1)) {
+            const int d = tid;
+            int32_t* meta = rx_meta(p, d, ep) + ((size_t)p.self * p.m_max + s_slot[t * W + d]) * p.meta;
             int n = 0;
-            for (int j = 0; j < p.topk; ++j) {
-                const int e = topk_idx[t * p.topk + j];
+            for (int j = 0; j < K; ++j) {
+                const int e = __ldg(topk_idx + t * K + j);
                 if (e / p.e_per_rank != d) continue;
                 meta[2 + 2 * n] = e;
-                meta[3 + 2 * n] = __float_as_int(topk_w[t * p.topk + j]);
+                meta[3 + 2 * n] = __float_as_int(__ldg(topk_w + t * K + j));
                 ++n;
             }
             meta[0] = t;
             meta[1] = n;
+            ++s_sent[d];
         }
     }
-    // last chunk: count, then the flag (covers every chunk's rows, see moe_chunk_done)
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        if (atomicAdd(p.disp_done + d, 1) == p.chunks - 1) {
-            atomicExch(p.disp_done + d, 0);
-            p.rx_count[d][p.self] = carry;
-            st_release_sys(p.rx_flag[d] + p.self, ep);
-        }
-    }
+    // one release per (CTA, destination) covers every row this CTA stored there
+    if (tid < W && s_sent[tid]) red_release_sys_add(rx_arr(p, tid, ep) + p.self, s_sent[tid]);
 }
 
-// K5a: wait for every source, compact received rows in (source, slot) order.  Grid-wide:
-// every CTA derives the per-source offsets from the published counts, then its warp groups
-// copy rows r = group_global, + total_groups, ...
-static __global__ void __launch_bounds__(256) moe_receive_kernel(const MoePeers* __restrict__ mp,
-                                                                 __nv_bfloat16* __restrict__ x_rows,
-                                                                 int32_t* __restrict__ meta_rows,
-                                                                 int32_t* __restrict__ row_src,
-                                                                 int32_t* __restrict__ counts) {
+// K5a (region mode): one warp; lane s waits for source s, then counts and offsets.
+static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const MoePeers* __restrict__ mp) {
+    const MoePeers& p = *mp;
+    const uint32_t ep = *p.epoch;
+    const int lane = threadIdx.x;
+    int c = 0;
+    if (lane < p.W) c = moe_wait_source(p, lane, ep);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane < p.W) {
+        p.counts[lane] = c;
+        p.offs[lane + 1] = incl;
+    }
+    if (lane == 0) p.offs[0] = 0;
+}
+
+// K5a (compact mode, legacy dcp_moe_receive): every CTA waits for every source, then warp
+// groups copy rows r = group_global, + total_groups, ... in (source, slot) order.
+static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const MoePeers* __restrict__ mp,
+                                                                         __nv_bfloat16* __restrict__ x_rows,
+                                                                         int32_t* __restrict__ meta_rows) {
     __shared__ int32_t cnt[PL_MAXW], off[PL_MAXW + 1];
     const MoePeers& p = *mp;
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H;
-    if (threadIdx.x < W) {
-        wait_flag(p.rx_flag[p.self] + threadIdx.x, ep);
-        cnt[threadIdx.x] = *((volatile int32_t*)p.rx_count[p.self] + threadIdx.x);
-    }
+    if (threadIdx.x < W) cnt[threadIdx.x] = moe_wait_source(p, threadIdx.x, ep);
     __syncthreads();
     if (threadIdx.x == 0) {
         off[0] = 0;
         for (int s = 0; s < W; ++s) off[s + 1] = off[s] + cnt[s];
-        if (blockIdx.x == 0)
-            for (int s = 0; s < W; ++s) counts[s] = cnt[s];
+        if (blockIdx.x == 0) {
+            for (int s = 0; s < W; ++s) p.counts[s] = cnt[s];
+            for (int s = 0; s <= W; ++s) p.offs[s] = off[s];
+        }
     }
     __syncthreads();
     const int R = off[W];
-    // a group of wpr warps per row, wpr ~ vectors / 128 (capped at the CTA's 8 warps): a
-    // 7,168-wide row (896 vectors) takes the whole CTA and is in flight at once, a 2,048-wide
-    // row two warps (one warp per row took H / 1,024 dependent load rounds)
     const int nvec = H / 8;
     const int wpr = nvec > 512 ? 8 : nvec > 256 ? 4 : nvec > 128 ? 2 : 1;
     const int gsz = 32 * wpr, groups = (blockDim.x >> 5) / wpr;
     const int grp = (threadIdx.x >> 5) / wpr, gt = threadIdx.x % gsz;
+    const __nv_bfloat16* rx = rx_x(p, p.self, ep);
+    const int32_t* rm = rx_meta(p, p.self, ep);
     for (int r = blockIdx.x * groups + grp; r < R; r += gridDim.x * groups) {
         int s = 0;
         while (off[s + 1] <= r) ++s;
-        const int slot = r - off[s];
-        const size_t row = (size_t)s * p.m_max + slot;
-        const uint4* src = reinterpret_cast<const uint4*>(p.rx_x[p.self] + row * H);
+        const size_t row = (size_t)s * p.m_max + (r - off[s]);
+        const uint4* src = reinterpret_cast<const uint4*>(rx + row * H);
         uint4* dst = reinterpret_cast<uint4*>(x_rows + (size_t)r * H);
         for (int base = gt; base < nvec; base += 4 * gsz) {
             uint4 v[4];
@@ -201,32 +290,47 @@ static __global__ void __launch_bounds__(256) moe_receive_kernel(const MoePeers*
             for (int u = 0; u < 4; ++u)
                 if (base + gsz * u < nvec) dst[base + gsz * u] = v[u];
         }
-        for (int i = gt; i < p.meta; i += gsz)
-            meta_rows[(size_t)r * p.meta + i] = __ldcg(p.rx_meta[p.self] + row * p.meta + i);
-        if (gt == 0) row_src[r] = s;
+        for (int i = gt; i < p.meta; i += gsz) meta_rows[(size_t)r * p.meta + i] = __ldcg(rm + row * p.meta + i);
     }
 }
 
-// K5b: CTA (chunk c, home s) returns received rows r = off[s] + c, + chunks, ... (the rows that
-// came from s, compacted contiguously by K5a) to their tokens' home slots.
-static __global__ void __launch_bounds__(128) moe_combine_put_kernel(const MoePeers* __restrict__ mp,
-                                                                     const __nv_bfloat16* __restrict__ y_rows,
-                                                                     const int32_t* __restrict__ meta_rows,
-                                                                     const int32_t* __restrict__ counts) {
+// K5b: CTA c returns received rows c, c + C, ... (flattened source-major) to their homes.
+// y_rows: compact [R][H] (row = offs[s] + j) or region [W][m_max][H] (row = s * m_max + j).
+static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const MoePeers* __restrict__ mp,
+                                                                             const __nv_bfloat16* __restrict__ y_rows,
+                                                                             int region) {
+    __shared__ int32_t s_off[PL_MAXW + 1], s_sent[PL_MAXW];
     const MoePeers& p = *mp;
-    const int s = blockIdx.y;
-    int off = 0;
-    for (int k = 0; k < s; ++k) off += counts[k];
-    const int n = counts[s];
     const uint32_t ep = *p.epoch;
-    const int H = p.H;
-    for (int i = blockIdx.x; i < n; i += p.chunks) {
-        const int r = off + i;
-        const int t = meta_rows[(size_t)r * p.meta];
-        copy_row(reinterpret_cast<uint4*>(p.cb_y[s] + ((size_t)t * p.W + p.self) * H),
-                 reinterpret_cast<const uint4*>(y_rows + (size_t)r * H), H / 8);
+    const int W = p.W, H = p.H, tid = threadIdx.x;
+    if (tid <= W) s_off[tid] = p.offs[tid];
+    if (tid < PL_MAXW) s_sent[tid] = 0;
+    __syncthreads();
+    const int R = s_off[W];
+    const int nvec = H / 8;
+    const int32_t* rm = rx_meta(p, p.self, ep);
+    constexpr int VPT = 4;
+    for (int r = blockIdx.x; r < R; r += gridDim.x) {
+        int s = 0;
+        while (s_off[s + 1] <= r) ++s;
+        const int j = r - s_off[s];
+        const int t = __ldcg(rm + ((size_t)s * p.m_max + j) * p.meta);
+        const uint4* src =
+            reinterpret_cast<const uint4*>(y_rows + (size_t)(region ? s * p.m_max + j : r) * H);
+        uint4* dst = reinterpret_cast<uint4*>(cb_y(p, s, ep) + ((size_t)t * W + p.self) * H);
+        for (int v0 = tid; v0 < nvec; v0 += VPT * MOE_THREADS) {
+            uint4 v[VPT];
+#pragma unroll
+            for (int u = 0; u < VPT; ++u)
+                if (v0 + u * MOE_THREADS < nvec) v[u] = __ldg(src + v0 + u * MOE_THREADS);
+#pragma unroll
+            for (int u = 0; u < VPT; ++u)
+                if (v0 + u * MOE_THREADS < nvec) dst[v0 + u * MOE_THREADS] = v[u];
+        }
+        if (tid == 0) ++s_sent[s];
     }
-    moe_chunk_done(p.cb_done + s, p.chunks, p.cb_flag[s] + p.self, ep);
+    __syncthreads();
+    if (tid < W && s_sent[tid]) red_release_sys_add(cb_arr(p, tid, ep) + p.self, s_sent[tid]);
 }
 
 // K5c: at home, sum the partials of every destination rank in ascending order.  CTA (token t,
@@ -234,26 +338,28 @@ static __global__ void __launch_bounds__(128) moe_combine_put_kernel(const MoePe
 // adding them (the W loads are in flight together).
 static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const MoePeers* __restrict__ mp,
                                                                         const int32_t* __restrict__ m_count,
-                                                                        const int32_t* __restrict__ slot_tbl,
                                                                         float* __restrict__ out) {
     const MoePeers& p = *mp;
     const int t = blockIdx.x;
     if (t >= *m_count) return;
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H;
-    if (threadIdx.x < W) wait_flag(p.cb_flag[p.self] + threadIdx.x, ep);
+    if (threadIdx.x < W)
+        wait_flag(cb_arr(p, p.self, ep) + threadIdx.x, p.cb_target[(ep & 1) * W + threadIdx.x], p.wc,
+                  (SITE_MOE_CB << 24) | (threadIdx.x << 16) | (t & 0xffff), true);
     __syncthreads();
     const int q = blockIdx.y * blockDim.x + threadIdx.x;  // 4-column group
     if (4 * q >= H) return;
+    const __nv_bfloat16* cy = cb_y(p, p.self, ep);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     uint2 v[PL_MAXW];
 #pragma unroll 8
     for (int d = 0; d < W; ++d)
-        if (slot_tbl[t * W + d] >= 0)
-            v[d] = __ldcg(reinterpret_cast<const uint2*>(p.cb_y[p.self] + ((size_t)t * W + d) * H) + q);
+        if (p.slot_tbl[t * W + d] >= 0)
+            v[d] = __ldcg(reinterpret_cast<const uint2*>(cy + ((size_t)t * W + d) * H) + q);
 #pragma unroll 8
     for (int d = 0; d < W; ++d) {
-        if (slot_tbl[t * W + d] < 0) continue;
+        if (p.slot_tbl[t * W + d] < 0) continue;
         const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[d].x));
         const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[d].y));
         a0 += lo.x;
@@ -264,8 +370,4 @@ static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const Mo
     reinterpret_cast<float4*>(out + (size_t)t * H)[q] = make_float4(a0, a1, a2, a3);
 }
 
-}  // namespace dcp
-
-namespace dcp {
-static __global__ void epoch_bump_kernel_moe(uint32_t* epoch) { *epoch += 1; }
 }  // namespace dcp

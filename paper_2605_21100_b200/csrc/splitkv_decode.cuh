@@ -48,31 +48,34 @@ struct AttnParams {
     int32_t* counters;           // [R]
     int32_t num_shards;
     float scale_log2;            // scale * log2(e)
-    // ---- routed mode (DCP exchange, exchange.cuh); all NULL for a local step
+    // ---- routed mode (DCP exchange, exchange.cuh); all NULL for a local step.  Q and the
+    // Q-route flags then come from this instance's receive pool (parity of the epoch).
     const XchgPeers* xp;         // peer pools; outputs go to m_r's result slot
     const int32_t* n_mrow;       // [R] row of the shard's request in m_r's M list
     const int32_t* n_moe;        // [R] m_r
-    const uint32_t* q_flag;      // [R] Q-route arrival flags (wait == *xp->epoch)
     const int32_t* num_shards_ptr;  // device-resident R (graph replay); overrides num_shards
 };
 
 // Destination of shard r's normalised partial O / LSE: local [R][HQ][D] for a
 // local step, else m_r's result pool slot [mrow][self] (Res-route put, fused).
-__device__ __forceinline__ float* row_out(const AttnParams& p, int r, int HQ, int D) {
+template <class P>
+__device__ __forceinline__ float* row_out(const P& p, int r, int HQ, int D, uint32_t ep) {
     if (!p.xp) return p.out + (size_t)r * HQ * D;
     const XchgPeers& x = *p.xp;
-    return x.res_o[p.n_moe[r]] + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ * D;
+    return xres_o(x, p.n_moe[r], ep) + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ * D;
 }
-__device__ __forceinline__ float* row_lse(const AttnParams& p, int r, int HQ) {
+template <class P>
+__device__ __forceinline__ float* row_lse(const P& p, int r, int HQ, uint32_t ep) {
     if (!p.xp) return p.lse + (size_t)r * HQ;
     const XchgPeers& x = *p.xp;
-    return x.res_lse[p.n_moe[r]] + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ;
+    return xres_lse(x, p.n_moe[r], ep) + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ;
 }
 // Called by thread 0 after a consumer barrier: every warp's stores of row r
 // happen-before this system-scope release.
-__device__ __forceinline__ void publish_row(const AttnParams& p, int r) {
+template <class P>
+__device__ __forceinline__ void publish_row(const P& p, int r, uint32_t ep) {
     const XchgPeers& x = *p.xp;
-    st_release_sys(x.res_flag[p.n_moe[r]] + (size_t)p.n_mrow[r] * x.W + x.self, *x.epoch);
+    st_release_sys(xres_flag(x, p.n_moe[r], ep) + (size_t)p.n_mrow[r] * x.W + x.self, ep);
 }
 
 // SPLIT = false: a ring stage is one whole frame (K and V of every kv-head).
@@ -131,6 +134,10 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int R = p.num_shards_ptr ? *p.num_shards_ptr : p.num_shards;
+    const uint32_t ep = p.xp ? *p.xp->epoch : 0u;
+    const __nv_bfloat16* qbase =
+        p.xp ? reinterpret_cast<const __nv_bfloat16*>(xq_recv(*p.xp, p.xp->self, ep)) : p.q;
+    const uint32_t* qflag = p.xp ? xq_flag(*p.xp, p.xp->self, ep) : nullptr;
     const int64_t P = p.cu_pages[R];
     const int64_t grid = gridDim.x;
     const int cta = blockIdx.x;
@@ -195,8 +202,8 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     // Zero-token shards: O = 0, LSE = -inf (weight 0 in any merge).
     for (int r = cta; r < R; r += gridDim.x) {
         if (p.cu_pages[r + 1] == p.cu_pages[r]) {
-            float* ob = row_out(p, r, C::HQ, C::D);
-            float* lb = row_lse(p, r, C::HQ);
+            float* ob = row_out(p, r, C::HQ, C::D, ep);
+            float* lb = row_lse(p, r, C::HQ, ep);
             for (int row = 0; row < G; ++row) {
                 float* o = ob + (h * G + row) * C::D;
                 reinterpret_cast<float4*>(o)[lane] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -204,7 +211,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             }
             if (p.xp) {
                 named_bar_sync(1, NCT);
-                if (threadIdx.x == 0) publish_row(p, r);
+                if (threadIdx.x == 0) publish_row(p, r, ep);
             }
         }
     }
@@ -260,14 +267,14 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
         const int64_t len = p.shard_len[r];
 
         // Q fragments (A operand, rows = q-heads of this kv group).
-        if (p.q_flag) {  // routed: wait for the Q-route put of this row
-            if (lane == 0) wait_flag(p.q_flag + r, *p.xp->epoch);
+        if (qflag) {  // routed: wait for the Q-route put of this row
+            if (lane == 0) wait_flag(qflag + r, ep, p.xp->wc, (SITE_K1_Q << 24) | (r & 0xffff));
             __syncwarp();
         }
         uint32_t qa[8][4];
         {
             const __nv_bfloat16* q0 =
-                p.q + (static_cast<size_t>(r) * C::HQ + h * G + g) * C::D + 2 * t;
+                qbase + (static_cast<size_t>(r) * C::HQ + h * G + g) * C::D + 2 * t;
             const __nv_bfloat16* q1 = q0 + 8 * C::D;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
@@ -421,16 +428,16 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 const float l = half == 0 ? l0 : l1;
                 const float m = half == 0 ? m0 : m1;
                 const float inv = 1.f / l;
-                float* o = row_out(p, r, C::HQ, C::D) + qh * C::D + 2 * t;
+                float* o = row_out(p, r, C::HQ, C::D, ep) + qh * C::D + 2 * t;
 #pragma unroll
                 for (int nt = 0; nt < 16; ++nt)
                     *reinterpret_cast<float2*>(o + nt * 8) =
                         make_float2(acc[nt][2 * half] * inv, acc[nt][2 * half + 1] * inv);
-                if (t == 0) row_lse(p, r, C::HQ)[qh] = (m + __log2f(l)) * ln2;
+                if (t == 0) row_lse(p, r, C::HQ, ep)[qh] = (m + __log2f(l)) * ln2;
             }
             if (p.xp) {
                 named_bar_sync(1, NCT);
-                if (threadIdx.x == 0) publish_row(p, r);
+                if (threadIdx.x == 0) publish_row(p, r, ep);
             }
         } else {
             const int slot = 2 * cta + (seg_begin == p_begin ? 0 : 1);
@@ -524,15 +531,15 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
                     const float inv = 1.f / den;
-                    float* o = row_out(p, r, C::HQ, C::D) + qh * C::D;
+                    float* o = row_out(p, r, C::HQ, C::D, ep) + qh * C::D;
                     reinterpret_cast<float4*>(o)[lane] =
                         make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
-                    if (lane == 0) row_lse(p, r, C::HQ)[qh] = (mmax + __log2f(den)) * ln2;
+                    if (lane == 0) row_lse(p, r, C::HQ, ep)[qh] = (mmax + __log2f(den)) * ln2;
                 }
                 if (threadIdx.x == 0) p.counters[r] = 0;  // re-arm for the next launch / graph replay
                 if (p.xp) {
                     named_bar_sync(2, NCT);
-                    if (threadIdx.x == 0) publish_row(p, r);
+                    if (threadIdx.x == 0) publish_row(p, r, ep);
                 }
             }
         }

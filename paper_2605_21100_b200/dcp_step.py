@@ -23,22 +23,33 @@ from .attention import DcpContext
 
 
 class DcpInstance:
-    """Exchange pools + KV pool + attention workspace of one instance."""
+    """Exchange pools + KV pool + attention workspace of one instance.
+
+    dtype "bf16": K1 (bf16 KV / Q, mma.sync GQA tiles); "f32": K1-f32 (fp32 KV / Q, the
+    reference's production precision, cfg1).  Partials and merged outputs are fp32 either way.
+    """
 
     def __init__(self, ctx: DcpContext, world: int, self_id: int, hq: int, hkv: int, capacity_pages: int,
                  head_dim: int = 128, page_size: int = 16, n_max: int = 512, m_max: int = 256,
-                 kv_pool: torch.Tensor | None = None):
+                 kv_pool: torch.Tensor | None = None, dtype: str = "bf16", timeout_ms: int = 0):
         L = _capi.lib()
+        if dtype not in ("bf16", "f32"):
+            raise ValueError(f"dtype {dtype!r}")
         self.ctx, self.world, self.id = ctx, world, self_id
         self.hq, self.hkv, self.d, self.page = hq, hkv, head_dim, page_size
-        self.n_max, self.m_max = n_max, m_max
-        cfg = _capi.XchgConfig(world, self_id, hq, head_dim, n_max, m_max)
+        self.n_max, self.m_max, self.dtype = n_max, m_max, dtype
+        tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.tdtype = tdt
+        cfg = _capi.XchgConfig(world, self_id, hq, head_dim, n_max, m_max, head_dim, head_dim,
+                               2 if dtype == "bf16" else 4, timeout_ms)
         h = ctypes.c_void_p()
         _capi.check(L.dcp_xchg_create(ctx.handle, ctypes.byref(cfg), ctypes.byref(h)))
         self.x = h
         dev = torch.device("cuda", ctx.device)
         self.kv_pool = kv_pool if kv_pool is not None else torch.zeros(
-            max(capacity_pages, 1), 2, hkv, page_size, head_dim, dtype=torch.bfloat16, device=dev)
+            max(capacity_pages, 1), 2, hkv, page_size, head_dim, dtype=tdt, device=dev)
+        if self.kv_pool.dtype != tdt:
+            raise TypeError(f"kv_pool dtype {self.kv_pool.dtype} for a {dtype} instance")
         nbytes = L.dcp_attn_workspace_bytes(ctx.handle, n_max, hq, head_dim)
         self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
         ql, qr, out, lse = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
@@ -52,6 +63,11 @@ class DcpInstance:
         a.kv_pool = self.kv_pool.data_ptr()
         a.scale = 1.0 / math.sqrt(head_dim)
         a.workspace, a.workspace_bytes = self.workspace.data_ptr(), self.workspace.numel()
+
+    def status(self):
+        """Raise ExchangeTimeout if a flag wait of this instance timed out (clears it)."""
+        info = (ctypes.c_uint32 * 4)()
+        _capi.check(_capi.lib().dcp_xchg_status(self.x, info))
 
     def ipc_handle(self) -> bytes:
         buf = ctypes.create_string_buffer(64)
@@ -69,8 +85,10 @@ class DcpInstance:
 
     # ---- per step ------------------------------------------------------------
     def write_queries(self, q_rows: torch.Tensor, stream=None):
-        """q_rows: bf16 [M, hq, d] in this instance's M-row order."""
+        """q_rows: [M, hq, d] (bf16, or fp32 for an f32 instance) in this instance's M-row order."""
         s = (stream or torch.cuda.current_stream(self.ctx.device)).cuda_stream
+        if q_rows.dtype != self.tdtype:
+            raise TypeError(f"queries are {q_rows.dtype}, instance is {self.dtype}")
         q_rows = q_rows.contiguous()
         self._q_keep = q_rows
         _capi.check(_capi.lib().dcp_xchg_write_queries(self.x, ctypes.c_void_p(q_rows.data_ptr()),
@@ -83,8 +101,8 @@ class DcpInstance:
             _capi.check(L.dcp_xchg_begin_step(self.x, s))
             _capi.check(L.dcp_route_q(self.x, ctypes.byref(view), s))
         if phase in ("all", "attn"):
-            _capi.check(L.dcp_decode_attn_routed(self.ctx.handle, self.x, ctypes.byref(view),
-                                                 ctypes.byref(self.args), s))
+            fn = L.dcp_decode_attn_routed if self.dtype == "bf16" else L.dcp_decode_attn_routed_f32
+            _capi.check(fn(self.ctx.handle, self.x, ctypes.byref(view), ctypes.byref(self.args), s))
         if phase in ("all", "merge"):
             _capi.check(L.dcp_merge_partials(self.x, ctypes.byref(view), s))
 
@@ -161,6 +179,8 @@ def run_local_step(planner, instances, q_of_request: dict, stream=None):
     for s, inst in enumerate(instances):
         inst.run(views[s], stream, "merge")
     torch.cuda.synchronize()
+    for inst in instances:
+        inst.status()
     res = {}
     for s, inst in enumerate(instances):
         o, l = inst.results(len(m_ids[s]))

@@ -21,10 +21,23 @@ def _s(stream, dev):
     return ctypes.c_void_p((stream or torch.cuda.current_stream(dev)).cuda_stream)
 
 
+def _view(ptr, shape, dtype, device):
+    """A torch tensor aliasing device memory owned by the library (no copy, no ownership)."""
+    n = int(np.prod(shape))
+    itemsize = torch.empty((), dtype=dtype).element_size()
+
+    class _Holder:
+        __cuda_array_interface__ = {
+            "shape": (n * itemsize,), "typestr": "|u1", "data": (ptr, False), "version": 3, "strides": None}
+
+    raw = torch.as_tensor(_Holder(), device=torch.device("cuda", device))
+    return raw.view(dtype).view(*shape)
+
+
 class MoeInstance:
-    def __init__(self, ctx, world, self_id, hidden, topk, num_experts, m_max):
+    def __init__(self, ctx, world, self_id, hidden, topk, num_experts, m_max, timeout_ms=0):
         L = _capi.lib()
-        cfg = _capi.MoeConfig(world, self_id, hidden, topk, num_experts, m_max)
+        cfg = _capi.MoeConfig(world, self_id, hidden, topk, num_experts, m_max, timeout_ms)
         h = ctypes.c_void_p()
         _capi.check(L.dcp_moe_create(ctx.handle, ctypes.byref(cfg), ctypes.byref(h)))
         self.h, self.ctx = h, ctx
@@ -36,6 +49,11 @@ class MoeInstance:
         self.y_rows = torch.zeros(world * m_max, hidden, dtype=torch.bfloat16, device=dev)
         self.out = torch.zeros(m_max, hidden, dtype=torch.float32, device=dev)
         self.m_count = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def status(self):
+        """Raise ExchangeTimeout if a flag wait of this instance timed out (clears it)."""
+        info = (ctypes.c_uint32 * 4)()
+        _capi.check(_capi.lib().dcp_moe_status(self.h, info))
 
     def ipc_handle(self):
         b = ctypes.create_string_buffer(64)
@@ -77,6 +95,31 @@ class MoeInstance:
         _capi.check(_capi.lib().dcp_moe_receive_async(self.h, ctypes.c_void_p(self.x_rows.data_ptr()),
                                                       ctypes.c_void_p(self.meta_rows.data_ptr()),
                                                       _s(stream, self.ctx.device)))
+
+    def receive_regions(self, stream=None):
+        """K5a region mode: wait for every source; rows stay in the pool regions."""
+        _capi.check(_capi.lib().dcp_moe_receive_regions(self.h, _s(stream, self.ctx.device)))
+
+    def regions(self, parity=None):
+        """(x_region bf16 [W, m_max, H], meta_region int32 [W, m_max, meta]) of a parity, as
+        torch views of the pool (the current step's parity by default)."""
+        L = _capi.lib()
+        if parity is None:
+            parity = L.dcp_moe_parity(self.h)
+        xp, mp = ctypes.c_void_p(), ctypes.c_void_p()
+        _capi.check(L.dcp_moe_regions(self.h, parity, ctypes.byref(xp), ctypes.byref(mp)))
+        return (_view(xp.value, (self.world, self.m_max, self.H), torch.bfloat16, self.ctx.device),
+                _view(mp.value, (self.world, self.m_max, self.meta_w), torch.int32, self.ctx.device))
+
+    def recv_counts(self):
+        """Per-source received row counts of the last receive (device -> host)."""
+        p = _capi.lib().dcp_moe_recv_counts_dev(self.h)
+        return _capi.device_to_numpy(p, self.world, np.int32)
+
+    def combine_put_regions(self, y_region, stream=None):
+        """K5b with y in region layout bf16 [W, m_max, H] (the expert stage's output in place)."""
+        _capi.check(_capi.lib().dcp_moe_combine_put_regions(self.h, ctypes.c_void_p(y_region.data_ptr()),
+                                                            _s(stream, self.ctx.device)))
 
     def expert_stage(self, R, w_gate, w_up, w_down):
         """Library-GEMM expert FFN over the R received rows (local experts

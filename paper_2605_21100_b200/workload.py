@@ -116,6 +116,19 @@ def cfg2_lengths():
     return lengths(0, 64, 1024, 32768)
 
 
+def cfg2_bench_inputs(device, seed: int = 1234, frame_order: str = "lifo"):
+    """The cfg2 step bench.py times, as (PagedBatch, pool, q): the 64 cfg2 requests laid out
+    with `frame_order`, a bf16 pool and bf16 queries drawn on `device` from a seeded
+    generator (pool first, then q).  The parity tests check these exact tensors."""
+    import torch
+    b = paged_batch(cfg2_lengths(), 32, 8, 128, 16, frame_order=frame_order, seed=seed,
+                    spare_frames=0 if frame_order == "lifo" else 4096)
+    g = torch.Generator(device=device).manual_seed(seed)
+    pool = torch.randn(b.num_frames, 2, 8, 16, 128, generator=g, device=device, dtype=torch.bfloat16)
+    q = torch.randn(64, 32, 128, generator=g, device=device, dtype=torch.bfloat16)
+    return b, pool, q
+
+
 # ------------------------------------------------------------------ traces
 # Input generation for the trace-driven benches: the reference's Table-1
 # distributions and gen_trace (workload.hpp:28-74, workload.cpp:11-106),

@@ -51,6 +51,7 @@ def _load(path, prefix):
     if prefix == "dcpora_":
         sigs["paged_decode_attn_f64"] = (c_int, [c_int, c_int, c_int, c_int, c_int, vp, vp, vp, vp, vp, vp,
                                                  c_double, vp, vp, c_int])
+        sigs["paged_decode_attn_any_f64"] = (c_int, [c_int] * 6 + [vp] * 6 + [c_double, vp, vp, c_int])
         sigs["sharded_attention_merge_f64"] = (c_int, [vp, vp, vp, c_int64, c_int, c_double, vp, c_int, vp])
         sigs["sharded_attention_merge_f32"] = (c_int, [vp, vp, vp, c_int64, c_int, c_float, vp, c_int, vp])
         sigs["world_instance_shards"] = (c_int, [c_void_p, c_int, vp, vp, vp, vp, c_int, c_int])
@@ -98,6 +99,23 @@ def paged_decode_f64(batch, q_bits: np.ndarray, pool_bits: np.ndarray, page_fill
     rc = L.dcpora_paged_decode_attn_f64(
         R, batch.num_q_heads, batch.num_kv_heads, batch.head_dim, batch.page_size,
         P(np.ascontiguousarray(q_bits)), P(np.ascontiguousarray(pool_bits)),
+        P(batch.block_table), P(batch.cu_pages), P(batch.shard_len),
+        P(page_fill), sc, P(out), P(lse), th)
+    assert rc == 0, rc
+    return out, lse
+
+
+def paged_decode_f32in_f64(batch, q: np.ndarray, pool: np.ndarray, page_fill=None, scale=None, threads: int = 0):
+    """Oracle fp64 decode attention over a PagedBatch with fp32 q / pool (numpy float32)."""
+    L = port()
+    R = len(batch.shard_len)
+    out = np.zeros((R, batch.num_q_heads, batch.head_dim), np.float64)
+    lse = np.zeros((R, batch.num_q_heads), np.float64)
+    sc = scale if scale is not None else 1.0 / np.sqrt(batch.head_dim)
+    th = threads or os.cpu_count() or 1
+    rc = L.dcpora_paged_decode_attn_any_f64(
+        R, batch.num_q_heads, batch.num_kv_heads, batch.head_dim, batch.page_size, 4,
+        P(np.ascontiguousarray(q, np.float32)), P(np.ascontiguousarray(pool, np.float32)),
         P(batch.block_table), P(batch.cu_pages), P(batch.shard_len),
         P(page_fill), sc, P(out), P(lse), th)
     assert rc == 0, rc

@@ -3,9 +3,9 @@
 4 instances (one node), 64 short requests of 2,048 tokens per instance plus 3 long
 requests of 131,073 tokens (CP 4 under the default BucketFn, scheduler.cpp:10-33), GQA
 32q / 8kv, d = 128, bf16 paged KV, page 16.  One routed step (K2 -> K1 + Res-route -> K3)
-over the whole batch; the three long requests and a sample of short ones are checked
-against shard_attention<double> + lse_merge over the device page table's per-instance
-tokens (bf16 rel-L2 <= 2e-2, LSE <= 1e-5).
+over the whole batch; every one of the 259 requests and all 32 heads is checked against
+shard_attention<double> + lse_merge over the device page table's per-instance tokens
+(bf16 rel-L2 <= 2e-2, LSE <= 1e-5).
 """
 import numpy as np
 import pytest
@@ -48,8 +48,7 @@ def test_cfg3_skewed_batch_full_size():
     out, views = run_local_step(pl, insts, q)
     assert sorted(out) == ids
 
-    rng = np.random.default_rng(3)
-    check = set(longs) | set(int(x) for x in rng.choice(ids[3:], 12, replace=False))
+    check = set(ids)
     port = oracle_lib.port()
     partial = {}
     for s in range(W):
@@ -82,6 +81,7 @@ def test_cfg3_skewed_batch_full_size():
             o, l = out[r][0][h].astype(np.float64), float(out[r][1][h])
             worst_o = max(worst_o, np.linalg.norm(o - ro) / np.linalg.norm(ro))
             worst_l = max(worst_l, abs(l - rl) / max(1.0, abs(rl)))
+    print(f"cfg3 all {len(check)} requests x {HQ} heads: worst O rel-L2 {worst_o:.3e}, LSE {worst_l:.3e}")
     assert worst_o <= 2e-2, worst_o
     assert worst_l <= 1e-5, worst_l
     for x in insts:

@@ -123,7 +123,7 @@ def test_512k_request_cp8_routed_step():
         tot = sum(int(device_to_numpy(views[s].shard_len, views[s].n_rows, np.int64)[
             list(device_to_numpy(views[s].n_ids, views[s].n_rows, np.int64)).index(r)]) for s in p["kv"])
         assert tot == lens[r] + 1                      # the appended token is attended
-        for h in (0, 13, 31):
+        for h in range(hq):
             ro, rl = _oracle_merge(port, [partial[(r, s)][0][h] for s in p["kv"]],
                                    [partial[(r, s)][1][h] for s in p["kv"]], 128)
             o = out[r][0][h].astype(np.float64)

@@ -328,6 +328,45 @@ def test_paged_oracle_matches_reference_on_gathered_kv(port, ref):
             assert np.array_equal(o, out[r, h]) and l[0] == lse[r, h]
 
 
+def test_paged_oracle_f32_pool_matches_reference(port, ref):
+    """The fp32-pool paged oracle (used to check K1-f32, cfg1) equals the reference's
+    shard_attention<double> on the same fp32 tokens gathered in page order, with page
+    fills from append_token's fallback (partial non-final pages)."""
+    from paper_2605_21100_b200 import workload
+    rng = np.random.default_rng(11)
+    lens = [3, 16, 40, 0, 129]
+    b = workload.paged_batch(lens, 8, 8, frame_order="shuffled", seed=4, spare_frames=5)
+    fill = np.zeros(int(b.cu_pages[-1]), np.uint8)
+    lens2 = []
+    for r, L in enumerate(lens):          # give every shard a partial page in the middle
+        n = int(b.cu_pages[r + 1] - b.cu_pages[r])
+        f = [16] * n
+        if n:
+            f[-1] = L - 16 * (n - 1)
+        if n >= 2:
+            f[0] = 9
+        fill[b.cu_pages[r]:b.cu_pages[r + 1]] = f
+        lens2.append(sum(f))
+    b.shard_len[:] = lens2
+    q = rng.standard_normal((len(lens), 8, 128)).astype(np.float32)
+    pool = rng.standard_normal((b.num_frames, 2, 8, 16, 128)).astype(np.float32)
+    out, lse = oracle_lib.paged_decode_f32in_f64(b, q, pool, page_fill=fill)
+    for r, L in enumerate(lens2):
+        frames = b.block_table[b.cu_pages[r]:b.cu_pages[r + 1]]
+        fl = fill[b.cu_pages[r]:b.cu_pages[r + 1]]
+        for h in range(8):
+            if L == 0:
+                assert np.isneginf(lse[r, h])
+                continue
+            kk = np.concatenate([pool[f, 0, h, :n] for f, n in zip(frames, fl)]).astype(np.float64)
+            vv = np.concatenate([pool[f, 1, h, :n] for f, n in zip(frames, fl)]).astype(np.float64)
+            o, l = np.zeros(128), np.zeros(1)
+            assert ref.dcpref_shard_attention_f64(P(q[r, h].astype(np.float64)), P(np.ascontiguousarray(kk)),
+                                                  P(np.ascontiguousarray(vv)), L, 128, 1 / np.sqrt(128),
+                                                  P(o), P(l)) == 0
+            assert np.array_equal(o, out[r, h]) and l[0] == lse[r, h]
+
+
 def test_trace_generator_matches_reference(ref):
     """The bench trace source (paper_2605_21100_b200.workload.gen_trace) is the
     reference's gen_trace (workload.cpp:73-106), draw for draw."""
