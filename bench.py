@@ -10,9 +10,11 @@ measured peak in the roofline object.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Multi-GPU (torchrun, one rank per GPU): every rank is an independent DP
-instance with its own cfg2 batch ("replicas", weak scaling); value is the
-whole-job tok/s = N * 64 * K / max-over-ranks device time.
+Multi-GPU (torchrun, one rank per GPU): the real DCP decode step across the
+GPUs (bench_multi.py: K2 -> K1 -> K3 attention exchange + K4/K5 MoE
+dispatch/combine over CUDA-IPC peer pools, weak scaling, value = whole-job
+tok/s over max-over-ranks device time).  --replicas keeps the old mode: N
+independent cfg2 replicas.
 --impl reference: the reference's own CPU implementation
 (dcpsim::sharded_attention_merge compiled from /root/reference sources into
 oracle/_ref) timed on the host cores on a bounded sample of the same workload.
@@ -37,6 +39,8 @@ sys.path.insert(0, ROOT)
 HQ, HKV, D, PAGE = 32, 8, 128, 16
 METRIC = "decode tok/s (split-KV paged decode attention step, cfg2: 64 req, KV 1K-32K, GQA 32q/8kv, d128, bf16 paged)"
 UNIT = "tok/s"
+METRIC_MULTI = ("decode tok/s (DCP decode step on N GPUs: K2 -> K1 -> K3 attention exchange + K4/K5 MoE "
+                "dispatch/combine, per attention+MoE layer)")
 WORKLOAD = "cfg2 single-GPU split-KV decode attention: 64 requests, KV len uniform_int(mt19937_64(0),1024,32768) sum=1068741, GQA 32q/8kv, d=128, bf16 paged KV page=16"
 
 
@@ -434,10 +438,15 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mla", action="store_true", help="skip the K10 MLA leg (SURVEY §8f #1)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: N independent cfg2 replicas instead of the multi-GPU DCP step")
     args = ap.parse_args()
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif ws > 1 and not args.replicas:
+        import bench_multi
+        bench_multi.run(args, ws, rank, local)
     else:
         run_ours(args, ws, rank, local)
 

@@ -34,7 +34,7 @@ CONFIGS = {
 }
 
 
-def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup):
+def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup, compact=False):
     import torch
     from paper_2605_21100_b200.moe import MoeInstance
     inst = [MoeInstance(ctx, W, s, H, k, E, M) for s in range(W)]
@@ -63,6 +63,7 @@ def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup):
     R = [int(sum(int((ranks[s2] == d).any(axis=1).sum()) for s2 in range(W))) for d in range(W)]
     mcnt = [torch.full((1,), M, dtype=torch.int32, device=dev) for _ in range(W)]
     phases = {"dispatch": [], "receive": [], "combine_put": [], "combine_reduce": []}
+    y_region = [torch.zeros(W, M, H, dtype=torch.bfloat16, device=dev) for _ in range(W)]
     for it in range(warmup + steps):
         ev = {p: [(E_(), E_()) for _ in range(W)] for p in phases}
         # a device sleep gates the step so the events below time device work, not host launch gaps
@@ -73,13 +74,22 @@ def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup):
             ev["dispatch"][s][1].record(stream)
         for s in range(W):
             ev["receive"][s][0].record(stream)
-            inst[s].receive_async()
+            if compact:
+                inst[s].receive_async()
+            else:
+                inst[s].receive_regions()
             ev["receive"][s][1].record(stream)
         for s in range(W):  # identity "experts" (untimed)
-            inst[s].y_rows[:R[s]].copy_(inst[s].x_rows[:R[s]])
+            if compact:
+                inst[s].y_rows[:R[s]].copy_(inst[s].x_rows[:R[s]])
+            else:
+                y_region[s].copy_(inst[s].regions()[0])
         for s in range(W):
             ev["combine_put"][s][0].record(stream)
-            inst[s].combine_put()
+            if compact:
+                inst[s].combine_put()
+            else:
+                inst[s].combine_put_regions(y_region[s])
             ev["combine_put"][s][1].record(stream)
         for s in range(W):
             ev["combine_reduce"][s][0].record(stream)
@@ -95,37 +105,41 @@ def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup):
         assert torch.allclose(inst[s].out[:M], ref, rtol=1e-2, atol=1e-2), f"instance {s} combine mismatch"
     res = {"workload": name, "instances": W, "tokens_per_instance": M, "hidden": H, "experts": E, "topk": k,
            "rows_dispatched": rows_total, "cross_instance_bytes_per_step": alg_xfer}
-    moved = {"dispatch": rows_total * H * 2, "receive": 2 * rows_total * H * 2,
+    moved = {"dispatch": rows_total * H * 2, "receive": 2 * rows_total * H * 2 if compact else 0,
              "combine_put": rows_total * H * 2, "combine_reduce": rows_total * H * 2 + W * M * H * 4}
     tot_sum = 0.0
     for p, v in phases.items():
         a = np.array(v)  # [steps][W] us
         s_sum = float(np.median(a.sum(axis=1)))
         tot_sum += s_sum
-        res[p] = {"us_sum_over_instances": s_sum, "us_max_instance": float(np.median(a.max(axis=1))),
+        res[p] = {"us_sum_over_instances": s_sum, "us_per_instance": s_sum / W,
+                  "us_max_instance": float(np.median(a.max(axis=1))),
                   "bytes": moved[p], "gbs": moved[p] / (s_sum * 1e-6) / 1e9}
     res["us_per_instance_step"] = tot_sum / W
+    res["receive_mode"] = "compact (rows copied out of the pool)" if compact else "region (rows read in place)"
     res["note"] = ("single GPU: cross-instance stores are local HBM stores; expert FFN = identity, untimed; "
-                   "each step gated behind a device sleep so CUDA events time device work only")
+                   "each step gated behind a device sleep so CUDA events time device work only; "
+                   "dispatch includes the begin_step fence kernel")
     for i in inst:
         i.close()
     return res
 
 
-def run_all(ctx, dev, steps=20, warmup=3):
-    return [run_config(ctx, dev, n, steps=steps, warmup=warmup, **c) for n, c in CONFIGS.items()]
+def run_all(ctx, dev, steps=20, warmup=3, compact=False):
+    return [run_config(ctx, dev, n, steps=steps, warmup=warmup, compact=compact, **c) for n, c in CONFIGS.items()]
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--compact", action="store_true", help="legacy compacting receive (dcp_moe_receive_async)")
     args = ap.parse_args()
     import torch
     from paper_2605_21100_b200.attention import DcpContext
     dev = torch.device("cuda", 0)
     ctx = DcpContext(0)
-    for r in run_all(ctx, dev, args.steps, args.warmup):
+    for r in run_all(ctx, dev, args.steps, args.warmup, args.compact):
         print(json.dumps(r), flush=True)
 
 

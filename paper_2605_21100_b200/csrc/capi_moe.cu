@@ -20,6 +20,7 @@ struct dcp_moe {
     uint32_t host_epoch = 0;           // mirror of the device epoch (begin_step calls)
     const int32_t* m_count_dev = nullptr;
     bool received = false;
+    bool committed = false;
     void* opened[PL_MAXW] = {};
 };
 
@@ -155,12 +156,13 @@ int dcp_moe_commit(dcp_moe* x) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
     for (int s = 0; s < x->cfg.world; ++s) DCP_REQUIRE(x->host.base[s], DCP_E_INVALID_ARG, "peer %d not set", s);
     DCP_CUDA_TRY(cudaMemcpy(x->dev, &x->host, sizeof(MoePeers), cudaMemcpyHostToDevice));
+    x->committed = true;
     return DCP_OK;
 }
 
 int dcp_moe_begin_step(dcp_moe* x, void* stream) {
-    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    moe_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->dev);
+    DCP_REQUIRE(x && x->committed, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange (dcp_moe_commit)");
+    moe_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->host);
     DCP_CUDA_TRY(cudaGetLastError());
     ++x->host_epoch;
     x->received = false;
@@ -200,14 +202,14 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
     moe_dispatch_kernel<<<x->host.chunks, MOE_THREADS, dispatch_smem(x), s>>>(
-        x->dev, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count);
+        x->host, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
 
 int dcp_moe_receive_regions(dcp_moe* x, void* stream) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    moe_receive_counts_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->dev);
+    moe_receive_counts_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->host);
     DCP_CUDA_TRY(cudaGetLastError());
     x->received = true;
     return DCP_OK;
@@ -219,7 +221,7 @@ int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* st
     const int rows = x->cfg.world * x->cfg.m_max;
     int grid = rows;  // up to one CTA per received row (warp groups per row, moe.cuh)
     if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
-    moe_receive_compact_kernel<<<grid, 256, 0, s>>>(x->dev, static_cast<__nv_bfloat16*>(x_rows), meta_rows);
+    moe_receive_compact_kernel<<<grid, 256, 0, s>>>(x->host, static_cast<__nv_bfloat16*>(x_rows), meta_rows);
     DCP_CUDA_TRY(cudaGetLastError());
     x->received = true;
     return DCP_OK;
@@ -244,7 +246,7 @@ int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* c
 static int combine_put(dcp_moe* x, const void* y, int region, void* stream) {
     DCP_REQUIRE(x && y && x->received, DCP_E_INVALID_ARG, "call a dcp_moe_receive* first");
     moe_combine_put_kernel<<<x->host.chunks, MOE_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, static_cast<const __nv_bfloat16*>(y), region);
+        x->host, static_cast<const __nv_bfloat16*>(y), region);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
@@ -259,7 +261,7 @@ int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {
     DCP_REQUIRE(x && out && x->m_count_dev, DCP_E_INVALID_ARG, "call dcp_moe_dispatch first");
     const int groups = x->cfg.hidden / 4;  // hidden % 8 == 0
     moe_combine_reduce_kernel<<<dim3(x->cfg.m_max, (groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, x->m_count_dev, out);
+        x->host, x->m_count_dev, out);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }

@@ -142,12 +142,13 @@ int dcp_xchg_commit(dcp_xchg* x) {
     for (int s = 0; s < x->cfg.world; ++s)
         DCP_REQUIRE(x->host.base[s] != nullptr, DCP_E_INVALID_ARG, "peer %d not set", s);
     DCP_CUDA_TRY(cudaMemcpy(x->dev, &x->host, sizeof(XchgPeers), cudaMemcpyHostToDevice));
+    x->committed = true;
     return DCP_OK;
 }
 
 int dcp_xchg_begin_step(dcp_xchg* x, void* stream) {
-    DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    xchg_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->dev);
+    DCP_REQUIRE(x && x->committed, DCP_E_INVALID_ARG, "NULL or uncommitted exchange (dcp_xchg_commit)");
+    xchg_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->host);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
@@ -194,7 +195,7 @@ int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
     DCP_REQUIRE(v->m_rows <= x->cfg.m_max && v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW,
                 "execution shape (%d,%d) exceeds the exchange pools (%d,%d)", v->m_rows, v->n_rows, x->cfg.m_max,
                 x->cfg.n_max);
-    q_route_put_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(x->dev, x->q_local,
+    q_route_put_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(x->host, x->q_local,
                                                                                   v->m_count_all, v->m_nrow);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
@@ -205,7 +206,7 @@ int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
     DCP_REQUIRE(v->m_rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", v->m_rows, x->cfg.m_max);
     lse_merge_kernel<<<x->cfg.m_max, 128, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
+        x->host, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
     DCP_CUDA_TRY(cudaGetLastError());
     return DCP_OK;
 }
@@ -232,10 +233,10 @@ int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
         const int mh = std::min(g->m_hat[i], x->cfg.m_max);
         cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
         if (e == cudaSuccess) {
-            xchg_begin_step_kernel<<<1, 32, 0, cs>>>(x->dev);
-            q_route_put_kernel<<<mh, 128, 0, cs>>>(x->dev, x->q_local, v->m_count_all, v->m_nrow);
+            xchg_begin_step_kernel<<<1, 32, 0, cs>>>(x->host);
+            q_route_put_kernel<<<mh, 128, 0, cs>>>(x->host, x->q_local, v->m_count_all, v->m_nrow);
             rc = dcp_decode_attn_routed(ctx, x, v, a, cs);
-            lse_merge_kernel<<<mh, 128, 0, cs>>>(x->dev, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
+            lse_merge_kernel<<<mh, 128, 0, cs>>>(x->host, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
             e = cudaStreamEndCapture(cs, &g->graph[i]);
         }
         if (e == cudaSuccess && rc == 0) e = cudaGraphInstantiate(&g->exec[i], g->graph[i], 0);

@@ -92,6 +92,9 @@ __device__ __forceinline__ uint32_t* xdone(const XchgPeers& x, int s) {
 __device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -140,11 +143,15 @@ __device__ __forceinline__ bool wait_flag(const uint32_t* p, uint32_t want, cons
 
 // begin_step: publish done = e-1 in our own pool, wait for every peer's done >= e-2, then
 // advance the epoch.  One warp; lane s watches peer s.  done_of(s) -> u32* of s's done word.
+// The done store needs no release fence (a MEMBAR.SYS costs microseconds): every access of
+// step e-1 belongs to kernels that completed before this one started (stream order), so
+// nothing of ours can be reordered after it.  The peers' done words are read with acquire
+// loads, which order this instance's later stores into their pools.
 template <class DoneOf>
 __device__ __forceinline__ void step_fence(uint32_t* epoch, DoneOf done_of, int W, int self, const WaitCtl& wc) {
     const uint32_t e = *epoch + 1;
     const int lane = threadIdx.x & 31;
-    if (lane == 0) st_release_sys(done_of(self), e - 1);
+    if (lane == 0) st_relaxed_sys(done_of(self), e - 1);
     __syncwarp();
     for (int s = lane; s < W; s += 32)
         if (s != self) wait_flag(done_of(s), e - 2, wc, (SITE_FENCE << 24) | (s << 16), true);

@@ -6,20 +6,18 @@
 namespace dcp {
 
 // begin_step: the step fence of exchange.cuh, then the epoch bump.  One warp.
-static __global__ void __launch_bounds__(32) xchg_begin_step_kernel(const XchgPeers* __restrict__ xp) {
-    const XchgPeers& x = *xp;
+static __global__ void __launch_bounds__(32) xchg_begin_step_kernel(const __grid_constant__ XchgPeers x) {
     step_fence(x.epoch, [&](int s) { return xdone(x, s); }, x.W, x.self, x.wc);
 }
 
 // K2: grid = m_max (graph-stable), block = 128.  q_local: [m_max][hq][q_dim] x q_bytes
 // in M-row order; m_nrow: [M][W] destination rows (-1 = not in P_r).  The payload is
 // moved as 16-byte vectors whatever its element type (bf16 Q, fp32 Q, MLA's 576-wide Q).
-static __global__ void __launch_bounds__(128) q_route_put_kernel(const XchgPeers* __restrict__ xp,
+static __global__ void __launch_bounds__(128) q_route_put_kernel(const __grid_constant__ XchgPeers x,
                                                                  const void* __restrict__ q_local,
                                                                  const int32_t* __restrict__ m_count,
                                                                  const int32_t* __restrict__ m_nrow) {
     const int r = blockIdx.x;
-    const XchgPeers& x = *xp;
     if (r >= m_count[x.self]) return;
     const uint32_t ep = *x.epoch;
     const int W = x.W;
@@ -49,14 +47,13 @@ static __global__ void __launch_bounds__(128) q_route_put_kernel(const XchgPeers
 // order.  out: [m_max][hq][o_dim] fp32, out_lse: [m_max][hq].  Weights follow lse_merge
 // (attn_merge.hpp:86-100): w_k = exp(lse_k - max lse), out = sum w_k o_k / sum w_k, folded
 // in kv_binding order; an empty shard (lse = -inf) has weight 0.
-static __global__ void __launch_bounds__(128) lse_merge_kernel(const XchgPeers* __restrict__ xp,
+static __global__ void __launch_bounds__(128) lse_merge_kernel(const __grid_constant__ XchgPeers x,
                                                                const int32_t* __restrict__ m_count,
                                                                const int32_t* __restrict__ m_k,
                                                                const int32_t* __restrict__ m_kv,
                                                                float* __restrict__ out,
                                                                float* __restrict__ out_lse) {
     const int r = blockIdx.x;
-    const XchgPeers& x = *xp;
     if (r >= m_count[x.self]) return;
     const uint32_t ep = *x.epoch;
     const int W = x.W, hq = x.hq, d = x.o_dim;

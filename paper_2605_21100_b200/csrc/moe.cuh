@@ -129,19 +129,17 @@ __device__ __forceinline__ int moe_wait_source(const MoePeers& p, int s, uint32_
     return static_cast<int>(a & 0xffffffffu);
 }
 
-static __global__ void __launch_bounds__(32) moe_begin_step_kernel(const MoePeers* __restrict__ mp) {
-    const MoePeers& p = *mp;
+static __global__ void __launch_bounds__(32) moe_begin_step_kernel(const __grid_constant__ MoePeers p) {
     step_fence(p.epoch, [&](int s) { return moe_done(p, s); }, p.W, p.self, p.wc);
 }
 
 // K4.  grid = chunks, block = MOE_THREADS; dynamic smem = m_max * (W + 1) * 4 bytes.
-static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const MoePeers* __restrict__ mp,
+static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const __grid_constant__ MoePeers p,
                                                                           const __nv_bfloat16* __restrict__ x,
                                                                           const int32_t* __restrict__ topk_idx,
                                                                           const float* __restrict__ topk_w,
                                                                           const int32_t* __restrict__ m_count) {
     extern __shared__ int32_t sm[];
-    const MoePeers& p = *mp;
     const int W = p.W, H = p.H, K = p.topk, M = *m_count;
     int32_t* s_mask = sm;               // [M] destination-rank bitmask of each token
     int32_t* s_slot = sm + p.m_max;     // [M][W] slot at each destination (-1 = not routed)
@@ -229,8 +227,7 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
 }
 
 // K5a (region mode): one warp; lane s waits for source s, then counts and offsets.
-static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const MoePeers* __restrict__ mp) {
-    const MoePeers& p = *mp;
+static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const __grid_constant__ MoePeers p) {
     const uint32_t ep = *p.epoch;
     const int lane = threadIdx.x;
     int c = 0;
@@ -250,11 +247,10 @@ static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const Moe
 
 // K5a (compact mode, legacy dcp_moe_receive): every CTA waits for every source, then warp
 // groups copy rows r = group_global, + total_groups, ... in (source, slot) order.
-static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const MoePeers* __restrict__ mp,
+static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const __grid_constant__ MoePeers p,
                                                                          __nv_bfloat16* __restrict__ x_rows,
                                                                          int32_t* __restrict__ meta_rows) {
     __shared__ int32_t cnt[PL_MAXW], off[PL_MAXW + 1];
-    const MoePeers& p = *mp;
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H;
     if (threadIdx.x < W) cnt[threadIdx.x] = moe_wait_source(p, threadIdx.x, ep);
@@ -296,11 +292,10 @@ static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const M
 
 // K5b: CTA c returns received rows c, c + C, ... (flattened source-major) to their homes.
 // y_rows: compact [R][H] (row = offs[s] + j) or region [W][m_max][H] (row = s * m_max + j).
-static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const MoePeers* __restrict__ mp,
+static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const __grid_constant__ MoePeers p,
                                                                              const __nv_bfloat16* __restrict__ y_rows,
                                                                              int region) {
     __shared__ int32_t s_off[PL_MAXW + 1], s_sent[PL_MAXW];
-    const MoePeers& p = *mp;
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H, tid = threadIdx.x;
     if (tid <= W) s_off[tid] = p.offs[tid];
@@ -336,10 +331,9 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(con
 // K5c: at home, sum the partials of every destination rank in ascending order.  CTA (token t,
 // hidden chunk); each thread owns 4 consecutive columns and loads all ranks' partials before
 // adding them (the W loads are in flight together).
-static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const MoePeers* __restrict__ mp,
+static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __grid_constant__ MoePeers p,
                                                                         const int32_t* __restrict__ m_count,
                                                                         float* __restrict__ out) {
-    const MoePeers& p = *mp;
     const int t = blockIdx.x;
     if (t >= *m_count) return;
     const uint32_t ep = *p.epoch;

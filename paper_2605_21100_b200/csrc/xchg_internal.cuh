@@ -18,4 +18,5 @@ struct dcp_xchg {
     float* out_lse = nullptr;
     uint32_t* epoch = nullptr;
     uint32_t* err = nullptr;
+    bool committed = false;
 };

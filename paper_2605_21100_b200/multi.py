@@ -54,3 +54,89 @@ def connect_peers(inst, handles: list[bytes]) -> None:
         else:
             inst.open_peer(peer, h)
     inst.commit()
+
+
+# ---------------------------------------------------------------------------------------------
+class RankStep:
+    """One rank of a multi-process DCP decode step: one DCP instance (one GPU in production).
+
+    Every rank runs the identical planner replica (K6 admission + K7 routing; SURVEY §8(e)
+    "replicas only"), checks the replicas agree, then maps every peer's exchange pools through
+    CUDA IPC.  A step is this instance's
+        begin_step -> K2 Q-route puts -> K1 (+ Res-route puts) -> K3 merge
+    and optionally the MoE layer on its M list
+        begin_step -> K4 dispatch -> K5a receive (region) -> experts -> K5b combine_put -> K5c reduce
+    with no host synchronisation between ranks: every cross-rank dependency is a device flag.
+
+    pool_fn(rank, capacity, hkv) -> KV pool tensor of this rank (bf16 [cap, 2, hkv, 16, 128]).
+    moe: None or dict(hidden, experts, topk, m_max).
+    """
+
+    def __init__(self, ctx, world, rank, lens, hq, hkv, capacity, pool_fn, bucket=None, moe=None,
+                 timeout_ms=30000, n_max=512, m_max=256, max_requests=None):
+        from .dcp_step import DcpInstance
+        from .moe import MoeInstance
+        from .planner import DevicePlanner
+        self.ctx, self.world, self.rank, self.hq, self.hkv = ctx, world, rank, hq, hkv
+        self.ids = list(range(len(lens)))
+        self.lens = list(lens)
+        mr = max_requests or max(64, 2 * len(lens))
+        self.planner = DevicePlanner(ctx, 1, world, 16, capacity, "dcp", bucket, max_requests=mr, reserve_pages=8)
+        self.planner.enqueue_many(self.ids, self.lens)
+        res = self.planner.step()
+        if len(res["committed"]) != len(self.ids):
+            raise RuntimeError(f"rank {rank}: only {len(res['committed'])} of {len(self.ids)} admitted")
+        self.planner.build_routing()
+        check_replicas(self.planner.routing_csv())
+        self.view = self.planner.instance_view(rank)
+        import numpy as np
+        from ._capi import device_to_numpy
+        self.m_ids = device_to_numpy(self.view.m_ids, self.view.m_rows, np.int64).tolist()
+        self.n_ids = device_to_numpy(self.view.n_ids, self.view.n_rows, np.int64).tolist()
+        self.inst = DcpInstance(ctx, world, rank, hq, hkv, capacity, kv_pool=pool_fn(rank, capacity, hkv),
+                                n_max=n_max, m_max=m_max, timeout_ms=timeout_ms)
+        connect_peers(self.inst, exchange_handles(self.inst.ipc_handle()))
+        self.moe = None
+        if moe:
+            self.moe = MoeInstance(ctx, world, rank, moe["hidden"], moe["topk"], moe["experts"], moe["m_max"],
+                                   timeout_ms=timeout_ms)
+            connect_peers(self.moe, exchange_handles(self.moe.ipc_handle()))
+            import torch
+            self.y_region = torch.zeros(world, moe["m_max"], moe["hidden"], dtype=torch.bfloat16,
+                                        device=torch.device("cuda", ctx.device))
+        # K7's device M count of this instance feeds K4 (no host round trip)
+        self.m_count_ptr = self.view.m_count_all + 4 * rank
+
+    def attention(self, q_rows, stream=None):
+        """q_rows bf16 [M, hq, 128] in this rank's M-row order."""
+        if len(self.m_ids):
+            self.inst.write_queries(q_rows, stream)
+        self.inst.run(self.view, stream)
+
+    def moe_layer(self, x, topk_idx, topk_w, expert_fn=None, stream=None):
+        """x bf16 [M, H] in M-row order; expert_fn(x_region, meta_region, counts) -> fills
+        self.y_region (identity experts when None: y = x, issued on the stream, no host sync)."""
+        m = self.moe
+        m.dispatch(x, topk_idx, topk_w, m_count_ptr=self.m_count_ptr, stream=stream)
+        m.receive_regions(stream)
+        xr, mr = m.regions()
+        if expert_fn is None:
+            self.y_region.copy_(xr)
+        else:
+            expert_fn(xr, mr, m.recv_counts(), self.y_region)
+        m.combine_put_regions(self.y_region, stream)
+        m.combine_reduce(stream)
+
+    def results(self):
+        return self.inst.results(len(self.m_ids))
+
+    def status(self):
+        self.inst.status()
+        if self.moe is not None:
+            self.moe.status()
+
+    def close(self):
+        self.inst.close()
+        if self.moe is not None:
+            self.moe.close()
+        self.planner.close()
