@@ -84,7 +84,13 @@ def reference():
 
 
 def P(a):
-    return ctypes.c_void_p(a.ctypes.data) if a is not None else None
+    """Pointer to a numpy array's data that keeps the array alive for the duration of the
+    foreign call (P(x.cpu().numpy()) would otherwise hand C a pointer into a freed temporary)."""
+    if a is None:
+        return None
+    p = ctypes.c_void_p(a.ctypes.data)
+    p._keep = a
+    return p
 
 
 def paged_decode_f64(batch, q_bits: np.ndarray, pool_bits: np.ndarray, page_fill=None, scale=None,

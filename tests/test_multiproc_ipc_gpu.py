@@ -11,7 +11,9 @@ with no phase ordering: every cross-rank wait is a device flag (the driver time-
 contexts).  Each rank checks its own M rows against the fp64 oracles.
 """
 import os
+import queue
 import socket
+import time
 import traceback
 
 import numpy as np
@@ -66,8 +68,15 @@ def _weights():
     return wg, wu, wd
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, log_dir):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import faulthandler
+    import sys
+    if log_dir:  # per-rank log with a stack dump if the rank is still running after 240 s
+        f = open(os.path.join(log_dir, f"ipc_rank{rank}.log"), "w", buffering=1)
+        sys.stdout = sys.stderr = f
+        faulthandler.enable(f)
+        faulthandler.dump_traceback_later(240, exit=False, file=f)
     import torch
     import torch.distributed as dist
     dist.init_process_group("gloo", rank=rank, world_size=W)
@@ -141,9 +150,10 @@ def _worker(rank, port, q):
             got = rs.moe.out[:M].cpu().double().numpy()
             worst_moe = max(worst_moe, (np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)).max())
         assert worst_o <= 2e-2 and worst_l <= 1e-5 and worst_moe <= 2e-2, (worst_o, worst_l, worst_moe)
-        dist.barrier()
-        rs.close()
         q.put((rank, "ok", len(rs.m_ids), worst_o, worst_l, worst_moe))
+        import datetime
+        dist.monitored_barrier(timeout=datetime.timedelta(seconds=300))  # the peer still maps our pools
+        rs.close()
     except Exception:
         q.put((rank, traceback.format_exc(), 0, 0, 0, 0))
     finally:
@@ -154,12 +164,25 @@ def test_two_processes_ipc_dcp_and_moe():
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(W)]
+    log_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(log_dir, exist_ok=True)
+    procs = [ctx.Process(target=_worker, args=(r, port, q, log_dir)) for r in range(W)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=600) for _ in range(W))
+    res = []
+    deadline = time.time() + 600
+    while len(res) < W and time.time() < deadline:
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [(i, p.exitcode) for i, p in enumerate(procs) if p.exitcode not in (None, 0)]
+            assert not dead, f"rank(s) died without a result: {dead} (see gpurun_out/ipc_rank*.log)"
     for p in procs:
         p.join(timeout=120)
+        if p.exitcode is None:
+            p.kill()
+    assert len(res) == W, f"only {len(res)} of {W} ranks reported: {res} (see gpurun_out/ipc_rank*.log)"
+    res.sort()
     for rank, msg, m, wo, wl, wm in res:
         assert msg == "ok", f"rank {rank}:\n{msg}"
         print(f"rank {rank}: {m} M rows, 3 steps: O rel-L2 {wo:.2e}, LSE {wl:.2e}, MoE {wm:.2e}")
