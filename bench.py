@@ -37,7 +37,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HQ, HKV, D, PAGE = 32, 8, 128, 16
-METRIC = "decode tok/s (split-KV paged decode attention step, cfg2: 64 req, KV 1K-32K, GQA 32q/8kv, d128, bf16 paged)"
+METRIC = ("decode tok/s per attention layer (split-KV paged decode attention step, cfg2: 64 req, KV 1K-32K, "
+          "GQA 32q/8kv, d128, bf16 paged)")
 UNIT = "tok/s"
 METRIC_MULTI = ("decode tok/s (DCP decode step on N GPUs: K2 -> K1 -> K3 attention exchange + K4/K5 MoE "
                 "dispatch/combine, per attention+MoE layer)")
@@ -130,11 +131,18 @@ def _max_over_ranks(x, ws, device):
 
 
 # ------------------------------------------------------------------ CPU reference
-def cpu_reference_sample(steps: int, token_budget: int = 262_144, threads: int = 0):
-    """Time dcpsim::sharded_attention_merge (the reference, oracle/_ref) over a
-    bounded prefix of the cfg2 requests, outer OpenMP over (request, q-head)
-    (BASELINE.md §4.3).  Returns (tok/s extrapolated to the full cfg2 step,
-    info dict)."""
+def _tiled(n, seed, block=1 << 24):
+    """n fp32 values: a seeded N(0,1) block of 64 MB (> L3) repeated; the reference's work is
+    independent of the values, so only the footprint matters."""
+    rng = np.random.default_rng(seed)
+    return np.resize(rng.standard_normal(min(n, block), dtype=np.float32), n)
+
+
+def cpu_reference_sample(steps: int, warmup: int = 0, token_budget: int | None = None, threads: int = 0):
+    """Time dcpsim::sharded_attention_merge (the reference compiled from its sources, oracle/_ref)
+    on the cfg2 step: all 64 requests (or the first requests up to token_budget), fp32, one
+    shard per request, outer OpenMP over (request, q-head) on all host threads (BASELINE.md
+    §4.3).  Returns (tok/s of the full cfg2 step, info)."""
     from tests import oracle_lib
     from paper_2605_21100_b200 import workload
     L = oracle_lib.reference()
@@ -142,18 +150,19 @@ def cpu_reference_sample(steps: int, token_budget: int = 262_144, threads: int =
     if L is None:
         raise RuntimeError("oracle/_ref/libdcpsim_ref.so missing (build with make -C oracle)")
     lens = workload.cfg2_lengths()
-    n, tot = 0, 0
-    while n < len(lens) and tot < token_budget:
-        tot += lens[n]
-        n += 1
+    n = len(lens)
+    if token_budget is not None:
+        n, tot = 0, 0
+        while n < len(lens) and tot < token_budget:
+            tot += lens[n]
+            n += 1
     sl = np.array(lens[:n], np.int64)
-    rng = np.random.default_rng(0)
-    q = rng.standard_normal((n, HQ, D), dtype=np.float32)
+    q = np.random.default_rng(0).standard_normal((n, HQ, D), dtype=np.float32)
     kv_off = np.zeros(n, np.int64)
     kv_off[1:] = np.cumsum(sl[:-1] * HKV * D)
     kv_elems = int(sl.sum()) * HKV * D
-    k = rng.standard_normal(kv_elems, dtype=np.float32)
-    v = rng.standard_normal(kv_elems, dtype=np.float32)
+    k = _tiled(kv_elems, 1)
+    v = _tiled(kv_elems, 2)
     bounds = sl.copy()                       # one shard per request (CP = 1 on one GPU)
     bounds_off = np.arange(n, dtype=np.int64)
     nb = np.ones(n, np.int32)
@@ -161,19 +170,23 @@ def cpu_reference_sample(steps: int, token_budget: int = 262_144, threads: int =
     th = threads or os.cpu_count() or 1
     P = oracle_lib.P
     times = []
-    for _ in range(max(steps, 1)):
+    for i in range(warmup + max(steps, 1)):
         t0 = time.perf_counter()
         rc = L.dcpref_batch_decode_attn_f32(n, HQ, HKV, D, 1.0 / math.sqrt(D), P(q), P(k), P(v),
                                             P(kv_off), P(sl), P(bounds), P(bounds_off), P(nb), P(out), th)
-        times.append(time.perf_counter() - t0)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
         assert rc == 0
     full_tokens = sum(lens)
-    per_step_full = min(times) * full_tokens / float(sl.sum())
+    full = n == len(lens)
+    per_step = float(np.mean(times)) * (1.0 if full else full_tokens / float(sl.sum()))
+    what = ("all 64 cfg2 requests" if full else
+            f"first {n} of 64 cfg2 requests ({int(sl.sum())} of {full_tokens} KV tokens), scaled by token ratio")
     info = {"kind": kind, "cores": th,
-            "sample": f"first {n} of 64 cfg2 requests ({int(sl.sum())} of {full_tokens} KV tokens, "
-                      f"fp32, one shard each), best of {len(times)}; tok/s scaled by token ratio",
-            "sample_s": min(times)}
-    return 64.0 / per_step_full, info
+            "sample": f"{what}: {int(sl.sum())} KV tokens, fp32, one shard each, mean of {len(times)} steps "
+                      f"after {warmup} warm-up",
+            "sample_s": float(np.mean(times)), "same_config": full}
+    return 64.0 / per_step, info
 
 
 # ------------------------------------------------------------------ planner path
@@ -189,7 +202,8 @@ def _planner_trace():
 
 
 def planner_device(ctx):
-    """K6 step + K7 routing on the device for PLANNER_SCENARIO (CUDA events)."""
+    """K6 + K7 on the device for PLANNER_SCENARIO (CUDA events): the 2,336-admission round,
+    the 64-admission round (which also rebalances the 2,336 actives), and K7 routing."""
     import torch
     from paper_2605_21100_b200.planner import DevicePlanner
     tr = _planner_trace()
@@ -197,60 +211,77 @@ def planner_device(ctx):
     times = []
     for rep in range(3):
         pl = DevicePlanner(ctx, 1, 8, 16, cap, "dcp", None, max_requests=4096, reserve_pages=8)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
         pl.enqueue_many([r[0] for r in tr[:2336]], [r[1] for r in tr[:2336]])
-        assert len(pl.step()["committed"]) == 2336
-        pl.enqueue_many([r[0] for r in tr[2336:]], [r[1] for r in tr[2336:]])
-        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        torch.cuda.synchronize()
         e[0].record()
         pl.step_async()
         e[1].record()
-        pl.build_routing()
+        assert len(pl.step_result()["committed"]) == 2336
+        pl.enqueue_many([r[0] for r in tr[2336:]], [r[1] for r in tr[2336:]])
+        torch.cuda.synchronize()
         e[2].record()
+        pl.step_async()
+        e[3].record()
+        pl.build_routing()
+        e[4].record()
         r = pl.step_result()
         torch.cuda.synchronize()
         assert len(r["committed"]) == 64
-        times.append((e[0].elapsed_time(e[1]) * 1e3, e[1].elapsed_time(e[2]) * 1e3))
+        times.append((e[2].elapsed_time(e[3]) * 1e3, e[3].elapsed_time(e[4]) * 1e3, e[0].elapsed_time(e[1]) * 1e3))
         pl.close()
-    best = min(times)
-    return {"device_step_us": best[0], "device_routing_us": best[1]}
+    best = [min(t[i] for t in times) for i in range(3)]
+    return {"device_step_us": best[0], "device_routing_us": best[1], "device_admit_2336_us": best[2]}
 
 
 def planner_cpu_reference():
-    """The same round through the reference (oracle/_ref, single thread)."""
+    """The same rounds through the reference (oracle/_ref, one host thread): Scheduler::step for
+    the 2,336- and the 64-admission rounds, and build_binding_config + derive_routing_tables
+    alone (no CSV writer)."""
     from tests import oracle_lib
     L = oracle_lib.reference()
     tr = _planner_trace()
-    best_s, best_r = 1e9, 1e9
+    best_a, best_s, best_r = 1e9, 1e9, 1e9
     for rep in range(3):
         w = oracle_lib.World(L, "dcpref_", 1, 8, 16, 1 << 21, "dcp")
         for rid, ln in tr[:2336]:
             w.enqueue(rid, ln)
-        w.step()
+        t0 = time.perf_counter()
+        assert len(w.step()["committed"]) == 2336
+        t1 = time.perf_counter()
         for rid, ln in tr[2336:]:
             w.enqueue(rid, ln)
-        t0 = time.perf_counter()
-        r = w.step()
-        t1 = time.perf_counter()
-        w.routing_csv()  # build_binding_config + derive_routing_tables + the CSV writer
         t2 = time.perf_counter()
+        r = w.step()
+        t3 = time.perf_counter()
         assert len(r["committed"]) == 64
-        best_s, best_r = min(best_s, t1 - t0), min(best_r, t2 - t1)
-    return {"cpu_reference_step_us": best_s * 1e6, "cpu_reference_routing_and_csv_us": best_r * 1e6, "cores": 1}
+        best_a, best_s = min(best_a, t1 - t0), min(best_s, t3 - t2)
+        best_r = min(best_r, w.time_routing_ns(5) * 1e-9)
+    return {"cpu_reference_admit_2336_us": best_a * 1e6, "cpu_reference_step_us": best_s * 1e6,
+            "cpu_reference_routing_us": best_r * 1e6, "cores": 1}
+
+
+def _host_ram_ok(gb):
+    try:
+        import psutil
+        return psutil.virtual_memory().available > gb * 1e9
+    except Exception:
+        return True
 
 
 def run_reference(args, ws, rank):
     if rank != 0:
         return
-    steps = max(1, min(args.steps, 5))
-    for _ in range(min(args.warmup, 1)):
-        cpu_reference_sample(1)
-    val, info = cpu_reference_sample(steps)
+    # the whole cfg2 step (1.07M tokens, 8.75 GB of fp32 K/V on the host) when RAM allows
+    budget = None if _host_ram_ok(12) else 262_144
+    val, info = cpu_reference_sample(args.steps, args.warmup, token_budget=budget)
     line = {
-        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
+        "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 64.0 / val * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": WORKLOAD, "parallelism": "cpu", "l2": "n/a (host)"},
+        "config": {"workload": WORKLOAD, "parallelism": "cpu", "l2": "n/a (host)",
+                   "same_config": info["same_config"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                          "sample": info["sample"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -369,6 +400,31 @@ def run_ours(args, ws, rank, local):
         except Exception:
             traffic = None
 
+    # ---- the same step over shuffled frames (a long-running instance after frees), not the
+    # fresh-instance LIFO layout above: every page a random 64 KB frame of the pool
+    shuffled = None
+    if rank == 0 and ws == 1:
+        del sets
+        b_s, pool_s, q_s = workload.cfg2_bench_inputs(dev, seed=1234 + rank, frame_order="shuffled")
+        att_s = DecodeAttention(ctx, HQ, HKV, D, PAGE, max_shards=64)
+        att_s.prepare(q_s, pool_s, torch.from_numpy(b_s.block_table).to(dev), torch.from_numpy(b_s.cu_pages).to(dev),
+                      torch.from_numpy(b_s.shard_len).to(dev))
+        for _ in range(3):
+            att_s.launch(stream)
+        ns = min(args.steps, 50)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        for _ in range(ns):
+            att_s.launch(stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ms_s = e0.elapsed_time(e1) / ns
+        gbs_s = b_s.algorithmic_bytes() / (ms_s / 1e3) / 1e9
+        shuffled = {"frame_order": "shuffled (seeded permutation of 70,925 frames)", "steps": ns, "ms_per_step": ms_s,
+                    "tok_s": 64 / (ms_s / 1e3), "achieved_gbs": gbs_s}
+        del att_s, pool_s, q_s
+
     planner = None
     if rank == 0:
         try:
@@ -388,7 +444,7 @@ def run_ours(args, ws, rank, local):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            v, info = cpu_reference_sample(1)
+            v, info = cpu_reference_sample(2, 1, token_budget=None if _host_ram_ok(12) else 262_144)
             cpu = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                    "sample": info["sample"]}
             if planner is not None and "error" not in planner:
@@ -414,6 +470,7 @@ def run_ours(args, ws, rank, local):
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel": "splitkv_decode_kernel<8,4>",
                          "algorithmic_bytes_per_launch": alg_bytes},
+            "shuffled_frames": dict(shuffled, frac=shuffled["achieved_gbs"] / peak) if shuffled else None,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "planner": planner,

@@ -33,7 +33,8 @@ def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p.get("bf16_tflops_sustained", p["bf16_tflops"])), "measured"
+        # K10 is timed alone over a short run: the burst bf16 figure is its tensor peak
+        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "measured (burst bf16)"
     except Exception:
         return 6650.0, 1590.0, "fallback"
 

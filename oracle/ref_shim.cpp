@@ -9,6 +9,7 @@
 // (git-ignored, shipped to the GPU box by gpurun).  Nothing here re-implements
 // reference behaviour; every function forwards to the dcpsim_ref:: symbol named
 // in its comment.
+#include <chrono>
 #include <omp.h>
 
 #include <cstdint>
@@ -356,6 +357,29 @@ int dcpref_world_dump_routing(void* h, char* buf, int64_t cap) {
     });
     if (rc) return rc;
     return copy_string(s, buf, cap);
+}
+
+// Timing of the reference's routing build alone: build_binding_config + derive_routing_tables
+// (routing.cpp:9-63) over the Active requests, no CSV; best of `reps` in nanoseconds.
+int dcpref_world_time_routing(void* h, int reps, int64_t* best_ns) {
+    auto* w = static_cast<World*>(h);
+    std::vector<const R::Request*> act;
+    for (auto& r : w->requests)
+        if (r.state == R::RequestState::Active) act.push_back(&r);
+    int64_t best = INT64_MAX;
+    size_t sink = 0;
+    int rc = guarded([&] {
+        for (int i = 0; i < reps; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            auto cfg = R::build_binding_config(act, w->cluster.topo.world_size());
+            auto rt = R::derive_routing_tables(cfg);
+            const auto t1 = std::chrono::steady_clock::now();
+            sink += rt.size();
+            best = std::min<int64_t>(best, std::chrono::duration_cast<std::chrono::nanoseconds>(t1 - t0).count());
+        }
+    });
+    *best_ns = sink ? best : best;
+    return rc;
 }
 
 // dcpsim::uniform_int / mt19937_64 (workload.hpp:18-26): n draws in [lo, hi].

@@ -63,6 +63,7 @@ def _load(path, prefix):
         sigs["sharded_attention_merge_f32"] = (c_int, [vp, vp, vp, c_int64, c_int, c_float, vp, c_int, c_int, vp])
         sigs["batch_decode_attn_f32"] = (c_int, [c_int, c_int, c_int, c_int, c_float] + [vp] * 9 + [c_int])
         sigs["gen_trace"] = (c_int, [c_uint64, c_double, c_double, c_double, c_int, vp, vp, vp, vp, c_int])
+        sigs["world_time_routing"] = (c_int, [c_void_p, c_int, vp])
     for name, (res, args) in sigs.items():
         f = getattr(L, prefix + name)
         f.restype = res
@@ -220,3 +221,9 @@ class World:
 
     def routing_csv(self):
         return self._dump("world_dump_routing")
+
+    def time_routing_ns(self, reps=5):
+        """Reference only: best-of-reps ns of build_binding_config + derive_routing_tables."""
+        t = np.zeros(1, np.int64)
+        assert self.L.dcpref_world_time_routing(self.h, reps, P(t)) == 0
+        return int(t[0])
