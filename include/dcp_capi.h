@@ -174,6 +174,7 @@ typedef struct dcp_mla_args {
 DCP_API size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards);
 DCP_API int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* args, void* stream);
 DCP_API int dcp_mla_launches_per_call(void);
+
 /* Diagnostics: record globaltimer stamps into a device buffer of 2048 + 3 x 256
  * int64: [0, 2048) = 256 x 8 for CTA pair 0 (per tile: MMA before-QK, after-QK,
  * after-P wait, after-PV; softmax S-ready / P-published for CTA 0 and CTA 1),
@@ -339,6 +340,16 @@ DCP_API int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance
  * created with q_elem_bytes 4 (fp32 Q rows); kv_pool fp32 as dcp_splitkv_decode_attn_f32. */
 DCP_API int dcp_decode_attn_routed_f32(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
                                        const dcp_attn_args* a, void* stream);
+/* K10 routed: the MLA decode of this instance's N list inside a DCP step (Fig. 7 phase 2
+ * for cfg5).  The exchange must be MLA-shaped (num_q_heads 128, q_dim 576, o_dim 512,
+ * q_elem_bytes 2): Q rows come from the receive pool after each row's Q-route flag, O and
+ * LSE are stored into m_r's result slot and its flag published (Res-route put), so
+ * dcp_route_q before and dcp_merge_partials after complete the step.  `a` supplies
+ * kv_pool, num_frames, page_size, scale and a workspace of
+ * dcp_mla_workspace_bytes(ctx, n_max) bytes; its q / shard arrays / out / lse are ignored.
+ * Four launches (tile scan, ticket reset, the CTA-pair kernel, merge + flag publish). */
+DCP_API int dcp_mla_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
+                                       const dcp_mla_args* a, void* stream);
 DCP_API int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream);
 /* Synchronizes the device and reports the exchange error word: DCP_OK, or
  * DCP_E_TIMEOUT with info[0..3] = {code, where (site << 24 | peer << 16 | row),

@@ -169,6 +169,7 @@ _SIGNATURES = [
     ("dcp_route_q", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
     ("dcp_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
     ("dcp_decode_attn_routed_f32", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
+    ("dcp_mla_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(MlaArgs), c_void_p]),
     ("dcp_merge_partials", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
     ("dcp_xchg_status", c_int, [c_void_p, c_void_p]),
     ("dcp_planner_set_policy", c_int, [c_void_p, c_int32, c_int32, c_void_p, c_void_p, c_int32, c_int32]),

@@ -7,6 +7,7 @@
 
 #include "capi_common.cuh"
 #include "mla_decode.cuh"
+#include "xchg_internal.cuh"
 
 namespace dcp {
 
@@ -52,8 +53,14 @@ static int mla_pairs(dcp_ctx* ctx, int* out) {
     return DCP_OK;
 }
 
+// Routed launch context (dcp_mla_decode_attn_routed); NULL for a local call.
+struct MlaRoute {
+    dcp_xchg* x;
+    const dcp_instance_view* v;
+};
+
 template <int PAGE>
-static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) {
+static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream, const MlaRoute* rt = nullptr) {
     auto fn = mla_encode_fn();
     DCP_REQUIRE(fn != nullptr, DCP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
     int pairs = 0;
@@ -61,11 +68,14 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
 
     CUtensorMap qmap, kvq, kvp;
     {
-        cuuint64_t dims[2] = {mla::DK, static_cast<cuuint64_t>(a->num_shards) * mla::H};
+        // routed: both parities of the receive pool, rows (parity * n_max + r) * H + head
+        const void* qbase = rt ? static_cast<const void*>(rt->x->pool + rt->x->host.off_qrecv) : a->q;
+        const cuuint64_t qrows = rt ? 2ull * rt->x->cfg.n_max * mla::H : static_cast<cuuint64_t>(a->num_shards) * mla::H;
+        cuuint64_t dims[2] = {mla::DK, qrows};
         cuuint64_t strides[1] = {mla::DK * 2};
         cuuint32_t box[2] = {64, 64};
         cuuint32_t estr[2] = {1, 1};
-        CUresult r = fn(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(a->q), dims, strides, box, estr,
+        CUresult r = fn(&qmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(qbase), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         DCP_REQUIRE(r == CUDA_SUCCESS, DCP_E_CUDA, "q tensor map (%d)", static_cast<int>(r));
@@ -98,7 +108,17 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream) 
     p.cu_tiles = reinterpret_cast<int32_t*>(ws);
     ws += (static_cast<size_t>(a->num_shards) + 1) * sizeof(int32_t);
     p.pair_t0 = reinterpret_cast<int32_t*>(ws);
+    ws += (static_cast<size_t>(pairs) + 1) * sizeof(int32_t);
     p.num_pairs = pairs;
+    if (rt) {
+        p.xp = rt->x->dev;
+        p.n_mrow = rt->v->n_mrow;
+        p.n_moe = rt->v->n_moe;
+        p.num_shards_ptr = rt->v->n_count_dev;
+        p.q_rows = rt->x->cfg.n_max;
+        p.tickets = reinterpret_cast<int32_t*>(ws);
+        DCP_CUDA_TRY(cudaMemsetAsync(p.tickets, 0, static_cast<size_t>(a->num_shards) * sizeof(int32_t), stream));
+    }
     static const int seg_tiles = [] { const char* e = std::getenv("DCP_MLA_SEG_TILES"); return e ? std::atoi(e) : 4; }();
     p.seg_tiles = seg_tiles;
     p.num_shards = a->num_shards;
@@ -133,6 +153,7 @@ size_t dcp_mla_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards) {
     b += slots * mla::H * 2 * sizeof(float);                      // ws_ml
     b += (static_cast<size_t>(num_shards) + 1) * sizeof(int32_t); // cu_tiles
     b += (slots / 2 + 1) * sizeof(int32_t);                       // pair_t0
+    b += static_cast<size_t>(num_shards) * sizeof(int32_t);       // routed-mode merge tickets
     return (b + 255) & ~size_t(255);
 }
 
@@ -168,6 +189,41 @@ int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* a, void* stream) {
     if (a->page_size == 16) return mla_launch<16>(ctx, a, s);
     if (a->page_size == 32) return mla_launch<32>(ctx, a, s);
     return mla_launch<64>(ctx, a, s);
+}
+
+int dcp_mla_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_mla_args* a0,
+                               void* stream) {
+    DCP_REQUIRE(ctx && x && v && a0, DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
+    DCP_REQUIRE(v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW, "N %d > n_max %d", v->n_rows, x->cfg.n_max);
+    DCP_REQUIRE(x->cfg.num_q_heads == mla::H && x->cfg.q_dim == mla::DK && x->cfg.o_dim == mla::DL &&
+                    x->cfg.q_elem_bytes == 2,
+                DCP_E_INVALID_ARG, "exchange pools must be MLA-shaped (128 heads, q_dim 576, o_dim 512, bf16 Q)");
+    DCP_REQUIRE(a0->num_q_heads == mla::H && a0->kv_lora_rank == mla::DL && a0->rope_dim == mla::DR,
+                DCP_E_UNSUPPORTED, "MLA shape");
+    DCP_REQUIRE(a0->page_size == 16 || a0->page_size == 32 || a0->page_size == 64, DCP_E_UNSUPPORTED,
+                "page_size %d (compiled: 16, 32, 64)", a0->page_size);
+    DCP_REQUIRE(a0->kv_pool && a0->workspace && a0->num_frames > 0 && a0->num_frames < (int64_t(1) << 31),
+                DCP_E_INVALID_ARG, "kv_pool / workspace / num_frames");
+    DCP_REQUIRE((reinterpret_cast<uintptr_t>(a0->kv_pool) & 15) == 0, DCP_E_INVALID_ARG, "kv_pool alignment");
+    // shard arrays from the view; grids sized for n_max shards (R is read on the device)
+    dcp_mla_args a = *a0;
+    a.num_shards = x->cfg.n_max;
+    a.block_table = v->block_table;
+    a.cu_pages = v->cu_pages;
+    a.shard_len = v->shard_len;
+    a.page_fill = v->page_fill;
+    a.q = nullptr;
+    a.out = nullptr;
+    a.lse = nullptr;
+    const size_t need = dcp_mla_workspace_bytes(ctx, a.num_shards);
+    DCP_REQUIRE(a.workspace_bytes >= need, DCP_E_INVALID_ARG, "workspace %zu < %zu bytes (size it for n_max)",
+                a.workspace_bytes, need);
+    const MlaRoute rt{x, v};
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (a.page_size == 16) return mla_launch<16>(ctx, &a, s, &rt);
+    if (a.page_size == 32) return mla_launch<32>(ctx, &a, s, &rt);
+    return mla_launch<64>(ctx, &a, s, &rt);
 }
 
 }  // extern "C"

@@ -36,6 +36,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include "exchange.cuh"
 #include "ptx.cuh"
 #include "tc05.cuh"
 
@@ -127,7 +128,33 @@ struct MlaParams {
     float scale_log2;
     int32_t dbg;                 // bottleneck experiments (compile-time -DDCP_MLA_DBG=n only): 1 = no MMAs, 2 = no softmax math
     long long* trace;            // optional [256][8] globaltimer stamps of pair 0 + [256][3] per pair (dcp_mla_set_trace)
+    // ---- routed mode (DCP exchange, exchange.cuh); NULL for a local call.  Q rows come from
+    // this instance's receive pool (the q map spans both parities: row (parity * q_rows + r) * H),
+    // each shard's Q-route flag is awaited before its Q load, and O / LSE go to m_r's result
+    // slot, whose flag the merge launch publishes once every write of the shard is done.
+    const XchgPeers* xp;
+    const int32_t* n_mrow;       // [R] row of the shard's request in m_r's M list
+    const int32_t* n_moe;        // [R] m_r
+    const int32_t* num_shards_ptr;  // device-resident R (overrides num_shards)
+    int32_t* tickets;            // [n_max] merge-CTA tickets per shard (self-resetting)
+    int32_t q_rows;              // rows of one parity of the receive pool (n_max)
 };
+
+__device__ __forceinline__ int num_shards_of(const MlaParams& p) {
+    return p.num_shards_ptr ? *p.num_shards_ptr : p.num_shards;
+}
+__device__ __forceinline__ uint32_t epoch_of(const MlaParams& p) { return p.xp ? *p.xp->epoch : 0u; }
+// shard r's normalised output row block [H][DL] and LSE [H]: local, or m_r's result slot
+__device__ __forceinline__ float* out_of(const MlaParams& p, int r, uint32_t ep) {
+    if (!p.xp) return p.out + static_cast<size_t>(r) * H * DL;
+    const XchgPeers& x = *p.xp;
+    return xres_o(x, p.n_moe[r], ep) + (static_cast<size_t>(p.n_mrow[r]) * x.W + x.self) * H * DL;
+}
+__device__ __forceinline__ float* lse_of(const MlaParams& p, int r, uint32_t ep) {
+    if (!p.xp) return p.lse + static_cast<size_t>(r) * H;
+    const XchgPeers& x = *p.xp;
+    return xres_lse(x, p.n_moe[r], ep) + (static_cast<size_t>(p.n_mrow[r]) * x.W + x.self) * H;
+}
 
 __device__ __forceinline__ long long gtime() {
     long long t;
@@ -163,7 +190,7 @@ __global__ void __launch_bounds__(1024) mla_tile_scan_kernel(MlaParams p) {
     __shared__ int32_t carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    const int R = p.num_shards;
+    const int R = num_shards_of(p);
     for (int base = 0; base < R; base += 1024) {
         const int r = base + threadIdx.x;
         int v = 0;
@@ -245,7 +272,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t cta = tc::cluster_ctarank();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int R = p.num_shards;
+    const int R = num_shards_of(p);
+    const uint32_t ep = epoch_of(p);
     const int pair = blockIdx.x >> 1;
     const int t_begin = p.pair_t0[pair];
     const int t_end = p.pair_t0[pair + 1];
@@ -327,12 +355,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 if (rk == RQA && ik == 0) {  // Q rows of this shard (this CTA's 64 heads), 9 boxes issued by lanes 0-8
                     if (lane == 0) {
                         if (seg > 0) tc::mbar_wait_sleep(misc + BAR_QEMPTY, (seg - 1) & 1);
+                        if (p.xp) {  // routed: the Q-route put of this row must have landed
+                            wait_flag(xq_flag(*p.xp, p.xp->self, ep) + r, ep, p.xp->wc,
+                                      (SITE_K10_Q << 24) | (r & 0xffff));
+                            asm volatile("fence.proxy.async.global;" ::: "memory");  // generic -> TMA reads
+                        }
                         if (cta == 0) mbar_arrive_expect_tx(misc + BAR_QFULL, 2 * Q_BYTES);
                     }
                     __syncwarp();
+                    const int qrow = p.xp ? (static_cast<int>(ep & 1) * p.q_rows + r) * H : r * H;
                     if (lane < NKB)
                         tc::tma_load_2d_pair(sbase + OFF_Q + lane * 8192, &q_map, 64 * lane,
-                                             r * H + 64 * static_cast<int>(cta), lead + BAR_QFULL, pol_norm);
+                                             qrow + 64 * static_cast<int>(cta), lead + BAR_QFULL, pol_norm);
                 }
                 for (int t = t0; t < t1; ++t) {
                     const int f_next = (t + 1 < t1) ? tile_frame(t + 1) : 0;
@@ -633,7 +667,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const bool complete = (t0 == r_first) && (t1 == r_last);
                 const int slot = 2 * pair + (t0 == t_begin ? 0 : 1);
                 const float inv = complete ? 1.f / l_tot : 1.f;
-                float* dst = complete ? p.out + (static_cast<size_t>(r) * H + head) * DL
+                float* dst = complete ? out_of(p, r, ep) + static_cast<size_t>(head) * DL
                                       : p.ws_acc + (static_cast<size_t>(slot) * H + head) * DL;
 #pragma unroll 1
                 for (int c = 0; c < 256; c += 32) {
@@ -651,7 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_OEMPTY);
                 if (complete) {
-                    if (half == 0) p.lse[static_cast<size_t>(r) * H + head] = (m_used + __log2f(l_tot)) * 0.69314718055994530942f;
+                    if (half == 0) lse_of(p, r, ep)[head] = (m_used + __log2f(l_tot)) * 0.69314718055994530942f;
                 } else if (half == 0) {  // cut segment: (max, sum) of the partial; mla_merge_kernel combines
                     __stcg(reinterpret_cast<float2*>(p.ws_ml) + (static_cast<size_t>(slot) * H + head),
                            make_float2(m_used, l_tot));
@@ -729,43 +763,66 @@ __device__ __forceinline__ void merge_cols(const MlaParams& p, int a, int b, int
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) den += __shfl_xor_sync(0xffffffffu, den, s);
     const float dinv = 1.f / den;
-    float4* o = reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL) + col4;
+    const uint32_t ep = epoch_of(p);
+    float4* o = reinterpret_cast<float4*>(out_of(p, r, ep) + static_cast<size_t>(qh) * DL) + col4;
 #pragma unroll
     for (int v = 0; v < NV; ++v)
         o[lane + 32 * v] = make_float4(num[v].x * dinv, num[v].y * dinv, num[v].z * dinv, num[v].w * dinv);
-    if (write_lse && lane == 0)
-        p.lse[static_cast<size_t>(r) * H + qh] = (mmax + __log2f(den)) * 0.69314718055994530942f;
+    if (write_lse && lane == 0) lse_of(p, r, ep)[qh] = (mmax + __log2f(den)) * 0.69314718055994530942f;
+}
+
+// Routed mode: the last of the shard's CTAs publishes its Res-route flag.  Every CTA fences
+// at system scope before its ticket, so the release covers all of the shard's remote writes,
+// including those of the decode launch (complete shards), which finished before this launch.
+__device__ __forceinline__ void merge_done(const MlaParams& p, int r) {
+    if (!p.xp) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        const int n = gridDim.y * gridDim.z;
+        if (atomicAdd(p.tickets + r, 1) == n - 1) {
+            p.tickets[r] = 0;
+            const XchgPeers& x = *p.xp;
+            const uint32_t ep = *x.epoch;
+            st_release_sys(xres_flag(x, p.n_moe[r], ep) + static_cast<size_t>(p.n_mrow[r]) * x.W + x.self, ep);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(512, 2) mla_merge_kernel(MlaParams p, int num_pairs) {
     const int r = blockIdx.x;
+    if (r >= num_shards_of(p)) return;  // routed launches cover n_max shards
     const int r_first = p.cu_tiles[r], r_last = p.cu_tiles[r + 1];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int qh = blockIdx.y * 16 + warp;
     constexpr int QV = DL / 4 / MERGE_QUARTERS;  // float4 columns per quarter (32)
+    const uint32_t ep = epoch_of(p);
     if (r_first == r_last) {  // zero-token shard: O = 0, LSE = -inf (its merge weight is 0)
-        reinterpret_cast<float4*>(p.out + (static_cast<size_t>(r) * H + qh) * DL)[blockIdx.z * QV + lane] =
+        reinterpret_cast<float4*>(out_of(p, r, ep) + static_cast<size_t>(qh) * DL)[blockIdx.z * QV + lane] =
             make_float4(0.f, 0.f, 0.f, 0.f);
-        if (blockIdx.z == 0 && lane == 0) p.lse[static_cast<size_t>(r) * H + qh] = -INFINITY;
+        if (blockIdx.z == 0 && lane == 0) lse_of(p, r, ep)[qh] = -INFINITY;
+        merge_done(p, r);
         return;
     }
     const int a = pair_of_tile(p.pair_t0, num_pairs, r_first);
     const int b = pair_of_tile(p.pair_t0, num_pairs, r_last - 1);
-    if (a == b) return;  // one pair covered the whole shard and wrote the final output
     const bool short_span = b - a < MERGE_SHORT;
-    if (short_span && blockIdx.z != 0) return;
-    auto slot_of = [&](int k) { return (k == a && r_first != p.pair_t0[k]) ? 2 * k + 1 : 2 * k; };
-    float mmax = -INFINITY;
-    for (int k = a + lane; k <= b; k += 32) {
-        if (!pair_nonempty(p.pair_t0, k)) continue;
-        mmax = fmaxf(mmax, __ldcg(p.ws_ml + (static_cast<size_t>(slot_of(k)) * H + qh) * 2));
-    }
+    // a == b: one pair covered the whole shard and wrote the final output
+    if (a != b && (!short_span || blockIdx.z == 0)) {
+        auto slot_of = [&](int k) { return (k == a && r_first != p.pair_t0[k]) ? 2 * k + 1 : 2 * k; };
+        float mmax = -INFINITY;
+        for (int k = a + lane; k <= b; k += 32) {
+            if (!pair_nonempty(p.pair_t0, k)) continue;
+            mmax = fmaxf(mmax, __ldcg(p.ws_ml + (static_cast<size_t>(slot_of(k)) * H + qh) * 2));
+        }
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, s));
-    if (short_span)
-        merge_cols<MERGE_QUARTERS, 2>(p, a, b, r_first, r, qh, 0, mmax, true);
-    else
-        merge_cols<1, 6>(p, a, b, r_first, r, qh, blockIdx.z * QV, mmax, blockIdx.z == 0);
+        for (int s = 16; s > 0; s >>= 1) mmax = fmaxf(mmax, __shfl_xor_sync(0xffffffffu, mmax, s));
+        if (short_span)
+            merge_cols<MERGE_QUARTERS, 2>(p, a, b, r_first, r, qh, 0, mmax, true);
+        else
+            merge_cols<1, 6>(p, a, b, r_first, r, qh, blockIdx.z * QV, mmax, blockIdx.z == 0);
+    }
+    merge_done(p, r);
 }
 
 }  // namespace mla

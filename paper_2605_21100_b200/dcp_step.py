@@ -123,6 +123,56 @@ class DcpInstance:
             pass
 
 
+class MlaDcpInstance(DcpInstance):
+    """One instance of a routed DCP step with MLA attention (cfg5, K10 on tcgen05 CTA pairs).
+
+    The exchange pools are MLA-shaped: Q rows of 128 heads x 576 (absorbed q_nope | q_pe,
+    bf16), partial O rows of 128 x 512 fp32 + LSE.  KV pool: bf16 [frames, page, 576]
+    (c_kv | k_pe).  Steps are dcp_route_q -> dcp_mla_decode_attn_routed -> dcp_merge_partials.
+    """
+
+    HEADS, DK, DV = 128, 576, 512
+
+    def __init__(self, ctx: DcpContext, world: int, self_id: int, capacity_pages: int, page_size: int = 16,
+                 n_max: int = 256, m_max: int = 128, kv_pool: torch.Tensor | None = None, timeout_ms: int = 0,
+                 scale: float | None = None):
+        L = _capi.lib()
+        self.ctx, self.world, self.id = ctx, world, self_id
+        self.hq, self.hkv, self.d, self.page = self.HEADS, 1, self.DV, page_size
+        self.n_max, self.m_max, self.dtype, self.tdtype = n_max, m_max, "bf16", torch.bfloat16
+        cfg = _capi.XchgConfig(world, self_id, self.HEADS, self.DV, n_max, m_max, self.DK, self.DV, 2, timeout_ms)
+        h = ctypes.c_void_p()
+        _capi.check(L.dcp_xchg_create(ctx.handle, ctypes.byref(cfg), ctypes.byref(h)))
+        self.x = h
+        dev = torch.device("cuda", ctx.device)
+        self.kv_pool = kv_pool if kv_pool is not None else torch.zeros(
+            max(capacity_pages, 1), page_size, self.DK, dtype=torch.bfloat16, device=dev)
+        nbytes = L.dcp_mla_workspace_bytes(ctx.handle, n_max)
+        self.workspace = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+        ql, qr, out, lse = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        _capi.check(L.dcp_xchg_buffers(h, ctypes.byref(ql), ctypes.byref(qr), ctypes.byref(out),
+                                       ctypes.byref(lse)))
+        self.q_local_ptr, self.out_ptr, self.lse_ptr = ql.value, out.value, lse.value
+        a = self.margs = _capi.MlaArgs()
+        a.num_q_heads, a.kv_lora_rank, a.rope_dim, a.page_size = self.HEADS, self.DV, self.DK - self.DV, page_size
+        a.num_frames = self.kv_pool.shape[0]
+        a.kv_pool = self.kv_pool.data_ptr()
+        a.scale = scale if scale is not None else 1.0 / math.sqrt(192.0)
+        a.workspace, a.workspace_bytes = self.workspace.data_ptr(), self.workspace.numel()
+
+    def run(self, view: _capi.InstanceView, stream=None, phase: str = "all"):
+        L = _capi.lib()
+        s = ctypes.c_void_p((stream or torch.cuda.current_stream(self.ctx.device)).cuda_stream)
+        if phase in ("all", "q"):
+            _capi.check(L.dcp_xchg_begin_step(self.x, s))
+            _capi.check(L.dcp_route_q(self.x, ctypes.byref(view), s))
+        if phase in ("all", "attn"):
+            _capi.check(L.dcp_mla_decode_attn_routed(self.ctx.handle, self.x, ctypes.byref(view),
+                                                     ctypes.byref(self.margs), s))
+        if phase in ("all", "merge"):
+            _capi.check(L.dcp_merge_partials(self.x, ctypes.byref(view), s))
+
+
 class StepGraph:
     """AOT step graphs of one instance (dcp_step_graph_*): one captured CUDA
     graph per M-bucket of the default ShapeSpace, replayed per decode step."""

@@ -123,3 +123,67 @@ def test_mla_many_shards(ctx):
     b, q, pool = _case(lens.tolist(), seed=21, spare=3)
     out, lse = _run(ctx, b, q, pool)
     _check(b, q, pool, out, lse)
+
+
+@pytest.mark.parametrize("W", [4, 8])
+def test_mla_routed_dcp_step(ctx, W):
+    """cfg5-shaped DCP attention split across W instances (one GPU, same code path as across
+    GPUs): K6 -> K7 -> K2 (576-wide Q rows) -> K10 routed (Q-route flag waits, O / LSE into
+    m_r's 512-wide result slots) -> K3, two consecutive steps; every request and head against
+    shard_attention<double> on each instance's tokens + lse_merge (bf16 bar)."""
+    from paper_2605_21100_b200._capi import device_to_numpy
+    from paper_2605_21100_b200.dcp_step import MlaDcpInstance, run_local_step
+    from paper_2605_21100_b200.planner import DevicePlanner
+    from tests.test_dcp_step_gpu import _oracle_merge
+    I64MAX = 2**63 - 1
+    dev = torch.device("cuda:0")
+    cap = 3000
+    pl = DevicePlanner(ctx, 1, W, 16, cap, "dcp", [[3000, 1], [20000, 2], [I64MAX, W]], max_requests=64)
+    rng = np.random.default_rng(W)
+    lens = [90000, 25000, 17, 1, 4000] + rng.integers(1, 6000, size=10).tolist()
+    pl.enqueue_many(list(range(len(lens))), lens)
+    assert len(pl.step()["committed"]) == len(lens)
+    assert len(pl.placement(0)["kv"]) == W
+    g = torch.Generator(device=dev).manual_seed(9)
+    insts = []
+    for s in range(W):
+        pool = torch.randn(cap, 16, DK, generator=g, device=dev).to(torch.bfloat16)
+        insts.append(MlaDcpInstance(ctx, W, s, cap, kv_pool=pool, n_max=64, m_max=32))
+    for s in range(W):
+        for t in range(W):
+            insts[s].set_peer_local(t, insts[t])
+        insts[s].commit()
+    port = oracle_lib.port()
+    active = list(range(len(lens)))
+    for step in range(2):
+        q = {i: torch.randn(128, DK, generator=g, device=dev).to(torch.bfloat16) for i in active}
+        res, views = run_local_step(pl, insts, q)
+        partial = {}
+        for s in range(W):
+            v = views[s]
+            n = v.n_rows
+            cu = device_to_numpy(v.cu_pages, n + 1, np.int32)
+            nid = device_to_numpy(v.n_ids, n, np.int64)
+            b = workload.PagedBatch(device_to_numpy(v.shard_len, n, np.int64), cu,
+                                    device_to_numpy(v.block_table, int(cu[-1]), np.int32), cap, 128, 1, DK, 16)
+            fill = device_to_numpy(v.page_fill, int(cu[-1]), np.uint8)
+            qs = torch.stack([q[int(r)] for r in nid]).cpu()
+            o, l = oracle_lib.mla_decode_f64(b, _bits(qs), _bits(insts[s].kv_pool.cpu()), fill)
+            for j, r in enumerate(nid):
+                partial[(int(r), s)] = (o[j], l[j])
+        worst_o = worst_l = 0.0
+        for r in active:
+            kv = pl.placement(r)["kv"]
+            for h in range(128):
+                ro, rl = _oracle_merge(port, [partial[(r, s)][0][h] for s in kv],
+                                       [partial[(r, s)][1][h] for s in kv], 512)
+                o = res[r][0][h].astype(np.float64)
+                worst_o = max(worst_o, np.linalg.norm(o - ro) / np.linalg.norm(ro))
+                worst_l = max(worst_l, abs(float(res[r][1][h]) - rl) / max(1.0, abs(rl)))
+        print(f"MLA routed W={W} step {step}: worst O rel-L2 {worst_o:.3e}, LSE {worst_l:.3e}")
+        assert worst_o <= O_TOL, worst_o
+        assert worst_l <= LSE_TOL, worst_l
+        pl.append_many(active)
+    for x in insts:
+        x.close()
+    pl.close()
