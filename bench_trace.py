@@ -182,6 +182,11 @@ def main():
     ap.add_argument("--max-iters", type=int, default=4000)
     ap.add_argument("--uniform-degree", type=int, default=8)
     ap.add_argument("--policies", default="dcp,least_batch,least_cache,uniform")
+    ap.add_argument("--trace-csv", default="",
+                    help="replay this trace file (the reference's id,arrival_ms,seq_len,output_len format, "
+                         "workload.cpp:108-137) instead of generating one")
+    ap.add_argument("--write-trace", default="",
+                    help="write the generated trace to this CSV file (write_trace_csv format) before replaying it")
     ap.add_argument("--sweep-rates", default="",
                     help="comma-separated ascending rates: P99-TPOT sweep + max sustainable rate (SPEC.md:449-455)")
     args = ap.parse_args()
@@ -198,8 +203,17 @@ def main():
     rates = [float(x) for x in args.sweep_rates.split(",") if x] or [args.rate]
     by_policy = {}
     for rate in rates:
-        trace = workload.gen_trace(args.seed, args.long_ratio, rate, args.duration, poisson=True,
-                                   output_len=(args.out_min, args.out_max))
+        if args.trace_csv:
+            with open(args.trace_csv) as f:
+                trace = workload.load_trace_csv(f.read())
+        else:
+            trace = workload.gen_trace(args.seed, args.long_ratio, rate, args.duration, poisson=True,
+                                       output_len=(args.out_min, args.out_max))
+            if args.write_trace:
+                with open(args.write_trace, "w") as f:
+                    f.write(workload.write_trace_csv(trace))
+                # replay exactly what the file holds (arrivals rounded to the file's 3 decimals)
+                trace = workload.load_trace_csv(workload.write_trace_csv(trace))
         longs = sum(1 for r in trace if r[2] >= 100000)
         print(json.dumps({"trace": {"requests": len(trace), "long": longs, "rate_per_s": rate,
                                     "duration_s": args.duration, "long_ratio": args.long_ratio,

@@ -133,6 +133,10 @@ DCP_API int dcp_splitkv_decode_attn_f32(dcp_ctx* ctx, const dcp_attn_args* args,
 /* Number of kernel launches the last dcp_splitkv_decode_attn issued (for the
  * bench's gpu_launches accounting). */
 DCP_API int dcp_attn_launches_per_call(void);
+/* Debug: per-CTA globaltimer stamps of later K1 launches into a device buffer of
+ * num_sms x 8 int64 (NULL = off): entry, first ring stage, last segment end, ticket,
+ * merge end, exit, SM id, pages. */
+DCP_API int dcp_k1_set_trace(void* dev_buf);
 
 /* ---- K10: MLA split-KV paged decode attention (tcgen05, CTA pairs) ------------
  *
@@ -474,6 +478,10 @@ DCP_API const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x);
 DCP_API int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream);
 DCP_API int dcp_moe_combine_put_regions(dcp_moe* x, const void* y_region, void* stream);
 /* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */
+/* Gate-weighted identity expert stage (region mode): y_region[s][j] = (sum of row j's local
+ * gate weights) * x_region[s][j] for every received row, reading this step's regions through
+ * the device epoch (graph-safe).  The stand-in for the expert FFN in benches and graphs. */
+DCP_API int dcp_moe_expert_identity(dcp_moe* x, void* y_region, void* stream);
 DCP_API int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream);
 
 /* ---- AOT step graphs (Alg. 2; ShapeSpace routing.hpp:60-85) --
@@ -493,6 +501,49 @@ DCP_API int dcp_step_graph_launch(dcp_step_graph* g, int32_t m_rows, int32_t n_r
 DCP_API int dcp_step_graph_count(const dcp_step_graph* g, int32_t* buckets);
 DCP_API int dcp_step_graph_destroy(dcp_step_graph* g);
 
+/* ---- Whole-layer AOT decode graphs (Alg. 2, 805-840, widened to the layer) ----
+ * One instance's decode layer captured per (M-bucket, MoE step parity):
+ *   [K7 dcp_planner_build_routing] -> dcp_xchg_begin_step -> K2 -> K1-routed -> K3
+ *   -> dcp_moe_begin_step -> K4 dispatch -> K5a receive (regions) -> expert stage
+ *   -> K5b combine_put (regions) -> K5c combine_reduce
+ * and replayed once per decode step with dcp_layer_graph_launch.  All per-step metadata
+ * is read on the device (K7 output), so a replay copies nothing in.  The M-bucket only
+ * sizes the K2 / K3 grids (ShapeSpace M-hat ladder 8..m_max); any bucket is correct.
+ * planner: optional; when set, K7 runs inside the graph (re-captured automatically if
+ *   the planner's page arena was compacted since).
+ * moe: optional (attention only when NULL); moe_x bf16 [m_max][hidden] (M-row order),
+ *   topk_idx / topk_w [m_max][topk], y_region bf16 [world][m_max][hidden], moe_out fp32
+ *   [m_max][hidden] — device buffers the graph reads / writes every replay.
+ * expert: the expert stage, called at capture time to enqueue its work on `stream`
+ *   (library GEMMs), with the receive regions of `parity` (bf16 [world][m_max][hidden],
+ *   meta int32 [world][m_max][dcp_moe_meta_width]) and the device per-source counts; it
+ *   must fill y_region.  NULL = dcp_moe_expert_identity.
+ * Every instance of the step must replay its own graph (or run the same calls eagerly) once
+ * per step; peers synchronise through the exchange flags as in the eager path. */
+typedef void (*dcp_expert_fn)(void* user, void* stream, int32_t parity, void* x_region,
+                              int32_t* meta_region, const int32_t* recv_counts_dev, void* y_region);
+typedef struct dcp_layer_graph_desc {
+    dcp_planner* planner;
+    dcp_xchg* xchg;
+    const dcp_instance_view* view;
+    const dcp_attn_args* attn;       /* bf16 routed K1 arguments (kv_pool, workspace, scale) */
+    dcp_moe* moe;
+    const void* moe_x;
+    const int32_t* topk_idx;
+    const float* topk_w;
+    void* y_region;
+    float* moe_out;
+    dcp_expert_fn expert;
+    void* expert_user;
+} dcp_layer_graph_desc;
+typedef struct dcp_layer_graph dcp_layer_graph;
+DCP_API int dcp_layer_graph_create(dcp_ctx* ctx, const dcp_layer_graph_desc* desc, dcp_layer_graph** out);
+/* m_rows: this step's M (or any upper bound <= m_max) picks the bucket. */
+DCP_API int dcp_layer_graph_launch(dcp_layer_graph* g, int32_t m_rows, void* stream);
+/* Returns the executable graph count; buckets / captures (1 + re-captures) if non-NULL. */
+DCP_API int dcp_layer_graph_info(const dcp_layer_graph* g, int32_t* buckets, int32_t* captures);
+DCP_API int dcp_layer_graph_destroy(dcp_layer_graph* g);
+
 /* ---- K8: kv_append — the decode step's new K/V into the paged pools ----------
  * After dcp_planner_append_token + dcp_planner_build_routing, write each
  * request's new-token K and V (bf16 [M][2][num_kv_heads][head_dim], in the
@@ -503,6 +554,22 @@ DCP_API int dcp_step_graph_destroy(dcp_step_graph* g);
  * from this device (local pointer, or a peer / CUDA-IPC mapping). */
 DCP_API int dcp_kv_append(dcp_planner* pl, int32_t instance, const void* kv_new, void* const* pools,
                           int32_t num_kv_heads, int32_t head_dim, void* stream);
+
+/* ---- KV migration: prefill -> decode (steps MIGRATE / TRANSFER) ----
+ * After dcp_planner_step admitted requests ids[0..n) (GlobalPageTable::allocate,
+ * page_table.cpp:9-49, chose their frames), copy each request's prefill K and V
+ * — src_k[i], src_v[i]: [seq_len][num_kv_heads][head_dim] elements of elem_bytes
+ * (2 = bf16, 4 = fp32), readable from this device (local or peer / CUDA-IPC
+ * mapped) — into those frames: logical page j, held by (instance, frame) of the
+ * page table, receives the request's tokens [sum of the earlier pages' fills, +
+ * fill_j), i.e. each kv_binding member its split in order.  pools[s] (host array
+ * of W device pointers) is instance s's pool [frames][2][num_kv_heads][page][head_dim]
+ * as addressable from this device; stores to remote instances go over NVLink.
+ * One kernel launch, stream-ordered.  UnknownRequest(-2) for an id the planner
+ * does not track, InvalidArgument for one that holds no pages. */
+DCP_API int dcp_kv_migrate(dcp_planner* pl, const int64_t* ids, int32_t n, const void* const* src_k,
+                           const void* const* src_v, void* const* pools, int32_t num_kv_heads,
+                           int32_t head_dim, int32_t elem_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -413,4 +413,42 @@ int dcpref_gen_trace(uint64_t seed, double long_ratio, double rate, double durat
     return (int)t.size();
 }
 
+// dcpsim::gen_trace + dcpsim::write_trace_csv (workload.cpp:108-115): the CSV text of a
+// generated trace; returns the full length (copies at most cap-1 bytes + NUL).
+int64_t dcpref_trace_csv(uint64_t seed, double long_ratio, double rate, double duration_s, int poisson,
+                         char* buf, int64_t cap) {
+    R::TraceConfig c;
+    c.short_dist = R::sharegpt4o_distribution();
+    c.long_dist = R::github_issue_distribution();
+    c.long_ratio = long_ratio;
+    c.arrival.kind = poisson ? R::ArrivalKind::Poisson : R::ArrivalKind::ConstantRate;
+    c.arrival.rate_per_s = rate;
+    c.duration_s = duration_s;
+    c.seed = seed;
+    std::ostringstream os;
+    int rc = guarded([&] { R::write_trace_csv(R::gen_trace(c), os); });
+    if (rc) return rc;
+    return copy_string(os.str(), buf, cap);
+}
+
+// dcpsim::load_trace_csv (workload.cpp:117-137) over CSV text; returns the request count
+// (fills at most cap) or a negative error code (ConfigError for an empty file).
+int dcpref_load_trace_csv(const char* text, int64_t* ids, double* arrival_ms, int64_t* seq_len,
+                          int64_t* out_len, int cap) {
+    std::vector<R::Request> t;
+    int rc = guarded([&] {
+        std::istringstream is(text);
+        t = R::load_trace_csv(is);
+    });
+    if (rc) return rc;
+    const int n = (int)t.size() < cap ? (int)t.size() : cap;
+    for (int i = 0; i < n; ++i) {
+        ids[i] = t[i].id;
+        arrival_ms[i] = t[i].arrival_ms;
+        seq_len[i] = t[i].seq_len;
+        out_len[i] = t[i].output_len;
+    }
+    return (int)t.size();
+}
+
 }  // extern "C"

@@ -124,6 +124,16 @@ class XchgConfig(Structure):
                 ("q_elem_bytes", c_int32), ("timeout_ms", c_int32)]
 
 
+EXPERT_FN = ctypes.CFUNCTYPE(None, c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p)
+
+
+class LayerGraphDesc(Structure):
+    _fields_ = [("planner", c_void_p), ("xchg", c_void_p), ("view", POINTER(InstanceView)),
+                ("attn", POINTER(AttnArgs)), ("moe", c_void_p), ("moe_x", c_void_p), ("topk_idx", c_void_p),
+                ("topk_w", c_void_p), ("y_region", c_void_p), ("moe_out", c_void_p), ("expert", EXPERT_FN),
+                ("expert_user", c_void_p)]
+
+
 _lib = None
 
 # (name, restype, argtypes) for every entry point of include/dcp_capi.h.
@@ -191,6 +201,9 @@ _SIGNATURES = [
     ("dcp_step_graph_count", c_int, [c_void_p, c_void_p]),
     ("dcp_step_graph_destroy", c_int, [c_void_p]),
     ("dcp_kv_append", c_int, [c_void_p, c_int32, c_void_p, c_void_p, c_int32, c_int32, c_void_p]),
+    ("dcp_k1_set_trace", c_int, [c_void_p]),
+    ("dcp_kv_migrate", c_int, [c_void_p, c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                               c_int32, c_void_p]),
     ("dcp_moe_create", c_int, [c_void_p, POINTER(MoeConfig), POINTER(c_void_p)]),
     ("dcp_moe_destroy", c_int, [c_void_p]),
     ("dcp_moe_ipc_handle", c_int, [c_void_p, c_void_p]),
@@ -210,6 +223,11 @@ _SIGNATURES = [
     ("dcp_moe_recv_counts_dev", c_void_p, [c_void_p]),
     ("dcp_moe_combine_put", c_int, [c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_combine_reduce", c_int, [c_void_p, c_void_p, c_void_p]),
+    ("dcp_moe_expert_identity", c_int, [c_void_p, c_void_p, c_void_p]),
+    ("dcp_layer_graph_create", c_int, [c_void_p, POINTER(LayerGraphDesc), POINTER(c_void_p)]),
+    ("dcp_layer_graph_launch", c_int, [c_void_p, c_int32, c_void_p]),
+    ("dcp_layer_graph_info", c_int, [c_void_p, c_void_p, c_void_p]),
+    ("dcp_layer_graph_destroy", c_int, [c_void_p]),
 ]
 
 

@@ -122,9 +122,13 @@ static bool k1_split() {
     return v != 0;
 }
 
-static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm, int hkv, int G,
+static long long* g_k1_trace = nullptr;
+
+static int dispatch_decode(dcp_ctx* ctx, const CUtensorMap* map, const AttnParams& prm0, int hkv, int G,
                            cudaStream_t s, int page = 16) {
     const bool sp = k1_split();
+    AttnParams prm = prm0;
+    prm.trace = g_k1_trace;
 #define DCP_K1(H_, G_)                                                                                  \
     if (hkv == H_ && G == G_) {                                                                          \
         if (page == 32) return launch_decode<H_, G_, true, 32>(ctx, map, prm, s);                        \
@@ -229,6 +233,14 @@ size_t dcp_attn_workspace_bytes(const dcp_ctx* ctx, int32_t num_shards, int32_t 
 }
 
 int dcp_attn_launches_per_call(void) { return 1; }
+
+/* Debug: per-CTA globaltimer stamps of the next K1 launches into a device buffer of
+ * num_sms x 8 int64 (NULL = off): entry, first ring stage, segment end, ticket, merge end,
+ * exit, SM id, pages. */
+int dcp_k1_set_trace(void* dev_buf) {
+    g_k1_trace = static_cast<long long*>(dev_buf);
+    return DCP_OK;
+}
 
 int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) {
     DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");

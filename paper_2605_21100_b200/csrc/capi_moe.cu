@@ -5,24 +5,10 @@
 #include "capi_common.cuh"
 #include <cstdlib>
 #include "moe.cuh"
+#include "moe_internal.cuh"
 
 using namespace dcp;
 
-struct dcp_moe {
-    dcp_ctx* ctx = nullptr;
-    dcp_moe_config cfg{};
-    char* pool = nullptr;
-    char* local = nullptr;
-    MoePeers host{};
-    MoePeers* dev = nullptr;
-    uint32_t* epoch = nullptr;
-    uint32_t* err = nullptr;
-    uint32_t host_epoch = 0;           // mirror of the device epoch (begin_step calls)
-    const int32_t* m_count_dev = nullptr;
-    bool received = false;
-    bool committed = false;
-    void* opened[PL_MAXW] = {};
-};
 
 namespace {
 size_t al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -255,6 +241,16 @@ int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream) { return c
 
 int dcp_moe_combine_put_regions(dcp_moe* x, const void* y_region, void* stream) {
     return combine_put(x, y_region, 1, stream);
+}
+
+int dcp_moe_expert_identity(dcp_moe* x, void* y_region, void* stream) {
+    DCP_REQUIRE(x && y_region && x->received, DCP_E_INVALID_ARG, "call dcp_moe_receive_regions first");
+    int grid = (x->cfg.world * x->cfg.m_max + 7) / 8;
+    if (grid > 2 * x->ctx->num_sms) grid = 2 * x->ctx->num_sms;
+    moe_expert_identity_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        x->host, static_cast<__nv_bfloat16*>(y_region));
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
 }
 
 int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {

@@ -51,6 +51,51 @@ __global__ void kv_append_kernel(PlannerState st, const int32_t* m_slot, const i
     }
 }
 
+// KV migration (MIGRATE / TRANSFER): request blockIdx.y's prefill K and V,
+// contiguous [len][hkv][row] (row = d * elem bytes), go into the frames its placement holds.
+// Logical page j holds the request's tokens [sum_{i<j} fill_i, + fill_j) — allocate lays the
+// pages out member by member in kv_binding order (page_table.cpp:28-44) and append_token only
+// extends the list — so each CTA sums the fills before its page range, then walks its pages.
+// Every (part, head, token) row is 16-byte vectors: consecutive threads take consecutive
+// vectors of a row, so source reads and frame writes (local or over NVLink) are coalesced.
+__global__ void __launch_bounds__(256) kv_migrate_kernel(PlannerState st, const int32_t* slots,
+                                                         const char* const* src_k, const char* const* src_v,
+                                                         char* const* pools, int hkv, int row_bytes) {
+    const int sl = slots[blockIdx.y];
+    const int64_t off = st.page_off[sl];
+    const int cnt = st.page_cnt[sl];
+    const int p0 = static_cast<int>((int64_t)blockIdx.x * cnt / gridDim.x);
+    const int p1 = static_cast<int>((int64_t)(blockIdx.x + 1) * cnt / gridDim.x);
+    if (p0 >= p1) return;
+    __shared__ int64_t s_part[8];
+    int64_t before = 0;
+    for (int j = threadIdx.x; j < p0; j += blockDim.x) before += st.pg_fill[off + j];
+    for (int o = 16; o; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+    if ((threadIdx.x & 31) == 0) s_part[threadIdx.x >> 5] = before;
+    __syncthreads();
+    int64_t tok0 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tok0 += s_part[w];
+    const int vec = row_bytes / 16;
+    const char* k = src_k[blockIdx.y];
+    const char* v = src_v[blockIdx.y];
+    const int64_t page = st.page;
+    for (int j = p0; j < p1; ++j) {
+        const int inst = st.pg_inst[off + j];
+        const int64_t frame = st.pg_frame[off + j];
+        const int fill = st.pg_fill[off + j];
+        char* fb = pools[inst] + frame * 2 * hkv * page * row_bytes;
+        const int per_part = hkv * fill * vec;
+        for (int i = threadIdx.x; i < 2 * per_part; i += blockDim.x) {
+            const int part = i / per_part, rem = i % per_part;
+            const int h = rem / (fill * vec), t = (rem / vec) % fill, x = rem % vec;
+            const uint4* s = reinterpret_cast<const uint4*>((part ? v : k) + ((tok0 + t) * hkv + h) * row_bytes) + x;
+            uint4* dd = reinterpret_cast<uint4*>(fb + ((part * hkv + h) * page + t) * row_bytes) + x;
+            *dd = __ldg(s);
+        }
+        tok0 += fill;
+    }
+}
+
 __global__ void enqueue_kernel(PlannerState st, const int32_t* slots, const int64_t* ids,
                                const int64_t* lens, int n) {
     const int base = *st.nwait;
@@ -104,6 +149,7 @@ int compact_arena(dcp_planner* pl) {
     std::swap(st.pg_inst, pl->arena2_inst);
     std::swap(st.pg_frame, pl->arena2_frame);
     std::swap(st.pg_fill, pl->arena2_fill);
+    ++pl->generation;  // captured graphs holding the old arena pointers must be re-captured
     return sync_arena_top(pl);
 }
 
@@ -648,6 +694,50 @@ int dcp_kv_append(dcp_planner* pl, int32_t s, const void* kv_new, void* const* p
                                          static_cast<const __nv_bfloat16*>(kv_new), pl->d_pools, hkv, d);
     DCP_CUDA_TRY(cudaGetLastError());
     DCP_CUDA_TRY(cudaStreamSynchronize(st));  // the staged pool table is reused
+    return DCP_OK;
+}
+
+int dcp_kv_migrate(dcp_planner* pl, const int64_t* ids, int32_t n, const void* const* src_k,
+                   const void* const* src_v, void* const* pools, int32_t hkv, int32_t head_dim, int32_t elem_bytes,
+                   void* stream) {
+    DCP_REQUIRE(pl && (n == 0 || (ids && src_k && src_v && pools)), DCP_E_INVALID_ARG, "NULL argument");
+    DCP_REQUIRE(n >= 0 && n <= 65535, DCP_E_INVALID_ARG, "n %d", n);
+    DCP_REQUIRE(hkv >= 1 && head_dim >= 1 && (elem_bytes == 2 || elem_bytes == 4), DCP_E_UNSUPPORTED,
+                "elem_bytes %d", elem_bytes);
+    const int row_bytes = head_dim * elem_bytes;
+    DCP_REQUIRE(row_bytes % 16 == 0, DCP_E_UNSUPPORTED, "head_dim x elem_bytes must be a multiple of 16");
+    if (n == 0) return DCP_OK;
+    const int W = pl->st.W;
+    std::vector<int32_t> slots(n);
+    for (int i = 0; i < n; ++i) {
+        auto it = pl->slot_of.find(ids[i]);
+        DCP_REQUIRE(it != pl->slot_of.end(), DCP_E_UNKNOWN_REQUEST, "unknown request %lld", (long long)ids[i]);
+        DCP_REQUIRE(pl->is_active[it->second], DCP_E_INVALID_ARG, "request %lld holds no pages (not admitted)",
+                    (long long)ids[i]);
+        DCP_REQUIRE(src_k[i] && src_v[i], DCP_E_INVALID_ARG, "NULL source of request %lld", (long long)ids[i]);
+        DCP_REQUIRE((reinterpret_cast<uintptr_t>(src_k[i]) | reinterpret_cast<uintptr_t>(src_v[i])) % 16 == 0,
+                    DCP_E_INVALID_ARG, "sources must be 16-byte aligned");
+        slots[i] = it->second;
+    }
+    for (int s = 0; s < W; ++s) DCP_REQUIRE(pools[s], DCP_E_INVALID_ARG, "pool of instance %d is NULL", s);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // one staging block: slots | src_k | src_v | pools
+    const size_t bytes = n * 4 + 8 + 2 * (size_t)n * 8 + (size_t)W * 8;
+    std::vector<char> h(bytes);
+    std::memcpy(h.data(), slots.data(), n * 4);
+    const size_t ok = (n * 4 + 7) & ~size_t(7);
+    std::memcpy(h.data() + ok, src_k, n * 8);
+    std::memcpy(h.data() + ok + n * 8, src_v, n * 8);
+    std::memcpy(h.data() + ok + 2 * n * 8, pools, W * 8);
+    char* d = nullptr;
+    DCP_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&d), bytes, st));
+    DCP_CUDA_TRY(cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st));
+    kv_migrate_kernel<<<dim3(64, n), 256, 0, st>>>(
+        pl->st, reinterpret_cast<const int32_t*>(d), reinterpret_cast<const char* const*>(d + ok),
+        reinterpret_cast<const char* const*>(d + ok + n * 8), reinterpret_cast<char* const*>(d + ok + 2 * n * 8),
+        hkv, row_bytes);
+    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(cudaFreeAsync(d, st));  // h was staged by the pageable copy before it returned
     return DCP_OK;
 }
 

@@ -14,6 +14,19 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+namespace dcp {
+int xchg_route_q_grid(dcp_xchg* x, const dcp_instance_view* v, int grid, cudaStream_t s) {
+    q_route_put_kernel<<<grid, 128, 0, s>>>(x->host, x->q_local, v->m_count_all, v->m_nrow);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+int xchg_merge_grid(dcp_xchg* x, const dcp_instance_view* v, int grid, cudaStream_t s) {
+    lse_merge_kernel<<<grid, 128, 0, s>>>(x->host, v->m_count_all, v->m_k, v->m_kv, x->out, x->out_lse);
+    DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+}  // namespace dcp
+
 extern "C" {
 
 int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c0, dcp_xchg** out) {

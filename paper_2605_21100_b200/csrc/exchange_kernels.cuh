@@ -17,29 +17,31 @@ static __global__ void __launch_bounds__(128) q_route_put_kernel(const __grid_co
                                                                  const void* __restrict__ q_local,
                                                                  const int32_t* __restrict__ m_count,
                                                                  const int32_t* __restrict__ m_nrow) {
-    const int r = blockIdx.x;
-    if (r >= m_count[x.self]) return;
+    const int M = m_count[x.self];
     const uint32_t ep = *x.epoch;
     const int W = x.W;
     const size_t row_bytes = (size_t)x.hq * x.q_dim * x.q_bytes;
     const int vecs = static_cast<int>(row_bytes / 16);
-    const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(q_local) + r * row_bytes);
     constexpr int U = 4;
-    for (int s = 0; s < W; ++s) {
-        const int row = m_nrow[(size_t)r * W + s];
-        if (row < 0) continue;
-        uint4* dst = reinterpret_cast<uint4*>(xq_recv(x, s, ep) + row * row_bytes);
-        for (int b = threadIdx.x; b < vecs; b += U * blockDim.x) {
-            uint4 v[U];
+    // grid-stride over the M rows: any grid (an M-bucket's, or fewer) covers every row
+    for (int r = blockIdx.x; r < M; r += gridDim.x) {
+        const uint4* src = reinterpret_cast<const uint4*>(static_cast<const char*>(q_local) + r * row_bytes);
+        for (int s = 0; s < W; ++s) {
+            const int row = m_nrow[(size_t)r * W + s];
+            if (row < 0) continue;
+            uint4* dst = reinterpret_cast<uint4*>(xq_recv(x, s, ep) + row * row_bytes);
+            for (int b = threadIdx.x; b < vecs; b += U * blockDim.x) {
+                uint4 v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (b + u * blockDim.x < vecs) v[u] = __ldg(src + b + u * blockDim.x);
+                for (int u = 0; u < U; ++u)
+                    if (b + u * blockDim.x < vecs) v[u] = __ldg(src + b + u * blockDim.x);
 #pragma unroll
-            for (int u = 0; u < U; ++u)
-                if (b + u * blockDim.x < vecs) dst[b + u * blockDim.x] = v[u];
+                for (int u = 0; u < U; ++u)
+                    if (b + u * blockDim.x < vecs) dst[b + u * blockDim.x] = v[u];
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) st_release_sys(xq_flag(x, s, ep) + row, ep);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) st_release_sys(xq_flag(x, s, ep) + row, ep);
     }
 }
 
@@ -53,51 +55,53 @@ static __global__ void __launch_bounds__(128) lse_merge_kernel(const __grid_cons
                                                                const int32_t* __restrict__ m_kv,
                                                                float* __restrict__ out,
                                                                float* __restrict__ out_lse) {
-    const int r = blockIdx.x;
-    if (r >= m_count[x.self]) return;
+    const int M = m_count[x.self];
     const uint32_t ep = *x.epoch;
     const int W = x.W, hq = x.hq, d = x.o_dim;
-    const int k = m_k[r];
     __shared__ int32_t parts[PL_MAXK];
-    if (threadIdx.x < k) {
-        const int s = m_kv[(size_t)r * PL_MAXK + threadIdx.x];
-        parts[threadIdx.x] = s;
-        wait_flag(xres_flag(x, x.self, ep) + (size_t)r * W + s, ep, x.wc,
-                  (SITE_K3_RES << 24) | (s << 16) | (r & 0xffff));
-    }
-    __syncthreads();
-    const float* po = xres_o(x, x.self, ep) + (size_t)r * W * hq * d;
-    const float* pl = xres_lse(x, x.self, ep) + (size_t)r * W * hq;
-    const int chunks = d / 32;  // 32 floats per work item
-    for (int w = threadIdx.x; w < hq * chunks; w += blockDim.x) {
-        const int h = w / chunks, q0 = (w % chunks) * 32;
-        float mx = -INFINITY;
-        for (int i = 0; i < k; ++i) mx = fmaxf(mx, __ldcg(pl + (size_t)parts[i] * hq + h));
-        float acc[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) acc[j] = 0.f;
-        float den = 0.f;
-        for (int i = 0; i < k; ++i) {
-            const int s = parts[i];
-            const float l = __ldcg(pl + (size_t)s * hq + h);
-            const float wgt = l == -INFINITY ? 0.f : expf(l - mx);
-            den += wgt;
-            const float4* v = reinterpret_cast<const float4*>(po + ((size_t)s * hq + h) * d + q0);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float4 t = __ldcg(v + j);
-                acc[4 * j] += wgt * t.x;
-                acc[4 * j + 1] += wgt * t.y;
-                acc[4 * j + 2] += wgt * t.z;
-                acc[4 * j + 3] += wgt * t.w;
-            }
+    for (int r = blockIdx.x; r < M; r += gridDim.x) {  // grid-stride: any grid covers every row
+        const int k = m_k[r];
+        if (threadIdx.x < k) {
+            const int s = m_kv[(size_t)r * PL_MAXK + threadIdx.x];
+            parts[threadIdx.x] = s;
+            wait_flag(xres_flag(x, x.self, ep) + (size_t)r * W + s, ep, x.wc,
+                      (SITE_K3_RES << 24) | (s << 16) | (r & 0xffff));
         }
-        const float inv = 1.f / den;
-        float4* o = reinterpret_cast<float4*>(out + ((size_t)r * hq + h) * d + q0);
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            o[j] = make_float4(acc[4 * j] * inv, acc[4 * j + 1] * inv, acc[4 * j + 2] * inv, acc[4 * j + 3] * inv);
-        if (q0 == 0) out_lse[(size_t)r * hq + h] = mx + logf(den);
+        __syncthreads();
+        const float* po = xres_o(x, x.self, ep) + (size_t)r * W * hq * d;
+        const float* pl = xres_lse(x, x.self, ep) + (size_t)r * W * hq;
+        const int chunks = d / 32;  // 32 floats per work item
+        for (int w = threadIdx.x; w < hq * chunks; w += blockDim.x) {
+            const int h = w / chunks, q0 = (w % chunks) * 32;
+            float mx = -INFINITY;
+            for (int i = 0; i < k; ++i) mx = fmaxf(mx, __ldcg(pl + (size_t)parts[i] * hq + h));
+            float acc[32];
+    #pragma unroll
+            for (int j = 0; j < 32; ++j) acc[j] = 0.f;
+            float den = 0.f;
+            for (int i = 0; i < k; ++i) {
+                const int s = parts[i];
+                const float l = __ldcg(pl + (size_t)s * hq + h);
+                const float wgt = l == -INFINITY ? 0.f : expf(l - mx);
+                den += wgt;
+                const float4* v = reinterpret_cast<const float4*>(po + ((size_t)s * hq + h) * d + q0);
+    #pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const float4 t = __ldcg(v + j);
+                    acc[4 * j] += wgt * t.x;
+                    acc[4 * j + 1] += wgt * t.y;
+                    acc[4 * j + 2] += wgt * t.z;
+                    acc[4 * j + 3] += wgt * t.w;
+                }
+            }
+            const float inv = 1.f / den;
+            float4* o = reinterpret_cast<float4*>(out + ((size_t)r * hq + h) * d + q0);
+    #pragma unroll
+            for (int j = 0; j < 8; ++j)
+                o[j] = make_float4(acc[4 * j] * inv, acc[4 * j + 1] * inv, acc[4 * j + 2] * inv, acc[4 * j + 3] * inv);
+            if (q0 == 0) out_lse[(size_t)r * hq + h] = mx + logf(den);
+        }
+        __syncthreads();  // parts[] is rewritten by the next row
     }
 }
 

@@ -290,6 +290,42 @@ static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const _
     }
 }
 
+// Gate-weighted identity expert stage (region mode): y[s][j] = (sum of the row's local gate
+// weights) * x[s][j] for every received row — the stand-in for the expert FFN (a library GEMM,
+// out of scope) in benches and whole-layer graphs.  Reads this step's region through the device
+// epoch, so a captured graph replays it on either parity.  One warp per row.
+static __global__ void __launch_bounds__(256) moe_expert_identity_kernel(const __grid_constant__ MoePeers p,
+                                                                         __nv_bfloat16* __restrict__ y_region) {
+    const uint32_t ep = *p.epoch;
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    const int R = p.offs[p.W];
+    const __nv_bfloat16* rx = rx_x(p, p.self, ep);
+    const int32_t* rm = rx_meta(p, p.self, ep);
+    const int nvec = p.H / 8;
+    for (int r = warp; r < R; r += nwarps) {
+        int s = 0;
+        while (p.offs[s + 1] <= r) ++s;
+        const size_t row = (size_t)s * p.m_max + (r - p.offs[s]);
+        const int32_t* meta = rm + row * p.meta;
+        const int n = __ldcg(meta + 1);
+        float wsum = 0.f;
+        for (int i = 0; i < n; ++i) wsum += __int_as_float(__ldcg(meta + 3 + 2 * i));
+        const uint4* src = reinterpret_cast<const uint4*>(rx + row * p.H);
+        uint4* dst = reinterpret_cast<uint4*>(y_region + row * p.H);
+        for (int i = lane; i < nvec; i += 32) {
+            uint4 v = __ldcg(src + i);
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float2 f = __bfloat1622float2(h[k]);
+                h[k] = __floats2bfloat162_rn(f.x * wsum, f.y * wsum);
+            }
+            dst[i] = v;
+        }
+    }
+}
+
 // K5b: CTA c returns received rows c, c + C, ... (flattened source-major) to their homes.
 // y_rows: compact [R][H] (row = offs[s] + j) or region [W][m_max][H] (row = s * m_max + j).
 static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const __grid_constant__ MoePeers p,

@@ -43,6 +43,7 @@ struct dcp_planner {
     cudaStream_t stream = nullptr;
     int last_launches = 0;
     bool routing_valid = false;
+    uint64_t generation = 0;         // bumped when device pointers inside `st` change (arena compaction)
     __nv_bfloat16** d_pools = nullptr;  // K8 pool table
 };
 

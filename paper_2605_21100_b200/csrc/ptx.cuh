@@ -106,6 +106,21 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Device-scope ticket with acquire-release semantics: the CTA's stores ordered before it by a
+// barrier are released to the last arriver, which acquires every earlier arriver's (the
+// barrier-then-single-thread pattern of a grid semaphore, without a MEMBAR.SC per thread).
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+    int old;
+    asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
+
+// n / d for non-negative operands, in 32-bit arithmetic when both fit (a 64-bit division is a
+// ~100-instruction software routine).
+__device__ __forceinline__ int64_t udiv64(int64_t n, int64_t d) {
+    return ((n | d) >> 32) == 0 ? static_cast<int64_t>(static_cast<uint32_t>(n) / static_cast<uint32_t>(d)) : n / d;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

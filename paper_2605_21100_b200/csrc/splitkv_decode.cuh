@@ -54,7 +54,14 @@ struct AttnParams {
     const int32_t* n_mrow;       // [R] row of the shard's request in m_r's M list
     const int32_t* n_moe;        // [R] m_r
     const int32_t* num_shards_ptr;  // device-resident R (graph replay); overrides num_shards
+    long long* trace;            // optional [grid][8] globaltimer stamps per CTA (dcp_k1_set_trace)
 };
+
+__device__ __forceinline__ long long k1_gtime() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // Destination of shard r's normalised partial O / LSE: local [R][HQ][D] for a
 // local step, else m_r's result pool slot [mrow][self] (Res-route put, fused).
@@ -112,11 +119,11 @@ struct DecodeCfg {
 
 __device__ __forceinline__ int cta_of_page(int64_t p, int64_t P, int64_t grid) {
     // CTA c owns pages [floor(c*P/grid), floor((c+1)*P/grid)).
-    return static_cast<int>(((p + 1) * grid + P - 1) / P - 1);
+    return static_cast<int>(udiv64((p + 1) * grid + P - 1, P) - 1);
 }
 // With fewer pages than CTAs some ranges are empty; those CTAs hold no partial.
 __device__ __forceinline__ bool cta_nonempty(int64_t k, int64_t P, int64_t grid) {
-    return P >= grid || (k * P / grid) < ((k + 1) * P / grid);
+    return P >= grid || udiv64(k * P, grid) < udiv64((k + 1) * P, grid);
 }
 
 template <int HKV, int G, bool SPLIT = false, int PAGE_ = 16>
@@ -141,9 +148,16 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     const int64_t P = p.cu_pages[R];
     const int64_t grid = gridDim.x;
     const int cta = blockIdx.x;
-    const int p_begin = static_cast<int>(cta * P / grid);
-    const int p_end = static_cast<int>((cta + 1) * P / grid);
+    const int p_begin = static_cast<int>(udiv64(cta * P, grid));
+    const int p_end = static_cast<int>(udiv64((cta + 1) * P, grid));
 
+    if (p.trace && threadIdx.x == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        p.trace[cta * 8 + 0] = k1_gtime();
+        p.trace[cta * 8 + 6] = smid;
+        p.trace[cta * 8 + 7] = p_end - p_begin;
+    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(full_bar + 8 * s, 1);
@@ -215,7 +229,10 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             }
         }
     }
-    if (p_begin >= p_end) return;
+    if (p_begin >= p_end) {
+        if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 5] = k1_gtime();
+        return;
+    }
 
     // Per-lane ldmatrix offsets (stage-relative).  Row & 7 == lane & 7 since
     // every head tile starts on an 8-row boundary (128B swizzle atom).
@@ -312,6 +329,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 fill = rem < C::PAGE ? static_cast<int>(rem) : C::PAGE;
             }
             mbar_wait(full_bar + 8 * s, ph);
+            if (p.trace && it == 0 && c == 0 && threadIdx.x == 0) p.trace[cta * 8 + 1] = k1_gtime();
             // valid tokens of this 16-token chunk (chunks past the page's fill are fully masked;
             // chunk 0 always holds >= 1 token, so the running max is finite before any empty chunk)
             fill = min(16, max(0, fill - 16 * c));
@@ -417,6 +435,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
             l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
         }
+        if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 2] = k1_gtime();
         const bool complete = (seg_begin == r_first) && (seg_end == r_last);
         if (complete) {
             const float ln2 = 0.69314718055994530942f;
@@ -455,88 +474,122 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                     __stcg(reinterpret_cast<float2*>(p.ws_ml) + (static_cast<size_t>(slot) * C::HQ + qh),
                            make_float2(half == 0 ? m0 : m1, half == 0 ? l0 : l1));
             }
-            __threadfence();
-            named_bar_sync(1, NCT);
+            named_bar_sync(1, NCT);  // every warp's partial stores happen-before thread 0's release
             if (threadIdx.x == 0) {
-                const int a = cta_of_page(r_first, P, grid);
-                const int b = cta_of_page(r_last - 1, P, grid);
-                int nparts = b - a + 1;
-                if (P < grid) {
-                    nparts = 0;
-                    for (int k = a; k <= b; ++k) nparts += cta_nonempty(k, P, grid);
-                }
-                const int prev = atomicAdd(p.counters + r, 1);
+                // P >= grid: every CTA of [a, b] holds pages of r; P < grid: every CTA holds at
+                // most one page, so r has one part per page
+                const int nparts = P < grid ? r_last - r_first
+                                            : cta_of_page(r_last - 1, P, grid) - cta_of_page(r_first, P, grid) + 1;
+                const int prev = atom_add_acq_rel_gpu(p.counters + r, 1);
                 *last_flag = (prev == nparts - 1) ? 1 : 0;
             }
             named_bar_sync(1, NCT);
+            if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 3] = k1_gtime();
             if (*last_flag) {
-                __threadfence();
-                const int a = cta_of_page(r_first, P, grid);
-                const int b = cta_of_page(r_last - 1, P, grid);
+                // K9: merge the shard's partials in page order.  Part i is CTA a + i when
+                // P >= grid (slot 2k, or 2k + 1 for CTA a when r starts inside its range), and the
+                // CTA of page r_first + i when P < grid (one page per CTA, slot 2k).  Warp h owns
+                // the G q-heads of kv-head h, lane j columns [4j, 4j+4).  Parts are taken 32 at a
+                // time: each lane loads its part's (max, sum) of all G rows (kept in registers
+                // when the shard has <= 32 parts), the live parts are a ballot, and the numerator
+                // walks them U at a time with all U * G partial rows in flight.
+                const bool sparse = P < grid;
+                const int a = sparse ? 0 : cta_of_page(r_first, P, grid);
+                const int nparts = sparse ? r_last - r_first : cta_of_page(r_last - 1, P, grid) - a + 1;
+                const bool a_mid = !sparse && r_first != static_cast<int>(udiv64((int64_t)a * P, grid));
                 const float ln2 = 0.69314718055994530942f;
-                // lane j handles parts a + j, a + j + 32, ... for (max, sum); the numerator walks the
-                // parts with 4 partial rows in flight (a shard spread over many CTAs -- a long
-                // request's shard on one instance spans ~20 -- would otherwise be a serial tail).
-                auto slot_of = [&](int k) {
-                    return (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;
+                constexpr int U = G >= 16 ? 1 : (G >= 8 ? 2 : 4);
+                auto slot_of_part = [&](int i) {
+                    if (sparse) return 2 * cta_of_page(r_first + i, P, grid);
+                    return 2 * (a + i) + ((i == 0 && a_mid) ? 1 : 0);
                 };
+                const float2* mlp = reinterpret_cast<const float2*>(p.ws_ml);
+                float mmax[G];
+                float2 ml0[G];  // this lane's part of the first 32
+                const int sl0 = lane < nparts ? slot_of_part(lane) : 0;
+#pragma unroll
                 for (int row = 0; row < G; ++row) {
-                    const int qh = h * G + row;
-                    float mloc = -INFINITY;
-                    for (int k = a + lane; k <= b; k += 32)
-                        if (cta_nonempty(k, P, grid))
-                            mloc = fmaxf(mloc, __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
-                                                      (static_cast<size_t>(slot_of(k)) * C::HQ + qh)).x);
+                    ml0[row] = lane < nparts ? __ldcg(mlp + (size_t)sl0 * C::HQ + h * G + row)
+                                             : make_float2(-INFINITY, 0.f);
+                    mmax[row] = ml0[row].x;
+                }
+                for (int base = 32; base < nparts; base += 32) {
+                    if (base + lane < nparts) {
+                        const size_t sl = slot_of_part(base + lane);
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
-                    const float mmax = mloc;
-                    float den = 0.f;
-                    float4 num = make_float4(0.f, 0.f, 0.f, 0.f);
-                    for (int base = a; base <= b; base += 32) {
-                        const int k = base + lane;
-                        float w = 0.f;
-                        int sl = -1;
-                        if (k <= b && cta_nonempty(k, P, grid)) {
-                            sl = slot_of(k);
-                            const float2 ml = __ldcg(reinterpret_cast<const float2*>(p.ws_ml) +
-                                                     (static_cast<size_t>(sl) * C::HQ + qh));
-                            w = fast_exp2(ml.x - mmax);
-                            den += w * ml.y;
-                        }
-                        const int cnt = min(32, b - base + 1);
-                        for (int j = 0; j < cnt; j += 4) {
-                            float4 v[4];
-                            float wj[4];
+                        for (int row = 0; row < G; ++row)
+                            mmax[row] = fmaxf(mmax[row], __ldcg(mlp + sl * C::HQ + h * G + row).x);
+                    }
+                }
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                const int jj = min(j + u, 31);
-                                wj[u] = __shfl_sync(0xffffffffu, w, jj);
-                                const int slj = __shfl_sync(0xffffffffu, sl, jj);
-                                v[u] = (j + u < cnt && slj >= 0)
-                                           ? __ldcg(reinterpret_cast<const float4*>(
-                                                        p.ws_acc + (static_cast<size_t>(slj) * C::HQ + qh) * C::D) +
-                                                    lane)
-                                           : make_float4(0.f, 0.f, 0.f, 0.f);
-                                if (j + u >= cnt) wj[u] = 0.f;
-                            }
+                for (int row = 0; row < G; ++row)
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                num.x += wj[u] * v[u].x;
-                                num.y += wj[u] * v[u].y;
-                                num.z += wj[u] * v[u].z;
-                                num.w += wj[u] * v[u].w;
-                            }
+                    for (int o = 16; o > 0; o >>= 1)
+                        mmax[row] = fmaxf(mmax[row], __shfl_xor_sync(0xffffffffu, mmax[row], o));
+                float den[G];
+                float4 num[G];
+#pragma unroll
+                for (int row = 0; row < G; ++row) {
+                    den[row] = 0.f;
+                    num[row] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                for (int base = 0; base < nparts; base += 32) {
+                    const bool live = base + lane < nparts;
+                    const int sl = base == 0 ? sl0 : (live ? slot_of_part(base + lane) : 0);
+                    float w[G];
+#pragma unroll
+                    for (int row = 0; row < G; ++row) {
+                        w[row] = 0.f;
+                        if (live) {
+                            const float2 ml = base == 0 ? ml0[row] : __ldcg(mlp + (size_t)sl * C::HQ + h * G + row);
+                            w[row] = fast_exp2(ml.x - mmax[row]);
+                            den[row] += w[row] * ml.y;
                         }
                     }
+                    unsigned mask = __ballot_sync(0xffffffffu, live);
+                    while (mask) {
+                        int src[U];
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) den += __shfl_xor_sync(0xffffffffu, den, o);
-                    const float inv = 1.f / den;
+                        for (int u = 0; u < U; ++u) {
+                            src[u] = mask ? __ffs(mask) - 1 : -1;
+                            mask &= mask - 1;
+                        }
+                        float4 v[U][G];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int su = __shfl_sync(0xffffffffu, sl, src[u] < 0 ? 0 : src[u]);
+                            const float4* rowp =
+                                reinterpret_cast<const float4*>(p.ws_acc + ((size_t)su * C::HQ + h * G) * C::D) + lane;
+#pragma unroll
+                            for (int row = 0; row < G; ++row)
+                                v[u][row] = src[u] >= 0 ? __ldcg(rowp + row * (C::D / 4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u)
+#pragma unroll
+                            for (int row = 0; row < G; ++row) {
+                                const float wu = __shfl_sync(0xffffffffu, w[row], src[u] < 0 ? 0 : src[u]);
+                                const float ww = src[u] >= 0 ? wu : 0.f;
+                                num[row].x += ww * v[u][row].x;
+                                num[row].y += ww * v[u][row].y;
+                                num[row].z += ww * v[u][row].z;
+                                num[row].w += ww * v[u][row].w;
+                            }
+                    }
+                }
+#pragma unroll
+                for (int row = 0; row < G; ++row) {
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) den[row] += __shfl_xor_sync(0xffffffffu, den[row], o);
+                    const int qh = h * G + row;
+                    const float inv = 1.f / den[row];
                     float* o = row_out(p, r, C::HQ, C::D, ep) + qh * C::D;
                     reinterpret_cast<float4*>(o)[lane] =
-                        make_float4(num.x * inv, num.y * inv, num.z * inv, num.w * inv);
-                    if (lane == 0) row_lse(p, r, C::HQ, ep)[qh] = (mmax + __log2f(den)) * ln2;
+                        make_float4(num[row].x * inv, num[row].y * inv, num[row].z * inv, num[row].w * inv);
+                    if (lane == 0) row_lse(p, r, C::HQ, ep)[qh] = (mmax[row] + __log2f(den[row])) * ln2;
                 }
                 if (threadIdx.x == 0) p.counters[r] = 0;  // re-arm for the next launch / graph replay
+                if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 4] = k1_gtime();
                 if (p.xp) {
                     named_bar_sync(2, NCT);
                     if (threadIdx.x == 0) publish_row(p, r, ep);
@@ -545,6 +598,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
         }
         ++r;
     }
+    if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 5] = k1_gtime();
 }
 
 }  // namespace dcp

@@ -53,10 +53,10 @@ constexpr int F32_D = 128;
 
 // Stream-K helpers shared with K1.
 __device__ __forceinline__ int f32_cta_of_page(int64_t p, int64_t P, int64_t grid) {
-    return static_cast<int>(((p + 1) * grid + P - 1) / P - 1);
+    return static_cast<int>(udiv64((p + 1) * grid + P - 1, P) - 1);
 }
 __device__ __forceinline__ bool f32_cta_nonempty(int64_t k, int64_t P, int64_t grid) {
-    return P >= grid || (k * P / grid) < ((k + 1) * P / grid);
+    return P >= grid || udiv64(k * P, grid) < udiv64((k + 1) * P, grid);
 }
 
 template <class P>
@@ -98,8 +98,8 @@ __global__ void __launch_bounds__(256) splitkv_decode_f32_kernel(const AttnF32Pa
     const int64_t P = p.cu_pages[R];
     const int64_t grid = gridDim.x;
     const int cta = blockIdx.x;
-    const int p_begin = static_cast<int>(cta * P / grid);
-    const int p_end = static_cast<int>((cta + 1) * P / grid);
+    const int p_begin = static_cast<int>(udiv64(cta * P, grid));
+    const int p_end = static_cast<int>(udiv64((cta + 1) * P, grid));
 
     // zero-token shards: O = 0, LSE = -inf
     for (int r = cta; r < R; r += gridDim.x) {
@@ -234,20 +234,14 @@ __global__ void __launch_bounds__(256) splitkv_decode_f32_kernel(const AttnF32Pa
                 if (lane == 0)
                     __stcg(reinterpret_cast<float2*>(p.ws_ml) + ((size_t)slot * HQ + qh), make_float2(m[g], l[g]));
             }
-            __threadfence();
-            named_bar_sync(1, nthreads);
+            named_bar_sync(1, nthreads);  // the partial stores happen-before thread 0's release
             if (threadIdx.x == 0) {
                 const int a = f32_cta_of_page(r_first, P, grid), b = f32_cta_of_page(r_last - 1, P, grid);
-                int nparts = b - a + 1;
-                if (P < grid) {
-                    nparts = 0;
-                    for (int k = a; k <= b; ++k) nparts += f32_cta_nonempty(k, P, grid);
-                }
-                s_last = atomicAdd(p.counters + r, 1) == nparts - 1;
+                const int nparts = P < grid ? r_last - r_first : b - a + 1;  // P < grid: one page per CTA
+                s_last = atom_add_acq_rel_gpu(p.counters + r, 1) == nparts - 1;
             }
             named_bar_sync(1, nthreads);
             if (s_last) {
-                __threadfence();
                 const int a = f32_cta_of_page(r_first, P, grid), b = f32_cta_of_page(r_last - 1, P, grid);
                 auto slot_of = [&](int k) {
                     return (k == a && r_first != static_cast<int>(k * P / grid)) ? 2 * k + 1 : 2 * k;

@@ -20,3 +20,10 @@ struct dcp_xchg {
     uint32_t* err = nullptr;
     bool committed = false;
 };
+
+namespace dcp {
+// K2 / K3 with an explicit grid (an M-bucket's; the kernels stride over the device M count,
+// so any grid is correct).  Stream-ordered, capturable.
+int xchg_route_q_grid(dcp_xchg* x, const dcp_instance_view* v, int grid, cudaStream_t s);
+int xchg_merge_grid(dcp_xchg* x, const dcp_instance_view* v, int grid, cudaStream_t s);
+}  // namespace dcp

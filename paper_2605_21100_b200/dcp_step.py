@@ -204,6 +204,62 @@ class StepGraph:
             pass
 
 
+class LayerGraph:
+    """Whole-layer AOT decode graphs of one instance (dcp_layer_graph_*; Alg. 2).
+
+    Captures [K7] -> begin -> K2 -> K1 -> K3 -> MoE begin -> K4 -> K5a -> expert -> K5b -> K5c
+    once per (M-bucket, MoE parity) and replays it per decode step.  moe: a MoeInstance or None;
+    moe_x bf16 [m_max, H], topk_idx int32 / topk_w fp32 [m_max, k] are the device buffers the
+    graph reads every replay (write the step's values into them before launch).  expert: a
+    ctypes EXPERT_FN (called at capture time to enqueue the expert stage) or None for the
+    built-in gate-weighted identity expert.  planner: include K7 in the graph.
+    """
+
+    def __init__(self, inst: DcpInstance, view, moe=None, moe_x=None, topk_idx=None, topk_w=None,
+                 planner=None, expert=None):
+        L = _capi.lib()
+        self.inst, self.view, self.moe = inst, view, moe
+        dev = torch.device("cuda", inst.ctx.device)
+        d = _capi.LayerGraphDesc()
+        d.planner = planner.h if planner is not None else None
+        d.xchg = inst.x
+        d.view = ctypes.pointer(view)
+        d.attn = ctypes.pointer(inst.args)
+        if moe is not None:
+            self.y_region = torch.zeros(moe.world, moe.m_max, moe.H, dtype=torch.bfloat16, device=dev)
+            d.moe, d.moe_x = moe.h, moe_x.data_ptr()
+            d.topk_idx, d.topk_w = topk_idx.data_ptr(), topk_w.data_ptr()
+            d.y_region, d.moe_out = self.y_region.data_ptr(), moe.out.data_ptr()
+            self._keep = (moe_x, topk_idx, topk_w)
+        if expert is not None:
+            d.expert = expert
+        self._expert = expert
+        self.desc = d
+        h = ctypes.c_void_p()
+        _capi.check(L.dcp_layer_graph_create(inst.ctx.handle, ctypes.byref(d), ctypes.byref(h)))
+        self.h = h
+
+    def info(self):
+        b, c = ctypes.c_int32(), ctypes.c_int32()
+        n = _capi.lib().dcp_layer_graph_info(self.h, ctypes.byref(b), ctypes.byref(c))
+        return dict(graphs=n, buckets=b.value, captures=c.value)
+
+    def launch(self, m_rows: int, stream=None):
+        s = (stream or torch.cuda.current_stream(self.inst.ctx.device)).cuda_stream
+        _capi.check(_capi.lib().dcp_layer_graph_launch(self.h, m_rows, ctypes.c_void_p(s)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _capi.lib().dcp_layer_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def run_local_step(planner, instances, q_of_request: dict, stream=None):
     """Run one routed step with all instances in this process.
 

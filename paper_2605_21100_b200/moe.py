@@ -146,6 +146,11 @@ class MoeInstance:
             y.index_add_(0, rows, o * wts[:, None])
         self.y_rows[:R] = y.to(torch.bfloat16)
 
+    def expert_identity(self, y_region, stream=None):
+        """Gate-weighted identity expert over this step's regions (dcp_moe_expert_identity)."""
+        _capi.check(_capi.lib().dcp_moe_expert_identity(self.h, ctypes.c_void_p(y_region.data_ptr()),
+                                                        _s(stream, self.ctx.device)))
+
     def combine_put(self, stream=None):
         _capi.check(_capi.lib().dcp_moe_combine_put(self.h, ctypes.c_void_p(self.y_rows.data_ptr()),
                                                     _s(stream, self.ctx.device)))

@@ -143,3 +143,25 @@ class DevicePlanner:
         s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
         hkv, d = kv_new.shape[2], kv_new.shape[3]
         _capi.check(_capi.lib().dcp_kv_append(self.h, instance, ctypes.c_void_p(kv_new.data_ptr()), arr, hkv, d, s))
+
+    def migrate_kv(self, ids, src_k, src_v, pools, stream=None):
+        """Prefill -> decode KV migration (MIGRATE / TRANSFER; dcp_kv_migrate).
+
+        src_k[i], src_v[i]: [seq_len, hkv, d] CUDA tensors (bf16 or fp32) of request ids[i];
+        pools[s]: instance s's pool [frames, 2, hkv, page, d] (same dtype), as addressable
+        from the launching device.  Each logical page of the request's page table receives
+        its tokens, on whichever instance holds the frame."""
+        n = len(ids)
+        if not (len(src_k) == len(src_v) == n) or len(pools) != self.W:
+            raise _capi.DcpInvalidArgument("migrate_kv: ids / sources / pools lengths")
+        idv = np.ascontiguousarray(ids, np.int64)
+        ks = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in src_k])
+        vs = (ctypes.c_void_p * max(n, 1))(*[t.data_ptr() for t in src_v])
+        arr = (ctypes.c_void_p * self.W)(*[p.data_ptr() for p in pools])
+        hkv, d = pools[0].shape[2], pools[0].shape[4]
+        for t in list(src_k) + list(src_v):
+            if t.dtype != pools[0].dtype or not t.is_contiguous() or t.shape[1:] != (hkv, d):
+                raise _capi.DcpInvalidArgument(f"migrate_kv: source {tuple(t.shape)} {t.dtype}")
+        s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else None
+        _capi.check(_capi.lib().dcp_kv_migrate(self.h, _p(idv), n, ks, vs, arr, hkv, d,
+                                               pools[0].element_size(), s))

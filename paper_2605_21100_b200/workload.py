@@ -180,3 +180,34 @@ def gen_trace(seed: int, long_ratio: float, rate_per_s: float, duration_s: float
         L = sample_length(long if is_long else short, rng)
         out.append((i, a, L, uniform_int(rng, output_len[0], output_len[1])))
     return out
+
+
+# ------------------------------------------------------------------ trace files
+# The reference's trace file format (workload.hpp:70-72, workload.cpp:108-137):
+# header "id,arrival_ms,seq_len,output_len", one request per line, arrival with three
+# decimals; loading skips the header and blank lines and orders by (arrival, id).
+TRACE_HEADER = "id,arrival_ms,seq_len,output_len"
+
+
+def write_trace_csv(trace) -> str:
+    """trace: [(id, arrival_ms, seq_len, output_len)] -> CSV text (write_trace_csv)."""
+    lines = [TRACE_HEADER]
+    lines += [f"{int(i)},{a:.3f},{int(L)},{int(o)}" for i, a, L, o in trace]
+    return "\n".join(lines) + "\n"
+
+
+def load_trace_csv(text: str):
+    """CSV text -> [(id, arrival_ms, seq_len, output_len)] sorted by (arrival, id) (load_trace_csv).
+    An empty file is a ConfigError, as in the reference (workload.cpp:120)."""
+    from ._capi import ConfigError
+    lines = text.split("\n")
+    if text == "":
+        raise ConfigError("empty trace file")
+    out = []
+    for line in lines[1:]:
+        if not line:
+            continue
+        f = line.split(",")
+        out.append((int(f[0]), float(f[1]), int(f[2]), int(f[3])))
+    out.sort(key=lambda r: (r[1], r[0]))
+    return out
