@@ -119,7 +119,7 @@ def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup, compact=False):
     res["receive_mode"] = "compact (rows copied out of the pool)" if compact else "region (rows read in place)"
     res["note"] = ("single GPU: cross-instance stores are local HBM stores; expert FFN = identity, untimed; "
                    "each step gated behind a device sleep so CUDA events time device work only; "
-                   "dispatch includes the begin_step fence kernel")
+                   "dispatch is one launch: K4 with the step fence folded in (dcp_moe_step_dispatch)")
     for i in inst:
         i.close()
     return res

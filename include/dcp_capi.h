@@ -355,6 +355,16 @@ DCP_API int dcp_decode_attn_routed_f32(dcp_ctx* ctx, dcp_xchg* x, const dcp_inst
 DCP_API int dcp_mla_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
                                        const dcp_mla_args* a, void* stream);
 DCP_API int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream);
+/* The whole routed step of one instance in ONE launch (Fig. 7 phases 1-4): the step fence
+ * and epoch bump of dcp_xchg_begin_step, K2's Q-route puts in K1's prologue (while the
+ * producer warp already streams KV), K1 + Res-route, and K3's LSE merges of this instance's
+ * M rows in K1's epilogue — outputs where dcp_merge_partials puts them.  Equivalent to
+ * begin_step + route_q + decode_attn_routed + merge_partials, bit for bit.  The epilogue
+ * waits for the peers' partials inside the kernel, so every instance must be able to run
+ * concurrently: one instance per GPU (or per process), or W = 1.  Instances sharing one GPU
+ * in one process use the four phased calls instead. */
+DCP_API int dcp_decode_step_fused(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
+                                  const dcp_attn_args* args, void* stream);
 /* Synchronizes the device and reports the exchange error word: DCP_OK, or
  * DCP_E_TIMEOUT with info[0..3] = {code, where (site << 24 | peer << 16 | row),
  * wanted flag value, last value seen}; the word is cleared.  info may be NULL. */
@@ -456,6 +466,10 @@ DCP_API int32_t dcp_moe_meta_width(const dcp_moe* x);
  * device M count, so the step needs no host round trip). */
 DCP_API int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* topk_idx,
                              const float* topk_w, const int32_t* m_count_dev, void* stream);
+/* dcp_moe_begin_step + dcp_moe_dispatch in ONE launch: K4 runs the step fence before its
+ * first peer store and its last CTA advances the epoch.  Same results, one launch less. */
+DCP_API int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* topk_idx,
+                                  const float* topk_w, const int32_t* m_count_dev, void* stream);
 /* K5a, region mode (the fast path): wait for every source; the received rows stay in
  * this instance's pool, source s's rows at x_region[s * m_max + j], j < count[s]
  * (meta likewise), for the expert stage to read in place.  Per-source counts and
@@ -535,6 +549,7 @@ typedef struct dcp_layer_graph_desc {
     float* moe_out;
     dcp_expert_fn expert;
     void* expert_user;
+    int32_t fused_step;              /* 1: the attention sub-step is one dcp_decode_step_fused launch */
 } dcp_layer_graph_desc;
 typedef struct dcp_layer_graph dcp_layer_graph;
 DCP_API int dcp_layer_graph_create(dcp_ctx* ctx, const dcp_layer_graph_desc* desc, dcp_layer_graph** out);

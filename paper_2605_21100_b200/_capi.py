@@ -131,7 +131,7 @@ class LayerGraphDesc(Structure):
     _fields_ = [("planner", c_void_p), ("xchg", c_void_p), ("view", POINTER(InstanceView)),
                 ("attn", POINTER(AttnArgs)), ("moe", c_void_p), ("moe_x", c_void_p), ("topk_idx", c_void_p),
                 ("topk_w", c_void_p), ("y_region", c_void_p), ("moe_out", c_void_p), ("expert", EXPERT_FN),
-                ("expert_user", c_void_p)]
+                ("expert_user", c_void_p), ("fused_step", c_int32)]
 
 
 _lib = None
@@ -178,6 +178,7 @@ _SIGNATURES = [
     ("dcp_xchg_write_queries", c_int, [c_void_p, c_void_p, c_int32, c_void_p]),
     ("dcp_route_q", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
     ("dcp_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
+    ("dcp_decode_step_fused", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
     ("dcp_decode_attn_routed_f32", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(AttnArgs), c_void_p]),
     ("dcp_mla_decode_attn_routed", c_int, [c_void_p, c_void_p, POINTER(InstanceView), POINTER(MlaArgs), c_void_p]),
     ("dcp_merge_partials", c_int, [c_void_p, POINTER(InstanceView), c_void_p]),
@@ -224,6 +225,7 @@ _SIGNATURES = [
     ("dcp_moe_combine_put", c_int, [c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_combine_reduce", c_int, [c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_expert_identity", c_int, [c_void_p, c_void_p, c_void_p]),
+    ("dcp_moe_step_dispatch", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("dcp_layer_graph_create", c_int, [c_void_p, POINTER(LayerGraphDesc), POINTER(c_void_p)]),
     ("dcp_layer_graph_launch", c_int, [c_void_p, c_int32, c_void_p]),
     ("dcp_layer_graph_info", c_int, [c_void_p, c_void_p, c_void_p]),

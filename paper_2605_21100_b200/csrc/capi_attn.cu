@@ -288,8 +288,8 @@ int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) 
     return dispatch_decode(ctx, map, prm, a->num_kv_heads, G, static_cast<cudaStream_t>(stream), a->page_size);
 }
 
-int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
-                           const dcp_attn_args* a, void* stream) {
+static int decode_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
+                         uint32_t fuse, void* stream) {
     DCP_REQUIRE(ctx && x && v && a, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
     DCP_REQUIRE(v->n_rows <= x->cfg.n_max, DCP_E_SHAPE_OVERFLOW, "N %d > n_max %d", v->n_rows, x->cfg.n_max);
@@ -327,8 +327,32 @@ int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v
     prm.n_mrow = v->n_mrow;
     prm.n_moe = v->n_moe;
     prm.num_shards_ptr = v->n_count_dev;
+    prm.fuse = fuse;
+    if (fuse) {
+        prm.q_local = x->q_local;
+        prm.m_count = v->m_count_all;
+        prm.m_nrow = v->m_nrow;
+        prm.m_k = v->m_k;
+        prm.m_kv = v->m_kv;
+        prm.mout = x->out;
+        prm.mout_lse = x->out_lse;
+        prm.exit_ticket = x->exit_ticket;
+    }
     return dispatch_decode(ctx, map, prm, a->num_kv_heads, a->num_q_heads / a->num_kv_heads,
                            static_cast<cudaStream_t>(stream), a->page_size);
+}
+
+int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
+                           void* stream) {
+    return decode_routed(ctx, x, v, a, 0u, stream);
+}
+
+int dcp_decode_step_fused(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
+                          void* stream) {
+    DCP_REQUIRE(x && x->committed, DCP_E_INVALID_ARG, "NULL or uncommitted exchange (dcp_xchg_commit)");
+    DCP_REQUIRE(v && v->m_rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", v ? v->m_rows : 0,
+                x->cfg.m_max);
+    return decode_routed(ctx, x, v, a, FUSE_STEP | FUSE_ROUTE | FUSE_MERGE, stream);
 }
 
 // ---- K1-f32 ------------------------------------------------------------------------------

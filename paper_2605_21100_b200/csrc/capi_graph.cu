@@ -56,14 +56,17 @@ int enqueue_layer(dcp_layer_graph* g, int mh, int parity, cudaStream_t s) {
         pl->stream = keep;
         if (rc) return rc;
     }
-    if ((rc = dcp_xchg_begin_step(d.xchg, s))) return rc;
-    if ((rc = xchg_route_q_grid(d.xchg, &g->view, mh, s))) return rc;
-    if ((rc = dcp_decode_attn_routed(g->ctx, d.xchg, &g->view, &g->attn, s))) return rc;
-    if ((rc = xchg_merge_grid(d.xchg, &g->view, mh, s))) return rc;
+    if (d.fused_step) {
+        if ((rc = dcp_decode_step_fused(g->ctx, d.xchg, &g->view, &g->attn, s))) return rc;
+    } else {
+        if ((rc = dcp_xchg_begin_step(d.xchg, s))) return rc;
+        if ((rc = xchg_route_q_grid(d.xchg, &g->view, mh, s))) return rc;
+        if ((rc = dcp_decode_attn_routed(g->ctx, d.xchg, &g->view, &g->attn, s))) return rc;
+        if ((rc = xchg_merge_grid(d.xchg, &g->view, mh, s))) return rc;
+    }
     if (!d.moe) return DCP_OK;
     dcp_moe* m = d.moe;
-    if ((rc = dcp_moe_begin_step(m, s))) return rc;
-    if ((rc = dcp_moe_dispatch(m, d.moe_x, d.topk_idx, d.topk_w, g->view.m_count_all + g->view.instance, s)))
+    if ((rc = dcp_moe_step_dispatch(m, d.moe_x, d.topk_idx, d.topk_w, g->view.m_count_all + g->view.instance, s)))
         return rc;
     if ((rc = dcp_moe_receive_regions(m, s))) return rc;
     if (d.expert) {
@@ -140,8 +143,8 @@ int dcp_layer_graph_create(dcp_ctx* ctx, const dcp_layer_graph_desc* d, dcp_laye
         DCP_REQUIRE(d->moe->cfg.self == d->view->instance && d->moe->cfg.world == d->view->world,
                     DCP_E_INVALID_ARG, "MoE exchange belongs to another instance / world");
         DCP_REQUIRE(d->y_region && d->moe_out, DCP_E_INVALID_ARG, "y_region / moe_out are required with MoE");
-        DCP_REQUIRE(d->moe->cfg.m_max >= d->xchg->cfg.m_max, DCP_E_INVALID_ARG,
-                    "MoE m_max %d < exchange m_max %d", d->moe->cfg.m_max, d->xchg->cfg.m_max);
+        DCP_REQUIRE(d->moe->cfg.m_max >= d->view->m_rows, DCP_E_SHAPE_OVERFLOW, "M %d > MoE m_max %d",
+                    d->view->m_rows, d->moe->cfg.m_max);
     }
     auto* g = new dcp_layer_graph();
     g->ctx = ctx;
@@ -168,6 +171,8 @@ int dcp_layer_graph_launch(dcp_layer_graph* g, int32_t m_rows, void* stream) {
     DCP_REQUIRE(g, DCP_E_INVALID_ARG, "NULL graph");
     DCP_REQUIRE(m_rows >= 0 && m_rows <= g->d.xchg->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", m_rows,
                 g->d.xchg->cfg.m_max);
+    DCP_REQUIRE(!g->d.moe || m_rows <= g->d.moe->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > MoE m_max %d", m_rows,
+                g->d.moe->cfg.m_max);
     if (g->d.planner && g->d.planner->generation != g->planner_gen) {
         // the planner's page arena moved (compaction): the captured K7 holds stale pointers
         if (int rc = capture_all(g)) return rc;

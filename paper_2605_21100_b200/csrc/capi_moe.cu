@@ -59,6 +59,7 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     const size_t o_ct = l;   l = al(l + 2 * W * 4);
     const size_t o_cnt = l;  l = al(l + W * 4);
     const size_t o_off = l;  l = al(l + (W + 1) * 4);
+    const size_t o_tk = l;   l = al(l + 4);
     DCP_CUDA_TRY(cudaMalloc(&x->local, l));
     DCP_CUDA_TRY(cudaMemset(x->local, 0, l));
     x->epoch = reinterpret_cast<uint32_t*>(x->local + o_ep);
@@ -79,6 +80,7 @@ int dcp_moe_create(dcp_ctx* ctx, const dcp_moe_config* c, dcp_moe** out) {
     h.cb_target = reinterpret_cast<uint32_t*>(x->local + o_ct);
     h.counts = reinterpret_cast<int32_t*>(x->local + o_cnt);
     h.offs = reinterpret_cast<int32_t*>(x->local + o_off);
+    h.exit_ticket = reinterpret_cast<int32_t*>(x->local + o_tk);
     // one wave of CTAs for K4 / K5b (a CTA per token / per received row beyond that)
     h.chunks = ctx->num_sms;
     h.base[c->self] = x->pool;
@@ -188,8 +190,21 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
     moe_dispatch_kernel<<<x->host.chunks, MOE_THREADS, dispatch_smem(x), s>>>(
-        x->host, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count);
+        x->host, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 0);
     DCP_CUDA_TRY(cudaGetLastError());
+    return DCP_OK;
+}
+
+int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const float* w,
+                          const int32_t* m_count, void* stream) {
+    DCP_REQUIRE(x && x->committed && m_count, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    x->m_count_dev = m_count;
+    moe_dispatch_kernel<<<x->host.chunks, MOE_THREADS, dispatch_smem(x), s>>>(
+        x->host, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 1);
+    DCP_CUDA_TRY(cudaGetLastError());
+    ++x->host_epoch;  // what dcp_moe_begin_step does on the host
+    x->received = false;
     return DCP_OK;
 }
 

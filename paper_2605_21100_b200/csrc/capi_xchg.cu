@@ -73,6 +73,7 @@ int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c0, dcp_xchg** out) {
     const size_t off_lse = lb; lb = align256(lb + m * hq * 4);
     const size_t off_ep = lb;  lb = align256(lb + 4);
     const size_t off_err = lb; lb = align256(lb + 16);
+    const size_t off_tk = lb;  lb = align256(lb + 4);
     const size_t off_dev = lb; lb = align256(lb + sizeof(XchgPeers));
     DCP_CUDA_TRY(cudaMalloc(&x->local, lb));
     DCP_CUDA_TRY(cudaMemset(x->local, 0, lb));
@@ -81,6 +82,7 @@ int dcp_xchg_create(dcp_ctx* ctx, const dcp_xchg_config* c0, dcp_xchg** out) {
     x->out_lse = reinterpret_cast<float*>(x->local + off_lse);
     x->epoch = reinterpret_cast<uint32_t*>(x->local + off_ep);
     x->err = reinterpret_cast<uint32_t*>(x->local + off_err);
+    x->exit_ticket = reinterpret_cast<int32_t*>(x->local + off_tk);
     x->dev = reinterpret_cast<XchgPeers*>(x->local + off_dev);
     h.W = c.world;
     h.self = c.self;

@@ -72,6 +72,7 @@ struct MoePeers {
     int32_t* counts;       // [W] rows received from each source this step
     int32_t* offs;         // [W + 1] exclusive prefix of counts
     int32_t chunks;        // CTAs of K4 / K5b
+    int32_t* exit_ticket;  // K4 with the step fence folded in: grid exit counter
 };
 
 template <class T>
@@ -134,17 +135,20 @@ static __global__ void __launch_bounds__(32) moe_begin_step_kernel(const __grid_
 }
 
 // K4.  grid = chunks, block = MOE_THREADS; dynamic smem = m_max * (W + 1) * 4 bytes.
+// with_fence: this launch is also the step's begin_step (the step fence of exchange.cuh before
+// the first peer store; epoch e = *epoch + 1, advanced by the last CTA out), one launch per step.
 static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const __grid_constant__ MoePeers p,
                                                                           const __nv_bfloat16* __restrict__ x,
                                                                           const int32_t* __restrict__ topk_idx,
                                                                           const float* __restrict__ topk_w,
-                                                                          const int32_t* __restrict__ m_count) {
+                                                                          const int32_t* __restrict__ m_count,
+                                                                          int with_fence) {
     extern __shared__ int32_t sm[];
     const int W = p.W, H = p.H, K = p.topk, M = *m_count;
     int32_t* s_mask = sm;               // [M] destination-rank bitmask of each token
     int32_t* s_slot = sm + p.m_max;     // [M][W] slot at each destination (-1 = not routed)
     __shared__ int32_t s_count[PL_MAXW], s_sent[PL_MAXW];
-    const uint32_t ep = *p.epoch;
+    const uint32_t ep = *p.epoch + (with_fence ? 1u : 0u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int NW = MOE_THREADS / 32;
     for (int t = tid; t < M; t += MOE_THREADS) {
@@ -165,6 +169,11 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
             carry += __popc(b);
         }
         if (lane == 0) s_count[d] = carry;
+    }
+    if (with_fence && warp == 0) {
+        if (blockIdx.x == 0 && lane == 0) st_relaxed_sys(moe_done(p, p.self), ep - 1);
+        for (int s = lane; s < W; s += 32)
+            if (s != p.self) wait_flag(moe_done(p, s), ep - 2, p.wc, (SITE_FENCE << 24) | (s << 16), true);
     }
     __syncthreads();
     if (blockIdx.x == 0) {
@@ -224,6 +233,14 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
     __syncthreads();
     // one release per (CTA, destination) covers every row this CTA stored there
     if (tid < W && s_sent[tid]) red_release_sys_add(rx_arr(p, tid, ep) + p.self, s_sent[tid]);
+    if (with_fence && tid == 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.exit_ticket) : "memory");
+        if (old == static_cast<int>(gridDim.x) - 1) {
+            *p.exit_ticket = 0;
+            *p.epoch = ep;
+        }
+    }
 }
 
 // K5a (region mode): one warp; lane s waits for source s, then counts and offsets.

@@ -55,7 +55,21 @@ struct AttnParams {
     const int32_t* n_moe;        // [R] m_r
     const int32_t* num_shards_ptr;  // device-resident R (graph replay); overrides num_shards
     long long* trace;            // optional [grid][8] globaltimer stamps per CTA (dcp_k1_set_trace)
+    // ---- fused routed step (dcp_decode_step_fused): one launch per step.  FUSE_STEP: this
+    // launch is the step's begin_step (fence, epoch e = *epoch + 1, bumped by the last CTA to
+    // exit); FUSE_ROUTE: K2's Q-route puts in the prologue; FUSE_MERGE: K3's LSE merges of this
+    // instance's M rows in the epilogue (spins on peers' Res-route flags: multi-GPU / W = 1 only).
+    uint32_t fuse;
+    const void* q_local;         // [m_max][HQ][D] bf16, M-row order (route)
+    const int32_t* m_count;      // [W] device M counts (K7)
+    const int32_t* m_nrow;       // [M][W] destination rows (route)
+    const int32_t* m_k;          // [M] |P_r| (merge)
+    const int32_t* m_kv;         // [M][PL_MAXK] P_r in kv_binding order (merge)
+    float* mout;                 // [m_max][HQ][D] merged O (merge)
+    float* mout_lse;             // [m_max][HQ]
+    int32_t* exit_ticket;        // grid exit counter (step)
 };
+enum : uint32_t { FUSE_STEP = 1, FUSE_ROUTE = 2, FUSE_MERGE = 4 };
 
 __device__ __forceinline__ long long k1_gtime() {
     long long t;
@@ -63,17 +77,27 @@ __device__ __forceinline__ long long k1_gtime() {
     return t;
 }
 
+// Fused step, shard r of a request homed here with P_r = {self} (CP 1, m_r = self): its output
+// is final — written straight to the merged output, no Res-route slot, flag or merge (the merge
+// of a single part is the identity: weight exp(0) = 1, lse unchanged, bit for bit).
+template <class P>
+__device__ __forceinline__ bool row_final_here(const P& p, int r) {
+    return (p.fuse & 4u) && p.n_moe[r] == p.xp->self && p.m_k[p.n_mrow[r]] == 1;
+}
+
 // Destination of shard r's normalised partial O / LSE: local [R][HQ][D] for a
 // local step, else m_r's result pool slot [mrow][self] (Res-route put, fused).
 template <class P>
 __device__ __forceinline__ float* row_out(const P& p, int r, int HQ, int D, uint32_t ep) {
     if (!p.xp) return p.out + (size_t)r * HQ * D;
+    if (row_final_here(p, r)) return p.mout + (size_t)p.n_mrow[r] * HQ * D;
     const XchgPeers& x = *p.xp;
     return xres_o(x, p.n_moe[r], ep) + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ * D;
 }
 template <class P>
 __device__ __forceinline__ float* row_lse(const P& p, int r, int HQ, uint32_t ep) {
     if (!p.xp) return p.lse + (size_t)r * HQ;
+    if (row_final_here(p, r)) return p.mout_lse + (size_t)p.n_mrow[r] * HQ;
     const XchgPeers& x = *p.xp;
     return xres_lse(x, p.n_moe[r], ep) + ((size_t)p.n_mrow[r] * x.W + x.self) * HQ;
 }
@@ -81,6 +105,7 @@ __device__ __forceinline__ float* row_lse(const P& p, int r, int HQ, uint32_t ep
 // happen-before this system-scope release.
 template <class P>
 __device__ __forceinline__ void publish_row(const P& p, int r, uint32_t ep) {
+    if (row_final_here(p, r)) return;
     const XchgPeers& x = *p.xp;
     st_release_sys(xres_flag(x, p.n_moe[r], ep) + (size_t)p.n_mrow[r] * x.W + x.self, ep);
 }
@@ -141,7 +166,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int R = p.num_shards_ptr ? *p.num_shards_ptr : p.num_shards;
-    const uint32_t ep = p.xp ? *p.xp->epoch : 0u;
+    const uint32_t ep = p.xp ? *p.xp->epoch + ((p.fuse & FUSE_STEP) ? 1u : 0u) : 0u;
     const __nv_bfloat16* qbase =
         p.xp ? reinterpret_cast<const __nv_bfloat16*>(xq_recv(*p.xp, p.xp->self, ep)) : p.q;
     const uint32_t* qflag = p.xp ? xq_flag(*p.xp, p.xp->self, ep) : nullptr;
@@ -213,6 +238,36 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     const int t = lane & 3;
     constexpr int NCT = C::CONSUMERS * 32;
 
+    if (p.fuse & FUSE_STEP) {
+        // begin_step (exchange.cuh): publish done = e-1, wait until every peer is done with e-2,
+        // before this CTA's first store into a peer pool (the producer warp only reads KV)
+        const XchgPeers& x = *p.xp;
+        if (warp == 0) {
+            if (cta == 0 && lane == 0) st_relaxed_sys(xdone(x, x.self), ep - 1);
+            for (int s = lane; s < x.W; s += 32)
+                if (s != x.self) wait_flag(xdone(x, s), ep - 2, x.wc, (SITE_FENCE << 24) | (s << 16), true);
+        }
+        named_bar_sync(1, NCT);
+    }
+    if (p.fuse & FUSE_ROUTE) {
+        // K2: this CTA's M rows r = cta, cta + grid, ... to every instance of P_r, 16-byte vectors,
+        // then a system-scope release of the row's arrival flag (exchange_kernels.cuh protocol)
+        const XchgPeers& x = *p.xp;
+        const int M = p.m_count[x.self];
+        constexpr int VEC = C::HQ * C::D * 2 / 16;
+        for (int r = cta; r < M; r += gridDim.x) {
+            const uint4* src = reinterpret_cast<const uint4*>(p.q_local) + (size_t)r * VEC;
+            for (int s = 0; s < x.W; ++s) {
+                const int row = p.m_nrow[(size_t)r * x.W + s];
+                if (row < 0 || s == x.self) continue;  // the home's own shard reads Q in place
+                uint4* dst = reinterpret_cast<uint4*>(xq_recv(x, s, ep)) + (size_t)row * VEC;
+                for (int i = threadIdx.x; i < VEC; i += NCT) dst[i] = __ldg(src + i);
+                named_bar_sync(1, NCT);
+                if (threadIdx.x == 0) st_release_sys(xq_flag(x, s, ep) + row, ep);
+            }
+        }
+    }
+
     // Zero-token shards: O = 0, LSE = -inf (weight 0 in any merge).
     for (int r = cta; r < R; r += gridDim.x) {
         if (p.cu_pages[r + 1] == p.cu_pages[r]) {
@@ -229,11 +284,8 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             }
         }
     }
-    if (p_begin >= p_end) {
-        if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 5] = k1_gtime();
-        return;
-    }
 
+    auto attend = [&]() {
     // Per-lane ldmatrix offsets (stage-relative).  Row & 7 == lane & 7 since
     // every head tile starts on an 8-row boundary (128B swizzle atom).
     const int mi = lane >> 3, rr = lane & 7;
@@ -283,15 +335,19 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
         const int seg_end = min(r_last, p_end);
         const int64_t len = p.shard_len[r];
 
-        // Q fragments (A operand, rows = q-heads of this kv group).
-        if (qflag) {  // routed: wait for the Q-route put of this row
+        // Q fragments (A operand, rows = q-heads of this kv group).  Fused step: a request homed
+        // here reads its Q row in place (no put to self, no flag).
+        const bool q_home = (p.fuse & FUSE_ROUTE) && p.n_moe[r] == p.xp->self;
+        if (qflag && !q_home) {  // routed: wait for the Q-route put of this row
             if (lane == 0) wait_flag(qflag + r, ep, p.xp->wc, (SITE_K1_Q << 24) | (r & 0xffff));
             __syncwarp();
         }
         uint32_t qa[8][4];
         {
-            const __nv_bfloat16* q0 =
-                qbase + (static_cast<size_t>(r) * C::HQ + h * G + g) * C::D + 2 * t;
+            const __nv_bfloat16* qrow = q_home ? static_cast<const __nv_bfloat16*>(p.q_local) +
+                                                     static_cast<size_t>(p.n_mrow[r]) * C::HQ * C::D
+                                               : qbase + static_cast<size_t>(r) * C::HQ * C::D;
+            const __nv_bfloat16* q0 = qrow + (h * G + g) * C::D + 2 * t;
             const __nv_bfloat16* q1 = q0 + 8 * C::D;
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {
@@ -597,6 +653,68 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             }
         }
         ++r;
+    }
+    };  // attend
+    if (p_begin < p_end) attend();
+
+    if (p.fuse & FUSE_MERGE) {
+        // K3: merge this CTA's M rows r = cta, cta + grid, ... once their |P_r| Res-route flags
+        // carry epoch e; weights as lse_merge (attn_merge.hpp:86-100), zero-token shards
+        // (LSE = -inf) weigh 0.  Every producer is co-resident (this kernel) or another GPU.
+        const XchgPeers& x = *p.xp;
+        __shared__ int32_t s_parts[PL_MAXK];
+        const int M = p.m_count[x.self];
+        for (int r = cta; r < M; r += gridDim.x) {
+            const int k = p.m_k[r];
+            if (k == 1 && p.m_kv[(size_t)r * PL_MAXK] == x.self) continue;  // written final by K1
+            if (threadIdx.x < k) {
+                const int s = p.m_kv[(size_t)r * PL_MAXK + threadIdx.x];
+                s_parts[threadIdx.x] = s;
+                wait_flag(xres_flag(x, x.self, ep) + (size_t)r * x.W + s, ep, x.wc,
+                          (SITE_K3_RES << 24) | (s << 16) | (r & 0xffff));
+            }
+            named_bar_sync(1, NCT);
+            const float* po = xres_o(x, x.self, ep) + (size_t)r * x.W * C::HQ * C::D;
+            const float* pl = xres_lse(x, x.self, ep) + (size_t)r * x.W * C::HQ;
+            // thread (head, 16-column quarter): C::HQ * 8 work items over NCT threads
+            for (int wi = threadIdx.x; wi < C::HQ * (C::D / 16); wi += NCT) {
+                const int qh = wi / (C::D / 16), c0 = (wi % (C::D / 16)) * 16;
+                float mx = -INFINITY;
+                for (int i = 0; i < k; ++i) mx = fmaxf(mx, __ldcg(pl + (size_t)s_parts[i] * C::HQ + qh));
+                float4 acc[4] = {};
+                float den = 0.f;
+                for (int i = 0; i < k; ++i) {
+                    const int s = s_parts[i];
+                    const float l = __ldcg(pl + (size_t)s * C::HQ + qh);
+                    const float wgt = l == -INFINITY ? 0.f : expf(l - mx);
+                    den += wgt;
+                    const float4* v = reinterpret_cast<const float4*>(po + ((size_t)s * C::HQ + qh) * C::D + c0);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float4 t4 = __ldcg(v + j);
+                        acc[j].x += wgt * t4.x;
+                        acc[j].y += wgt * t4.y;
+                        acc[j].z += wgt * t4.z;
+                        acc[j].w += wgt * t4.w;
+                    }
+                }
+                const float inv = 1.f / den;
+                float4* o = reinterpret_cast<float4*>(p.mout + ((size_t)r * C::HQ + qh) * C::D + c0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    o[j] = make_float4(acc[j].x * inv, acc[j].y * inv, acc[j].z * inv, acc[j].w * inv);
+                if (c0 == 0) p.mout_lse[(size_t)r * C::HQ + qh] = mx + logf(den);
+            }
+            named_bar_sync(1, NCT);  // s_parts is rewritten by the next row
+        }
+    }
+    if (p.fuse & FUSE_STEP) {
+        // the last CTA out advances the epoch for the next step's launches
+        named_bar_sync(1, NCT);
+        if (threadIdx.x == 0 && atom_add_acq_rel_gpu(p.exit_ticket, 1) == static_cast<int>(gridDim.x) - 1) {
+            *p.exit_ticket = 0;
+            *p.xp->epoch = ep;
+        }
     }
     if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 5] = k1_gtime();
 }

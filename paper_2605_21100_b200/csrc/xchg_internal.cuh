@@ -18,6 +18,7 @@ struct dcp_xchg {
     float* out_lse = nullptr;
     uint32_t* epoch = nullptr;
     uint32_t* err = nullptr;
+    int32_t* exit_ticket = nullptr;  // fused step (dcp_decode_step_fused): grid exit counter
     bool committed = false;
 };
 

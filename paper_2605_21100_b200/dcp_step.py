@@ -95,8 +95,13 @@ class DcpInstance:
                                                        q_rows.shape[0], ctypes.c_void_p(s)))
 
     def run(self, view: _capi.InstanceView, stream=None, phase: str = "all"):
+        """phase "all" / "q" / "attn" / "merge": the four phased calls (or a subset); "fused": the
+        whole step in one launch (dcp_decode_step_fused; bf16, one instance per GPU / process)."""
         L = _capi.lib()
         s = ctypes.c_void_p((stream or torch.cuda.current_stream(self.ctx.device)).cuda_stream)
+        if phase == "fused":
+            _capi.check(L.dcp_decode_step_fused(self.ctx.handle, self.x, ctypes.byref(view), ctypes.byref(self.args), s))
+            return
         if phase in ("all", "q"):
             _capi.check(L.dcp_xchg_begin_step(self.x, s))
             _capi.check(L.dcp_route_q(self.x, ctypes.byref(view), s))
@@ -216,7 +221,7 @@ class LayerGraph:
     """
 
     def __init__(self, inst: DcpInstance, view, moe=None, moe_x=None, topk_idx=None, topk_w=None,
-                 planner=None, expert=None):
+                 planner=None, expert=None, fused=False):
         L = _capi.lib()
         self.inst, self.view, self.moe = inst, view, moe
         dev = torch.device("cuda", inst.ctx.device)
@@ -234,6 +239,7 @@ class LayerGraph:
         if expert is not None:
             d.expert = expert
         self._expert = expert
+        d.fused_step = int(fused)
         self.desc = d
         h = ctypes.c_void_p()
         _capi.check(L.dcp_layer_graph_create(inst.ctx.handle, ctypes.byref(d), ctypes.byref(h)))

@@ -69,17 +69,22 @@ class MoeInstance:
     def commit(self):
         _capi.check(_capi.lib().dcp_moe_commit(self.h))
 
-    def dispatch(self, x, topk_idx, topk_w, m_count_ptr=None, stream=None):
-        """x bf16 [M, H], topk_idx int32 [M, k], topk_w fp32 [M, k] (device)."""
+    def dispatch(self, x, topk_idx, topk_w, m_count_ptr=None, stream=None, fused=True):
+        """x bf16 [M, H], topk_idx int32 [M, k], topk_w fp32 [M, k] (device).  Starts the step:
+        fused (default) = one launch (dcp_moe_step_dispatch), else begin_step + dispatch."""
         L = _capi.lib()
         s = _s(stream, self.ctx.device)
         if m_count_ptr is None:
             self.m_count.fill_(x.shape[0])
             m_count_ptr = self.m_count.data_ptr()
         self._keep = (x, topk_idx, topk_w)
-        _capi.check(L.dcp_moe_begin_step(self.h, s))
-        _capi.check(L.dcp_moe_dispatch(self.h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(topk_idx.data_ptr()),
-                                       ctypes.c_void_p(topk_w.data_ptr()), ctypes.c_void_p(m_count_ptr), s))
+        args = (self.h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(topk_idx.data_ptr()),
+                ctypes.c_void_p(topk_w.data_ptr()), ctypes.c_void_p(m_count_ptr), s)
+        if fused:
+            _capi.check(L.dcp_moe_step_dispatch(*args))
+        else:
+            _capi.check(L.dcp_moe_begin_step(self.h, s))
+            _capi.check(L.dcp_moe_dispatch(*args))
 
     def receive(self, stream=None):
         counts = np.zeros(self.world, np.int32)

@@ -114,14 +114,15 @@ class RankStep:
         self.inst.run(self.view, stream)
 
     def moe_layer(self, x, topk_idx, topk_w, expert_fn=None, stream=None):
-        """x bf16 [M, H] in M-row order; expert_fn(x_region, meta_region, counts) -> fills
-        self.y_region (identity experts when None: y = x, issued on the stream, no host sync)."""
+        """x bf16 [M, H] in M-row order; expert_fn(x_region, meta_region, counts, y_region) fills
+        self.y_region (None: the gate-weighted identity expert, dcp_moe_expert_identity, issued
+        on the stream, no host sync)."""
         m = self.moe
         m.dispatch(x, topk_idx, topk_w, m_count_ptr=self.m_count_ptr, stream=stream)
         m.receive_regions(stream)
         xr, mr = m.regions()
         if expert_fn is None:
-            self.y_region.copy_(xr)
+            m.expert_identity(self.y_region, stream)
         else:
             expert_fn(xr, mr, m.recv_counts(), self.y_region)
         m.combine_put_regions(self.y_region, stream)

@@ -5,9 +5,9 @@ dcp_layer_graph captures one instance's decode layer — [K7] -> K2 -> K1 -> K3 
 
 * W = 1 with K7 inside the graph, over several replays (both parities), plus a replay after
   the planner state changed (append_token): the in-graph K7 sees the new lengths;
-* W = 4 instances on one GPU, each replaying its own graph on its own stream with no host
-  synchronisation between instances (cross-instance dependencies are the exchange flags),
-  against a phase-ordered eager step;
+* several instances each replaying their own graph: tests/test_multiproc_ipc_gpu.py (one
+  process per instance — instances sharing one GPU inside one process cannot run whole-layer
+  graphs concurrently: a K1 spinning on a peer's Q-route occupies every SM the peer needs);
 * an expert-stage callback (captured cudaMemcpyAsync of the parity's receive region) gets
   the right region pointer on both parities;
 * the MoE output against the numpy definition of the gate-weighted identity expert.
@@ -161,56 +161,38 @@ def test_layer_graph_w1_k7_inside_matches_eager():
     g.close()
 
 
-def test_layer_graph_w4_concurrent_replay_matches_eager():
-    from paper_2605_21100_b200.dcp_step import LayerGraph
-    rng = np.random.default_rng(9)
-    lens = [int(v) for v in rng.integers(1, 6000, size=40)]
-    ctx, pl, insts, moes, views, bufs = _world(4, lens, bucket=[[1500, 1], [4000, 2], [I64MAX, 4]], cap=4000)
-    ref = _eager(insts, moes, views, bufs)
-    graphs = [LayerGraph(insts[s], views[s], moes[s], *bufs[s]) for s in range(4)]
-    streams = [torch.cuda.Stream() for _ in range(4)]
-    torch.cuda.synchronize()
-    for step in range(4):
-        for s in range(4):
-            graphs[s].launch(views[s].m_rows, streams[s])
-        torch.cuda.synchronize()
-        _same(ref, _snap(insts, moes, views))
-    for s, r in _moe_reference(bufs, views):
-        np.testing.assert_allclose(ref[s][2], r, rtol=1e-2, atol=1e-2)
-    for g in graphs:
-        g.close()
-
-
 def test_layer_graph_expert_callback_gets_parity_regions():
     from paper_2605_21100_b200 import _capi
     from paper_2605_21100_b200.dcp_step import LayerGraph
     rt = _cudart()
     lens = [700, 33, 1200, 5]
-    ctx, pl, insts, moes, views, bufs = _world(2, lens, bucket=[[800, 1], [I64MAX, 2]])
+    Wn = 1
+    ctx, pl, insts, moes, views, bufs = _world(Wn, lens)
     calls = []
 
     def copy_expert(user, stream, parity, x_region, meta, counts, y_region):
         calls.append(parity)
-        rc = rt.cudaMemcpyAsync(y_region, x_region, 2 * 64 * H * 2, 3, stream)  # D2D
+        rc = rt.cudaMemcpyAsync(y_region, x_region, Wn * 64 * H * 2, 3, stream)  # D2D
         assert rc == 0
 
     cb = _capi.EXPERT_FN(copy_expert)
-    graphs = [LayerGraph(insts[s], views[s], moes[s], *bufs[s], expert=cb) for s in range(2)]
-    assert sorted(calls) == [0] * (2 * graphs[0].info()["buckets"]) + [1] * (2 * graphs[0].info()["buckets"])
-    streams = [torch.cuda.Stream() for _ in range(2)]
+    graphs = [LayerGraph(insts[s], views[s], moes[s], *bufs[s], expert=cb) for s in range(Wn)]
+    nb = graphs[0].info()["buckets"]
+    assert sorted(calls) == [0] * (Wn * nb) + [1] * (Wn * nb)
+    streams = [torch.cuda.Stream() for _ in range(Wn)]
     for step in range(3):
-        for s in range(2):  # a fresh token batch every step: a stale parity would return old rows
+        for s in range(Wn):  # a fresh token batch every step: a stale parity would return old rows
             x, idx, w = bufs[s]
             x.copy_(torch.randn_like(x, dtype=torch.float32).to(torch.bfloat16))
         torch.cuda.synchronize()
-        for s in range(2):
+        for s in range(Wn):
             graphs[s].launch(views[s].m_rows, streams[s])
         torch.cuda.synchronize()
-        for s in range(2):
+        for s in range(Wn):
             moes[s].status()
             x, idx, _ = (t.cpu() for t in bufs[s])
             M = views[s].m_rows
-            nranks = np.array([len(set((idx[t] // (E // 2)).tolist())) for t in range(M)], np.float32)
+            nranks = np.array([len(set((idx[t] // (E // Wn)).tolist())) for t in range(M)], np.float32)
             want = x[:M].float().numpy() * nranks[:, None]
             np.testing.assert_allclose(moes[s].out[:M].cpu().numpy(), want, rtol=1e-2, atol=1e-2)
     for g in graphs:

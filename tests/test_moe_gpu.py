@@ -46,9 +46,10 @@ def test_dispatch_combine_matches_oracle(W, E, k, H, I, m_max):
         idx = top.indices.to(torch.int32).contiguous()
         wts = torch.softmax(top.values, dim=-1).float().contiguous()   # renormalised gate weights
         toks.append((x, idx, wts))
-    # K4 at every instance, then the expert stage, then K5
+    # K4 at every instance (one launch with the step fence folded in, or begin_step + K4 on the
+    # odd instances), then the expert stage, then K5
     for s in range(W):
-        inst[s].dispatch(*toks[s])
+        inst[s].dispatch(*toks[s], fused=(s % 2 == 0))
     rows = [inst[s].receive() for s in range(W)]
     per = E // W
     for s in range(W):

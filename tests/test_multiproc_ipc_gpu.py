@@ -160,13 +160,85 @@ def _worker(rank, port, q, log_dir):
         dist.destroy_process_group()
 
 
-def test_two_processes_ipc_dcp_and_moe():
+def _graph_worker(rank, port, q, log_dir):
+    """Whole-layer graph replay across processes: step 0 eager, steps 1-3 replayed from each
+    rank's dcp_layer_graph (K7 of its planner replica inside), bit-identical to step 0."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import sys
+    if log_dir:
+        f = open(os.path.join(log_dir, f"ipc_graph_rank{rank}.log"), "w", buffering=1)
+        sys.stdout = sys.stderr = f
+    import torch
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=W)
+    try:
+        from paper_2605_21100_b200.attention import DcpContext
+        from paper_2605_21100_b200.dcp_step import LayerGraph
+        from paper_2605_21100_b200.multi import RankStep
+        dev = torch.device("cuda:0")
+        ctx = DcpContext(0)
+        rs = RankStep(ctx, W, rank, LENS, HQ, HKV, CAP, lambda r, c, h: _pool(r, c, h).to(dev), bucket=BUCKET,
+                      moe=MOE, timeout_ms=60000, n_max=64, m_max=32)
+        H, E, k = MOE["hidden"], MOE["experts"], MOE["topk"]
+        M = len(rs.m_ids)
+        mm = MOE["m_max"]
+        xb = torch.zeros(mm, H, dtype=torch.bfloat16, device=dev)
+        ib = torch.zeros(mm, k, dtype=torch.int32, device=dev)
+        wb = torch.zeros(mm, k, dtype=torch.float32, device=dev)
+        if M:
+            toks = [_tok(r, 0, H, E, k) for r in rs.m_ids]
+            xb[:M] = torch.stack([t[0] for t in toks]).to(dev)
+            ib[:M] = torch.stack([t[1] for t in toks]).to(dev)
+            wb[:M] = torch.stack([t[2] for t in toks]).to(dev)
+            rs.inst.write_queries(torch.stack([_q(r, 0) for r in rs.m_ids]).to(dev))
+        rs.inst.run(rs.view)
+        rs.moe_layer(xb[:M], ib[:M], wb[:M])
+        torch.cuda.synchronize()
+        rs.status()
+        o0, l0 = (a.copy() for a in rs.results())
+        m0 = rs.moe.out[:M].cpu().numpy().copy()
+        g = LayerGraph(rs.inst, rs.view, rs.moe, xb, ib, wb, planner=rs.planner)
+        for step in range(3):
+            g.launch(M)
+            torch.cuda.synchronize()
+            rs.status()
+            o, l = rs.results()
+            assert np.array_equal(o, o0) and np.array_equal(l, l0), f"attention differs at replay {step}"
+            assert np.array_equal(rs.moe.out[:M].cpu().numpy(), m0), f"MoE differs at replay {step}"
+        # the one-launch step (dcp_decode_step_fused): eager, then inside a fused layer graph
+        for step in range(2):
+            rs.inst.run(rs.view, None, "fused")
+            torch.cuda.synchronize()
+            rs.status()
+            o, l = rs.results()
+            assert np.array_equal(o, o0) and np.array_equal(l, l0), f"fused step {step} differs"
+        gf = LayerGraph(rs.inst, rs.view, rs.moe, xb, ib, wb, planner=rs.planner, fused=True)
+        for step in range(3):
+            gf.launch(M)
+            torch.cuda.synchronize()
+            rs.status()
+            o, l = rs.results()
+            assert np.array_equal(o, o0) and np.array_equal(l, l0), f"fused graph replay {step} differs"
+            assert np.array_equal(rs.moe.out[:M].cpu().numpy(), m0), f"MoE differs at fused replay {step}"
+        q.put((rank, "ok", M, g.info()["graphs"], 0, 0))
+        import datetime
+        dist.monitored_barrier(timeout=datetime.timedelta(seconds=300))
+        g.close()
+        gf.close()
+        rs.close()
+    except Exception:
+        q.put((rank, traceback.format_exc(), 0, 0, 0, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def _spawn(target):
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     log_dir = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
     os.makedirs(log_dir, exist_ok=True)
-    procs = [ctx.Process(target=_worker, args=(r, port, q, log_dir)) for r in range(W)]
+    procs = [ctx.Process(target=target, args=(r, port, q, log_dir)) for r in range(W)]
     for p in procs:
         p.start()
     res = []
@@ -183,9 +255,22 @@ def test_two_processes_ipc_dcp_and_moe():
             p.kill()
     assert len(res) == W, f"only {len(res)} of {W} ranks reported: {res} (see gpurun_out/ipc_rank*.log)"
     res.sort()
-    for rank, msg, m, wo, wl, wm in res:
+    for rank, msg, *_ in res:
         assert msg == "ok", f"rank {rank}:\n{msg}"
-        print(f"rank {rank}: {m} M rows, 3 steps: O rel-L2 {wo:.2e}, LSE {wl:.2e}, MoE {wm:.2e}")
-    assert sum(r[2] for r in res) == len(LENS)
     for p in procs:
         assert p.exitcode == 0
+    return res
+
+
+def test_two_processes_ipc_dcp_and_moe():
+    res = _spawn(_worker)
+    for rank, msg, m, wo, wl, wm in res:
+        print(f"rank {rank}: {m} M rows, 3 steps: O rel-L2 {wo:.2e}, LSE {wl:.2e}, MoE {wm:.2e}")
+    assert sum(r[2] for r in res) == len(LENS)
+
+
+def test_two_processes_layer_graph_replay():
+    res = _spawn(_graph_worker)
+    for rank, msg, m, n_graphs, *_ in res:
+        print(f"rank {rank}: {m} M rows, {n_graphs} layer graphs, 3 replays bit-identical to the eager step")
+    assert sum(r[2] for r in res) == len(LENS)

@@ -10,6 +10,7 @@ from paper_2605_21100_b200.attention import DcpContext, DecodeAttention  # noqa:
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--sizes", default="4x100,16x1000,64x2048")
+ap.add_argument("--fused", action="store_true", help="trace the one-launch routed step (W = 1) instead")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 ctx = DcpContext(0)
@@ -19,9 +20,29 @@ for sz in a.sizes.split(","):
     b = workload.paged_batch([ln] * n, 32, 8, frame_order="shuffled", seed=1)
     pool = torch.randn(b.num_frames, 2, 8, 16, 128, device=dev).to(torch.bfloat16)
     q = torch.randn(n, 32, 128, device=dev).to(torch.bfloat16)
-    att = DecodeAttention(ctx, 32, 8, max_shards=n)
-    att.prepare(q, pool, torch.from_numpy(b.block_table).to(dev), torch.from_numpy(b.cu_pages).to(dev),
-                torch.from_numpy(b.shard_len).to(dev))
+    if a.fused:
+        from paper_2605_21100_b200.dcp_step import DcpInstance
+        from paper_2605_21100_b200.planner import DevicePlanner
+        cap = b.num_frames + 64
+        pl = DevicePlanner(ctx, 1, 1, 16, cap, "dcp", None, max_requests=max(64, 2 * n), reserve_pages=8)
+        pl.enqueue_many(list(range(n)), [ln] * n)
+        pl.step()
+        pl.build_routing()
+        view = pl.instance_view(0)
+        pool = torch.randn(cap, 2, 8, 16, 128, device=dev).to(torch.bfloat16)
+        inst = DcpInstance(ctx, 1, 0, 32, 8, cap, kv_pool=pool, n_max=max(512, n), m_max=max(256, n))
+        inst.set_peer_local(0, inst)
+        inst.commit()
+        inst.write_queries(q)
+
+        class _F:
+            def launch(self):
+                inst.run(view, None, "fused")
+        att = _F()
+    else:
+        att = DecodeAttention(ctx, 32, 8, max_shards=n)
+        att.prepare(q, pool, torch.from_numpy(b.block_table).to(dev), torch.from_numpy(b.cu_pages).to(dev),
+                    torch.from_numpy(b.shard_len).to(dev))
     for _ in range(5):
         att.launch()
     tr = torch.zeros(ctx.num_sms * 8, dtype=torch.int64, device=dev)

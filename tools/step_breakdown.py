@@ -69,6 +69,20 @@ def main():
     import ctypes
     out = {"reqs": args.reqs, "len": args.len}
     out["step_us"] = timed(lambda: inst.run(view, None, "all"))
+    out["fused_us"] = timed(lambda: inst.run(view, None, "fused"))
+
+    def graphed(phase, n=20):
+        gr = torch.cuda.CUDAGraph()
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            with torch.cuda.graph(gr, stream=st):
+                for _ in range(n):
+                    inst.run(view, st, phase)
+        torch.cuda.synchronize()
+        return timed(gr.replay) / n
+
+    out["step_graph_us"] = graphed("all")
+    out["fused_graph_us"] = graphed("fused")
     out["begin_us"] = timed(lambda: L.dcp_xchg_begin_step(inst.x, sp))
     out["k2_us"] = timed(lambda: L.dcp_route_q(inst.x, ctypes.byref(view), sp))
     out["k1_routed_us"] = timed(lambda: L.dcp_decode_attn_routed(ctx.handle, inst.x, ctypes.byref(view),
