@@ -497,6 +497,8 @@ def main():
     ap.add_argument("--no-mla", action="store_true", help="skip the K10 MLA leg (SURVEY §8f #1)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent cfg2 replicas instead of the multi-GPU DCP step")
+    ap.add_argument("--phased", action="store_true",
+                    help="N > 1: the routed attention as 4 launches (begin, K2, K1, K3) instead of one fused launch")
     args = ap.parse_args()
     ws, rank, local = dist_init()
     if args.impl == "reference":

@@ -17,9 +17,15 @@ instances, and the simulated clock advances by layers x that latency.
     python bench_trace.py [--instances 8] [--rate 8] [--duration 20] [--long-ratio 0.01]
     python bench_trace.py --sweep-rates 8,16,32,64 --long-ratio 0.05 --slo-ms 20   (P99-TPOT sweep)
 
-TPOT here counts the attention layers only (no expert FFN / MoE time), so an
-SLO passed with --slo-ms is an attention-share budget, not the paper's
-whole-model 50 ms.
+Per layer the iteration follows the simengine's critical path:
+  QRoute -> Attn -> ResRoute -> Merge (K2 + K1 + K3, per instance)
+  -> DS (K4) -> [barrier: DR starts at max_j DS.finish(j)] -> DR (K5a) -> MLP -> CS (K5b)
+  -> [barrier] -> CR (K5c)
+with every phase but MLP measured on the device for each instance (the MoE exchange of
+--moe-hidden / --moe-experts / --moe-topk over each instance's M list), and MLP from the
+linear model mu0 + mu_b * B_s of SPEC.md:398 with mu_b derived from the expert FFN's
+flops at --mlp-tflops (the expert GEMMs are library GEMMs, out of scope).  --no-moe keeps
+the attention-only TPOT of round 1.
 """
 from __future__ import annotations
 
@@ -61,6 +67,24 @@ def run(policy, trace, args, ctx, pools):
         insts[s].commit()
     g = torch.Generator(device=dev).manual_seed(11)
     qbank = torch.randn(64, HQ, 128, generator=g, device=dev).to(torch.bfloat16)
+    moes = []
+    if args.moe:
+        from paper_2605_21100_b200.moe import MoeInstance
+        Hm, Em, Km = args.moe_hidden, args.moe_experts, args.moe_topk
+        moes = [MoeInstance(ctx, W, s, Hm, Km, Em, 256) for s in range(W)]
+        for s in range(W):
+            for t in range(W):
+                moes[s].set_peer_local(t, moes[t])
+            moes[s].commit()
+        xbank = torch.randn(256, Hm, generator=g, device=dev).to(torch.bfloat16)
+        top = torch.topk(torch.randn(256, Em, generator=g, device=dev), Km, dim=-1)
+        ibank = top.indices.to(torch.int32).contiguous()
+        wbank = torch.softmax(top.values, -1).float().contiguous()
+        yreg = [torch.zeros(W, 256, Hm, dtype=torch.bfloat16, device=dev) for _ in range(W)]
+        # MLP model: mu0 + mu_b * B_s, mu_b = one token's top-k expert FFN flops
+        # (3 GEMMs of hidden x moe_intermediate) at --mlp-tflops
+        mu_b_ms = Km * 3 * 2 * Hm * args.moe_intermediate / (args.mlp_tflops * 1e12) * 1e3
+    moe_ms, mlp_ms, layer_ms = [], [], []
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     t_ms, it = 0.0, 0
     nxt = 0
@@ -124,11 +148,43 @@ def run(policy, trace, args, ctx, pools):
                 insts[s].run(views[s], None, ph)
                 b.record()
                 marks.append((s, a, b))
+        mph = {}
+        if moes:
+            for ph in ("ds", "dr", "cs", "cr"):
+                for s in range(W):
+                    a, b = ev(), ev()
+                    a.record()
+                    m = moes[s]
+                    if ph == "ds":
+                        m.dispatch(xbank, ibank, wbank, m_count_ptr=views[s].m_count_all + 4 * s)
+                    elif ph == "dr":
+                        m.receive_regions()
+                        m.expert_identity(yreg[s])  # stand-in output for CS (the MLP is modelled)
+                    elif ph == "cs":
+                        m.combine_put_regions(yreg[s])
+                    else:
+                        m.combine_reduce()
+                    b.record()
+                    mph[(ph, s)] = (a, b)
         torch.cuda.synchronize(dev)
         for s, a, b in marks:
             per[s] += a.elapsed_time(b)
-        lat = max(per)
-        step_ms.append(lat)
+        attn_lat = max(per)
+        lat = attn_lat
+        if moes:
+            # SPEC.md:422-427 critical path over the measured phases
+            t = lambda ph, s: mph[(ph, s)][0].elapsed_time(mph[(ph, s)][1])  # noqa: E731
+            bsz = [views[s].m_rows for s in range(W)]
+            mlp = [args.mlp_mu0_us / 1e3 + mu_b_ms * bsz[s] for s in range(W)]
+            ds_end = [per[s] + t("ds", s) for s in range(W)]
+            dr_end = [max(ds_end) + t("dr", s) for s in range(W)]
+            cs_end = [dr_end[s] + mlp[s] + t("cs", s) for s in range(W)]
+            cr_end = [max(cs_end) + t("cr", s) for s in range(W)]
+            lat = max(cr_end)
+            moe_ms.append(lat - attn_lat - max(mlp))
+            mlp_ms.append(max(mlp))
+        step_ms.append(attn_lat)
+        layer_ms.append(lat)
         red_attn.append(metrics.imbalance_metrics(per)[1])
         t_ms += args.layers * lat
         done = []
@@ -142,7 +198,7 @@ def run(policy, trace, args, ctx, pools):
             tpot.append((t_ms - start[rid]) / out_len[rid])
             finished += 1
         it += 1
-    for x in insts:
+    for x in insts + moes:
         x.close()
     pl.close()
     st, tp = np.array(step_ms), np.array(tpot) if tpot else np.array([0.0])
@@ -163,6 +219,12 @@ def run(policy, trace, args, ctx, pools):
         "cp_gt1_active_frac_max": float(max(cp_frac)) if cp_frac else 0.0,
         "cp_gt1_active_frac_mean": float(np.mean(cp_frac)) if cp_frac else 0.0,
         "sim_time_s": t_ms / 1e3,
+        "layer_model": ("attention + MoE exchange measured, MLP modelled (SPEC.md:422-427 critical path)"
+                        if moes else "attention only"),
+        "layer_ms_p50": float(np.percentile(layer_ms, 50)) if layer_ms else None,
+        "layer_ms_p99": float(np.percentile(layer_ms, 99)) if layer_ms else None,
+        "moe_exchange_ms_per_layer_p50": float(np.percentile(moe_ms, 50)) if moe_ms else None,
+        "mlp_model_ms_per_layer_p50": float(np.percentile(mlp_ms, 50)) if mlp_ms else None,
     }
 
 
@@ -182,6 +244,15 @@ def main():
     ap.add_argument("--max-iters", type=int, default=4000)
     ap.add_argument("--uniform-degree", type=int, default=8)
     ap.add_argument("--policies", default="dcp,least_batch,least_cache,uniform")
+    ap.add_argument("--no-moe", dest="moe", action="store_false",
+                    help="attention-only TPOT (no DS/DR/MLP/CS/CR phases)")
+    ap.add_argument("--moe-hidden", type=int, default=2048, help="cfg4 (Qwen3-30B-A3B) hidden size")
+    ap.add_argument("--moe-experts", type=int, default=128)
+    ap.add_argument("--moe-topk", type=int, default=8)
+    ap.add_argument("--moe-intermediate", type=int, default=768)
+    ap.add_argument("--mlp-tflops", type=float, default=800.0,
+                    help="effective bf16 TFLOP/s of the expert GEMMs in the MLP model")
+    ap.add_argument("--mlp-mu0-us", type=float, default=10.0, help="fixed MLP cost per layer (mu0)")
     ap.add_argument("--trace-csv", default="",
                     help="replay this trace file (the reference's id,arrival_ms,seq_len,output_len format, "
                          "workload.cpp:108-137) instead of generating one")
@@ -199,7 +270,9 @@ def main():
     pools = [torch.randn(args.capacity, 2, 8, 16, 128, generator=g, device=dev, dtype=torch.bfloat16)
              for _ in range(args.instances)]
     setup = (f"{args.instances} instances (single-GPU emulation), GQA 32q/8kv d128 bf16, "
-             f"{args.layers} layers/iteration, SLO {args.slo_ms} ms TPOT (attention layers only)")
+             f"{args.layers} layers/iteration, SLO {args.slo_ms} ms TPOT "
+             + (f"(attention + MoE exchange hidden {args.moe_hidden} / {args.moe_experts} experts top-{args.moe_topk} "
+                f"measured, MLP modelled at {args.mlp_tflops} TFLOP/s)" if args.moe else "(attention layers only)"))
     rates = [float(x) for x in args.sweep_rates.split(",") if x] or [args.rate]
     by_policy = {}
     for rate in rates:

@@ -253,6 +253,7 @@ typedef struct dcp_instance_view {
     const int32_t* n_count_dev; /* device copy of this instance's N */
     int32_t world;
     int32_t instance;
+    const int32_t* total_pages_dev; /* device copy of cu_pages[N] (K1 reads it with N, not after it) */
 } dcp_instance_view;
 
 DCP_API int dcp_planner_create(dcp_ctx* ctx, const dcp_planner_config* cfg, dcp_planner** out);

@@ -110,6 +110,7 @@ class InstanceView(Structure):
         ("block_table", c_void_p), ("page_fill", c_void_p),
         ("n_mrow", c_void_p), ("m_nrow", c_void_p), ("m_k", c_void_p), ("m_kv", c_void_p),
         ("m_count_all", c_void_p), ("n_count_dev", c_void_p), ("world", c_int32), ("instance", c_int32),
+        ("total_pages_dev", c_void_p),
     ]
 
 

@@ -327,6 +327,7 @@ static int decode_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, 
     prm.n_mrow = v->n_mrow;
     prm.n_moe = v->n_moe;
     prm.num_shards_ptr = v->n_count_dev;
+    prm.total_pages_ptr = v->total_pages_dev;
     prm.fuse = fuse;
     if (fuse) {
         prm.q_local = x->q_local;

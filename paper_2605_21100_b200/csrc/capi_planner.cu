@@ -769,6 +769,7 @@ int dcp_planner_instance_view(dcp_planner* pl, int32_t s, dcp_instance_view* v) 
     v->m_kv = pl->ro.m_kv + (size_t)s * S * PL_MAXK;
     v->m_count_all = pl->ro.m_count;
     v->n_count_dev = pl->ro.n_count + s;
+    v->total_pages_dev = pl->ro.cu_pages + (size_t)s * (S + 1) + S;
     v->world = W;
     v->instance = s;
     return DCP_OK;

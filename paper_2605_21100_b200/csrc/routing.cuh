@@ -452,6 +452,9 @@ static __global__ void __launch_bounds__(1024) routing_scan_kernel(PlannerState 
         run += cu[j + 1];
         cu[j + 1] = (int32_t)run;
     }
+    // the instance's total pages also at the fixed index S (== cu[rows] when rows == S), so K1 can
+    // load it together with N instead of after it
+    if (tid == blockDim.x - 1 && rows < S) cu[S] = (int32_t)part[tid];
 }
 
 static __global__ void __launch_bounds__(256) routing_scatter_kernel(PlannerState st, RoutingOut ro) {

@@ -54,6 +54,7 @@ struct AttnParams {
     const int32_t* n_mrow;       // [R] row of the shard's request in m_r's M list
     const int32_t* n_moe;        // [R] m_r
     const int32_t* num_shards_ptr;  // device-resident R (graph replay); overrides num_shards
+    const int32_t* total_pages_ptr; // device-resident cu_pages[R] (routed: loaded alongside R)
     long long* trace;            // optional [grid][8] globaltimer stamps per CTA (dcp_k1_set_trace)
     // ---- fused routed step (dcp_decode_step_fused): one launch per step.  FUSE_STEP: this
     // launch is the step's begin_step (fence, epoch e = *epoch + 1, bumped by the last CTA to
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
     const __nv_bfloat16* qbase =
         p.xp ? reinterpret_cast<const __nv_bfloat16*>(xq_recv(*p.xp, p.xp->self, ep)) : p.q;
     const uint32_t* qflag = p.xp ? xq_flag(*p.xp, p.xp->self, ep) : nullptr;
-    const int64_t P = p.cu_pages[R];
+    const int64_t P = p.total_pages_ptr ? *p.total_pages_ptr : p.cu_pages[R];
     const int64_t grid = gridDim.x;
     const int cta = blockIdx.x;
     const int p_begin = static_cast<int>(udiv64(cta * P, grid));

@@ -101,10 +101,10 @@ std::vector<T> merge_device(const std::vector<T>& outs, const std::vector<T>& ls
 
 }  // namespace
 
-#pragma GCC visibility push(default)
+namespace impl {
 
 template <typename T>
-AttnShardResult<T> shard_attention(std::span<const T> q, std::span<const T> keys, std::span<const T> values,
+AttnShardResult<T> shard_attention_t(std::span<const T> q, std::span<const T> keys, std::span<const T> values,
                                    std::int64_t length, int head_dim, T scale) {
     if (length < 1) throw EmptyShard("shard_attention over zero keys");  // attn_merge.hpp:57
     std::vector<T> outs, lses;
@@ -116,14 +116,14 @@ AttnShardResult<T> shard_attention(std::span<const T> q, std::span<const T> keys
 }
 
 template <typename T>
-std::vector<T> reference_attention(std::span<const T> q, std::span<const T> keys, std::span<const T> values,
+std::vector<T> reference_attention_t(std::span<const T> q, std::span<const T> keys, std::span<const T> values,
                                    std::int64_t length, int head_dim, T scale) {
     if (length < 1) return std::vector<T>(static_cast<size_t>(head_dim), std::numeric_limits<T>::quiet_NaN());
-    return shard_attention<T>(q, keys, values, length, head_dim, scale).partial_out;
+    return shard_attention_t<T>(q, keys, values, length, head_dim, scale).partial_out;
 }
 
 template <typename T>
-std::vector<T> lse_merge(std::span<const AttnShardResult<T>> partials) {
+std::vector<T> lse_merge_t(std::span<const AttnShardResult<T>> partials) {
     if (partials.empty()) throw EmptyShard("lse_merge of zero partials");  // attn_merge.hpp:88
     const int d = static_cast<int>(partials.front().partial_out.size());
     std::vector<T> outs, lses;
@@ -135,7 +135,7 @@ std::vector<T> lse_merge(std::span<const AttnShardResult<T>> partials) {
 }
 
 template <typename T>
-std::vector<AttnShardResult<T>> partitioned_shard_attention(std::span<const T> q, std::span<const T> keys,
+std::vector<AttnShardResult<T>> partitioned_shard_attention_t(std::span<const T> q, std::span<const T> keys,
                                                             std::span<const T> values, int head_dim, T scale,
                                                             std::span<const std::int64_t> bounds) {
     // contiguous partition, exclusive ends; zero-width shards receive no query
@@ -163,15 +163,19 @@ std::vector<AttnShardResult<T>> partitioned_shard_attention(std::span<const T> q
     return res;
 }
 
+}  // namespace impl
+
+#pragma GCC visibility push(default)
+
 namespace {
 template <typename T>
 std::vector<T> merge_impl(std::span<const T> q, std::span<const T> keys, std::span<const T> values, int d, T scale,
                           std::span<const std::int64_t> bounds) {
-    auto parts = partitioned_shard_attention<T>(q, keys, values, d, scale, bounds);
+    auto parts = impl::partitioned_shard_attention_t<T>(q, keys, values, d, scale, bounds);
     std::vector<AttnShardResult<T>> live;
     for (auto& p : parts)
         if (!p.partial_out.empty()) live.push_back(std::move(p));  // drop empty shards, keep order
-    return lse_merge<T>(live);
+    return impl::lse_merge_t<T>(live);
 }
 }  // namespace
 
@@ -187,21 +191,48 @@ std::vector<double> sharded_attention_merge(std::span<const double> q, std::span
     return merge_impl<double>(q, keys, values, head_dim, scale, bounds);
 }
 
-template std::vector<float> reference_attention<float>(std::span<const float>, std::span<const float>,
-                                                       std::span<const float>, std::int64_t, int, float);
-template std::vector<double> reference_attention<double>(std::span<const double>, std::span<const double>,
-                                                         std::span<const double>, std::int64_t, int, double);
-template AttnShardResult<float> shard_attention<float>(std::span<const float>, std::span<const float>,
-                                                       std::span<const float>, std::int64_t, int, float);
-template AttnShardResult<double> shard_attention<double>(std::span<const double>, std::span<const double>,
-                                                         std::span<const double>, std::int64_t, int, double);
-template std::vector<float> lse_merge<float>(std::span<const AttnShardResult<float>>);
-template std::vector<double> lse_merge<double>(std::span<const AttnShardResult<double>>);
-template std::vector<AttnShardResult<float>> partitioned_shard_attention<float>(
-    std::span<const float>, std::span<const float>, std::span<const float>, int, float, std::span<const std::int64_t>);
-template std::vector<AttnShardResult<double>> partitioned_shard_attention<double>(
-    std::span<const double>, std::span<const double>, std::span<const double>, int, double,
-    std::span<const std::int64_t>);
+template <>
+std::vector<float> reference_attention<float>(std::span<const float> q, std::span<const float> k,
+                                              std::span<const float> v, std::int64_t n, int d, float sc) {
+    return impl::reference_attention_t<float>(q, k, v, n, d, sc);
+}
+template <>
+std::vector<double> reference_attention<double>(std::span<const double> q, std::span<const double> k,
+                                                std::span<const double> v, std::int64_t n, int d, double sc) {
+    return impl::reference_attention_t<double>(q, k, v, n, d, sc);
+}
+template <>
+AttnShardResult<float> shard_attention<float>(std::span<const float> q, std::span<const float> k,
+                                              std::span<const float> v, std::int64_t n, int d, float sc) {
+    return impl::shard_attention_t<float>(q, k, v, n, d, sc);
+}
+template <>
+AttnShardResult<double> shard_attention<double>(std::span<const double> q, std::span<const double> k,
+                                                std::span<const double> v, std::int64_t n, int d, double sc) {
+    return impl::shard_attention_t<double>(q, k, v, n, d, sc);
+}
+template <>
+std::vector<float> lse_merge<float>(std::span<const AttnShardResult<float>> p) {
+    return impl::lse_merge_t<float>(p);
+}
+template <>
+std::vector<double> lse_merge<double>(std::span<const AttnShardResult<double>> p) {
+    return impl::lse_merge_t<double>(p);
+}
+template <>
+std::vector<AttnShardResult<float>> partitioned_shard_attention<float>(std::span<const float> q,
+                                                                       std::span<const float> k,
+                                                                       std::span<const float> v, int d, float sc,
+                                                                       std::span<const std::int64_t> b) {
+    return impl::partitioned_shard_attention_t<float>(q, k, v, d, sc, b);
+}
+template <>
+std::vector<AttnShardResult<double>> partitioned_shard_attention<double>(std::span<const double> q,
+                                                                         std::span<const double> k,
+                                                                         std::span<const double> v, int d,
+                                                                         double sc, std::span<const std::int64_t> b) {
+    return impl::partitioned_shard_attention_t<double>(q, k, v, d, sc, b);
+}
 
 #pragma GCC visibility pop
 

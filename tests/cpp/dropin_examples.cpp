@@ -210,6 +210,30 @@ int main() {
             threw = true;
         }
         CHECK("empty_shard", threw);
+        // other T compile and run like the reference's header templates (attn_merge.hpp:25-100):
+        // long double goes through the double device path
+        {
+            const int d = 16, L = 300;
+            std::vector<long double> q(d), k(static_cast<size_t>(L) * d), v(static_cast<size_t>(L) * d);
+            std::vector<double> qd(d), kd(k.size()), vd(v.size());
+            for (int i = 0; i < d; ++i) qd[i] = q[i] = std::sin(0.3 * i);
+            for (size_t i = 0; i < k.size(); ++i) {
+                kd[i] = k[i] = std::cos(0.01 * i);
+                vd[i] = v[i] = std::sin(0.02 * i + 1.0);
+            }
+            auto rl = shard_attention<long double>(q, k, v, L, d, 0.25L);
+            auto rd = shard_attention<double>(qd, kd, vd, L, d, 0.25);
+            bool same = std::abs(static_cast<double>(rl.lse) - rd.lse) == 0.0;
+            for (int i = 0; i < d; ++i) same = same && static_cast<double>(rl.partial_out[i]) == rd.partial_out[i];
+            std::vector<std::int64_t> b2 = {100, 300};
+            auto pl = partitioned_shard_attention<long double>(q, k, v, d, 0.25L, b2);
+            auto ml = lse_merge<long double>(std::span<const AttnShardResult<long double>>(pl));
+            auto md = sharded_attention_merge(std::span<const double>(qd), kd, vd, d, 0.25, b2, false);
+            for (int i = 0; i < d; ++i) same = same && static_cast<double>(ml[i]) == md[i];
+            auto ra = reference_attention<long double>(q, k, v, L, d, 0.25L);
+            for (int i = 0; i < d; ++i) same = same && static_cast<double>(ra[i]) == rd.partial_out[i];
+            CHECK("long_double_templates", same);
+        }
     }
     std::cout << (fails ? "FAILED" : "ALL OK") << "\n";
     return fails ? 1 : 0;
