@@ -43,6 +43,25 @@ struct TmapCacheEntry {
     CUtensorMap map;
 };
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while its stream
+// predecessor is still running and must pdl_wait() (ptx.cuh) before reading that kernel's
+// output; the launch gap between dependent short kernels disappears.  Graph-capturable.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 }  // namespace dcp
 
 // Sets K1's dynamic shared-memory attribute for (hkv, group) outside any capture.

@@ -150,8 +150,7 @@ int dcp_moe_commit(dcp_moe* x) {
 
 int dcp_moe_begin_step(dcp_moe* x, void* stream) {
     DCP_REQUIRE(x && x->committed, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange (dcp_moe_commit)");
-    moe_begin_step_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->host);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_begin_step_kernel, dim3(1), dim3(32), 0, static_cast<cudaStream_t>(stream), x->host));
     ++x->host_epoch;
     x->received = false;
     return DCP_OK;
@@ -189,9 +188,8 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
     DCP_REQUIRE(x && m_count, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
-    moe_dispatch_kernel<<<x->host.chunks, MOE_THREADS, dispatch_smem(x), s>>>(
-        x->host, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 0);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_dispatch_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), dispatch_smem(x), s, x->host,
+                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 0));
     return DCP_OK;
 }
 
@@ -200,9 +198,8 @@ int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, c
     DCP_REQUIRE(x && x->committed && m_count, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
-    moe_dispatch_kernel<<<x->host.chunks, MOE_THREADS, dispatch_smem(x), s>>>(
-        x->host, static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 1);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_dispatch_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), dispatch_smem(x), s, x->host,
+                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 1));
     ++x->host_epoch;  // what dcp_moe_begin_step does on the host
     x->received = false;
     return DCP_OK;
@@ -210,8 +207,7 @@ int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, c
 
 int dcp_moe_receive_regions(dcp_moe* x, void* stream) {
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
-    moe_receive_counts_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(x->host);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_receive_counts_kernel, dim3(1), dim3(32), 0, static_cast<cudaStream_t>(stream), x->host));
     x->received = true;
     return DCP_OK;
 }
@@ -222,8 +218,8 @@ int dcp_moe_receive_async(dcp_moe* x, void* x_rows, int32_t* meta_rows, void* st
     const int rows = x->cfg.world * x->cfg.m_max;
     int grid = rows;  // up to one CTA per received row (warp groups per row, moe.cuh)
     if (grid > 4 * x->ctx->num_sms) grid = 4 * x->ctx->num_sms;
-    moe_receive_compact_kernel<<<grid, 256, 0, s>>>(x->host, static_cast<__nv_bfloat16*>(x_rows), meta_rows);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_receive_compact_kernel, dim3(grid), dim3(256), 0, s, x->host,
+                            static_cast<__nv_bfloat16*>(x_rows), meta_rows));
     x->received = true;
     return DCP_OK;
 }
@@ -246,9 +242,8 @@ int32_t dcp_moe_receive(dcp_moe* x, void* x_rows, int32_t* meta_rows, int32_t* c
 
 static int combine_put(dcp_moe* x, const void* y, int region, void* stream) {
     DCP_REQUIRE(x && y && x->received, DCP_E_INVALID_ARG, "call a dcp_moe_receive* first");
-    moe_combine_put_kernel<<<x->host.chunks, MOE_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->host, static_cast<const __nv_bfloat16*>(y), region);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_combine_put_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), 0,
+                            static_cast<cudaStream_t>(stream), x->host, static_cast<const __nv_bfloat16*>(y), region));
     return DCP_OK;
 }
 
@@ -262,18 +257,16 @@ int dcp_moe_expert_identity(dcp_moe* x, void* y_region, void* stream) {
     DCP_REQUIRE(x && y_region && x->received, DCP_E_INVALID_ARG, "call dcp_moe_receive_regions first");
     int grid = (x->cfg.world * x->cfg.m_max + 7) / 8;
     if (grid > 2 * x->ctx->num_sms) grid = 2 * x->ctx->num_sms;
-    moe_expert_identity_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->host, static_cast<__nv_bfloat16*>(y_region));
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_expert_identity_kernel, dim3(grid), dim3(256), 0, static_cast<cudaStream_t>(stream),
+                            x->host, static_cast<__nv_bfloat16*>(y_region)));
     return DCP_OK;
 }
 
 int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {
     DCP_REQUIRE(x && out && x->m_count_dev, DCP_E_INVALID_ARG, "call dcp_moe_dispatch first");
     const int groups = x->cfg.hidden / 4;  // hidden % 8 == 0
-    moe_combine_reduce_kernel<<<dim3(x->cfg.m_max, (groups + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        x->host, x->m_count_dev, out);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(moe_combine_reduce_kernel, dim3(x->cfg.m_max, (groups + 255) / 256), dim3(256), 0,
+                            static_cast<cudaStream_t>(stream), x->host, x->m_count_dev, out));
     return DCP_OK;
 }
 

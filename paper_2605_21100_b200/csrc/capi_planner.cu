@@ -382,8 +382,7 @@ int dcp_planner_step(dcp_planner* pl, void* stream) {
     }
     planner_step_kernel<<<1, PL_THREADS, 0, pl->stream>>>(pl->st);
     DCP_CUDA_TRY(cudaGetLastError());
-    planner_pages_kernel<<<pl->ctx->num_sms * 2, 256, 0, pl->stream>>>(pl->st);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(planner_pages_kernel, dim3(pl->ctx->num_sms * 2), dim3(256), 0, pl->stream, pl->st));
     pl->last_launches += 2;
     pl->routing_valid = false;
     // conservative bound until the result is read back
@@ -620,10 +619,9 @@ int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
     set_stream(pl, stream);
     DCP_CUDA_TRY(launch_routing_rows(pl->st, pl->ro, pl->stream));
     const dim3 wide(pl->st.W, RT_SPLIT);
-    routing_count_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
-    routing_scan_kernel<<<pl->st.W, 1024, 0, pl->stream>>>(pl->st, pl->ro);
-    routing_scatter_kernel<<<wide, 256, 0, pl->stream>>>(pl->st, pl->ro);
-    DCP_CUDA_TRY(cudaGetLastError());
+    DCP_CUDA_TRY(launch_pdl(routing_count_kernel, wide, dim3(256), 0, pl->stream, pl->st, pl->ro));
+    DCP_CUDA_TRY(launch_pdl(routing_scan_kernel, dim3(pl->st.W), dim3(1024), 0, pl->stream, pl->st, pl->ro));
+    DCP_CUDA_TRY(launch_pdl(routing_scatter_kernel, wide, dim3(256), 0, pl->stream, pl->st, pl->ro));
     pl->last_launches = ROWS_SMEM_MAX >= pl->st.max_slots ? 7 : 4;
     pl->routing_valid = true;
     return DCP_OK;

@@ -44,6 +44,7 @@
 
 #include "exchange.cuh"
 #include "limits.cuh"
+#include "ptx.cuh"
 
 namespace dcp {
 
@@ -131,6 +132,8 @@ __device__ __forceinline__ int moe_wait_source(const MoePeers& p, int s, uint32_
 }
 
 static __global__ void __launch_bounds__(32) moe_begin_step_kernel(const __grid_constant__ MoePeers p) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     step_fence(p.epoch, [&](int s) { return moe_done(p, s); }, p.W, p.self, p.wc);
 }
 
@@ -143,6 +146,8 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
                                                                           const float* __restrict__ topk_w,
                                                                           const int32_t* __restrict__ m_count,
                                                                           int with_fence) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     extern __shared__ int32_t sm[];
     const int W = p.W, H = p.H, K = p.topk, M = *m_count;
     int32_t* s_mask = sm;               // [M] destination-rank bitmask of each token
@@ -245,6 +250,8 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
 
 // K5a (region mode): one warp; lane s waits for source s, then counts and offsets.
 static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const __grid_constant__ MoePeers p) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     const uint32_t ep = *p.epoch;
     const int lane = threadIdx.x;
     int c = 0;
@@ -267,6 +274,8 @@ static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const __g
 static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const __grid_constant__ MoePeers p,
                                                                          __nv_bfloat16* __restrict__ x_rows,
                                                                          int32_t* __restrict__ meta_rows) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     __shared__ int32_t cnt[PL_MAXW], off[PL_MAXW + 1];
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H;
@@ -313,6 +322,8 @@ static __global__ void __launch_bounds__(256) moe_receive_compact_kernel(const _
 // epoch, so a captured graph replays it on either parity.  One warp per row.
 static __global__ void __launch_bounds__(256) moe_expert_identity_kernel(const __grid_constant__ MoePeers p,
                                                                          __nv_bfloat16* __restrict__ y_region) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     const uint32_t ep = *p.epoch;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -348,6 +359,8 @@ static __global__ void __launch_bounds__(256) moe_expert_identity_kernel(const _
 static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const __grid_constant__ MoePeers p,
                                                                              const __nv_bfloat16* __restrict__ y_rows,
                                                                              int region) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     __shared__ int32_t s_off[PL_MAXW + 1], s_sent[PL_MAXW];
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H, tid = threadIdx.x;
@@ -387,6 +400,8 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(con
 static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __grid_constant__ MoePeers p,
                                                                         const int32_t* __restrict__ m_count,
                                                                         float* __restrict__ out) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
     const int t = blockIdx.x;
     if (t >= *m_count) return;
     const uint32_t ep = *p.epoch;

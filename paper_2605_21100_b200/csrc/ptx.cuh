@@ -106,6 +106,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// Programmatic dependent launch (launches made with launch_pdl, capi_common.cuh): let the next
+// kernel of the stream launch now (its CTAs park in pdl_wait), and wait until the previous one
+// has completed with its memory visible before touching its results.  Both are no-ops for a
+// kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Device-scope ticket with acquire-release semantics: the CTA's stores ordered before it by a
 // barrier are released to the last arriver, which acquires every earlier arriver's (the
 // barrier-then-single-thread pattern of a grid semaphore, without a MEMBAR.SC per thread).

@@ -20,6 +20,7 @@
 #include <cstdint>
 
 #include "planner.cuh"
+#include "ptx.cuh"
 
 namespace dcp {
 
@@ -68,6 +69,8 @@ __device__ __forceinline__ void bucket_shape_default_d(int m, int n, int32_t* ou
 }
 
 static __global__ void __launch_bounds__(1024, 1) routing_rows_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     __shared__ int32_t s_n;
     __shared__ int32_t s_bad;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -174,6 +177,8 @@ __device__ __forceinline__ void store_route_row(uint8_t* row, int W, uint32_t ma
 constexpr int RK_SPLIT = 8;
 
 static __global__ void __launch_bounds__(1024) routing_collect_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     __shared__ int32_t s_n;
     if (threadIdx.x == 0) s_n = 0;
     __syncthreads();
@@ -189,6 +194,8 @@ static __global__ void __launch_bounds__(1024) routing_collect_kernel(PlannerSta
 }
 
 static __global__ void __launch_bounds__(256) routing_rank_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     __shared__ int64_t tile[256];
     const int n = *ro.n_active;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -209,6 +216,8 @@ static __global__ void __launch_bounds__(256) routing_rank_kernel(PlannerState s
 }
 
 static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(PlannerState st, RoutingOut ro, int np2cap) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
 #ifdef DCP_PLANNER_PROF
     long long rt_ts[6];
     int rt_n = 0;
@@ -280,6 +289,8 @@ static __global__ void __launch_bounds__(1024, 1) routing_rows_smem_kernel(Plann
 // routing.cpp:9-63): 32 warps split the id-ordered actives; pass 1 counts each warp's N / M
 // members, pass 2 writes them after the counts of the lower warps.
 static __global__ void __launch_bounds__(1024) routing_write_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     __shared__ int32_t seg_n[32], seg_m[32];
     if (*ro.status != 0) return;
     const int s = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -355,12 +366,14 @@ static inline cudaError_t launch_routing_rows(const PlannerState& st, const Rout
         cudaError_t e = cudaFuncSetAttribute(routing_rows_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              static_cast<int>(sm));
         if (e != cudaSuccess) return e;
-        routing_collect_kernel<<<1, 1024, 0, stream>>>(st, ro);
-        routing_rank_kernel<<<dim3((st.max_slots + 255) / 256, RK_SPLIT), 256, 0, stream>>>(st, ro);
-        routing_rows_smem_kernel<<<1, 1024, sm, stream>>>(st, ro, np2);
-        routing_write_kernel<<<st.W, 1024, 0, stream>>>(st, ro);
+        if ((e = launch_pdl(routing_collect_kernel, dim3(1), dim3(1024), 0, stream, st, ro))) return e;
+        if ((e = launch_pdl(routing_rank_kernel, dim3((st.max_slots + 255) / 256, RK_SPLIT), dim3(256), 0, stream, st,
+                            ro)))
+            return e;
+        if ((e = launch_pdl(routing_rows_smem_kernel, dim3(1), dim3(1024), sm, stream, st, ro, np2))) return e;
+        if ((e = launch_pdl(routing_write_kernel, dim3(st.W), dim3(1024), 0, stream, st, ro))) return e;
     } else {
-        routing_rows_kernel<<<1, 1024, 0, stream>>>(st, ro);
+        if (cudaError_t e = launch_pdl(routing_rows_kernel, dim3(1), dim3(1024), 0, stream, st, ro)) return e;
     }
     return cudaGetLastError();
 }
@@ -394,6 +407,8 @@ __device__ __forceinline__ void row_segment(const PlannerState& st, int sl, int 
 }
 
 static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     const int s = blockIdx.x;
     const int lane = threadIdx.x & 31;
     const int gw = blockIdx.y * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -430,6 +445,8 @@ static __global__ void __launch_bounds__(256) routing_count_kernel(PlannerState 
 }
 
 static __global__ void __launch_bounds__(1024) routing_scan_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     __shared__ int64_t part[1024];
     const int s = blockIdx.x, tid = threadIdx.x;
     const int S = st.max_slots;
@@ -458,6 +475,8 @@ static __global__ void __launch_bounds__(1024) routing_scan_kernel(PlannerState 
 }
 
 static __global__ void __launch_bounds__(256) routing_scatter_kernel(PlannerState st, RoutingOut ro) {
+    pdl_trigger();  // K7 launches are PDL-chained (launch_routing_rows / dcp_planner_build_routing)
+    pdl_wait();
     const int s = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gw = blockIdx.y * (blockDim.x >> 5) + warp;

@@ -1,0 +1,9 @@
+#!/bin/bash
+set -u
+TAG=${1:-r2p}
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_moe_gpu.py tests/test_layer_graph_gpu.py tests/test_multiproc_ipc_gpu.py tests/test_planner_gpu.py tests/test_cfg1_gpu.py tests/test_exchange_protocol_gpu.py tests/test_fused_step_gpu.py -m gpu -q -x > gpurun_out/pytest_$TAG.log 2>&1
+echo "pytest rc=$?" >> gpurun_out/pytest_$TAG.log
+timeout 300 python bench_moe.py --steps 20 > gpurun_out/bench_moe_$TAG.jsonl 2>&1
+timeout 600 python bench.py --steps 20 --warmup 3 --no-mla --no-cpu-baseline > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
+tail -2 gpurun_out/pytest_$TAG.log
