@@ -488,134 +488,8 @@ static __device__ void rebalance_core(const PlannerState& st, SmemInst& si, int3
     __syncthreads();
 }
 
-// ------------------------------------------------------------------ K6 batched CP-1 admission
-// A run of queue entries that all place at CP 1 under a pure MoE-batch argmin (DualBalancedDCP
-// on one node, or LeastBatch) commits in one warp step.  Their MoE bindings do not depend on the
-// KV loads, only on B: commit c (c-th fitting entry of the run) takes the c-th element of the
-// multiset {(B_s + t, s) : t >= 0} in (value, id) order, exactly what c sequential argmins with
-// B[m]++ would pick (scheduler.cpp:118-126, 172-187).  can_allocate is then a per-instance
-// prefix over the run; the batch ends before the first entry that would not fit, which the
-// sequential path defers.  Returns the number of entries decided here (committed or
-// unschedulable), 0 when the fast path does not apply at entry i.
-static __device__ int admit_cp1_batch(const PlannerState& st, SmemInst& si, int lane, int i, int nw,
-                                      int64_t& arena_top, int64_t& pbase, int32_t* s_cnt) {
-    const unsigned FULL = 0xffffffffu;
-    const int S = st.max_slots, W = st.W;
-    const int j = i + lane;
-    const bool in = j < nw;
-    int sl = 0;
-    int64_t L = 0;
-    if (in) {
-        sl = st.waiting[j];
-        L = st.seq_len[sl];
-    }
-    const int k = in ? (st.kind == KIND_DCP ? cp_degree_d(st, L) : 1) : 0;
-    const unsigned stopm = __ballot_sync(FULL, !(in && k == 1 && L >= 1));
-    const int run = stopm ? __ffs(stopm) - 1 : 32;
-    if (run == 0) return 0;
-    const bool act = lane < run;
-    const bool unsched = act && never_fits_d(st, L, 1);
-    const bool fit = act && !unsched;
-    const unsigned fitm = __ballot_sync(FULL, fit);
-    const unsigned lt = (1u << lane) - 1u;
-    const int c = __popc(fitm & lt);  // pick index of this entry
-    int m = 0;
-    if (fit) {
-        int bmin = INT32_MAX;
-        for (int s = 0; s < W; ++s) bmin = min(bmin, si.B[s]);
-        // level v: the largest v with F(v) = sum_s max(0, v - B_s) <= c (F(v) picks come before v)
-        int v = bmin, f = 0;
-        for (;;) {
-            int f1 = 0;
-            for (int s = 0; s < W; ++s) f1 += max(0, v + 1 - si.B[s]);
-            if (f1 > c) break;
-            f = f1;
-            ++v;
-        }
-        int r = c - f;  // r-th instance, in id order, of those with B_s <= v
-        for (int s = 0; s < W; ++s)
-            if (si.B[s] <= v) {
-                if (r == 0) {
-                    m = s;
-                    break;
-                }
-                --r;
-            }
-    }
-    const int64_t need = fit ? pages_for_d(L, st.page) : 0;
-    int64_t before = 0;  // pages earlier entries of the run take from the same instance
-    for (int q = 0; q < 32; ++q) {
-        const int mq = __shfl_sync(FULL, m, q);
-        const int64_t nq = __shfl_sync(FULL, need, q);
-        if (q < lane && ((fitm >> q) & 1u) && mq == m) before += nq;
-    }
-    const unsigned failm = __ballot_sync(FULL, fit && si.nfree[m] - before < need);
-    const int stop = failm ? __ffs(failm) - 1 : run;
-    if (stop == 0) return 0;
-    const bool com = fit && lane < stop;
-    const int64_t capv = com ? need + st.reserve_pages : 0;
-    const int64_t nv = com ? need : 0;
-    int64_t cap_incl = capv, need_incl = nv;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int64_t a = __shfl_up_sync(FULL, cap_incl, o);
-        const int64_t b = __shfl_up_sync(FULL, need_incl, o);
-        if (lane >= o) {
-            cap_incl += a;
-            need_incl += b;
-        }
-    }
-    const int64_t cap_tot = __shfl_sync(FULL, cap_incl, 31), need_tot = __shfl_sync(FULL, need_incl, 31);
-    if (arena_top + cap_tot > st.arena_cap) return 0;  // the sequential path raises PL_E_ARENA
-    const unsigned comm = __ballot_sync(FULL, com);
-    const unsigned unm = __ballot_sync(FULL, unsched && lane < stop);
-    const int c0 = s_cnt[0], c2 = s_cnt[2];
-    if (com) {
-        const int rank = __popc(comm & lt);
-        PageRec& rc = st.recs[c0 + rank];
-        rc.kv[0] = m;
-        rc.top[0] = si.nfree[m] - before;
-        rc.split[0] = L;
-        rc.need_off[0] = 0;
-        rc.need_off[1] = need;
-        *reinterpret_cast<longlong2*>(&rc.base) = make_longlong2(pbase + need_incl - nv, arena_top + cap_incl - capv);
-        *reinterpret_cast<int4*>(&rc.k) = make_int4(1, sl, m, static_cast<int32_t>(capv));
-        st.res_slots[c0 + rank] = sl;
-    }
-    if (unsched && lane < stop) st.res_slots[2 * S + c2 + __popc(unm & lt)] = sl;
-    // instance state: lane s folds in its commits
-    int cnt = 0;
-    int64_t sumL = 0, sumN = 0;
-    for (int q = 0; q < 32; ++q) {
-        const int mq = __shfl_sync(FULL, m, q);
-        const int64_t Lq = __shfl_sync(FULL, L, q);
-        const int64_t nq = __shfl_sync(FULL, need, q);
-        if (((comm >> q) & 1u) && mq == lane) {
-            ++cnt;
-            sumL += Lq;
-            sumN += nq;
-        }
-    }
-    __syncwarp();  // every lane has read si / s_cnt before they change
-    if (lane < W && cnt) {
-        si.B[lane] += cnt;
-        si.K[lane] += sumL;
-        si.nfree[lane] -= sumN;
-        si.shards[lane] += cnt;
-    }
-    if (lane == 0) {
-        s_cnt[0] = c0 + __popc(comm);
-        s_cnt[2] = c2 + __popc(unm);
-    }
-    arena_top += cap_tot;
-    pbase += need_tot;
-    __syncwarp();
-    return stop;
-}
-
 // ------------------------------------------------------------------ K6 step
 static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(PlannerState st) {
-    pdl_trigger();  // planner_pages_kernel's CTAs may become resident while admission runs
     __shared__ SmemInst si;
     __shared__ SmemPlace pl;
     __shared__ int32_t s_n2;
@@ -688,16 +562,7 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
         int32_t q_sl = 0;        // lane j holds queue entry i0 + j (prefetched 32 at a time)
         int64_t q_len = 0;
         int i0 = -64;
-        const bool cp1_fast = (st.kind == KIND_DCP && st.nodes == 1) || st.kind == KIND_LEAST_BATCH;
         for (; i < nw; ++i) {
-            if (cp1_fast) {
-                const int n = admit_cp1_batch(st, si, lane, i, nw, arena_top, pbase, s_cnt);
-                if (n > 0) {
-                    i += n - 1;
-                    i0 = -64;  // the sequential path's prefetch window is stale
-                    continue;
-                }
-            }
             if (i - i0 >= 32) {
                 i0 = i;
                 if (i + lane < nw) {
@@ -778,6 +643,10 @@ static __global__ void __launch_bounds__(PL_THREADS, 1) planner_step_kernel(Plan
         }
     }
     __syncthreads();
+    // planner_pages_kernel's CTAs may launch now.  Not earlier: its parked CTAs would share this
+    // SM with the one-warp admission loop above (K6 64-admission round 110 -> 165 us when the
+    // trigger sat at the kernel's entry).
+    pdl_trigger();
     PL_PROF("admission");
 #ifdef DCP_PLANNER_PROF
     if (tid == 0) printf("sections(cycles): prefetch %lld nf %lld place %lld commit %lld\n", plp[1], plp[2], plp[3], plp[4]);
