@@ -99,6 +99,28 @@ def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup, compact=False):
         if it >= warmup:
             for p in phases:
                 phases[p].append([a.elapsed_time(b) * 1e3 for a, b in ev[p]])
+    # whole-step leg: every instance's four launches back to back (PDL-chained, no events in
+    # between), gated behind a device sleep so the host has queued them all before the device
+    # starts; the identity expert is the receive region itself (no copy).  step time / W is the
+    # device time of one instance's exchange, as each of W GPUs would spend it.
+    whole = []
+    if not compact:
+        for it in range(warmup + steps):
+            a, b = E_(), E_()
+            _capi.lib().dcp_device_sleep(ctx.handle, 2000, ctypes.c_void_p(stream.cuda_stream))
+            a.record(stream)
+            for s in range(W):
+                inst[s].dispatch(*toks[s], m_count_ptr=mcnt[s].data_ptr())
+            for s in range(W):
+                inst[s].receive_regions()
+            for s in range(W):
+                inst[s].combine_put_regions(inst[s].regions()[0])
+            for s in range(W):
+                inst[s].combine_reduce()
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            if it >= warmup:
+                whole.append(a.elapsed_time(b) * 1e3)
     # correctness of the identity round trip: out[t] = (#distinct ranks of t) * x[t]
     for s in range(W):
         ref = toks[s][0].float() * torch.from_numpy(distinct[s]).to(dev)[:, None].float()
@@ -116,6 +138,13 @@ def run_config(ctx, dev, name, H, E, k, W, M, steps, warmup, compact=False):
                   "us_max_instance": float(np.median(a.max(axis=1))),
                   "bytes": moved[p], "gbs": moved[p] / (s_sum * 1e-6) / 1e9}
     res["us_per_instance_step"] = tot_sum / W
+    if whole:
+        res["whole_step"] = {"us": float(np.median(whole)), "us_per_instance": float(np.median(whole)) / W,
+                             "us_p99_per_instance": float(np.percentile(whole, 99)) / W,
+                             "cross_instance_gbs": alg_xfer / (float(np.median(whole)) * 1e-6) / 1e9,
+                             "note": "all W instances' K4 -> K5a -> K5b -> K5c launched back to back "
+                                     "behind a device sleep (no per-launch events); identity expert = the "
+                                     "receive region itself; per instance = step / W"}
     res["receive_mode"] = "compact (rows copied out of the pool)" if compact else "region (rows read in place)"
     res["note"] = ("single GPU: cross-instance stores are local HBM stores; expert FFN = identity, untimed; "
                    "each step gated behind a device sleep so CUDA events time device work only; "

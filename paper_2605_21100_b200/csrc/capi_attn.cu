@@ -243,6 +243,7 @@ int dcp_k1_set_trace(void* dev_buf) {
 }
 
 int dcp_splitkv_decode_attn(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) {
+    DCP_NVTX("K1 splitkv_decode");
     DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");
     DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
     if (a->num_shards == 0) return DCP_OK;
@@ -345,11 +346,13 @@ static int decode_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, 
 
 int dcp_decode_attn_routed(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
                            void* stream) {
+    DCP_NVTX("K1 routed");
     return decode_routed(ctx, x, v, a, 0u, stream);
 }
 
 int dcp_decode_step_fused(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v, const dcp_attn_args* a,
                           void* stream) {
+    DCP_NVTX("DCP fused step (fence + K2 + K1 + K3)");
     DCP_REQUIRE(x && x->committed, DCP_E_INVALID_ARG, "NULL or uncommitted exchange (dcp_xchg_commit)");
     DCP_REQUIRE(v && v->m_rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", v ? v->m_rows : 0,
                 x->cfg.m_max);
@@ -395,6 +398,7 @@ static int f32_common(dcp_ctx* ctx, const dcp_attn_args* a, AttnF32Params& prm) 
 }
 
 int dcp_splitkv_decode_attn_f32(dcp_ctx* ctx, const dcp_attn_args* a, void* stream) {
+    DCP_NVTX("K1 splitkv_decode f32");
     DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");
     DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
     if (a->num_shards == 0) return DCP_OK;

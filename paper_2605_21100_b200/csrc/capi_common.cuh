@@ -10,6 +10,8 @@
 #include <cstring>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "dcp_capi.h"
 
 namespace dcp {
@@ -74,3 +76,14 @@ struct dcp_ctx {
     dcp::TmapCacheEntry kv_maps[4];
     int kv_map_next = 0;
 };
+
+// NVTX range over one C-ABI call (SURVEY §5 tracing): a profiler (nsys / ncu --nvtx) sees each
+// host-side phase of the step (planner, routing, attention, exchange, MoE) as a named range.
+// NVTX v3 is header-only; without an attached tool a push / pop is one predictable branch.
+struct DcpNvtxRange {
+    explicit DcpNvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~DcpNvtxRange() { nvtxRangePop(); }
+    DcpNvtxRange(const DcpNvtxRange&) = delete;
+    DcpNvtxRange& operator=(const DcpNvtxRange&) = delete;
+};
+#define DCP_NVTX(name) DcpNvtxRange dcp_nvtx_range_(name)

@@ -168,6 +168,7 @@ int dcp_layer_graph_create(dcp_ctx* ctx, const dcp_layer_graph_desc* d, dcp_laye
 }
 
 int dcp_layer_graph_launch(dcp_layer_graph* g, int32_t m_rows, void* stream) {
+    DCP_NVTX("layer graph replay");
     DCP_REQUIRE(g, DCP_E_INVALID_ARG, "NULL graph");
     DCP_REQUIRE(m_rows >= 0 && m_rows <= g->d.xchg->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", m_rows,
                 g->d.xchg->cfg.m_max);

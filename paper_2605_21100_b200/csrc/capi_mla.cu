@@ -166,6 +166,7 @@ int dcp_mla_set_trace(void* dev_buf) {
 }
 
 int dcp_mla_decode_attn(dcp_ctx* ctx, const dcp_mla_args* a, void* stream) {
+    DCP_NVTX("K10 mla_decode");
     DCP_REQUIRE(ctx && a, DCP_E_INVALID_ARG, "NULL ctx/args");
     DCP_REQUIRE(a->num_shards >= 0, DCP_E_INVALID_ARG, "num_shards < 0");
     if (a->num_shards == 0) return DCP_OK;

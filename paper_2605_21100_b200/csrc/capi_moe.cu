@@ -184,6 +184,7 @@ int dcp_moe_regions(dcp_moe* x, int32_t parity, void** x_region, int32_t** meta_
 
 int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const float* w, const int32_t* m_count,
                      void* stream) {
+    DCP_NVTX("K4 moe dispatch");
     // x_local / idx / w may be NULL when the instance has no MoE-bound tokens (M = 0)
     DCP_REQUIRE(x && m_count, DCP_E_INVALID_ARG, "NULL argument");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -195,6 +196,7 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
 
 int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const float* w,
                           const int32_t* m_count, void* stream) {
+    DCP_NVTX("K4 moe step dispatch");
     DCP_REQUIRE(x && x->committed && m_count, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
@@ -206,6 +208,7 @@ int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, c
 }
 
 int dcp_moe_receive_regions(dcp_moe* x, void* stream) {
+    DCP_NVTX("K5a moe receive");
     DCP_REQUIRE(x, DCP_E_INVALID_ARG, "NULL argument");
     DCP_CUDA_TRY(launch_pdl(moe_receive_counts_kernel, dim3(1), dim3(32), 0, static_cast<cudaStream_t>(stream), x->host));
     x->received = true;
@@ -250,6 +253,7 @@ static int combine_put(dcp_moe* x, const void* y, int region, void* stream) {
 int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream) { return combine_put(x, y_rows, 0, stream); }
 
 int dcp_moe_combine_put_regions(dcp_moe* x, const void* y_region, void* stream) {
+    DCP_NVTX("K5b moe combine_put");
     return combine_put(x, y_region, 1, stream);
 }
 
@@ -263,6 +267,7 @@ int dcp_moe_expert_identity(dcp_moe* x, void* y_region, void* stream) {
 }
 
 int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {
+    DCP_NVTX("K5c moe combine_reduce");
     DCP_REQUIRE(x && out && x->m_count_dev, DCP_E_INVALID_ARG, "call dcp_moe_dispatch first");
     const int groups = x->cfg.hidden / 4;  // hidden % 8 == 0
     DCP_CUDA_TRY(launch_pdl(moe_combine_reduce_kernel, dim3(x->cfg.m_max, (groups + 255) / 256), dim3(256), 0,

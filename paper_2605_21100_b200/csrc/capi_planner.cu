@@ -372,6 +372,7 @@ int dcp_planner_enqueue(dcp_planner* pl, const int64_t* ids, const int64_t* lens
 }
 
 int dcp_planner_step(dcp_planner* pl, void* stream) {
+    DCP_NVTX("K6 planner step");
     DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
     set_stream(pl, stream);
     pl->last_launches = 0;
@@ -615,6 +616,7 @@ int64_t dcp_planner_dump_page_table(dcp_planner* pl, char* buf, int64_t cap) {
 }
 
 int dcp_planner_build_routing(dcp_planner* pl, void* stream) {
+    DCP_NVTX("K7 routing tables");
     DCP_REQUIRE(pl, DCP_E_INVALID_ARG, "NULL planner");
     set_stream(pl, stream);
     DCP_CUDA_TRY(launch_routing_rows(pl->st, pl->ro, pl->stream));
@@ -698,6 +700,7 @@ int dcp_kv_append(dcp_planner* pl, int32_t s, const void* kv_new, void* const* p
 int dcp_kv_migrate(dcp_planner* pl, const int64_t* ids, int32_t n, const void* const* src_k,
                    const void* const* src_v, void* const* pools, int32_t hkv, int32_t head_dim, int32_t elem_bytes,
                    void* stream) {
+    DCP_NVTX("KV migrate");
     DCP_REQUIRE(pl && (n == 0 || (ids && src_k && src_v && pools)), DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(n >= 0 && n <= 65535, DCP_E_INVALID_ARG, "n %d", n);
     DCP_REQUIRE(hkv >= 1 && head_dim >= 1 && (elem_bytes == 2 || elem_bytes == 4), DCP_E_UNSUPPORTED,

@@ -203,6 +203,7 @@ int dcp_xchg_write_queries(dcp_xchg* x, const void* q_rows, int32_t rows, void* 
 }
 
 int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
+    DCP_NVTX("K2 q_route");
     DCP_REQUIRE(x && v, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self && v->world == x->cfg.world, DCP_E_INVALID_ARG,
                 "view of instance %d used on instance %d", v->instance, x->cfg.self);
@@ -217,6 +218,7 @@ int dcp_route_q(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
 }
 
 int dcp_merge_partials(dcp_xchg* x, const dcp_instance_view* v, void* stream) {
+    DCP_NVTX("K3 lse_merge");
     DCP_REQUIRE(x && v, DCP_E_INVALID_ARG, "NULL argument");
     DCP_REQUIRE(v->instance == x->cfg.self, DCP_E_INVALID_ARG, "view/instance mismatch");
     DCP_REQUIRE(v->m_rows <= x->cfg.m_max, DCP_E_SHAPE_OVERFLOW, "M %d > m_max %d", v->m_rows, x->cfg.m_max);
@@ -269,6 +271,7 @@ int dcp_step_graph_create(dcp_ctx* ctx, dcp_xchg* x, const dcp_instance_view* v,
 }
 
 int dcp_step_graph_launch(dcp_step_graph* g, int32_t m, int32_t n, void* stream) {
+    DCP_NVTX("step graph replay");
     DCP_REQUIRE(g, DCP_E_INVALID_ARG, "NULL graph");
     DCP_REQUIRE(m <= 256 && n <= 512 && m >= 0 && n >= 0, DCP_E_SHAPE_OVERFLOW,
                 "execution shape (%d,%d) exceeds (256,512)", m, n);

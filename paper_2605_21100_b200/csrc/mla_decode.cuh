@@ -53,6 +53,10 @@ constexpr int HT = TILE / 2;         // tokens per CTA in S = Q K^T
 constexpr int STAGE = 8192;          // ring stage bytes
 constexpr int Q_BYTES = NKB * 8192;  // 64 heads x 576 bf16 per CTA
 constexpr int P_BYTES = 2 * 8192;    // 64 heads x 128 tokens bf16 per CTA
+#ifndef MLA_NP
+#define MLA_NP 2
+#endif
+constexpr int NP = MLA_NP;           // P buffers (softmax -> PV); 3 only fits with 2 + 2 PV stages, which starves PV (profiles/r2_k10_ab.md)
 // Four accumulator chains, each issued by its own MMA warp and fed by its own ring: an
 // accumulating 2-CTA M=128 MMA costs ~120 ns whatever its N, but chains issued by different
 // warps overlap (tools/probe/mma_rate.cu).  S = Q K^T is split over K into two accumulators
@@ -75,7 +79,7 @@ static_assert(MLA_RS_QA == QA_BOXES, "the QA ring has one stage per QA box");
 constexpr int NSTAGES = ring_first(NRING);  // 15 stages of 8 KB
 constexpr int OFF_Q = 0;
 constexpr int OFF_P = OFF_Q + Q_BYTES;
-constexpr int OFF_RING = OFF_P + 2 * P_BYTES;
+constexpr int OFF_RING = OFF_P + NP * P_BYTES;
 constexpr int OFF_MISC = OFF_RING + NSTAGES * STAGE;
 // misc: barriers then exchange scratch.  Ring "full" barriers live in the leader: 1 arrival
 // (the leader's issuer, expecting both CTAs' bytes) + tx; "empty" in each CTA: 1 (MMA commit multicast).
@@ -85,9 +89,9 @@ constexpr int BAR_QFULL = BAR_EMPTY + 8 * NSTAGES; // leader: 1 + tx
 constexpr int BAR_QEMPTY = BAR_QFULL + 8;     // each: 2 (both QK MMA warps)
 constexpr int BAR_SFULL = BAR_QEMPTY + 8;     // [2 S buffers][A, B] each: 1
 constexpr int BAR_SEMPTY = BAR_SFULL + 32;    // [2] leader: 8 softmax warps
-constexpr int BAR_PFULL = BAR_SEMPTY + 16;    // [2] leader: 8
-constexpr int BAR_PEMPTY = BAR_PFULL + 16;    // [2] each: 2 (both PV MMA warps)
-constexpr int BAR_OEMPTY = BAR_PEMPTY + 16;   // leader: 8
+constexpr int BAR_PFULL = BAR_SEMPTY + 16;    // [NP] leader: 8
+constexpr int BAR_PEMPTY = BAR_PFULL + 8 * NP;  // [NP] each: 2 (both PV MMA warps)
+constexpr int BAR_OEMPTY = BAR_PEMPTY + 8 * NP; // leader: 8
 constexpr int TMEM_SLOT = BAR_OEMPTY + 8;
 constexpr int RED = 512;                      // float[2][128] exchange scratch
 constexpr int MISC_BYTES = RED + 2 * 128 * 4;
@@ -290,6 +294,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             mbar_init(misc + BAR_SFULL + 16 * b, 1);
             mbar_init(misc + BAR_SFULL + 16 * b + 8, 1);
             mbar_init(misc + BAR_SEMPTY + 8 * b, 8);
+        }
+        for (int b = 0; b < NP; ++b) {
             mbar_init(misc + BAR_PFULL + 8 * b, 8);
             mbar_init(misc + BAR_PEMPTY + 8 * b, 2);
         }
@@ -493,11 +499,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             // ---- O[j] += P[sb] V[j] over 4 token quarters ----
                             const int j = rk - RV0;
                             const bool first = t == t0;
-                            tc::mbar_wait_sleep(misc + BAR_PFULL + 8 * sb, (g >> 1) & 1);
+                            const uint32_t pb = g % NP;
+                            tc::mbar_wait_sleep(misc + BAR_PFULL + 8 * pb, (g / NP) & 1);
                             if (first && seg > 0) tc::mbar_wait_sleep(misc + BAR_OEMPTY, (seg - 1) & 1);
                             tc::fence_after_sync();
                             if (lane == 0 && rk == RV0) MLA_TRACE(g, 2);
-                            const uint64_t pd = dP + ((sb * P_BYTES) >> 4);
+                            const uint64_t pd = dP + ((pb * P_BYTES) >> 4);
                             for (int q = 0; q < TILE / 32; ++q) {
                                 const uint32_t s = wait_full();
                                 const uint64_t b0 = dRV + ((s * STAGE) >> 4);
@@ -511,7 +518,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 }
                                 tc::commit2_mc_warp(misc + BAR_EMPTY + 8 * (s0 + s), 0x3);
                             }
-                            tc::commit2_mc_warp(misc + BAR_PEMPTY + 8 * sb, 0x3);
+                            tc::commit2_mc_warp(misc + BAR_PEMPTY + 8 * pb, 0x3);
                             if (lane == 0 && rk == RV0) MLA_TRACE(g, 3);
                         }
                     }
@@ -572,13 +579,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_SFULL + 16 * sb, (g >> 1) & 1);
                     tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_SFULL + 16 * sb + 8, (g >> 1) & 1);
                     tc::fence_after_sync();
-                    if (tid == 0) MLA_TRACE(g, 4 + 2 * static_cast<int>(cta));
+                    if (tid == 0 && cta == 0) MLA_TRACE(g, 4);
                     if (p.dbg & 2) {  // experiment: pass S / P through without the softmax math
                         __syncwarp();
                         if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_SEMPTY + 8 * sb);
-                        if (g >= 2) tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
+                        if (g >= NP) tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * (g % NP), ((g / NP) + 1) & 1);
                         __syncwarp();
-                        if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_PFULL + 8 * sb);
+                        if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_PFULL + 8 * (g % NP));
                         m_used = 0.f;
                         l_run = 1.f;
                         continue;
@@ -606,6 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     named_bar_sync(1, 128);
                     mx = fmaxf(mx, red[partner]);
                     named_bar_sync(1, 128);  // red reusable
+                    if (tid == 0 && cta == 0) MLA_TRACE(g, 6);
                     bool rescale = false;
                     float alpha = 1.f;
                     if (t == t0) {
@@ -622,10 +630,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         ps += s[j];
                     }
                     l_run = l_run * alpha + ps;
-                    // P buffer sb is free once PV(g-2) completed
-                    if (g >= 2) tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * sb, ((g >> 1) + 1) & 1);
+                    // P buffer g % NP is free once PV(g - NP) completed
+                    const uint32_t pb = g % NP;
+                    if (g >= NP) tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * pb, ((g / NP) + 1) & 1);
+                    if (tid == 0 && cta == 0) MLA_TRACE(g, 7);
                     {
-                        uint8_t* prow = smem + OFF_P + sb * P_BYTES + half * 8192 + hl * 128;
+                        uint8_t* prow = smem + OFF_P + pb * P_BYTES + half * 8192 + hl * 128;
 #pragma unroll
                         for (int ch = 0; ch < 8; ++ch) {
                             uint4 v;
@@ -639,7 +649,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     // O *= alpha once PV(g-1) has landed.  tcgen05.ld/st are warp-collective, so the
                     // whole warp waits and rewrites its lanes if any lane needs it (alpha = 1 elsewhere).
                     if (__any_sync(0xffffffffu, rescale)) {
-                        tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) & 1), ((g - 1) >> 1) & 1);
+                        tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) % NP), ((g - 1) / NP) & 1);
                         tc::fence_after_sync();
                         for (int c = 0; c < 256; c += 32) {
                             uint32_t ov[32];
@@ -654,11 +664,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     tc::fence_proxy_async_smem();
                     tc::fence_before_sync();
                     __syncwarp();
-                    if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_PFULL + 8 * sb);
-                    if (tid == 0) MLA_TRACE(g, 5 + 2 * static_cast<int>(cta));
+                    if (lane == 0) tc::mbar_arrive_cluster(lead + BAR_PFULL + 8 * pb);
+                    if (tid == 0 && cta == 0) MLA_TRACE(g, 5);
                 }
                 // ---- epilogue of segment [t0, t1) of shard r ----
-                tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) & 1), ((g - 1) >> 1) & 1);
+                tc::mbar_wait_sleep(sbase + OFF_MISC + BAR_PEMPTY + 8 * ((g - 1) % NP), ((g - 1) / NP) & 1);
                 tc::fence_after_sync();
                 red[tid] = l_run;
                 named_bar_sync(1, 128);

@@ -49,6 +49,21 @@
 namespace dcp {
 
 constexpr int MOE_MAXK = 16;
+#ifndef MOE_K5B_WARP
+#define MOE_K5B_WARP 1  // K5b: one warp per row (1) or one CTA per row (0)
+#endif
+#ifndef MOE_K4_FENCE_FIRST
+#define MOE_K4_FENCE_FIRST 1  // K4: warp 0 runs the step fence while warps 1.. build the token masks (1)
+#endif
+#ifndef MOE_K5C_PREFETCH
+#define MOE_K5C_PREFETCH 1  // K5c: read the token's destination set before the arrival-counter wait
+#endif
+#ifndef MOE_K4_PRELOAD
+#define MOE_K4_PRELOAD 1  // K4: load the CTA's first token row before the layout / fence
+#endif
+#ifndef MOE_SINGLE_RELEASE
+#define MOE_SINGLE_RELEASE 1  // K4 / K5b: CTAs meet on a gpu-scope ticket; the last one issues ONE system fence
+#endif                        // and the per-destination row counts (instead of a red.release.sys per CTA)
 constexpr int MOE_THREADS = 256;
 
 struct MoePeers {
@@ -153,10 +168,31 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
     int32_t* s_mask = sm;               // [M] destination-rank bitmask of each token
     int32_t* s_slot = sm + p.m_max;     // [M][W] slot at each destination (-1 = not routed)
     __shared__ int32_t s_count[PL_MAXW], s_sent[PL_MAXW];
-    const uint32_t ep = *p.epoch + (with_fence ? 1u : 0u);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ep = *p.epoch + (with_fence ? 1u : 0u);
     constexpr int NW = MOE_THREADS / 32;
+    constexpr int VPT = 4;  // 16-byte vectors in registers per thread per pass (4 x 256 x 16 B = 16 KB)
+    const int nvec = H / 8;
+    uint4 v[VPT];
+#if MOE_K4_PRELOAD
+    if (static_cast<int>(blockIdx.x) < M) {
+        const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)blockIdx.x * H);
+#pragma unroll
+        for (int u = 0; u < VPT; ++u)
+            if (u * MOE_THREADS + tid < nvec) v[u] = __ldg(src + u * MOE_THREADS + tid);
+    }
+#endif
+#if MOE_K4_FENCE_FIRST
+    if (with_fence && warp == 0) {
+        if (blockIdx.x == 0 && lane == 0) st_relaxed_sys(moe_done(p, p.self), ep - 1);
+        for (int s = lane; s < W; s += 32)
+            if (s != p.self) wait_flag(moe_done(p, s), ep - 2, p.wc, (SITE_FENCE << 24) | (s << 16), true);
+    }
+    for (int t = tid - 32; t < M; t += MOE_THREADS - 32) {
+        if (t < 0) break;
+#else
     for (int t = tid; t < M; t += MOE_THREADS) {
+#endif
         uint32_t m = 0;
         for (int j = 0; j < K; ++j) m |= 1u << (__ldg(topk_idx + t * K + j) / p.e_per_rank);
         s_mask[t] = static_cast<int32_t>(m);
@@ -175,7 +211,7 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
         }
         if (lane == 0) s_count[d] = carry;
     }
-    if (with_fence && warp == 0) {
+    if (!MOE_K4_FENCE_FIRST && with_fence && warp == 0) {
         if (blockIdx.x == 0 && lane == 0) st_relaxed_sys(moe_done(p, p.self), ep - 1);
         for (int s = lane; s < W; s += 32)
             if (s != p.self) wait_flag(moe_done(p, s), ep - 2, p.wc, (SITE_FENCE << 24) | (s << 16), true);
@@ -195,17 +231,16 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
     }
     // rows: CTA c sends tokens c, c + C, ...; each token's hidden state is read once and
     // stored to all of its destination ranks.
-    const int nvec = H / 8;
-    constexpr int VPT = 4;  // 16-byte vectors in registers per thread per pass (4 x 256 x 16 B = 16 KB)
     for (int t = blockIdx.x; t < M; t += gridDim.x) {
         const uint32_t mask = static_cast<uint32_t>(s_mask[t]);
         const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * H);
         for (int v0 = 0; v0 < nvec; v0 += VPT * MOE_THREADS) {
-            uint4 v[VPT];
+            if (!MOE_K4_PRELOAD || t != static_cast<int>(blockIdx.x) || v0 != 0) {
 #pragma unroll
-            for (int u = 0; u < VPT; ++u) {
-                const int i = v0 + u * MOE_THREADS + tid;
-                if (i < nvec) v[u] = __ldg(src + i);
+                for (int u = 0; u < VPT; ++u) {
+                    const int i = v0 + u * MOE_THREADS + tid;
+                    if (i < nvec) v[u] = __ldg(src + i);
+                }
             }
             for (uint32_t mm = mask; mm; mm &= mm - 1) {
                 const int d = __ffs(mm) - 1;
@@ -236,6 +271,23 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
         }
     }
     __syncthreads();
+#if MOE_SINGLE_RELEASE
+    // The CTAs meet on a gpu-scope acq_rel ticket; the last one has acquired every CTA's row stores
+    // and publishes them with one system fence (release cumulativity) and relaxed count adds.
+    if (tid == 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.exit_ticket) : "memory");
+        if (old == static_cast<int>(gridDim.x) - 1) {
+            *p.exit_ticket = 0;
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (int d = 0; d < W; ++d)
+                if (s_count[d]) asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(rx_arr(p, d, ep) + p.self),
+                                             "r"(s_count[d]) : "memory");
+            if (with_fence) *p.epoch = ep;
+        }
+    }
+    return;
+#endif
     // one release per (CTA, destination) covers every row this CTA stored there
     if (tid < W && s_sent[tid]) red_release_sys_add(rx_arr(p, tid, ep) + p.self, s_sent[tid]);
     if (with_fence && tid == 0) {
@@ -370,6 +422,31 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(con
     const int R = s_off[W];
     const int nvec = H / 8;
     const int32_t* rm = rx_meta(p, p.self, ep);
+#if MOE_K5B_WARP
+    // one warp per received row, 8 vectors per lane in flight
+    constexpr int VPL = 8;
+    const int lane = tid & 31;
+    const int nwarps = gridDim.x * (MOE_THREADS / 32);
+    for (int r = blockIdx.x * (MOE_THREADS / 32) + (tid >> 5); r < R; r += nwarps) {
+        int s = 0;
+        while (s_off[s + 1] <= r) ++s;
+        const int j = r - s_off[s];
+        const int t = __ldcg(rm + ((size_t)s * p.m_max + j) * p.meta);
+        const uint4* src =
+            reinterpret_cast<const uint4*>(y_rows + (size_t)(region ? s * p.m_max + j : r) * H);
+        uint4* dst = reinterpret_cast<uint4*>(cb_y(p, s, ep) + ((size_t)t * W + p.self) * H);
+        for (int v0 = lane; v0 < nvec; v0 += VPL * 32) {
+            uint4 v[VPL];
+#pragma unroll
+            for (int u = 0; u < VPL; ++u)
+                if (v0 + u * 32 < nvec) v[u] = __ldg(src + v0 + u * 32);
+#pragma unroll
+            for (int u = 0; u < VPL; ++u)
+                if (v0 + u * 32 < nvec) dst[v0 + u * 32] = v[u];
+        }
+        if (lane == 0) atomicAdd(&s_sent[s], 1);
+    }
+#else
     constexpr int VPT = 4;
     for (int r = blockIdx.x; r < R; r += gridDim.x) {
         int s = 0;
@@ -390,7 +467,23 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(con
         }
         if (tid == 0) ++s_sent[s];
     }
+#endif
     __syncthreads();
+#if MOE_SINGLE_RELEASE
+    if (tid == 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.exit_ticket) : "memory");
+        if (old == static_cast<int>(gridDim.x) - 1) {
+            *p.exit_ticket = 0;
+            asm volatile("fence.acq_rel.sys;" ::: "memory");
+            for (int d = 0; d < W; ++d)
+                if (s_off[d + 1] > s_off[d])
+                    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(cb_arr(p, d, ep) + p.self),
+                                 "r"(s_off[d + 1] - s_off[d]) : "memory");
+        }
+    }
+    return;
+#endif
     if (tid < W && s_sent[tid]) red_release_sys_add(cb_arr(p, tid, ep) + p.self, s_sent[tid]);
 }
 
@@ -406,6 +499,12 @@ static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __
     if (t >= *m_count) return;
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H;
+#if MOE_K5C_PREFETCH
+    // the token's destination set (this instance's own K4 layout) is read before the flag wait
+    uint32_t dm = 0;
+#pragma unroll 8
+    for (int d = 0; d < W; ++d) dm |= (p.slot_tbl[t * W + d] >= 0 ? 1u : 0u) << d;
+#endif
     if (threadIdx.x < W)
         wait_flag(cb_arr(p, p.self, ep) + threadIdx.x, p.cb_target[(ep & 1) * W + threadIdx.x], p.wc,
                   (SITE_MOE_CB << 24) | (threadIdx.x << 16) | (t & 0xffff), true);
@@ -415,13 +514,18 @@ static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __
     const __nv_bfloat16* cy = cb_y(p, p.self, ep);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     uint2 v[PL_MAXW];
+#if !MOE_K5C_PREFETCH
+    uint32_t dm = 0;
+#pragma unroll 8
+    for (int d = 0; d < W; ++d) dm |= (p.slot_tbl[t * W + d] >= 0 ? 1u : 0u) << d;
+#endif
 #pragma unroll 8
     for (int d = 0; d < W; ++d)
-        if (p.slot_tbl[t * W + d] >= 0)
+        if ((dm >> d) & 1u)
             v[d] = __ldcg(reinterpret_cast<const uint2*>(cy + ((size_t)t * W + d) * H) + q);
 #pragma unroll 8
     for (int d = 0; d < W; ++d) {
-        if (p.slot_tbl[t * W + d] < 0) continue;
+        if (!((dm >> d) & 1u)) continue;
         const float2 lo = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[d].x));
         const float2 hi = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v[d].y));
         a0 += lo.x;

@@ -128,27 +128,34 @@ class MoeInstance:
 
     def expert_stage(self, R, w_gate, w_up, w_down):
         """Library-GEMM expert FFN over the R received rows (local experts
-        w_*[e - first_local_expert])."""
+        w_*[e - first_local_expert]): the (row, expert, gate weight) pairs of the meta rows are
+        grouped by expert on the device, then one gate / up / down GEMM triple per local expert
+        in ascending expert order, y = sum_e w_e * W_down(silu(W_gate x) * W_up x)."""
         e0 = self.id * (self.E // self.world)
-        meta = self.meta_rows[:R].cpu().numpy()
-        x = self.x_rows[:R].float()
-        y = torch.zeros(R, self.H, dtype=torch.float32, device=x.device)
-        per = {}
-        for r in range(R):
-            n = int(meta[r, 1])
-            for j in range(n):
-                e = int(meta[r, 2 + 2 * j])
-                wv = float(np.int32(meta[r, 3 + 2 * j]).view(np.float32))
-                per.setdefault(e, []).append((r, wv))
-        for e in sorted(per):
-            rows = torch.tensor([r for r, _ in per[e]], device=x.device)
-            wts = torch.tensor([wv for _, wv in per[e]], device=x.device, dtype=torch.float32)
-            xe = x[rows].to(torch.bfloat16)
-            g = xe @ w_gate[e - e0].T
-            u = xe @ w_up[e - e0].T
-            a = (torch.nn.functional.silu(g.float()) * u.float()).to(torch.bfloat16)
-            o = (a @ w_down[e - e0].T).float()
-            y.index_add_(0, rows, o * wts[:, None])
+        y = torch.zeros(R, self.H, dtype=torch.float32, device=self.x_rows.device)
+        if R > 0:
+            meta = self.meta_rows[:R]
+            k = (meta.shape[1] - 2) // 2
+            n = meta[:, 1:2]
+            ex = meta[:, 2:2 + 2 * k:2]
+            wt = meta[:, 3:3 + 2 * k:2].contiguous().view(torch.float32)
+            valid = torch.arange(k, device=meta.device)[None, :] < n
+            rows = torch.arange(R, device=meta.device)[:, None].expand(R, k)[valid]
+            ex, wt = ex[valid], wt[valid]
+            order = torch.argsort(ex * R + rows)  # by expert, then row
+            rows, ex, wt = rows[order], ex[order], wt[order]
+            uniq, cnt = torch.unique_consecutive(ex, return_counts=True)
+            x = self.x_rows[:R]
+            start = 0
+            for e, c in zip(uniq.tolist(), cnt.tolist()):
+                rr, ww = rows[start:start + c], wt[start:start + c]
+                start += c
+                xe = x[rr]
+                g = xe @ w_gate[e - e0].T
+                u = xe @ w_up[e - e0].T
+                a = (torch.nn.functional.silu(g.float()) * u.float()).to(torch.bfloat16)
+                o = (a @ w_down[e - e0].T).float()
+                y.index_add_(0, rr, o * ww[:, None])
         self.y_rows[:R] = y.to(torch.bfloat16)
 
     def expert_identity(self, y_region, stream=None):

@@ -51,12 +51,15 @@ t[252:] = 0
 n = int((t[:, 0] > 0).sum())
 t0 = t[0, 0]
 t = t[:n].astype(np.int64) - t0
-print("tile  qk_start qk_issued  pfull(g) pv_done | S0ready P0pub S1ready P1pub   (ns from tile 0)")
+print("tile  qk_start qk_issued  pfull(g) pv_issued | S_ready P_pub max_done P_free  (CTA0 softmax; ns from tile 0)")
 for g in range(n):
     print(f"{g:4d} " + " ".join(f"{x:8d}" for x in t[g]))
 d = np.diff(t[:, 0])
 print("per-tile period (ns): median", np.median(d), "mean", d.mean())
 sm = t[:, 5] - t[:, 4]
 print("softmax CTA0 S-ready -> P-published: median", np.median(sm))
+print("  S-ready -> max done: median", np.median(t[:, 6] - t[:, 4]), " max done -> P buffer free:", np.median(t[:, 7] - t[:, 6]),
+      " P free -> P published:", np.median(t[:, 5] - t[:, 7]))
+print("  softmax idle (S-ready(g) - P-pub(g-1)): median", np.median(t[1:, 4] - t[:-1, 5]))
 print("S-ready(g) after qk_issued(g): median", np.median(t[:, 4] - t[:, 1]))
 print("MMA P(g) wait return after P-published(g) (max of CTAs):", np.median(t[:-1, 2] - np.maximum(t[:-1, 5], t[:-1, 7])))
