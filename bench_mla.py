@@ -57,14 +57,22 @@ def alg_flops(b):
     return 2.0 * int(b.shard_len.sum()) * HEADS * (DK + DV)
 
 
-def run_workload(ctx, dev, name, lens, steps, warmup):
+def inputs(dev, lens):
+    """The bench's own batch, cache pool and queries (device, seeded): tests check these."""
     import torch
     from paper_2605_21100_b200 import workload
-    from paper_2605_21100_b200.attention import MlaDecodeAttention
     b = workload.paged_batch(lens, HEADS, 1, DK, PAGE)
     g = torch.Generator(device=dev).manual_seed(99)
     pool = torch.randn(b.num_frames, PAGE, DK, generator=g, device=dev, dtype=torch.bfloat16)
     q = torch.randn(len(lens), HEADS, DK, generator=g, device=dev, dtype=torch.bfloat16)
+    return b, pool, q
+
+
+def run_workload(ctx, dev, name, lens, steps, warmup):
+    import torch
+    from paper_2605_21100_b200 import workload
+    from paper_2605_21100_b200.attention import MlaDecodeAttention
+    b, pool, q = inputs(dev, lens)
     att = MlaDecodeAttention(ctx, PAGE, max_shards=len(lens))
     att.prepare(q, pool, torch.from_numpy(b.block_table).to(dev), torch.from_numpy(b.cu_pages).to(dev),
                 torch.from_numpy(b.shard_len).to(dev))

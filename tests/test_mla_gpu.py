@@ -187,3 +187,20 @@ def test_mla_routed_dcp_step(ctx, W):
     for x in insts:
         x.close()
     pl.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2-shaped (64 req, KV 1K-32K)", "long-mix (1 x 512K + 63 x 1K-8K)"])
+def test_mla_bench_inputs_all_shards(ctx, name):
+    """bench_mla.py's own workloads at full size (the K10 numbers in bench.py's line): every
+    shard and head of the bench's seeded pool and queries against the fp64 oracle."""
+    import bench_mla
+    from paper_2605_21100_b200.attention import MlaDecodeAttention
+    dev = torch.device("cuda:0")
+    lens = bench_mla.workloads()[name]
+    b, pool, q = bench_mla.inputs(dev, lens)
+    att = MlaDecodeAttention(ctx, b.page_size, max_shards=len(lens))
+    out, lse = att(q, pool, torch.from_numpy(b.block_table).to(dev), torch.from_numpy(b.cu_pages).to(dev),
+                   torch.from_numpy(b.shard_len).to(dev))
+    torch.cuda.synchronize()
+    rel, dl = _check(b, q.cpu(), pool.cpu(), out.cpu().double().numpy(), lse.cpu().double().numpy())
+    print(f"{name}: {len(lens)} shards x 128 heads, worst O rel-L2 {rel:.3e}, LSE |d| {dl:.3e}")
