@@ -71,6 +71,9 @@ struct AttnParams {
     int32_t* exit_ticket;        // grid exit counter (step)
 };
 enum : uint32_t { FUSE_STEP = 1, FUSE_ROUTE = 2, FUSE_MERGE = 4 };
+#ifndef K9_U
+#define K9_U 8  // K9 merge: parts whose partial rows are in flight together (GQA <= 4)
+#endif
 
 __device__ __forceinline__ long long k1_gtime() {
     long long t;
@@ -228,6 +231,15 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                     }
                 }
                 __syncwarp();
+            }
+        }
+        if ((p.fuse & FUSE_STEP) && lane == 0) {
+            // Fused step: the last CTA to have read the epoch advances it (nothing in this grid
+            // reads it again; the next launch reads it after this grid completed).  Taken by the
+            // producer once its loads are issued, so the atomic is off the consumers' tail.
+            if (atom_add_acq_rel_gpu(p.exit_ticket, 1) == static_cast<int>(gridDim.x) - 1) {
+                *p.exit_ticket = 0;
+                *p.xp->epoch = ep;
             }
         }
         return;
@@ -555,7 +567,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 const int nparts = sparse ? r_last - r_first : cta_of_page(r_last - 1, P, grid) - a + 1;
                 const bool a_mid = !sparse && r_first != static_cast<int>(udiv64((int64_t)a * P, grid));
                 const float ln2 = 0.69314718055994530942f;
-                constexpr int U = G >= 16 ? 1 : (G >= 8 ? 2 : 4);
+                constexpr int U = G >= 16 ? 1 : (G >= 8 ? 2 : K9_U);
                 auto slot_of_part = [&](int i) {
                     if (sparse) return 2 * cta_of_page(r_first + i, P, grid);
                     return 2 * (a + i) + ((i == 0 && a_mid) ? 1 : 0);
@@ -664,7 +676,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
         // (LSE = -inf) weigh 0.  Every producer is co-resident (this kernel) or another GPU.
         const XchgPeers& x = *p.xp;
         __shared__ int32_t s_parts[PL_MAXK];
-        const int M = p.m_count[x.self];
+        const int M = x.W > 1 ? p.m_count[x.self] : 0;  // W = 1: every row was written final by K1
         for (int r = cta; r < M; r += gridDim.x) {
             const int k = p.m_k[r];
             if (k == 1 && p.m_kv[(size_t)r * PL_MAXK] == x.self) continue;  // written final by K1
@@ -707,14 +719,6 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 if (c0 == 0) p.mout_lse[(size_t)r * C::HQ + qh] = mx + logf(den);
             }
             named_bar_sync(1, NCT);  // s_parts is rewritten by the next row
-        }
-    }
-    if (p.fuse & FUSE_STEP) {
-        // the last CTA out advances the epoch for the next step's launches
-        named_bar_sync(1, NCT);
-        if (threadIdx.x == 0 && atom_add_acq_rel_gpu(p.exit_ticket, 1) == static_cast<int>(gridDim.x) - 1) {
-            *p.exit_ticket = 0;
-            *p.xp->epoch = ep;
         }
     }
     if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 5] = k1_gtime();

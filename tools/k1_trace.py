@@ -62,6 +62,9 @@ for sz in a.sizes.split(","):
     print(f"   entry us  min {np.nanmin(entry):.2f} median {np.nanmedian(entry):.2f} max {np.nanmax(entry):.2f}")
     print(f"   first stage (after entry) median {np.nanmedian(first - entry):.2f} max {np.nanmax(first - entry):.2f}")
     print(f"   exit us   min {np.nanmin(ex):.2f} median {np.nanmedian(ex):.2f} max {np.nanmax(ex):.2f}")
+    print(f"   seg end   median {np.nanmedian(seg):.2f} max {np.nanmax(seg):.2f}; ticket median {np.nanmedian(tick):.2f} "
+          f"max {np.nanmax(tick):.2f}; merge (merging CTAs: {int(np.sum(~np.isnan(merge)))}) ticket->done median "
+          f"{np.nanmedian(merge - tick):.2f} max {np.nanmax(merge - tick):.2f}")
     o = np.argsort(-np.nan_to_num(ex))[:6]
     for c in o:
         print(f"   slow cta {c:3d} sm {t[c,6]:3d} pages {t[c,7]:3d}: entry {entry[c]:.2f} first {first[c]:.2f} "
