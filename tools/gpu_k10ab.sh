@@ -11,7 +11,7 @@ for v in base "$@"; do
   if [ $v != base ]; then cp tools/probe/_bin/k10_$v/libdcp_b200.so $L; else cp /tmp/lib_base.so $L; fi
   timeout 300 python bench_mla.py --steps 50 > $OUT/bench_$v.jsonl 2>&1
   timeout 120 python tools/mla_trace.py > $OUT/trace_$v.txt 2>&1
-  if [ $v != base ]; then timeout 300 python -m pytest tests/test_mla_gpu.py -m gpu -q -x > $OUT/pytest_$v.log 2>&1; echo "rc=$?" >> $OUT/pytest_$v.log; fi
+  if [ $v != base ] && [ -z "${NOTEST:-}" ]; then timeout 300 python -m pytest tests/test_mla_gpu.py -m gpu -q -x > $OUT/pytest_$v.log 2>&1; echo "rc=$?" >> $OUT/pytest_$v.log; fi
 done
 cp /tmp/lib_base.so $L
 for v in base "$@"; do echo "== $v"; python -c "
