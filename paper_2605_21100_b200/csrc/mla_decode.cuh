@@ -54,9 +54,12 @@ constexpr int STAGE = 8192;          // ring stage bytes
 constexpr int Q_BYTES = NKB * 8192;  // 64 heads x 576 bf16 per CTA
 constexpr int P_BYTES = 2 * 8192;    // 64 heads x 128 tokens bf16 per CTA
 #ifndef MLA_NP
-#define MLA_NP 2
+#define MLA_NP 1
 #endif
-constexpr int NP = MLA_NP;           // P buffers (softmax -> PV); 3 only fits with 2 + 2 PV stages, which starves PV (profiles/r2_k10_ab.md)
+// P buffers (softmax -> PV).  One buffer frees 16 KB for a fourth stage on each PV ring: the
+// L2-fed PV rings were the ones starving (0.381 -> 0.364 ms cfg2-shaped; P x3 with 2 + 2 PV stages:
+// 0.51 ms; QB below 4 stages: 0.41-0.54 ms; profiles/r2_k10_ab.md)
+constexpr int NP = MLA_NP;
 // Four accumulator chains, each issued by its own MMA warp and fed by its own ring: an
 // accumulating 2-CTA M=128 MMA costs ~120 ns whatever its N, but chains issued by different
 // warps overlap (tools/probe/mma_rate.cu).  S = Q K^T is split over K into two accumulators
@@ -67,8 +70,8 @@ constexpr int QB_SHARE = 2;          // ... except box 4's last 2 k-steps, issue
 #ifndef MLA_RS_QA
 #define MLA_RS_QA 5
 #define MLA_RS_QB 4
-#define MLA_RS_V0 3
-#define MLA_RS_V1 3
+#define MLA_RS_V0 4
+#define MLA_RS_V1 4
 #endif
 __host__ __device__ constexpr int ring_stages(int k) {
     return k == RQA ? MLA_RS_QA : k == RQB ? MLA_RS_QB : k == RV0 ? MLA_RS_V0 : MLA_RS_V1;
