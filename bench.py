@@ -269,8 +269,114 @@ def _host_ram_ok(gb):
         return True
 
 
+def cpu_reference_multi(ws: int, steps: int, warmup: int, token_budget: int | None = None, threads: int = 0):
+    """The N > 1 arm's workload (bench_multi.py: one node of `ws` instances, 64 x 2,048 tokens per
+    instance + ws-1 x 131,073 per node, then the cfg4 MoE exchange with identity experts) through
+    the reference on the host cores: its Scheduler::step places every request (kv binding and
+    splits), then per step dcpsim::sharded_attention_merge of every request over its shard bounds
+    (fp32, OpenMP over (request, q-head)).  The reference has no MoE code: the exchange with
+    identity experts is a numpy restatement (out_t = sum over t's destination ranks, ascending, of
+    that rank's gate-weight sum times x_t), timed with the step.  Returns (tok/s, info)."""
+    import bench_multi
+    from tests import oracle_lib
+    L = oracle_lib.reference()
+    if L is None:
+        raise RuntimeError("oracle/_ref/libdcpsim_ref.so missing (build with make -C oracle)")
+    lens = bench_multi.workload_lens(ws)
+    n_all = len(lens)
+    cap = (64 * bench_multi.SHORT + (ws - 1) * bench_multi.LONG) // PAGE + 4096
+    w = oracle_lib.World(L, "dcpref_", 1, ws, PAGE, cap, "dcp")
+    for i, ln in enumerate(lens):
+        w.enqueue(i, ln)
+    assert len(w.step()["committed"]) == n_all
+    pl = [w.placement(i) for i in range(n_all)]
+    # bounded sample for host RAM (fp32 K and V: 8 KB per token): every s-th request keeps the mix
+    pick = list(range(n_all))
+    if token_budget is not None and sum(lens) > token_budget:
+        # interleaved order (every s-th request, then the next offset, ...), each taken if it still fits
+        s = -(-sum(lens) // token_budget)
+        pick, tot = [], 0
+        for i in [j for o in range(s) for j in range(o, n_all, s)]:
+            if tot + lens[i] <= token_budget:
+                pick.append(i)
+                tot += lens[i]
+        pick.sort()
+    sl = np.array([lens[i] for i in pick], np.int64)
+    n = len(pick)
+    q = np.random.default_rng(0).standard_normal((n, HQ, D), dtype=np.float32)
+    kv_off = np.zeros(n, np.int64)
+    kv_off[1:] = np.cumsum(sl[:-1] * HKV * D)
+    kv_elems = int(sl.sum()) * HKV * D
+    k = _tiled(kv_elems, 1)
+    v = _tiled(kv_elems, 2)
+    bl = [np.cumsum(np.array(pl[i]["split"], np.int64)) for i in pick]   # shard end offsets
+    bounds = np.concatenate(bl).astype(np.int64)
+    nb = np.array([len(b) for b in bl], np.int32)
+    bounds_off = np.zeros(n, np.int64)
+    bounds_off[1:] = np.cumsum(nb[:-1])
+    out = np.zeros((n, HQ, D), np.float32)
+    # MoE: every picked request is one token of its MoE instance; top-k experts and gate weights
+    H, E, K = bench_multi.MOE["hidden"], bench_multi.MOE["experts"], bench_multi.MOE["topk"]
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((n, H), dtype=np.float32)
+    logits = rng.standard_normal((n, E), dtype=np.float32)
+    top = np.argsort(-logits, axis=1)[:, :K]
+    tv = np.take_along_axis(logits, top, axis=1)
+    gw = np.exp(tv - tv.max(axis=1, keepdims=True))
+    gw /= gw.sum(axis=1, keepdims=True)
+    rank_of = top // (E // ws)
+    th = threads or os.cpu_count() or 1
+    P = oracle_lib.P
+    times = []
+    for it in range(warmup + max(steps, 1)):
+        t0 = time.perf_counter()
+        rc = L.dcpref_batch_decode_attn_f32(n, HQ, HKV, D, 1.0 / math.sqrt(D), P(q), P(k), P(v), P(kv_off),
+                                            P(sl), P(bounds), P(bounds_off), P(nb), P(out), th)
+        assert rc == 0
+        moe_out = np.zeros_like(x)
+        for d in range(ws):                      # dispatch -> identity experts -> combine, rank order
+            wd = (gw * (rank_of == d)).sum(axis=1)
+            rows = np.nonzero(wd)[0]
+            moe_out[rows] += wd[rows, None] * x[rows]
+        if it >= warmup:
+            times.append(time.perf_counter() - t0)
+    per_step = float(np.mean(times)) * (sum(lens) / float(sl.sum()))
+    full = n == n_all
+    what = (f"all {n_all} requests" if full else
+            f"{n} of {n_all} requests within a {token_budget}-token budget ({int(sl.sum())} of {sum(lens)} "
+            f"KV tokens), scaled by token ratio")
+    info = {"kind": "reference", "cores": th,
+            "sample": f"{what}: reference Scheduler::step placements (CP histogram "
+                      f"{sorted(set(len(p['kv']) for p in pl))}), sharded_attention_merge over each request's "
+                      f"shard bounds (fp32) + the MoE exchange with identity experts (numpy; the reference has "
+                      f"no MoE code); mean of {len(times)} steps after {warmup} warm-up",
+            "same_config": full}
+    return n_all / per_step, info
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
+        return
+    if ws > 1 and not args.replicas:
+        # the N > 1 arm's metric and workload (bench_multi.py)
+        import bench_multi
+        budget = None if _host_ram_ok(2.5 * (64 * ws * bench_multi.SHORT + (ws - 1) * bench_multi.LONG) * 8192 / 1e9) \
+            else 1_000_000
+        val, info = cpu_reference_multi(ws, args.steps, args.warmup, token_budget=budget)
+        line = {
+            "metric": METRIC_MULTI, "value": val, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": len(bench_multi.workload_lens(ws)) / val * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"DCP decode step on {ws} GPUs: per GPU 64 x {bench_multi.SHORT} tokens + "
+                                   f"{ws - 1} x {bench_multi.LONG} per node, GQA 32q/8kv d128; then the cfg4 MoE "
+                                   f"exchange (identity experts)", "parallelism": "cpu", "l2": "n/a (host)",
+                       "requests": len(bench_multi.workload_lens(ws)), "same_config": info["same_config"]},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
+                             "sample": info["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
         return
     # the whole cfg2 step (1.07M tokens, 8.75 GB of fp32 K/V on the host) when RAM allows
     budget = None if _host_ram_ok(12) else 262_144
