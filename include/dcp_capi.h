@@ -492,12 +492,17 @@ DCP_API const int32_t* dcp_moe_recv_counts_dev(const dcp_moe* x);
  * y_region bf16 [world][m_max][hidden] in region order. */
 DCP_API int dcp_moe_combine_put(dcp_moe* x, const void* y_rows, void* stream);
 DCP_API int dcp_moe_combine_put_regions(dcp_moe* x, const void* y_region, void* stream);
-/* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */
 /* Gate-weighted identity expert stage (region mode): y_region[s][j] = (sum of row j's local
  * gate weights) * x_region[s][j] for every received row, reading this step's regions through
  * the device epoch (graph-safe).  The stand-in for the expert FFN in benches and graphs. */
 DCP_API int dcp_moe_expert_identity(dcp_moe* x, void* y_region, void* stream);
+/* K5c: out fp32 [M][hidden] = sum over ranks (ascending) of the returned partials. */
 DCP_API int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream);
+/* K5b + K5c in one launch (region mode): the puts, then this instance's reduction once every
+ * rank's rows have landed.  Bit-identical to dcp_moe_combine_put_regions + dcp_moe_combine_reduce.
+ * Only when the peers run concurrently (one instance per process / GPU): instances sharing a
+ * GPU in one process must use the two launches (the reduction spins on peers' puts). */
+DCP_API int dcp_moe_combine_fused(dcp_moe* x, const void* y_region, float* out, void* stream);
 
 /* ---- AOT step graphs (Alg. 2; ShapeSpace routing.hpp:60-85) --
  * One CUDA graph per M-bucket of ShapeSpace::default_space(), each replaying

@@ -78,6 +78,8 @@ int enqueue_layer(dcp_layer_graph* g, int mh, int parity, cudaStream_t s) {
     } else if ((rc = dcp_moe_expert_identity(m, d.y_region, s))) {
         return rc;
     }
+    // one instance per process / GPU (the fused step's condition): K5b + K5c in one launch
+    if (d.fused_step) return dcp_moe_combine_fused(m, d.y_region, d.moe_out, s);
     if ((rc = dcp_moe_combine_put_regions(m, d.y_region, s))) return rc;
     return dcp_moe_combine_reduce(m, d.moe_out, s);
 }

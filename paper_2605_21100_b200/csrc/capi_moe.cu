@@ -275,4 +275,14 @@ int dcp_moe_combine_reduce(dcp_moe* x, float* out, void* stream) {
     return DCP_OK;
 }
 
+int dcp_moe_combine_fused(dcp_moe* x, const void* y_region, float* out, void* stream) {
+    DCP_NVTX("K5b+K5c moe combine (fused)");
+    DCP_REQUIRE(x && y_region && out && x->received && x->m_count_dev, DCP_E_INVALID_ARG,
+                "call dcp_moe_dispatch and dcp_moe_receive_regions first");
+    DCP_CUDA_TRY(launch_pdl(moe_combine_fused_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), 0,
+                            static_cast<cudaStream_t>(stream), x->host, static_cast<const __nv_bfloat16*>(y_region),
+                            x->m_count_dev, out));
+    return DCP_OK;
+}
+
 }  // extern "C"

@@ -55,9 +55,6 @@ constexpr int MOE_MAXK = 16;
 #ifndef MOE_K4_FENCE_FIRST
 #define MOE_K4_FENCE_FIRST 1  // K4: warp 0 runs the step fence while warps 1.. build the token masks (1)
 #endif
-#ifndef MOE_K5C_PREFETCH
-#define MOE_K5C_PREFETCH 1  // K5c: read the token's destination set before the arrival-counter wait
-#endif
 #ifndef MOE_K4_PRELOAD
 #define MOE_K4_PRELOAD 1  // K4: load the CTA's first token row before the layout / fence
 #endif
@@ -406,13 +403,10 @@ static __global__ void __launch_bounds__(256) moe_expert_identity_kernel(const _
     }
 }
 
-// K5b: CTA c returns received rows c, c + C, ... (flattened source-major) to their homes.
+// K5b body: returns received rows (flattened source-major) to their homes, one warp per row.
 // y_rows: compact [R][H] (row = offs[s] + j) or region [W][m_max][H] (row = s * m_max + j).
-static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const __grid_constant__ MoePeers p,
-                                                                             const __nv_bfloat16* __restrict__ y_rows,
-                                                                             int region) {
-    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
-    pdl_wait();
+__device__ __forceinline__ void combine_put_body(const MoePeers& p, const __nv_bfloat16* __restrict__ y_rows,
+                                                 int region) {
     __shared__ int32_t s_off[PL_MAXW + 1], s_sent[PL_MAXW];
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H, tid = threadIdx.x;
@@ -482,43 +476,28 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(con
                                  "r"(s_off[d + 1] - s_off[d]) : "memory");
         }
     }
-    return;
-#endif
+#else
     if (tid < W && s_sent[tid]) red_release_sys_add(cb_arr(p, tid, ep) + p.self, s_sent[tid]);
+#endif
 }
 
-// K5c: at home, sum the partials of every destination rank in ascending order.  CTA (token t,
-// hidden chunk); each thread owns 4 consecutive columns and loads all ranks' partials before
-// adding them (the W loads are in flight together).
-static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __grid_constant__ MoePeers p,
-                                                                        const int32_t* __restrict__ m_count,
-                                                                        float* __restrict__ out) {
+// K5b: one launch of the body.
+static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_put_kernel(const __grid_constant__ MoePeers p,
+                                                                             const __nv_bfloat16* __restrict__ y_rows,
+                                                                             int region) {
     pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
     pdl_wait();
-    const int t = blockIdx.x;
-    if (t >= *m_count) return;
-    const uint32_t ep = *p.epoch;
+    combine_put_body(p, y_rows, region);
+}
+
+// K5c's per-(token, 4-column group) reduction: every routed rank's bf16 partial, ascending rank
+// (= ascending expert) order, fp32; the W loads are in flight together.
+__device__ __forceinline__ void reduce_token_cols(const MoePeers& p, int t, int q, uint32_t dm, uint32_t ep,
+                                                  float* __restrict__ out) {
     const int W = p.W, H = p.H;
-#if MOE_K5C_PREFETCH
-    // the token's destination set (this instance's own K4 layout) is read before the flag wait
-    uint32_t dm = 0;
-#pragma unroll 8
-    for (int d = 0; d < W; ++d) dm |= (p.slot_tbl[t * W + d] >= 0 ? 1u : 0u) << d;
-#endif
-    if (threadIdx.x < W)
-        wait_flag(cb_arr(p, p.self, ep) + threadIdx.x, p.cb_target[(ep & 1) * W + threadIdx.x], p.wc,
-                  (SITE_MOE_CB << 24) | (threadIdx.x << 16) | (t & 0xffff), true);
-    __syncthreads();
-    const int q = blockIdx.y * blockDim.x + threadIdx.x;  // 4-column group
-    if (4 * q >= H) return;
     const __nv_bfloat16* cy = cb_y(p, p.self, ep);
     float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
     uint2 v[PL_MAXW];
-#if !MOE_K5C_PREFETCH
-    uint32_t dm = 0;
-#pragma unroll 8
-    for (int d = 0; d < W; ++d) dm |= (p.slot_tbl[t * W + d] >= 0 ? 1u : 0u) << d;
-#endif
 #pragma unroll 8
     for (int d = 0; d < W; ++d)
         if ((dm >> d) & 1u)
@@ -534,6 +513,57 @@ static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __
         a3 += hi.y;
     }
     reinterpret_cast<float4*>(out + (size_t)t * H)[q] = make_float4(a0, a1, a2, a3);
+}
+
+// K5c: at home, sum the partials of every destination rank in ascending order.  CTA (token t,
+// hidden chunk); each thread owns 4 consecutive columns.
+static __global__ void __launch_bounds__(256) moe_combine_reduce_kernel(const __grid_constant__ MoePeers p,
+                                                                        const int32_t* __restrict__ m_count,
+                                                                        float* __restrict__ out) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
+    const int t = blockIdx.x;
+    if (t >= *m_count) return;
+    const uint32_t ep = *p.epoch;
+    const int W = p.W, H = p.H;
+    // the token's destination set (this instance's own K4 layout) is read before the flag wait
+    uint32_t dm = 0;
+#pragma unroll 8
+    for (int d = 0; d < W; ++d) dm |= (p.slot_tbl[t * W + d] >= 0 ? 1u : 0u) << d;
+    if (threadIdx.x < W)
+        wait_flag(cb_arr(p, p.self, ep) + threadIdx.x, p.cb_target[(ep & 1) * W + threadIdx.x], p.wc,
+                  (SITE_MOE_CB << 24) | (threadIdx.x << 16) | (t & 0xffff), true);
+    __syncthreads();
+    const int q = blockIdx.y * blockDim.x + threadIdx.x;  // 4-column group
+    if (4 * q >= H) return;
+    reduce_token_cols(p, t, q, dm, ep, out);
+}
+
+// Fused combine (multi-process / multi-GPU only): K5b's puts, then K5c's reduction of this
+// instance's tokens, in one grid.  The reduction waits for every rank's rows, this grid's own
+// included (its last CTA publishes them, single release); the CTAs are co-resident (grid =
+// SMs) and the peers run concurrently on their own GPUs.  Instances sharing one GPU in one
+// process keep the two launches: a spinning reduction would hold the SMs a peer's puts need.
+static __global__ void __launch_bounds__(MOE_THREADS) moe_combine_fused_kernel(const __grid_constant__ MoePeers p,
+                                                                               const __nv_bfloat16* __restrict__ y_region,
+                                                                               const int32_t* __restrict__ m_count,
+                                                                               float* __restrict__ out) {
+    pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
+    pdl_wait();
+    combine_put_body(p, y_region, 1);
+    const uint32_t ep = *p.epoch;
+    const int W = p.W, H = p.H, M = *m_count;
+    if (static_cast<int>(blockIdx.x) >= M) return;
+    if (threadIdx.x < W)
+        wait_flag(cb_arr(p, p.self, ep) + threadIdx.x, p.cb_target[(ep & 1) * W + threadIdx.x], p.wc,
+                  (SITE_MOE_CB << 24) | (threadIdx.x << 16) | (blockIdx.x & 0xffff), true);
+    __syncthreads();
+    for (int t = blockIdx.x; t < M; t += gridDim.x) {
+        uint32_t dm = 0;
+#pragma unroll 8
+        for (int d = 0; d < W; ++d) dm |= (p.slot_tbl[t * W + d] >= 0 ? 1u : 0u) << d;
+        for (int q = threadIdx.x; 4 * q < H; q += blockDim.x) reduce_token_cols(p, t, q, dm, ep, out);
+    }
 }
 
 }  // namespace dcp

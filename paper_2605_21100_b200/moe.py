@@ -171,6 +171,12 @@ class MoeInstance:
         _capi.check(_capi.lib().dcp_moe_combine_reduce(self.h, ctypes.c_void_p(self.out.data_ptr()),
                                                        _s(stream, self.ctx.device)))
 
+    def combine_fused(self, y_region, stream=None):
+        """K5b + K5c in one launch (dcp_moe_combine_fused): one instance per process / GPU only."""
+        _capi.check(_capi.lib().dcp_moe_combine_fused(self.h, ctypes.c_void_p(y_region.data_ptr()),
+                                                      ctypes.c_void_p(self.out.data_ptr()),
+                                                      _s(stream, self.ctx.device)))
+
     def close(self):
         if getattr(self, "h", None):
             _capi.lib().dcp_moe_destroy(self.h)

@@ -113,10 +113,11 @@ class RankStep:
             self.inst.write_queries(q_rows, stream)
         self.inst.run(self.view, stream)
 
-    def moe_layer(self, x, topk_idx, topk_w, expert_fn=None, stream=None):
+    def moe_layer(self, x, topk_idx, topk_w, expert_fn=None, stream=None, fused_combine=False):
         """x bf16 [M, H] in M-row order; expert_fn(x_region, meta_region, counts, y_region) fills
         self.y_region (None: the gate-weighted identity expert, dcp_moe_expert_identity, issued
-        on the stream, no host sync)."""
+        on the stream, no host sync).  fused_combine: K5b + K5c in one launch
+        (dcp_moe_combine_fused; valid here, one instance per process)."""
         m = self.moe
         m.dispatch(x, topk_idx, topk_w, m_count_ptr=self.m_count_ptr, stream=stream)
         m.receive_regions(stream)
@@ -125,8 +126,11 @@ class RankStep:
             m.expert_identity(self.y_region, stream)
         else:
             expert_fn(xr, mr, m.recv_counts(), self.y_region)
-        m.combine_put_regions(self.y_region, stream)
-        m.combine_reduce(stream)
+        if fused_combine:
+            m.combine_fused(self.y_region, stream)
+        else:
+            m.combine_put_regions(self.y_region, stream)
+            m.combine_reduce(stream)
 
     def results(self):
         return self.inst.results(len(self.m_ids))

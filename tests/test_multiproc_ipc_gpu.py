@@ -212,6 +212,12 @@ def _graph_worker(rank, port, q, log_dir):
             rs.status()
             o, l = rs.results()
             assert np.array_equal(o, o0) and np.array_equal(l, l0), f"fused step {step} differs"
+        # K5b + K5c in one launch (dcp_moe_combine_fused), eager: bit-identical to the two launches
+        for step in range(2):
+            rs.moe_layer(xb[:M], ib[:M], wb[:M], fused_combine=True)
+            torch.cuda.synchronize()
+            rs.status()
+            assert np.array_equal(rs.moe.out[:M].cpu().numpy(), m0), f"fused MoE combine {step} differs"
         gf = LayerGraph(rs.inst, rs.view, rs.moe, xb, ib, wb, planner=rs.planner, fused=True)
         for step in range(3):
             gf.launch(M)
