@@ -471,6 +471,11 @@ DCP_API int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* top
  * first peer store and its last CTA advances the epoch.  Same results, one launch less. */
 DCP_API int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* topk_idx,
                                   const float* topk_w, const int32_t* m_count_dev, void* stream);
+/* dcp_moe_step_dispatch + dcp_moe_receive_regions in ONE launch: K4's last CTA waits for every
+ * source's rows and writes the receive counts.  Only when the peers run concurrently (one
+ * instance per process / GPU); instances sharing a GPU in one process use the two calls. */
+DCP_API int dcp_moe_step_dispatch_recv(dcp_moe* x, const void* x_local, const int32_t* topk_idx,
+                                       const float* topk_w, const int32_t* m_count_dev, void* stream);
 /* K5a, region mode (the fast path): wait for every source; the received rows stay in
  * this instance's pool, source s's rows at x_region[s * m_max + j], j < count[s]
  * (meta likewise), for the expert stage to read in place.  Per-source counts and

@@ -228,6 +228,7 @@ _SIGNATURES = [
     ("dcp_moe_combine_fused", c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_expert_identity", c_int, [c_void_p, c_void_p, c_void_p]),
     ("dcp_moe_step_dispatch", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("dcp_moe_step_dispatch_recv", c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("dcp_layer_graph_create", c_int, [c_void_p, POINTER(LayerGraphDesc), POINTER(c_void_p)]),
     ("dcp_layer_graph_launch", c_int, [c_void_p, c_int32, c_void_p]),
     ("dcp_layer_graph_info", c_int, [c_void_p, c_void_p, c_void_p]),

@@ -66,9 +66,15 @@ int enqueue_layer(dcp_layer_graph* g, int mh, int parity, cudaStream_t s) {
     }
     if (!d.moe) return DCP_OK;
     dcp_moe* m = d.moe;
-    if ((rc = dcp_moe_step_dispatch(m, d.moe_x, d.topk_idx, d.topk_w, g->view.m_count_all + g->view.instance, s)))
-        return rc;
-    if ((rc = dcp_moe_receive_regions(m, s))) return rc;
+    if (d.fused_step) {  // one instance per process / GPU: K4 + K5a in one launch
+        if ((rc = dcp_moe_step_dispatch_recv(m, d.moe_x, d.topk_idx, d.topk_w,
+                                             g->view.m_count_all + g->view.instance, s)))
+            return rc;
+    } else {
+        if ((rc = dcp_moe_step_dispatch(m, d.moe_x, d.topk_idx, d.topk_w, g->view.m_count_all + g->view.instance, s)))
+            return rc;
+        if ((rc = dcp_moe_receive_regions(m, s))) return rc;
+    }
     if (d.expert) {
         void* xr = nullptr;
         int32_t* mr = nullptr;

@@ -190,7 +190,7 @@ int dcp_moe_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, const 
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
     DCP_CUDA_TRY(launch_pdl(moe_dispatch_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), dispatch_smem(x), s, x->host,
-                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 0));
+                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 0, 0));
     return DCP_OK;
 }
 
@@ -201,9 +201,23 @@ int dcp_moe_step_dispatch(dcp_moe* x, const void* x_local, const int32_t* idx, c
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
     DCP_CUDA_TRY(launch_pdl(moe_dispatch_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), dispatch_smem(x), s, x->host,
-                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 1));
+                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 1, 0));
     ++x->host_epoch;  // what dcp_moe_begin_step does on the host
     x->received = false;
+    return DCP_OK;
+}
+
+int dcp_moe_step_dispatch_recv(dcp_moe* x, const void* x_local, const int32_t* idx, const float* w,
+                               const int32_t* m_count, void* stream) {
+    DCP_NVTX("K4+K5a moe step dispatch + receive (fused)");
+    DCP_REQUIRE(x && x->committed && m_count, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange");
+    DCP_REQUIRE(MOE_SINGLE_RELEASE, DCP_E_UNSUPPORTED, "fused receive needs the single-release K4 build");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    x->m_count_dev = m_count;
+    DCP_CUDA_TRY(launch_pdl(moe_dispatch_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), dispatch_smem(x), s, x->host,
+                            static_cast<const __nv_bfloat16*>(x_local), idx, w, m_count, 1, 1));
+    ++x->host_epoch;
+    x->received = true;  // the counts / offsets of dcp_moe_receive_regions are written by this launch
     return DCP_OK;
 }
 

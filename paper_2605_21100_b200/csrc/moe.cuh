@@ -149,6 +149,25 @@ static __global__ void __launch_bounds__(32) moe_begin_step_kernel(const __grid_
     step_fence(p.epoch, [&](int s) { return moe_done(p, s); }, p.W, p.self, p.wc);
 }
 
+// K5a body (one warp): lane s waits for source s's count record and rows of epoch ep, then the
+// per-source counts and their exclusive prefix go to the device (graph-capturable, no host copy).
+__device__ __forceinline__ void receive_counts_warp(const MoePeers& p, uint32_t ep) {
+    const int lane = threadIdx.x & 31;
+    int c = 0;
+    if (lane < p.W) c = moe_wait_source(p, lane, ep);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane < p.W) {
+        p.counts[lane] = c;
+        p.offs[lane + 1] = incl;
+    }
+    if (lane == 0) p.offs[0] = 0;
+}
+
 // K4.  grid = chunks, block = MOE_THREADS; dynamic smem = m_max * (W + 1) * 4 bytes.
 // with_fence: this launch is also the step's begin_step (the step fence of exchange.cuh before
 // the first peer store; epoch e = *epoch + 1, advanced by the last CTA out), one launch per step.
@@ -157,7 +176,7 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
                                                                           const int32_t* __restrict__ topk_idx,
                                                                           const float* __restrict__ topk_w,
                                                                           const int32_t* __restrict__ m_count,
-                                                                          int with_fence) {
+                                                                          int with_fence, int with_recv) {
     pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
     pdl_wait();
     extern __shared__ int32_t sm[];
@@ -271,10 +290,12 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
 #if MOE_SINGLE_RELEASE
     // The CTAs meet on a gpu-scope acq_rel ticket; the last one has acquired every CTA's row stores
     // and publishes them with one system fence (release cumulativity) and relaxed count adds.
+    __shared__ int32_t s_last;
     if (tid == 0) {
         int old;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.exit_ticket) : "memory");
-        if (old == static_cast<int>(gridDim.x) - 1) {
+        s_last = old == static_cast<int>(gridDim.x) - 1;
+        if (s_last) {
             *p.exit_ticket = 0;
             asm volatile("fence.acq_rel.sys;" ::: "memory");
             for (int d = 0; d < W; ++d)
@@ -282,6 +303,12 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
                                              "r"(s_count[d]) : "memory");
             if (with_fence) *p.epoch = ep;
         }
+    }
+    if (with_recv) {
+        // fused K5a (one instance per process / GPU only): the last CTA's warp 0 waits for every
+        // source's rows of this epoch and writes the counts the expert stage reads
+        __syncthreads();
+        if (s_last && warp == 0) receive_counts_warp(p, ep);
     }
     return;
 #endif
@@ -301,21 +328,7 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
 static __global__ void __launch_bounds__(32) moe_receive_counts_kernel(const __grid_constant__ MoePeers p) {
     pdl_trigger();  // MoE launches are PDL-chained (capi_moe.cu)
     pdl_wait();
-    const uint32_t ep = *p.epoch;
-    const int lane = threadIdx.x;
-    int c = 0;
-    if (lane < p.W) c = moe_wait_source(p, lane, ep);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane < p.W) {
-        p.counts[lane] = c;
-        p.offs[lane + 1] = incl;
-    }
-    if (lane == 0) p.offs[0] = 0;
+    receive_counts_warp(p, *p.epoch);
 }
 
 // K5a (compact mode, legacy dcp_moe_receive): every CTA waits for every source, then warp

@@ -69,9 +69,11 @@ class MoeInstance:
     def commit(self):
         _capi.check(_capi.lib().dcp_moe_commit(self.h))
 
-    def dispatch(self, x, topk_idx, topk_w, m_count_ptr=None, stream=None, fused=True):
+    def dispatch(self, x, topk_idx, topk_w, m_count_ptr=None, stream=None, fused=True, with_receive=False):
         """x bf16 [M, H], topk_idx int32 [M, k], topk_w fp32 [M, k] (device).  Starts the step:
-        fused (default) = one launch (dcp_moe_step_dispatch), else begin_step + dispatch."""
+        fused (default) = one launch (dcp_moe_step_dispatch), else begin_step + dispatch.
+        with_receive: the region-mode receive in the same launch (dcp_moe_step_dispatch_recv; one
+        instance per process / GPU only)."""
         L = _capi.lib()
         s = _s(stream, self.ctx.device)
         if m_count_ptr is None:
@@ -80,7 +82,9 @@ class MoeInstance:
         self._keep = (x, topk_idx, topk_w)
         args = (self.h, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(topk_idx.data_ptr()),
                 ctypes.c_void_p(topk_w.data_ptr()), ctypes.c_void_p(m_count_ptr), s)
-        if fused:
+        if with_receive:
+            _capi.check(L.dcp_moe_step_dispatch_recv(*args))
+        elif fused:
             _capi.check(L.dcp_moe_step_dispatch(*args))
         else:
             _capi.check(L.dcp_moe_begin_step(self.h, s))

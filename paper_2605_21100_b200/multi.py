@@ -113,14 +113,16 @@ class RankStep:
             self.inst.write_queries(q_rows, stream)
         self.inst.run(self.view, stream)
 
-    def moe_layer(self, x, topk_idx, topk_w, expert_fn=None, stream=None, fused_combine=False):
+    def moe_layer(self, x, topk_idx, topk_w, expert_fn=None, stream=None, fused_combine=False, fused_receive=False):
         """x bf16 [M, H] in M-row order; expert_fn(x_region, meta_region, counts, y_region) fills
         self.y_region (None: the gate-weighted identity expert, dcp_moe_expert_identity, issued
         on the stream, no host sync).  fused_combine: K5b + K5c in one launch
-        (dcp_moe_combine_fused; valid here, one instance per process)."""
+        (dcp_moe_combine_fused); fused_receive: K4 + K5a in one launch (dcp_moe_step_dispatch_recv);
+        both valid here, one instance per process."""
         m = self.moe
-        m.dispatch(x, topk_idx, topk_w, m_count_ptr=self.m_count_ptr, stream=stream)
-        m.receive_regions(stream)
+        m.dispatch(x, topk_idx, topk_w, m_count_ptr=self.m_count_ptr, stream=stream, with_receive=fused_receive)
+        if not fused_receive:
+            m.receive_regions(stream)
         xr, mr = m.regions()
         if expert_fn is None:
             m.expert_identity(self.y_region, stream)

@@ -212,12 +212,13 @@ def _graph_worker(rank, port, q, log_dir):
             rs.status()
             o, l = rs.results()
             assert np.array_equal(o, o0) and np.array_equal(l, l0), f"fused step {step} differs"
-        # K5b + K5c in one launch (dcp_moe_combine_fused), eager: bit-identical to the two launches
-        for step in range(2):
-            rs.moe_layer(xb[:M], ib[:M], wb[:M], fused_combine=True)
+        # K5b + K5c in one launch (dcp_moe_combine_fused), eager: bit-identical to the two launches;
+        # and K4 + K5a in one launch (dcp_moe_step_dispatch_recv): the whole MoE layer in 2 launches
+        for step in range(3):
+            rs.moe_layer(xb[:M], ib[:M], wb[:M], fused_combine=True, fused_receive=step > 0)
             torch.cuda.synchronize()
             rs.status()
-            assert np.array_equal(rs.moe.out[:M].cpu().numpy(), m0), f"fused MoE combine {step} differs"
+            assert np.array_equal(rs.moe.out[:M].cpu().numpy(), m0), f"fused MoE layer {step} differs"
         gf = LayerGraph(rs.inst, rs.view, rs.moe, xb, ib, wb, planner=rs.planner, fused=True)
         for step in range(3):
             gf.launch(M)
