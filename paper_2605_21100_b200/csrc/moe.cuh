@@ -127,19 +127,26 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned 
 }
 
 // Wait for source s's count record of epoch ep and for all of its rows; returns the count.
+// The record {epoch << 32 | count, cumulative row target} (one 16-byte acquire load) and the
+// cumulative arrival counter are polled in the same round: when the record carries ep and the
+// counter has reached its target, every row is visible (the counter's releases cover them).
+// One L2 round trip when the rows are already there, instead of three dependent ones.
 __device__ __forceinline__ int moe_wait_source(const MoePeers& p, int s, uint32_t ep) {
     const unsigned long long* rec = rx_cnt(p, p.self, ep) + 2 * s;
+    const uint32_t* arr = rx_arr(p, p.self, ep) + s;
     const uint32_t where = (SITE_MOE_RX << 24) | (s << 16);
-    unsigned long long a = 0;
+    unsigned long long a = 0, tgt = 0;
     wait_until(
         [&](uint32_t& seen) {
-            a = ld_acquire_sys_u64(rec);
+            uint32_t c;
+            asm volatile("ld.acquire.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(tgt) : "l"(rec) : "memory");
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(c) : "l"(arr) : "memory");
             seen = static_cast<uint32_t>(a >> 32);
-            return seen == ep;
+            if (seen != ep) return false;
+            seen = c;
+            return static_cast<int32_t>(c - static_cast<uint32_t>(tgt)) >= 0;
         },
         ep, p.wc, where);
-    const uint32_t target = static_cast<uint32_t>(__ldcg(rec + 1));
-    wait_flag(rx_arr(p, p.self, ep) + s, target, p.wc, where | 0x8000u, true);
     return static_cast<int>(a & 0xffffffffu);
 }
 
