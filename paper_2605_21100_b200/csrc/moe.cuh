@@ -120,11 +120,6 @@ __device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
 __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // Wait for source s's count record of epoch ep and for all of its rows; returns the count.
 // The record {epoch << 32 | count, cumulative row target} (one 16-byte acquire load) and the
