@@ -215,7 +215,7 @@ def main():
     ap.add_argument("--long", type=int, default=3)
     ap.add_argument("--long-len", type=int, default=131073)
     ap.add_argument("--capacity", type=int, default=40000)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=1000)  # P99 over >= 1,000 steps
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--n-sched", type=int, default=8)
     ap.add_argument("--policies", default="dcp,least_batch,least_cache")

@@ -9,7 +9,7 @@ timeout 1500 python -m pytest tests -m gpu -q -rA --durations=10 > $OUT/pytest_g
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke_$TAG.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke_$TAG.log
 timeout 600 python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?" >> $OUT/bench_$TAG.err
 timeout 900 python bench.py --impl reference --steps 20 --warmup 3 > $OUT/bench_ref_$TAG.json 2> $OUT/bench_ref_$TAG.err
-timeout 900 python bench_dcp.py --steps 300 > $OUT/bench_dcp_$TAG.jsonl 2> $OUT/bench_dcp_$TAG.err
+timeout 900 python bench_dcp.py --steps 1000 > $OUT/bench_dcp_$TAG.jsonl 2> $OUT/bench_dcp_$TAG.err
 timeout 300 python bench_moe.py --steps 20 > $OUT/bench_moe_$TAG.jsonl 2>&1
 timeout 300 python bench_graph.py > $OUT/bench_graph_$TAG.json 2>&1
 timeout 900 python bench_trace.py --duration 10 --rate 16 > $OUT/bench_trace_$TAG.jsonl 2> $OUT/bench_trace_$TAG.err
