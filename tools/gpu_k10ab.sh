@@ -8,7 +8,7 @@ mkdir -p $OUT
 L=paper_2605_21100_b200/_build/libdcp_b200.so
 cp $L /tmp/lib_base.so
 for v in base "$@"; do
-  if [ $v != base ]; then cp tools/probe/_bin/k10_$v/libdcp_b200.so $L; else cp /tmp/lib_base.so $L; fi
+  if [ $v != base ]; then cp tools/probe/_bin/k10_$v/libdcp_b200.so $L || { echo "missing variant k10_$v" > $OUT/bench_$v.jsonl; continue; }; else cp /tmp/lib_base.so $L; fi
   timeout 300 python bench_mla.py --steps 50 > $OUT/bench_$v.jsonl 2>&1
   timeout 120 python tools/mla_trace.py > $OUT/trace_$v.txt 2>&1
   if [ $v != base ] && [ -z "${NOTEST:-}" ]; then timeout 300 python -m pytest tests/test_mla_gpu.py -m gpu -q -x > $OUT/pytest_$v.log 2>&1; echo "rc=$?" >> $OUT/pytest_$v.log; fi
