@@ -114,6 +114,37 @@ __device__ __forceinline__ void publish_row(const P& p, int r, uint32_t ep) {
     st_release_sys(xres_flag(x, p.n_moe[r], ep) + (size_t)p.n_mrow[r] * x.W + x.self, ep);
 }
 
+// The same destinations from the shard's routing fields loaded once at the shard's start
+// (nm = n_moe[r], nr = n_mrow[r], mk = m_k[nr]): the epilogue / K9 merge after the page loop
+// then has no dependent loads on its tail.
+struct RowRoute {
+    int nm, nr, mk;
+};
+template <class P>
+__device__ __forceinline__ RowRoute row_route(const P& p, int r) {
+    RowRoute rr{0, 0, 0};
+    if (p.xp) {
+        rr.nm = p.n_moe[r];
+        rr.nr = p.n_mrow[r];
+        if (p.fuse & 4u) rr.mk = p.m_k[rr.nr];
+    }
+    return rr;
+}
+template <class P>
+__device__ __forceinline__ float* row_out_c(const P& p, int r, const RowRoute& rr, int HQ, int D, uint32_t ep) {
+    if (!p.xp) return p.out + (size_t)r * HQ * D;
+    const XchgPeers& x = *p.xp;
+    if ((p.fuse & 4u) && rr.nm == x.self && rr.mk == 1) return p.mout + (size_t)rr.nr * HQ * D;
+    return xres_o(x, rr.nm, ep) + ((size_t)rr.nr * x.W + x.self) * HQ * D;
+}
+template <class P>
+__device__ __forceinline__ float* row_lse_c(const P& p, int r, const RowRoute& rr, int HQ, uint32_t ep) {
+    if (!p.xp) return p.lse + (size_t)r * HQ;
+    const XchgPeers& x = *p.xp;
+    if ((p.fuse & 4u) && rr.nm == x.self && rr.mk == 1) return p.mout_lse + (size_t)rr.nr * HQ;
+    return xres_lse(x, rr.nm, ep) + ((size_t)rr.nr * x.W + x.self) * HQ;
+}
+
 // SPLIT = false: a ring stage is one whole frame (K and V of every kv-head).
 // SPLIT = true:  a ring stage is half a frame (the K part or the V part); the
 // K half is released right after QK^T, and the finer ring fits 3.5 frames in
@@ -350,7 +381,8 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
 
         // Q fragments (A operand, rows = q-heads of this kv group).  Fused step: a request homed
         // here reads its Q row in place (no put to self, no flag).
-        const bool q_home = (p.fuse & FUSE_ROUTE) && p.n_moe[r] == p.xp->self;
+        const RowRoute rrt = row_route(p, r);
+        const bool q_home = (p.fuse & FUSE_ROUTE) && rrt.nm == p.xp->self;
         if (qflag && !q_home) {  // routed: wait for the Q-route put of this row
             if (lane == 0) wait_flag(qflag + r, ep, p.xp->wc, (SITE_K1_Q << 24) | (r & 0xffff));
             __syncwarp();
@@ -358,7 +390,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
         uint32_t qa[8][4];
         {
             const __nv_bfloat16* qrow = q_home ? static_cast<const __nv_bfloat16*>(p.q_local) +
-                                                     static_cast<size_t>(p.n_mrow[r]) * C::HQ * C::D
+                                                     static_cast<size_t>(rrt.nr) * C::HQ * C::D
                                                : qbase + static_cast<size_t>(r) * C::HQ * C::D;
             const __nv_bfloat16* q0 = qrow + (h * G + g) * C::D + 2 * t;
             const __nv_bfloat16* q1 = q0 + 8 * C::D;
@@ -516,12 +548,12 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 const float l = half == 0 ? l0 : l1;
                 const float m = half == 0 ? m0 : m1;
                 const float inv = 1.f / l;
-                float* o = row_out(p, r, C::HQ, C::D, ep) + qh * C::D + 2 * t;
+                float* o = row_out_c(p, r, rrt, C::HQ, C::D, ep) + qh * C::D + 2 * t;
 #pragma unroll
                 for (int nt = 0; nt < 16; ++nt)
                     *reinterpret_cast<float2*>(o + nt * 8) =
                         make_float2(acc[nt][2 * half] * inv, acc[nt][2 * half + 1] * inv);
-                if (t == 0) row_lse(p, r, C::HQ, ep)[qh] = (m + __log2f(l)) * ln2;
+                if (t == 0) row_lse_c(p, r, rrt, C::HQ, ep)[qh] = (m + __log2f(l)) * ln2;
             }
             if (p.xp) {
                 named_bar_sync(1, NCT);
@@ -652,10 +684,10 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                     for (int o = 16; o > 0; o >>= 1) den[row] += __shfl_xor_sync(0xffffffffu, den[row], o);
                     const int qh = h * G + row;
                     const float inv = 1.f / den[row];
-                    float* o = row_out(p, r, C::HQ, C::D, ep) + qh * C::D;
+                    float* o = row_out_c(p, r, rrt, C::HQ, C::D, ep) + qh * C::D;
                     reinterpret_cast<float4*>(o)[lane] =
                         make_float4(num[row].x * inv, num[row].y * inv, num[row].z * inv, num[row].w * inv);
-                    if (lane == 0) row_lse(p, r, C::HQ, ep)[qh] = (mmax[row] + __log2f(den[row])) * ln2;
+                    if (lane == 0) row_lse_c(p, r, rrt, C::HQ, ep)[qh] = (mmax[row] + __log2f(den[row])) * ln2;
                 }
                 if (threadIdx.x == 0) p.counters[r] = 0;  // re-arm for the next launch / graph replay
                 if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 4] = k1_gtime();
