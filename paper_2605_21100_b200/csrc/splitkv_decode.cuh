@@ -144,6 +144,12 @@ __device__ __forceinline__ float* row_lse_c(const P& p, int r, const RowRoute& r
     if ((p.fuse & 4u) && rr.nm == x.self && rr.mk == 1) return p.mout_lse + (size_t)rr.nr * HQ;
     return xres_lse(x, rr.nm, ep) + ((size_t)rr.nr * x.W + x.self) * HQ;
 }
+template <class P>
+__device__ __forceinline__ void publish_row_c(const P& p, const RowRoute& rr, uint32_t ep) {
+    const XchgPeers& x = *p.xp;
+    if ((p.fuse & 4u) && rr.nm == x.self && rr.mk == 1) return;
+    st_release_sys(xres_flag(x, rr.nm, ep) + (size_t)rr.nr * x.W + x.self, ep);
+}
 
 // SPLIT = false: a ring stage is one whole frame (K and V of every kv-head).
 // SPLIT = true:  a ring stage is half a frame (the K part or the V part); the
@@ -557,7 +563,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
             }
             if (p.xp) {
                 named_bar_sync(1, NCT);
-                if (threadIdx.x == 0) publish_row(p, r, ep);
+                if (threadIdx.x == 0) publish_row_c(p, rrt, ep);
             }
         } else {
             const int slot = 2 * cta + (seg_begin == p_begin ? 0 : 1);
@@ -693,7 +699,7 @@ __global__ void __launch_bounds__(DecodeCfg<HKV, G, SPLIT, PAGE_>::THREADS, 1)
                 if (p.trace && threadIdx.x == 0) p.trace[cta * 8 + 4] = k1_gtime();
                 if (p.xp) {
                     named_bar_sync(2, NCT);
-                    if (threadIdx.x == 0) publish_row(p, r, ep);
+                    if (threadIdx.x == 0) publish_row_c(p, rrt, ep);
                 }
             }
         }
