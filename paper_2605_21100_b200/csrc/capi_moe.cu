@@ -211,6 +211,7 @@ int dcp_moe_step_dispatch_recv(dcp_moe* x, const void* x_local, const int32_t* i
                                const int32_t* m_count, void* stream) {
     DCP_NVTX("K4+K5a moe step dispatch + receive (fused)");
     DCP_REQUIRE(x && x->committed && m_count, DCP_E_INVALID_ARG, "NULL or uncommitted MoE exchange");
+    DCP_REQUIRE(MOE_SINGLE_RELEASE, DCP_E_UNSUPPORTED, "fused receive needs the single-release K4 build");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     x->m_count_dev = m_count;
     DCP_CUDA_TRY(launch_pdl(moe_dispatch_kernel, dim3(x->host.chunks), dim3(MOE_THREADS), dispatch_smem(x), s, x->host,

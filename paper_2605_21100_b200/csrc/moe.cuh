@@ -15,12 +15,12 @@
 //                      c, c + C, ...: the hidden state is loaded ONCE into
 //                      registers and stored to every destination rank it is
 //                      routed to (16-byte vectors, remote NVLink stores on a
-//                      multi-GPU node).  Completion: the CTAs meet on a
-//                      gpu-scope ticket; the last one issues one system fence
-//                      and adds each destination's row count to its arrival
-//                      counter (relaxed system-scope reds); CTA 0 publishes the
-//                      count record {epoch, count} and the cumulative row
-//                      target.  No per-row flag, one system fence per launch.
+//                      multi-GPU node).  Completion (MOE_SINGLE_RELEASE, the
+//                      default): the CTAs meet on a gpu-scope ticket; the last
+//                      one issues one system fence and adds each destination's
+//                      row count to its arrival counter (relaxed system-scope
+//                      reds); CTA 0 publishes the count record {epoch, count}
+//                      and the cumulative row target.  No per-row flag.
 //   K5a moe_receive    wait, per source, for the count record and for the
 //                      arrival counter to reach its target; the rows stay in
 //                      the pool's per-source regions [W][m_max][H] (the expert
@@ -52,6 +52,18 @@
 namespace dcp {
 
 constexpr int MOE_MAXK = 16;
+#ifndef MOE_K5B_WARP
+#define MOE_K5B_WARP 1  // K5b: one warp per row (1) or one CTA per row (0)
+#endif
+#ifndef MOE_K4_FENCE_FIRST
+#define MOE_K4_FENCE_FIRST 1  // K4: warp 0 runs the step fence while warps 1.. build the token masks (1)
+#endif
+#ifndef MOE_K4_PRELOAD
+#define MOE_K4_PRELOAD 1  // K4: load the CTA's first token row before the layout / fence
+#endif
+#ifndef MOE_SINGLE_RELEASE
+#define MOE_SINGLE_RELEASE 1  // K4 / K5b: CTAs meet on a gpu-scope ticket; the last one issues ONE system fence
+#endif                        // and the per-destination row counts (instead of a red.release.sys per CTA)
 constexpr int MOE_THREADS = 256;
 
 struct MoePeers {
@@ -105,6 +117,9 @@ __device__ __forceinline__ uint32_t* moe_done(const MoePeers& p, int s) {
     return reinterpret_cast<uint32_t*>(p.base[s] + p.off_done);
 }
 
+__device__ __forceinline__ void red_release_sys_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -173,21 +188,22 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
     const int W = p.W, H = p.H, K = p.topk, M = *m_count;
     int32_t* s_mask = sm;               // [M] destination-rank bitmask of each token
     int32_t* s_slot = sm + p.m_max;     // [M][W] slot at each destination (-1 = not routed)
-    __shared__ int32_t s_count[PL_MAXW];
+    __shared__ int32_t s_count[PL_MAXW], s_sent[PL_MAXW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ep = *p.epoch + (with_fence ? 1u : 0u);
     constexpr int NW = MOE_THREADS / 32;
     constexpr int VPT = 4;  // 16-byte vectors in registers per thread per pass (4 x 256 x 16 B = 16 KB)
     const int nvec = H / 8;
     uint4 v[VPT];
-    // this CTA's first token row, loaded before the layout work (its latency overlaps it)
+#if MOE_K4_PRELOAD
     if (static_cast<int>(blockIdx.x) < M) {
         const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)blockIdx.x * H);
 #pragma unroll
         for (int u = 0; u < VPT; ++u)
             if (u * MOE_THREADS + tid < nvec) v[u] = __ldg(src + u * MOE_THREADS + tid);
     }
-    // the step fence (warp 0) runs while warps 1.. build the token masks
+#endif
+#if MOE_K4_FENCE_FIRST
     if (with_fence && warp == 0) {
         if (blockIdx.x == 0 && lane == 0) st_relaxed_sys(moe_done(p, p.self), ep - 1);
         for (int s = lane; s < W; s += 32)
@@ -195,10 +211,14 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
     }
     for (int t = tid - 32; t < M; t += MOE_THREADS - 32) {
         if (t < 0) break;
+#else
+    for (int t = tid; t < M; t += MOE_THREADS) {
+#endif
         uint32_t m = 0;
         for (int j = 0; j < K; ++j) m |= 1u << (__ldg(topk_idx + t * K + j) / p.e_per_rank);
         s_mask[t] = static_cast<int32_t>(m);
     }
+    if (tid < PL_MAXW) s_sent[tid] = 0;
     __syncthreads();
     // slots: warp d scans the tokens for destination d (ballot prefix, ascending token order)
     for (int d = warp; d < W; d += NW) {
@@ -211,6 +231,11 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
             carry += __popc(b);
         }
         if (lane == 0) s_count[d] = carry;
+    }
+    if (!MOE_K4_FENCE_FIRST && with_fence && warp == 0) {
+        if (blockIdx.x == 0 && lane == 0) st_relaxed_sys(moe_done(p, p.self), ep - 1);
+        for (int s = lane; s < W; s += 32)
+            if (s != p.self) wait_flag(moe_done(p, s), ep - 2, p.wc, (SITE_FENCE << 24) | (s << 16), true);
     }
     __syncthreads();
     if (blockIdx.x == 0) {
@@ -231,7 +256,7 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
         const uint32_t mask = static_cast<uint32_t>(s_mask[t]);
         const uint4* src = reinterpret_cast<const uint4*>(x + (size_t)t * H);
         for (int v0 = 0; v0 < nvec; v0 += VPT * MOE_THREADS) {
-            if (t != static_cast<int>(blockIdx.x) || v0 != 0) {  // (the first pass of the first token is preloaded)
+            if (!MOE_K4_PRELOAD || t != static_cast<int>(blockIdx.x) || v0 != 0) {
 #pragma unroll
                 for (int u = 0; u < VPT; ++u) {
                     const int i = v0 + u * MOE_THREADS + tid;
@@ -263,9 +288,11 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
             }
             meta[0] = t;
             meta[1] = n;
+            ++s_sent[d];
         }
     }
     __syncthreads();
+#if MOE_SINGLE_RELEASE
     // The CTAs meet on a gpu-scope acq_rel ticket; the last one has acquired every CTA's row stores
     // and publishes them with one system fence (release cumulativity) and relaxed count adds.
     __shared__ int32_t s_last;
@@ -287,6 +314,18 @@ static __global__ void __launch_bounds__(MOE_THREADS) moe_dispatch_kernel(const 
         // source's rows of this epoch and writes the counts the expert stage reads
         __syncthreads();
         if (s_last && warp == 0) receive_counts_warp(p, ep);
+    }
+    return;
+#endif
+    // one release per (CTA, destination) covers every row this CTA stored there
+    if (tid < W && s_sent[tid]) red_release_sys_add(rx_arr(p, tid, ep) + p.self, s_sent[tid]);
+    if (with_fence && tid == 0) {
+        int old;
+        asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.exit_ticket) : "memory");
+        if (old == static_cast<int>(gridDim.x) - 1) {
+            *p.exit_ticket = 0;
+            *p.epoch = ep;
+        }
     }
 }
 
@@ -386,14 +425,16 @@ static __global__ void __launch_bounds__(256) moe_expert_identity_kernel(const _
 // y_rows: compact [R][H] (row = offs[s] + j) or region [W][m_max][H] (row = s * m_max + j).
 __device__ __forceinline__ void combine_put_body(const MoePeers& p, const __nv_bfloat16* __restrict__ y_rows,
                                                  int region) {
-    __shared__ int32_t s_off[PL_MAXW + 1];
+    __shared__ int32_t s_off[PL_MAXW + 1], s_sent[PL_MAXW];
     const uint32_t ep = *p.epoch;
     const int W = p.W, H = p.H, tid = threadIdx.x;
     if (tid <= W) s_off[tid] = p.offs[tid];
+    if (tid < PL_MAXW) s_sent[tid] = 0;
     __syncthreads();
     const int R = s_off[W];
     const int nvec = H / 8;
     const int32_t* rm = rx_meta(p, p.self, ep);
+#if MOE_K5B_WARP
     // one warp per received row, 8 vectors per lane in flight
     constexpr int VPL = 8;
     const int lane = tid & 31;
@@ -415,8 +456,32 @@ __device__ __forceinline__ void combine_put_body(const MoePeers& p, const __nv_b
             for (int u = 0; u < VPL; ++u)
                 if (v0 + u * 32 < nvec) dst[v0 + u * 32] = v[u];
         }
+        if (lane == 0) atomicAdd(&s_sent[s], 1);
     }
+#else
+    constexpr int VPT = 4;
+    for (int r = blockIdx.x; r < R; r += gridDim.x) {
+        int s = 0;
+        while (s_off[s + 1] <= r) ++s;
+        const int j = r - s_off[s];
+        const int t = __ldcg(rm + ((size_t)s * p.m_max + j) * p.meta);
+        const uint4* src =
+            reinterpret_cast<const uint4*>(y_rows + (size_t)(region ? s * p.m_max + j : r) * H);
+        uint4* dst = reinterpret_cast<uint4*>(cb_y(p, s, ep) + ((size_t)t * W + p.self) * H);
+        for (int v0 = tid; v0 < nvec; v0 += VPT * MOE_THREADS) {
+            uint4 v[VPT];
+#pragma unroll
+            for (int u = 0; u < VPT; ++u)
+                if (v0 + u * MOE_THREADS < nvec) v[u] = __ldg(src + v0 + u * MOE_THREADS);
+#pragma unroll
+            for (int u = 0; u < VPT; ++u)
+                if (v0 + u * MOE_THREADS < nvec) dst[v0 + u * MOE_THREADS] = v[u];
+        }
+        if (tid == 0) ++s_sent[s];
+    }
+#endif
     __syncthreads();
+#if MOE_SINGLE_RELEASE
     if (tid == 0) {
         int old;
         asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(p.exit_ticket) : "memory");
@@ -429,6 +494,9 @@ __device__ __forceinline__ void combine_put_body(const MoePeers& p, const __nv_b
                                  "r"(s_off[d + 1] - s_off[d]) : "memory");
         }
     }
+#else
+    if (tid < W && s_sent[tid]) red_release_sys_add(cb_arr(p, tid, ep) + p.self, s_sent[tid]);
+#endif
 }
 
 // K5b: one launch of the body.
