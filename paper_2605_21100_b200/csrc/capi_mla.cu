@@ -133,10 +133,11 @@ static int mla_launch(dcp_ctx* ctx, const dcp_mla_args* a, cudaStream_t stream, 
 
     mla::mla_tile_scan_kernel<PAGE><<<1, 1024, 0, stream>>>(p);
     DCP_CUDA_TRY(cudaGetLastError());
-    mla::mla_decode_kernel<PAGE><<<2 * pairs, mla::THREADS, mla::SMEM, stream>>>(qmap, kvq, kvp, p);
-    DCP_CUDA_TRY(cudaGetLastError());
-    mla::mla_merge_kernel<<<dim3(a->num_shards, mla::H / 16, mla::MERGE_QUARTERS), 512, 0, stream>>>(p, pairs);
-    DCP_CUDA_TRY(cudaGetLastError());
+    // PDL chain: scan -> decode (prologue overlaps the scan) -> merge (launch overlaps the decode tail)
+    DCP_CUDA_TRY(launch_pdl(mla::mla_decode_kernel<PAGE>, dim3(2 * pairs), dim3(mla::THREADS), mla::SMEM, stream,
+                            qmap, kvq, kvp, p));
+    DCP_CUDA_TRY(launch_pdl(mla::mla_merge_kernel, dim3(a->num_shards, mla::H / 16, mla::MERGE_QUARTERS), dim3(512), 0,
+                            stream, p, pairs));
     return DCP_OK;
 }
 

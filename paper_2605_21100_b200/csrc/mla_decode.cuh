@@ -192,6 +192,7 @@ __device__ __forceinline__ bool pair_nonempty(const int32_t* pair_t0, int k) { r
 // cu_tiles[r] = sum_{s<r} ceil(pages_s / pages_per_tile).
 template <int PAGE>
 __global__ void __launch_bounds__(1024) mla_tile_scan_kernel(MlaParams p) {
+    pdl_trigger();  // the decode launch's prologue may overlap this scan
     constexpr int PPT = TILE / PAGE;
     __shared__ int32_t warp_sum[32];
     __shared__ int32_t carry;
@@ -279,11 +280,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t cta = tc::cluster_ctarank();
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int R = num_shards_of(p);
-    const uint32_t ep = epoch_of(p);
     const int pair = blockIdx.x >> 1;
-    const int t_begin = p.pair_t0[pair];
-    const int t_end = p.pair_t0[pair + 1];
+    // PDL-launched after the tile scan: the merge launch may queue now; this grid's prologue
+    // (barriers, TMEM, cluster sync) overlaps the scan, which it waits for before reading its
+    // tile ranges (griddepcontrol is a no-op for a plain launch)
+    pdl_trigger();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NSTAGES; ++s) {
@@ -316,6 +317,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc::fence_after_sync();
     const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(smem + OFF_MISC + TMEM_SLOT);
     const uint32_t lead = tc::mapa(misc, 0);  // leader's misc block (shared::cluster)
+    pdl_wait();
+    const int R = num_shards_of(p);
+    const uint32_t ep = epoch_of(p);
+    const int t_begin = p.pair_t0[pair];
+    const int t_end = p.pair_t0[pair + 1];
     // trace tail (dcp_mla_set_trace): per pair start, end and SM at [2048 + 3 pair + 0..2]
     if (p.trace && cta == 0 && threadIdx.x == 0 && pair < 256) {
         uint32_t smid;
@@ -803,6 +809,8 @@ __device__ __forceinline__ void merge_done(const MlaParams& p, int r) {
 }
 
 __global__ void __launch_bounds__(512, 2) mla_merge_kernel(MlaParams p, int num_pairs) {
+    pdl_trigger();
+    pdl_wait();  // PDL-launched after the decode grid: its partials
     const int r = blockIdx.x;
     if (r >= num_shards_of(p)) return;  // routed launches cover n_max shards
     const int r_first = p.cu_tiles[r], r_last = p.cu_tiles[r + 1];
