@@ -18,18 +18,23 @@
 //     (cluster of 2, cta_group::2, M = 128) shares every MMA: CTA c owns heads
 //     [64c, 64c+64) and half of each B operand; its TMEM holds its 64 rows
 //     folded into 128 lanes (lanes 64.. carry the second half of N).  Per CTA:
-//     S double-buffered 2 x 64 columns, O 256 columns.
+//     S split over K into S_A + S_B (two MMA chains), each double-buffered,
+//     4 x 64 columns; O 256 columns.
 //   * A tile is 128 tokens of one shard.  S = Q K^T: N = 128 tokens, CTA c
 //     streams tokens [64c, 64c+64) x 576 (9 K boxes of 64).  O += P V: N = 256
 //     latent dims per MMA, CTA c streams dims [256j+128c, +128) of all 128
 //     tokens (MN-major B straight from the cache rows; the re-read hits L2).
-//   * One producer warp per CTA (TMA, 2-CTA form: completion bytes land on the
-//     leader's barrier), one MMA thread in the leader, four softmax warps per
-//     CTA (thread t <-> TMEM lane t).  The softmax keeps a per-row reference
-//     max and rescales O in TMEM only when the max grows by more than 2^8.
+//   * Warps: 4 softmax warps per CTA (thread t <-> TMEM lane t); 4 MMA warps in
+//     the leader, one per accumulator chain (S_A, S_B, O's two latent halves);
+//     2 TMA issuer warps per ring (QA: K boxes 0-4, QB: 5-8 from HBM; V0, V1 from
+//     L2), 2-CTA TMA completing on the leader's barriers.  Shared memory: Q 72
+//     KB, one P buffer (16 KB), 17 ring stages of 8 KB (5 + 4 + 4 + 4).  The
+//     softmax keeps a per-row reference max and rescales O in TMEM only when
+//     the max grows by more than 2^8.
 //   * Persistent pairs, stream-K over tiles: every pair streams the same number
 //     of tiles whatever the 1K..512K length skew; cut shards leave partials in
-//     a per-pair slot and a second, fully parallel launch merges them.
+//     a per-pair slot and a third, fully parallel launch merges them.  Tile
+//     scan -> decode -> merge are PDL-chained.
 #pragma once
 
 #include <cstdint>
