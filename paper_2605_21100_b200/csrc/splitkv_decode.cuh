@@ -57,8 +57,8 @@ struct AttnParams {
     const int32_t* total_pages_ptr; // device-resident cu_pages[R] (routed: loaded alongside R)
     long long* trace;            // optional [grid][8] globaltimer stamps per CTA (dcp_k1_set_trace)
     // ---- fused routed step (dcp_decode_step_fused): one launch per step.  FUSE_STEP: this
-    // launch is the step's begin_step (fence, epoch e = *epoch + 1, bumped by the last CTA to
-    // exit); FUSE_ROUTE: K2's Q-route puts in the prologue; FUSE_MERGE: K3's LSE merges of this
+    // launch is the step's begin_step (fence, epoch e = *epoch + 1, advanced by the CTA whose
+    // producer warp takes the grid's ticket last); FUSE_ROUTE: K2's Q-route puts in the prologue; FUSE_MERGE: K3's LSE merges of this
     // instance's M rows in the epilogue (spins on peers' Res-route flags: multi-GPU / W = 1 only).
     uint32_t fuse;
     const void* q_local;         // [m_max][HQ][D] bf16, M-row order (route)
