@@ -204,3 +204,30 @@ def test_mla_bench_inputs_all_shards(ctx, name):
     torch.cuda.synchronize()
     rel, dl = _check(b, q.cpu(), pool.cpu(), out.cpu().double().numpy(), lse.cpu().double().numpy())
     print(f"{name}: {len(lens)} shards x 128 heads, worst O rel-L2 {rel:.3e}, LSE |d| {dl:.3e}")
+
+
+def test_mla_graph_replay(ctx):
+    """K10's three launches (tile scan -> decode -> merge, PDL-chained) captured in a CUDA graph
+    and replayed: bit-identical to the eager call."""
+    from paper_2605_21100_b200.attention import MlaDecodeAttention
+    dev = torch.device("cuda:0")
+    b, q, pool = _case(workload.lengths(3, 24, 200, 9000), seed=31)
+    att = MlaDecodeAttention(ctx, b.page_size, max_shards=len(b.shard_len))
+    out, lse = att.prepare(q.to(dev), pool.to(dev), torch.from_numpy(b.block_table).to(dev),
+                           torch.from_numpy(b.cu_pages).to(dev), torch.from_numpy(b.shard_len).to(dev))
+    att.launch()
+    torch.cuda.synchronize()
+    o0, l0 = out.clone(), lse.clone()
+    out.zero_()
+    g = torch.cuda.CUDAGraph()
+    st = torch.cuda.Stream()
+    st.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(st):
+        with torch.cuda.graph(g, stream=st):
+            att.launch(st)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, o0) and torch.equal(lse, l0)
+    _check(b, q, pool, out.cpu().double().numpy(), lse.cpu().double().numpy())
