@@ -547,6 +547,22 @@ def run_ours(args, ws, rank, local):
             mla = [{k: r[k] for k in keep} for r in bench_mla.run_all(ctx, dev, steps=min(args.steps, 50), warmup=3)]
         except Exception as e:  # reported, not fatal
             mla = {"error": str(e)}
+    moe = None
+    if rank == 0 and ws == 1 and not args.no_moe:
+        # the cfg4 / cfg5 EP exchange (K4 / K5, W = 8 instances emulated on this
+        # GPU; peer stores are local), device time per instance of the whole step back to back
+        try:
+            import bench_moe
+            moe = []
+            for r in bench_moe.run_all(ctx, dev, steps=min(args.steps, 20), warmup=3):
+                moe.append({"workload": r["workload"], "us_per_instance_whole_step": r["whole_step"]["us_per_instance"],
+                            "us_p99_per_instance": r["whole_step"]["us_p99_per_instance"],
+                            "us_per_instance_event_timed_phases": r["us_per_instance_step"],
+                            "cross_instance_bytes_per_step": r["cross_instance_bytes_per_step"],
+                            "note": "emulation: one GPU hosts all 8 instances, cross-instance stores are local HBM "
+                                    "stores; identity experts; multi-GPU NVLink timing needs an 8-GPU box"})
+        except Exception as e:  # reported, not fatal
+            moe = {"error": str(e)}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -581,6 +597,7 @@ def run_ours(args, ws, rank, local):
             "cpu_baseline": cpu,
             "planner": planner,
             "mla": mla,
+            "moe": moe,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -601,6 +618,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mla", action="store_true", help="skip the K10 MLA leg (SURVEY §8f #1)")
+    ap.add_argument("--no-moe", action="store_true", help="skip the K4/K5 MoE exchange leg (emulated, 8 instances)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent cfg2 replicas instead of the multi-GPU DCP step")
     ap.add_argument("--phased", action="store_true",
