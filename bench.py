@@ -563,6 +563,29 @@ def run_ours(args, ws, rank, local):
                                     "stores; identity experts; multi-GPU NVLink timing needs an 8-GPU box"})
         except Exception as e:  # reported, not fatal
             moe = {"error": str(e)}
+    dcp_p99 = None
+    if rank == 0 and ws == 1 and not args.no_dcp:
+        # the metric's "P99 step ms": bench_dcp's skewed cfg3-shaped batch (4 instances emulated on
+        # this GPU, 3 x 131K + 256 x 2K requests), DCP vs the CP = 1 policies, P99 over 1,000 steps
+        try:
+            import types
+            import bench_dcp
+            a = types.SimpleNamespace(instances=4, short_per=64, short_len=2048, long=3, long_len=131073,
+                                      capacity=40000, steps=1000, warmup=5, n_sched=8)
+            gd = torch.Generator(device=dev).manual_seed(1)
+            pools = [torch.randn(a.capacity, 2, 8, 16, 128, generator=gd, device=dev, dtype=torch.bfloat16)
+                     for _ in range(a.instances)]
+            res = {}
+            for pol in ("dcp", "least_batch", "least_cache"):
+                r = bench_dcp.run_policy(pol, a, ctx, pools)
+                res[pol] = {k: r[k] for k in ("step_ms_p50", "step_ms_p99", "imbalance_pct", "cp_histogram")}
+            del pools
+            best = min(v["step_ms_p99"] for k, v in res.items() if k != "dcp")
+            dcp_p99 = {"workload": "cfg3-shaped skewed batch, 4 instances emulated on one GPU (step = max over "
+                                   "instances of the routed K2 + K1 + K3 device time), 1,000 steps",
+                       "policies": res, "p99_best_cp1_over_dcp": best / res["dcp"]["step_ms_p99"]}
+        except Exception as e:  # reported, not fatal
+            dcp_p99 = {"error": str(e)}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -598,6 +621,7 @@ def run_ours(args, ws, rank, local):
             "planner": planner,
             "mla": mla,
             "moe": moe,
+            "dcp_p99": dcp_p99,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -619,6 +643,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mla", action="store_true", help="skip the K10 MLA leg (SURVEY §8f #1)")
     ap.add_argument("--no-moe", action="store_true", help="skip the K4/K5 MoE exchange leg (emulated, 8 instances)")
+    ap.add_argument("--no-dcp", action="store_true", help="skip the DCP vs CP=1 P99 leg (emulated, 4 instances)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: N independent cfg2 replicas instead of the multi-GPU DCP step")
     ap.add_argument("--phased", action="store_true",

@@ -15,7 +15,7 @@ timeout 300 python bench_graph.py > $OUT/bench_graph_$TAG.json 2>&1
 timeout 900 python bench_trace.py --duration 10 --rate 16 > $OUT/bench_trace_$TAG.jsonl 2> $OUT/bench_trace_$TAG.err
 DCP_BENCH_ONE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 > $OUT/bench_multi2_$TAG.json 2> $OUT/bench_multi2_$TAG.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
-    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-mla --no-moe > $OUT/ncu_launch_bench_$TAG.log 2>&1
+    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-mla --no-moe --no-dcp > $OUT/ncu_launch_bench_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:splitkv_decode -s 3 -c 1 \
-    -o $OUT/k1_$TAG -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-mla --no-moe > $OUT/ncu_full_$TAG.log 2>&1
+    -o $OUT/k1_$TAG -f python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-mla --no-moe --no-dcp > $OUT/ncu_full_$TAG.log 2>&1
 echo done
